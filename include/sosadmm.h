@@ -1,0 +1,153 @@
+/*
+ * sosadmm.h — C ABI of the B200-native HSDE-ADMM hot path for SOS-derived SDPs
+ * (arXiv 1708.04174, Zheng, Fantuzzi, Papachristodoulou: "Fast ADMM for sum-of-squares programs
+ * using partial orthogonality").  Citations "P:n" are lines of the paper's LaTeX source
+ * (PAPER.md); "S:n" are lines of SPEC.md; labels are the paper's equation labels.
+ *
+ * Problem (`eq:generalSDP`):  min c^T xi  s.t.  A xi = b,  xi in K = R^t x S+(N_1) x ...
+ * Dual:  max b^T y  s.t.  A^T y + z = c,  z in K*.
+ * The library runs the ADMM of `eq:ADMMSteps` on the homogeneous self-dual embedding
+ * with u = (xi, y, tau), v = (z, s, kappa):
+ *     u_hat = (I + Q)^{-1}(u + v);   u = P_C(u_hat - v);   v = v - u_hat + u.
+ * The linear step uses partial orthogonality (Proposition 1; Prop. 3):
+ * every PSD column with at most one nonzero (and c_j = 0) is "orthogonal", the rest (the t free
+ * columns and any other PSD column) form A_low, and (I + A A^T)^{-1} = P^{-1} - P^{-1} A_low
+ * (I + A_low^T P^{-1} A_low)^{-1} A_low^T P^{-1} with P = I + A_orth A_orth^T diagonal,
+ * plus the rank-one HSDE correction with cached M^{-1} zeta (`E:MatrixInverseResult`).
+ *
+ * Layouts (all host pointers unless stated):
+ *  - column order of xi, z, c and of A: t free columns, then one svec block per PSD cone;
+ *  - svec = LAPACK 'U' packed column-major: position p(i,j) = i + j(j+1)/2 for i <= j, with the
+ *    off-diagonal entries scaled by sqrt(2) (an isometry of S^N; reading C1);
+ *  - A is CSC (m x n, n = t + sum N_b(N_b+1)/2), 0-based, int64 column pointers, int32 rows;
+ *  - FP64 everywhere; indices int32/int64 as declared.
+ * Ownership: inputs are borrowed for the duration of the call and copied.  The context owns its
+ *  device state, which lives in the caller-provided device workspace (e.g. a torch tensor) or,
+ *  if settings.workspace is NULL, in memory the library allocates itself.  Outputs are written
+ *  to caller buffers.  A context is not thread-safe; distinct contexts are independent.
+ * Errors: every call returns sosadmm_err (0 = OK).  The first error is latched in the context and
+ *  returned by every later call; sosadmm_last_error_message() gives a human-readable detail.
+ * Initialisation (reading C7): u0 = (0, 0, 1), v0 = (0, 0, 0).  No scaling, no
+ *  relaxation (reading C8).  Residuals and termination: DESIGN.md reading C9.
+ */
+#ifndef SOSADMM_H
+#define SOSADMM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SOSADMM_OK = 0,
+  SOSADMM_E_ARG = -1,       /* malformed input (sizes, pointers, CSC structure) */
+  SOSADMM_E_STRUCT = -2,    /* unsupported structure (e.g. low-rank width too large) */
+  SOSADMM_E_FACTOR = -3,    /* I + A_low^T P^{-1} A_low not numerically SPD (impossible in exact arithmetic) */
+  SOSADMM_E_CUDA = -4,      /* CUDA runtime error (message has the detail) */
+  SOSADMM_E_NCCL = -5,      /* reserved for the sharded mode */
+  SOSADMM_E_NONFINITE = -6, /* non-finite iterate; message names the iteration */
+  SOSADMM_E_OOM = -7        /* workspace too small / allocation failed */
+} sosadmm_err;
+
+typedef enum {
+  SOSADMM_RUNNING = 0,
+  SOSADMM_OPTIMAL = 1,            /* max(res_pri, res_dual, res_gap) <= tol */
+  SOSADMM_PRIMAL_INFEASIBLE = 2,  /* b^T y > 0 and ||A^T y + z|| / b^T y <= tol (reading C9) */
+  SOSADMM_DUAL_INFEASIBLE = 3,    /* c^T xi < 0 and ||A xi|| / (-c^T xi) <= tol (reading C9) */
+  SOSADMM_MAX_ITERS = 4,
+  SOSADMM_INCONCLUSIVE = 5
+} sosadmm_status;
+
+/* Conic data of `eq:generalSDP`.  psd_dim[b] = N_b; block b owns N_b(N_b+1)/2 svec columns. */
+typedef struct {
+  int64_t m;
+  int64_t n_free;
+  int32_t n_psd;
+  const int32_t* psd_dim;
+  const int64_t* A_colptr; /* n + 1 */
+  const int32_t* A_rowidx; /* nnz */
+  const double* A_val;     /* nnz */
+  const double* b;         /* m */
+  const double* c;         /* n */
+} sosadmm_problem;
+
+typedef struct {
+  double tol;            /* termination tolerance on the C9 residuals (default 1e-4) */
+  int64_t max_iters;     /* status MAX_ITERS once this many iterations ran */
+  int32_t check_every;   /* residual check stride (1 = every iteration; the only supported value) */
+  int32_t device;        /* CUDA device ordinal */
+  void* stream;          /* cudaStream_t to launch on (NULL = the library's own stream) */
+  void* workspace;       /* device memory of >= sosadmm_workspace_size() bytes, or NULL */
+  size_t workspace_bytes;
+} sosadmm_settings;
+
+typedef struct {
+  int64_t iter;       /* iterations completed (k of u^k) */
+  int32_t status;     /* sosadmm_status */
+  double res_pri;     /* ||A xi/tau - b|| / (1 + ||b||) at u^k (inf if tau = 0) */
+  double res_dual;    /* ||A^T y/tau + z/tau - c|| / (1 + ||c||) */
+  double res_gap;     /* |c^T xi/tau - b^T y/tau| / (1 + |c^T xi/tau| + |b^T y/tau|) */
+  double pobj;        /* c^T xi / tau */
+  double dobj;        /* b^T y / tau */
+  double tau, kappa;
+  double pinf, dinf;  /* certificate ratios of reading C9 (inf when the sign test fails) */
+} sosadmm_info;
+
+typedef struct sosadmm_ctx sosadmm_ctx;
+
+/* Structural analysis only (no factorisation): device bytes the context needs. 0 on bad input. */
+size_t sosadmm_workspace_size(const sosadmm_problem* prob);
+
+/* Setup ("can be cached"): classify columns, build the
+ * alpha-map, D and P = I + D, A_low in CSR/CSC, K = I + A_low^T P^{-1} A_low and its inverse,
+ * h = M^{-1} zeta (zeta = (c, -b)) and 1 + zeta^T h; copy the data to the device; set u0, v0. */
+sosadmm_err sosadmm_setup(const sosadmm_problem* prob, const sosadmm_settings* settings, sosadmm_ctx** out);
+
+/* Run up to k ADMM iterations (`eq:ADMMSteps`) on the device, stopping early when the C9 rule
+ * fires or max_iters is reached; every iteration's residuals are checked.  Asynchronous work is
+ * completed before return; *out (may be NULL) receives the state after the last iteration. */
+sosadmm_err sosadmm_iterate(sosadmm_ctx* ctx, int64_t k, sosadmm_info* out);
+
+/* Same iterations launched without the CUDA graph, with CUDA events around each phase; adds the
+ * phase durations (ms) to ms_phase[0..3] = {affine gather+t-phase, scatter, PSD projection,
+ * pack/dual update}.  Used by bench.py for the per-kernel-class roofline. */
+sosadmm_err sosadmm_iterate_profiled(sosadmm_ctx* ctx, int64_t k, sosadmm_info* out, double* ms_phase);
+
+/* Current info without iterating (residuals of u^k are computed on demand). */
+sosadmm_err sosadmm_get_info(sosadmm_ctx* ctx, sosadmm_info* out);
+
+/* Copy the unscaled iterates u = (xi, y, tau), v = (z, s, kappa) to host buffers (n, m, n, m). */
+sosadmm_err sosadmm_get_iterate(sosadmm_ctx* ctx, double* xi, double* y, double* z, double* s,
+                                double* tau, double* kappa, int64_t* iter);
+
+/* Overwrite the iterates (resume / fixed-point tests).  s may be NULL (= 0).  Resets status. */
+sosadmm_err sosadmm_set_iterate(sosadmm_ctx* ctx, const double* xi, const double* y, const double* z,
+                                const double* s, double tau, double kappa, int64_t iter);
+
+/* Partial-orthogonality structure found by setup (Proposition 1):
+ * row_of[j] for every column j: the row of its single nonzero if the column is orthogonal
+ * (-1 for an empty orthogonal column), -2 if it belongs to A_low;  D[alpha] = sum over orthogonal
+ * columns of (A_alpha,j / w_j)^2 * w_j^2 with w_j the svec weight, i.e. the exact integer count
+ * n_alpha for indicator data;  *t_low = number of A_low columns (t').  Buffers: n, m. */
+sosadmm_err sosadmm_get_structure(sosadmm_ctx* ctx, int32_t* row_of, double* D, int64_t* t_low);
+
+/* Unit entry points of the two kernels classes (tests and bench), host buffers:
+ * affine projection u_hat = (I + Q)^{-1} w  (`eq:HsdeStep1`, P:396 via P:426-481). */
+sosadmm_err sosadmm_project_affine(sosadmm_ctx* ctx, const double* w1, const double* w2, double w3,
+                                   double* u1, double* u2, double* u3);
+/* PSD projection of one block in svec coordinates (`eq:HsdeStep2`). */
+sosadmm_err sosadmm_project_psd(sosadmm_ctx* ctx, int32_t block, const double* a_svec, double* out_svec);
+
+/* Number of kernel launches one iteration issues (for the bench's gpu_launches claim). */
+int64_t sosadmm_launches_per_iter(const sosadmm_ctx* ctx);
+
+void sosadmm_destroy(sosadmm_ctx* ctx);
+const char* sosadmm_strerror(sosadmm_err e);
+const char* sosadmm_last_error_message(const sosadmm_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SOSADMM_H */

@@ -1,0 +1,432 @@
+// Affine-projection kernels: u_hat = (I + Q)^{-1}(u + v) with partial orthogonality.
+//
+// PAPER.md P:426-446 (tau elimination + rank-one SMW with cached h = M^{-1} zeta)
+// (sigma_1 elimination: (I + A A^T) sigma_2 = w2 - A w1), P:469-480 (Woodbury with P = I + D
+// diagonal, D = A_orth A_orth^T, Proposition 1) and the Appendix op list P:870-877.
+//
+// Data flow per iteration:
+//   k_gather   (rows)     : g = A r1, x = P^{-1}(r2 - g), partial b^T x; residual partials of u^k
+//   k_lowT     (t' cols)  : y_t = A_low^T x, A_low^T y
+//   k_kinv     (t' rows)  : z_t = K^{-1} y_t         (K = I + A_low^T P^{-1} A_low)
+//   k_tphase   (1 CTA)    : residuals/termination of u^k (reading C9); coef, u_hat_low, u_hat_3,
+//                           tau/kappa update, free columns (A_low^T sigma_2 = z_t by the Woodbury
+//                           identity, b^T sigma_2 = b^T x - (A_low^T P^{-1} b)^T z_t)
+//   k_rowupdate(rows)     : sigma_2 = x - P^{-1} A_low z_t, u_hat_2 = sigma_2 - coef h_2, y, s update
+//   k_scatter  (svec pos) : a = u_hat_xi - z (= xi + A_orth^T u_hat_2 on orthogonal columns), into the
+//                           per-block symmetric matrices (input of the PSD projection)
+//   k_pack     (svec pos) : xi = svec(Pi(a)), z = xi - a (Moreau); commit tau, kappa, k
+#pragma once
+#include "common.cuh"
+
+struct AffineArgs {
+  int m, n, t_free, tl, npsd;
+  // orthogonal columns, grouped by row (CSR of A_orth)
+  const int* seg_ptr;
+  const int* seg_col;
+  const double* seg_val;
+  // A_low: columns low_col[j]; CSR (rows) and CSC (low columns)
+  const int* low_col;
+  const int* lr_ptr;
+  const int* lr_idx;
+  const double* lr_val;
+  const int* lc_ptr;
+  const int* lc_row;
+  const double* lc_val;
+  const double* c_low;
+  const double* h1_low;
+  const double* beta_low;
+  const double* Kinv;  // tl x tl, symmetric
+  const int* empty_cols;
+  int n_empty;
+  // row data
+  const double* b;
+  const double* Pinv;
+  const double* h2;
+  double denom, bh2, nb, nc;
+  // per-column data (size n): code >= 0 orth row, -1 empty orth column, <= -2 low index (-2 - j)
+  const int* code;
+  const double* aval;
+  // state
+  double* xi;
+  double* z;
+  double* y;
+  double* s;
+  DevState* st;
+  IterScal* is;
+  // scratch
+  double* x;
+  double* uhat2;
+  double* yt;
+  double* zt;
+  double* ulow;
+  double* aty;
+  double* part;
+  int gather_blocks;
+  double* asvec;  // PSD part of u_hat_xi - z (size npsd)
+  // PSD blocks
+  int nblk;
+  const long long* blk_col;   // first column of block b
+  const int* blk_N;
+  const long long* blk_mat;   // offset of block b's N x N matrix in mats
+  double* mats;
+  const int* cta_blk;         // position-parallel kernels: CTA -> (block, first local svec index)
+  const long long* cta_q0;
+  int pos_ctas;
+};
+
+constexpr int GATHER_NT = 256;
+constexpr int POS_NT = 256;
+constexpr int POS_PER_CTA = 1024;
+
+// ---------------------------------------------------------------------------------------------
+// k_gather: one thread per row alpha.
+//   g_alpha  = sum_{orth j in seg(alpha)} A_{alpha j}(xi_j + z_j) + sum_{low j} A_{alpha j} r1_j
+//              (r1 = w1 - c w3 with w1 = xi + z; c vanishes on orthogonal columns)
+//   x_alpha  = (y_alpha + s_alpha + b_alpha w3 - g_alpha) / P_alpha
+// and, for the residuals of u^k (reading C9), (A xi)_alpha and sum_{j in seg(alpha)} (A^T y + z)_j^2.
+__global__ void __launch_bounds__(GATHER_NT) k_gather(AffineArgs a) {
+  __shared__ double sh[GATHER_NT / 32];
+  if (a.st->done) return;
+  const double tau = a.st->tau, w3 = tau + a.st->kappa;
+  const int r = blockIdx.x * GATHER_NT + threadIdx.x;
+  double p_bx = 0, p_pres = 0, p_axi = 0, p_dres = 0, p_by = 0;
+  if (r < a.m) {
+    const double yr = a.y[r];
+    double gx = 0.0, gz = 0.0, dres = 0.0;
+    const int e0 = a.seg_ptr[r], e1 = a.seg_ptr[r + 1];
+    for (int e = e0; e < e1; ++e) {
+      const int j = a.seg_col[e];
+      const double v = a.seg_val[e];
+      const double xj = a.xi[j], zj = a.z[j];
+      gx = fma(v, xj, gx);
+      gz = fma(v, zj, gz);
+      const double d = fma(v, yr, zj);
+      dres = fma(d, d, dres);
+    }
+    double gl = 0.0, axl = 0.0;
+    const int l0 = a.lr_ptr[r], l1 = a.lr_ptr[r + 1];
+    for (int e = l0; e < l1; ++e) {
+      const int jl = a.lr_idx[e];
+      const int j = a.low_col[jl];
+      const double v = a.lr_val[e];
+      const double xj = a.xi[j];
+      const double r1 = (xj + a.z[j]) - a.c_low[jl] * w3;
+      gl = fma(v, r1, gl);
+      axl = fma(v, xj, axl);
+    }
+    const double g = (gx + gz) + gl;
+    const double r2 = (yr + a.s[r]) + a.b[r] * w3;
+    const double xr = (r2 - g) * a.Pinv[r];
+    a.x[r] = xr;
+    const double axi = gx + axl;
+    const double pr = axi - a.b[r] * tau;
+    p_bx = a.b[r] * xr;
+    p_pres = pr * pr;
+    p_axi = axi * axi;
+    p_dres = dres;
+    p_by = a.b[r] * yr;
+  }
+  double v;
+  v = block_sum<GATHER_NT>(p_bx, sh);
+  if (threadIdx.x == 0) a.part[PART_BX * a.gather_blocks + blockIdx.x] = v;
+  v = block_sum<GATHER_NT>(p_pres, sh);
+  if (threadIdx.x == 0) a.part[PART_PRES * a.gather_blocks + blockIdx.x] = v;
+  v = block_sum<GATHER_NT>(p_axi, sh);
+  if (threadIdx.x == 0) a.part[PART_AXI * a.gather_blocks + blockIdx.x] = v;
+  v = block_sum<GATHER_NT>(p_dres, sh);
+  if (threadIdx.x == 0) a.part[PART_DRES * a.gather_blocks + blockIdx.x] = v;
+  v = block_sum<GATHER_NT>(p_by, sh);
+  if (threadIdx.x == 0) a.part[PART_BY * a.gather_blocks + blockIdx.x] = v;
+}
+
+// k_lowT: one warp per low column j:  y_t[j] = (A_low^T x)_j,  aty[j] = (A_low^T y)_j.
+__global__ void __launch_bounds__(256) k_lowT(AffineArgs a) {
+  if (a.st->done) return;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= a.tl) return;
+  double sx = 0.0, sy = 0.0;
+  for (int e = a.lc_ptr[wid] + lane; e < a.lc_ptr[wid + 1]; e += 32) {
+    const int r = a.lc_row[e];
+    const double v = a.lc_val[e];
+    sx = fma(v, a.x[r], sx);
+    sy = fma(v, a.y[r], sy);
+  }
+  sx = warp_sum(sx);
+  sy = warp_sum(sy);
+  if (lane == 0) {
+    a.yt[wid] = sx;
+    a.aty[wid] = sy;
+  }
+}
+
+// k_kinv: one warp per row i:  z_t[i] = sum_j Kinv[i, j] y_t[j]  (P:874 with the cached factor
+// applied as an explicit SPD inverse; K symmetric so row i = column i).
+__global__ void __launch_bounds__(256) k_kinv(AffineArgs a) {
+  if (a.st->done) return;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= a.tl) return;
+  const double* row = a.Kinv + (size_t)wid * a.tl;
+  double acc = 0.0;
+  for (int j = lane; j < a.tl; j += 32) acc = fma(row[j], a.yt[j], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) a.zt[wid] = acc;
+}
+
+// k_tphase: single CTA.  mode 0 = full iteration, 1 = check-only (residuals of u^k, no update),
+// 2 = affine-only (unit entry point: no termination logic, no writes to xi/z).
+constexpr int TP_NT = 512;
+__global__ void __launch_bounds__(TP_NT) k_tphase(AffineArgs a, int mode) {
+  __shared__ double sh[TP_NT / 32];
+  __shared__ double bc[8];
+  DevState* st = a.st;
+  if (st->done) return;
+  const int tid = threadIdx.x;
+  // 1. fixed-order reductions of the gather partials
+  double sums[NPART];
+#pragma unroll
+  for (int k = 0; k < NPART; ++k) {
+    double v = 0.0;
+    for (int i = tid; i < a.gather_blocks; i += TP_NT) v += a.part[k * a.gather_blocks + i];
+    v = block_sum<TP_NT>(v, sh);
+    if (tid == 0) bc[k] = v;
+  }
+  // low / free columns: c^T xi, dual residual of low columns, (A_low xi part already in gather)
+  const double tau = st->tau, kappa = st->kappa, w3 = tau + kappa;
+  double cx = 0.0, dl = 0.0, dl0 = 0.0;
+  for (int j = tid; j < a.tl; j += TP_NT) {
+    const int col = a.low_col[j];
+    const double cj = a.c_low[j];
+    cx = fma(cj, a.xi[col], cx);
+    const double d0 = a.aty[j] + a.z[col];
+    const double d = d0 - cj * tau;
+    dl = fma(d, d, dl);
+    dl0 = fma(d0, d0, dl0);
+  }
+  for (int j = tid; j < a.n_empty; j += TP_NT) {
+    const double zj = a.z[a.empty_cols[j]];
+    dl = fma(zj, zj, dl);
+    dl0 = fma(zj, zj, dl0);
+  }
+  cx = block_sum<TP_NT>(cx, sh);
+  if (tid == 0) bc[5] = cx;
+  dl = block_sum<TP_NT>(dl, sh);
+  if (tid == 0) bc[6] = dl;
+  dl0 = block_sum<TP_NT>(dl0, sh);
+  if (tid == 0) bc[7] = dl0;
+  __syncthreads();
+  for (int k = 0; k < NPART; ++k) sums[k] = bc[k];
+  cx = bc[5];
+  dl = bc[6];
+  dl0 = bc[7];
+
+  // 2. residuals of u^k and the termination rule (reading C9)
+  if (mode != 2 && tid == 0) {
+    const double by = sums[PART_BY];
+    const double nATyz = sqrt(sums[PART_DRES] + dl0);  // ||A^T y + z|| (certificate test)
+    const double nAxi = sqrt(sums[PART_AXI]);
+    const double pinf = (by > 0.0) ? nATyz / by : INFINITY;
+    const double dinf = (cx < 0.0) ? nAxi / (-cx) : INFINITY;
+    double pres = INFINITY, dres = INFINITY, gap = INFINITY, pobj = NAN, dobj = NAN;
+    if (tau > 0.0) {
+      pres = sqrt(sums[PART_PRES]) / tau / (1.0 + a.nb);
+      pobj = cx / tau;
+      dobj = by / tau;
+      gap = fabs(pobj - dobj) / (1.0 + fabs(pobj) + fabs(dobj));
+    }
+    // ||A^T y + z - c tau||: c vanishes on orthogonal columns, dl holds the low columns
+    if (tau > 0.0) dres = sqrt(sums[PART_DRES] + dl) / tau / (1.0 + a.nc);
+    st->res_pri = pres;
+    st->res_dual = dres;
+    st->res_gap = gap;
+    st->pobj = pobj;
+    st->dobj = dobj;
+    st->pinf = pinf;
+    st->dinf = dinf;
+    int status = 0;
+    const bool bad = !(isfinite(sums[PART_PRES]) && isfinite(sums[PART_DRES]) && isfinite(dl) &&
+                       isfinite(tau) && isfinite(kappa));
+    if (bad) {
+      st->nonfinite = 1;
+      st->nonfinite_iter = st->iter;
+      st->done = 1;
+      status = 5;  // INCONCLUSIVE
+    } else if (st->iter >= 1) {
+      if (fmax(pres, fmax(dres, gap)) <= st->tol) status = 1;
+      else if (pinf <= st->tol) status = 2;
+      else if (dinf <= st->tol) status = 3;
+      if (status == 0 && st->iter >= st->max_iters) status = 4;
+    }
+    st->status = status;
+    if (status != 0) st->done = 1;
+    a.is->proceed = (mode == 0 && status == 0) ? 1 : 0;
+  }
+  if (mode == 2 && tid == 0) a.is->proceed = 1;
+  __syncthreads();
+  if (mode == 1) return;
+  if (!a.is->proceed) return;
+
+  // 3. rank-one HSDE correction and tau-elimination
+  //    p1_low = r1_low + A_low^T sigma_2 = r1_low + z_t;  b^T sigma_2 = b^T x - beta_low^T z_t
+  double bz = 0.0, cp = 0.0;
+  for (int j = tid; j < a.tl; j += TP_NT) {
+    const int col = a.low_col[j];
+    const double cj = a.c_low[j];
+    const double p1 = ((a.xi[col] + a.z[col]) - cj * w3) + a.zt[j];
+    a.ulow[j] = p1;  // temporarily p1_low
+    bz = fma(a.beta_low[j], a.zt[j], bz);
+    cp = fma(cj, p1, cp);
+  }
+  bz = block_sum<TP_NT>(bz, sh);
+  if (tid == 0) bc[0] = bz;
+  cp = block_sum<TP_NT>(cp, sh);
+  if (tid == 0) bc[1] = cp;
+  __syncthreads();
+  const double bsig2 = sums[PART_BX] - bc[0];
+  const double zp = bc[1] - bsig2;            // zeta^T p = c^T p1 - b^T p2
+  const double coef = zp / a.denom;           // (M^{-1}zeta)zeta^T / (1 + zeta^T M^{-1} zeta)
+  double cu = 0.0;
+  for (int j = tid; j < a.tl; j += TP_NT) {
+    const double u = a.ulow[j] - coef * a.h1_low[j];
+    a.ulow[j] = u;
+    cu = fma(a.c_low[j], u, cu);
+  }
+  cu = block_sum<TP_NT>(cu, sh);
+  if (tid == 0) {
+    const double bu2 = bsig2 - coef * a.bh2;  // b^T u_hat_2 = b^T sigma_2 - coef b^T h_2
+    const double u3 = w3 + cu - bu2;          // E:FirstBlockElimination
+    a.is->omega3 = w3;
+    a.is->coef = coef;
+    a.is->u3 = u3;
+    a.is->bsig2 = bsig2;
+    const double tn = fmax(0.0, u3 - kappa);  // P_{R+}
+    a.is->tau_new = tn;
+    a.is->kappa_new = kappa - u3 + tn;
+  }
+  __syncthreads();
+  if (mode == 2) return;
+  // 4. free columns: cone R^t -> identity; xi = u_hat - z, z = z - u_hat + xi
+  for (int j = tid; j < a.tl; j += TP_NT) {
+    const int col = a.low_col[j];
+    if (col < a.t_free) {
+      const double u = a.ulow[j];
+      const double zo = a.z[col];
+      const double xn = u - zo;
+      a.xi[col] = xn;
+      a.z[col] = (zo - u) + xn;
+    }
+  }
+}
+
+// k_rowupdate: sigma_2 = x - P^{-1} A_low z_t; u_hat_2 = sigma_2 - coef h_2;
+// y = u_hat_2 - s (R^m cone: identity); s = s - u_hat_2 + y.
+__global__ void __launch_bounds__(256) k_rowupdate(AffineArgs a, int write_state) {
+  if (a.st->done || !a.is->proceed) return;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= a.m) return;
+  double v = 0.0;
+  for (int e = a.lr_ptr[r]; e < a.lr_ptr[r + 1]; ++e) v = fma(a.lr_val[e], a.zt[a.lr_idx[e]], v);
+  const double sig2 = a.x[r] - a.Pinv[r] * v;
+  const double u2 = sig2 - a.is->coef * a.h2[r];
+  a.uhat2[r] = u2;
+  if (write_state) {
+    const double so = a.s[r];
+    const double yn = u2 - so;
+    a.y[r] = yn;
+    a.s[r] = (so - u2) + yn;
+  }
+}
+
+// k_scatter: projection input a = u_hat_xi - z for every PSD svec position, written to
+// asvec and unpacked (÷sqrt 2 off the diagonal) into both triangles of the block's matrix.
+__global__ void __launch_bounds__(POS_NT) k_scatter(AffineArgs a, int zero_z) {
+  if (a.st->done || !a.is->proceed) return;
+  const int b = a.cta_blk[blockIdx.x];
+  const long long q0 = a.cta_q0[blockIdx.x];
+  const int N = a.blk_N[b];
+  const long long L = (long long)N * (N + 1) / 2;
+  const long long col0 = a.blk_col[b];
+  double* M = a.mats + a.blk_mat[b];
+  for (int k = threadIdx.x; k < POS_PER_CTA; k += POS_NT) {
+    const long long q = q0 + k;
+    if (q >= L) break;
+    const long long col = col0 + q;
+    const int code = a.code[col];
+    const double zc = zero_z ? 0.0 : a.z[col];
+    double v;
+    if (code >= 0) v = fma(a.aval[col], a.uhat2[code], a.xi[col]);
+    else if (code == -1) v = a.xi[col];
+    else v = a.ulow[-2 - code] - zc;
+    a.asvec[col - a.t_free] = v;
+    int i, j;
+    svec_ij(q, i, j);
+    if (i == j) {
+      M[(size_t)i * N + i] = v;
+    } else {
+      const double h = v * SOS_IRT2;
+      M[(size_t)j * N + i] = h;
+      M[(size_t)i * N + j] = h;
+    }
+  }
+}
+
+// k_pack: xi = svec(Pi(a)) (x sqrt 2 off the diagonal), z = xi - a (P:399-400 with the Moreau
+// decomposition); CTA 0 commits tau, kappa and the iteration counter.
+__global__ void __launch_bounds__(POS_NT) k_pack(AffineArgs a, double* out_xi, int commit) {
+  if (a.st->done || !a.is->proceed) return;
+  const int b = a.cta_blk[blockIdx.x];
+  const long long q0 = a.cta_q0[blockIdx.x];
+  const int N = a.blk_N[b];
+  const long long L = (long long)N * (N + 1) / 2;
+  const long long col0 = a.blk_col[b];
+  const double* M = a.mats + a.blk_mat[b];
+  for (int k = threadIdx.x; k < POS_PER_CTA; k += POS_NT) {
+    const long long q = q0 + k;
+    if (q >= L) break;
+    const long long col = col0 + q;
+    int i, j;
+    svec_ij(q, i, j);
+    // the projection kernels leave Pi(a) in the lower triangle (row j, column i, j >= i)
+    const double pij = M[(size_t)i * N + j];
+    const double xn = (i == j) ? pij : pij * SOS_RT2;
+    if (out_xi) {
+      out_xi[col - a.t_free] = xn;
+    } else {
+      a.xi[col] = xn;
+      a.z[col] = xn - a.asvec[col - a.t_free];
+    }
+  }
+  if (commit && blockIdx.x == 0 && threadIdx.x == 0) {
+    DevState* st = a.st;
+    st->tau = a.is->tau_new;
+    st->kappa = a.is->kappa_new;
+    st->iter += 1;
+  }
+}
+
+// For configurations without PSD positions the commit happens here.
+__global__ void k_commit(AffineArgs a) {
+  if (a.st->done || !a.is->proceed) return;
+  a.st->tau = a.is->tau_new;
+  a.st->kappa = a.is->kappa_new;
+  a.st->iter += 1;
+}
+
+// Unit entry point helper: unpack one block's svec vector src into its matrix (and asvec).
+__global__ void k_unpack_block(AffineArgs a, int b, const double* src) {
+  const int N = a.blk_N[b];
+  const long long L = (long long)N * (N + 1) / 2;
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= L) return;
+  double* M = a.mats + a.blk_mat[b];
+  const double v = src[q];
+  a.asvec[a.blk_col[b] - a.t_free + q] = v;
+  int i, j;
+  svec_ij(q, i, j);
+  if (i == j) {
+    M[(size_t)i * N + i] = v;
+  } else {
+    const double h = v * SOS_IRT2;
+    M[(size_t)j * N + i] = h;
+    M[(size_t)i * N + j] = h;
+  }
+}

@@ -1,0 +1,70 @@
+// Common device helpers for the sosadmm kernels (sm_100a, FP64).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#define SOS_WARP 32
+
+// Device-resident scalar state of the iterate (u, v) = ((xi, y, tau), (z, s, kappa)).
+struct DevState {
+  double tau, kappa;
+  long long iter;        // k of u^k
+  int done;              // latched termination (all kernels early-exit when set)
+  int status;            // sosadmm_status of the last check
+  double res_pri, res_dual, res_gap, pobj, dobj, pinf, dinf;
+  int nonfinite;         // set when a non-finite residual / scalar is seen
+  long long nonfinite_iter;
+  long long max_iters;
+  double tol;
+};
+
+// Per-iteration scratch scalars written by the t-phase kernel.
+struct IterScal {
+  double omega3;   // tau + kappa
+  double coef;     // zeta^T p / (1 + zeta^T h)   (E:MatrixInverseResult)
+  double u3;       // u_hat_3 (E:FirstBlockElimination)
+  double tau_new, kappa_new;
+  double bsig2;    // b^T sigma_2
+  int proceed;     // 1 if this iteration continues past the t-phase
+};
+
+// Number of per-CTA partial sums the gather kernel produces.
+enum { PART_BX = 0, PART_PRES, PART_AXI, PART_DRES, PART_BY, NPART };
+
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  // deterministic: fixed shuffle tree then fixed smem order
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) r += sh[i];
+  }
+  return r;  // valid in thread 0
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ bool sos_finite(double x) { return isfinite(x); }
+
+constexpr double SOS_RT2 = 1.4142135623730951;       // fl(sqrt 2)
+constexpr double SOS_IRT2 = 0.70710678118654757;     // fl(1/sqrt 2)
+
+// svec position q (0-based, 'U' packed column-major) -> (i, j), i <= j.
+__device__ __forceinline__ void svec_ij(long long q, int& i, int& j) {
+  double jd = floor((sqrt(8.0 * (double)q + 1.0) - 1.0) * 0.5);
+  long long jj = (long long)jd;
+  while (jj * (jj + 1) / 2 > q) --jj;
+  while ((jj + 1) * (jj + 2) / 2 <= q) ++jj;
+  j = (int)jj;
+  i = (int)(q - jj * (jj + 1) / 2);
+}

@@ -1,0 +1,842 @@
+// sosadmm — C ABI implementation (see include/sosadmm.h for the contract and citations).
+//
+// Host side: structural analysis and the once-per-problem cache of SURVEY §8(a) row a0
+// (P^{-1}, the t' x t' factor, M^{-1} zeta, 1 + zeta^T M^{-1} zeta).
+// Device side: the per-iteration kernels of affine.cuh, psd_jacobi.cuh and psd_large.cuh, captured
+// once into a CUDA graph and replayed; termination is decided on the device (done flag), so
+// iterate(k) needs no host round trip inside the loop.
+#include "../../include/sosadmm.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "affine.cuh"
+#include "psd_jacobi.cuh"
+#include "psd_large.cuh"
+
+namespace {
+
+constexpr size_t kAlign = 256;
+
+struct Arena {
+  char* base = nullptr;  // nullptr = dry run (size accounting only)
+  size_t used = 0;
+  template <class T>
+  T* take(size_t count) {
+    used = (used + kAlign - 1) / kAlign * kAlign;
+    T* p = base ? reinterpret_cast<T*>(base + used) : nullptr;
+    used += std::max<size_t>(count, 1) * sizeof(T);
+    return p;
+  }
+};
+
+struct Analysis {
+  int m = 0, n = 0, t = 0, tl = 0, npsd = 0, nblk = 0;
+  std::vector<int> code;
+  std::vector<double> aval;
+  std::vector<int> seg_ptr, seg_col;
+  std::vector<double> seg_val;
+  std::vector<int> low_col, lr_ptr, lr_idx, lc_ptr, lc_row;
+  std::vector<double> lr_val, lc_val;
+  std::vector<int> empty_cols;
+  std::vector<double> D, Pinv, b, c;
+  std::vector<long long> blk_col, blk_mat;
+  std::vector<int> blk_N;
+  std::vector<int> cta_blk;
+  std::vector<long long> cta_q0;
+  std::vector<int> small_blk, large_blk;
+  long long mat_total = 0;
+  int max_small_N = 0;
+};
+
+// Column classification and the orthogonal / low-rank split (Proposition 1, P:302-311;
+// Proposition 3): a PSD column with at most one nonzero and c_j = 0 is orthogonal.
+sosadmm_err analyse(const sosadmm_problem* p, Analysis& an, std::string& msg) {
+  if (!p || p->m <= 0 || p->n_free < 0 || p->n_psd < 0 || !p->A_colptr || !p->b || !p->c) {
+    msg = "null pointer or negative size in sosadmm_problem";
+    return SOSADMM_E_ARG;
+  }
+  if (p->m > (1LL << 30)) {
+    msg = "m too large";
+    return SOSADMM_E_ARG;
+  }
+  an.m = (int)p->m;
+  an.t = (int)p->n_free;
+  long long n = p->n_free;
+  for (int b = 0; b < p->n_psd; ++b) {
+    const int N = p->psd_dim[b];
+    if (N <= 0) {
+      msg = "PSD block dimension must be positive";
+      return SOSADMM_E_ARG;
+    }
+    n += (long long)N * (N + 1) / 2;
+  }
+  if (n > (1LL << 30)) {
+    msg = "n too large";
+    return SOSADMM_E_ARG;
+  }
+  an.n = (int)n;
+  an.npsd = an.n - an.t;
+  an.nblk = p->n_psd;
+  const long long nnz = p->A_colptr[n];
+  if (p->A_colptr[0] != 0 || nnz < 0) {
+    msg = "bad CSC column pointers";
+    return SOSADMM_E_ARG;
+  }
+  for (long long j = 0; j < n; ++j)
+    if (p->A_colptr[j + 1] < p->A_colptr[j]) {
+      msg = "CSC column pointers must be nondecreasing";
+      return SOSADMM_E_ARG;
+    }
+  for (long long e = 0; e < nnz; ++e)
+    if (p->A_rowidx[e] < 0 || p->A_rowidx[e] >= an.m) {
+      msg = "CSC row index out of range at entry " + std::to_string(e);
+      return SOSADMM_E_ARG;
+    }
+  an.b.assign(p->b, p->b + an.m);
+  an.c.assign(p->c, p->c + an.n);
+  an.code.assign(an.n, -2);
+  an.aval.assign(an.n, 0.0);
+  // svec weight of each PSD column (1 on the diagonal, sqrt 2 off it)
+  std::vector<double> wsv(an.n, 1.0);
+  {
+    long long col = an.t;
+    for (int b = 0; b < an.nblk; ++b) {
+      const int N = p->psd_dim[b];
+      for (int j = 0; j < N; ++j)
+        for (int i = 0; i <= j; ++i) wsv[col++] = (i == j) ? 1.0 : std::sqrt(2.0);
+    }
+  }
+  std::vector<int> cnt(an.m, 0);
+  for (int j = an.t; j < an.n; ++j) {
+    const long long e0 = p->A_colptr[j], e1 = p->A_colptr[j + 1];
+    if (e1 - e0 <= 1 && p->c[j] == 0.0) {
+      if (e1 == e0 || p->A_val[e0] == 0.0) {
+        an.code[j] = -1;
+        an.empty_cols.push_back(j);
+      } else {
+        an.code[j] = p->A_rowidx[e0];
+        an.aval[j] = p->A_val[e0];
+        cnt[p->A_rowidx[e0]]++;
+      }
+    }
+  }
+  // low columns: free ones and every non-orthogonal PSD column
+  for (int j = 0; j < an.n; ++j)
+    if (j < an.t || an.code[j] <= -2) {
+      an.code[j] = -2 - (int)an.low_col.size();
+      an.low_col.push_back(j);
+    }
+  an.tl = (int)an.low_col.size();
+  if (an.tl > 16384) {
+    msg = "low-rank width t' = " + std::to_string(an.tl) + " exceeds the supported 16384";
+    return SOSADMM_E_STRUCT;
+  }
+  // CSR of A_orth (rows -> columns), D exactly: sum of (A/w)^2 w^2 per row
+  an.seg_ptr.assign(an.m + 1, 0);
+  for (int r = 0; r < an.m; ++r) an.seg_ptr[r + 1] = an.seg_ptr[r] + cnt[r];
+  an.seg_col.resize(an.seg_ptr[an.m]);
+  an.seg_val.resize(an.seg_ptr[an.m]);
+  an.D.assign(an.m, 0.0);
+  {
+    std::vector<int> fill(an.seg_ptr.begin(), an.seg_ptr.end() - 1);
+    for (int j = an.t; j < an.n; ++j)
+      if (an.code[j] >= 0) {
+        const int r = an.code[j];
+        an.seg_col[fill[r]] = j;
+        an.seg_val[fill[r]] = an.aval[j];
+        fill[r]++;
+        const double s = an.aval[j] / wsv[j];  // indicator coefficient (exactly 1 for B_alpha data)
+        an.D[r] += s * s * (wsv[j] == 1.0 ? 1.0 : 2.0);
+      }
+  }
+  an.Pinv.resize(an.m);
+  for (int r = 0; r < an.m; ++r) an.Pinv[r] = 1.0 / (1.0 + an.D[r]);
+  // A_low CSC and CSR
+  an.lc_ptr.assign(an.tl + 1, 0);
+  for (int jl = 0; jl < an.tl; ++jl) {
+    const int j = an.low_col[jl];
+    an.lc_ptr[jl + 1] = an.lc_ptr[jl] + (int)(p->A_colptr[j + 1] - p->A_colptr[j]);
+  }
+  an.lc_row.resize(an.lc_ptr[an.tl]);
+  an.lc_val.resize(an.lc_ptr[an.tl]);
+  std::vector<int> rc(an.m, 0);
+  for (int jl = 0; jl < an.tl; ++jl) {
+    const int j = an.low_col[jl];
+    int o = an.lc_ptr[jl];
+    for (long long e = p->A_colptr[j]; e < p->A_colptr[j + 1]; ++e, ++o) {
+      an.lc_row[o] = p->A_rowidx[e];
+      an.lc_val[o] = p->A_val[e];
+      rc[p->A_rowidx[e]]++;
+    }
+  }
+  an.lr_ptr.assign(an.m + 1, 0);
+  for (int r = 0; r < an.m; ++r) an.lr_ptr[r + 1] = an.lr_ptr[r] + rc[r];
+  an.lr_idx.resize(an.lr_ptr[an.m]);
+  an.lr_val.resize(an.lr_ptr[an.m]);
+  {
+    std::vector<int> fill(an.lr_ptr.begin(), an.lr_ptr.end() - 1);
+    for (int jl = 0; jl < an.tl; ++jl)
+      for (int o = an.lc_ptr[jl]; o < an.lc_ptr[jl + 1]; ++o) {
+        const int r = an.lc_row[o];
+        an.lr_idx[fill[r]] = jl;
+        an.lr_val[fill[r]] = an.lc_val[o];
+        fill[r]++;
+      }
+  }
+  // PSD blocks
+  long long col = an.t;
+  an.mat_total = 0;
+  for (int b = 0; b < an.nblk; ++b) {
+    const int N = p->psd_dim[b];
+    an.blk_col.push_back(col);
+    an.blk_N.push_back(N);
+    an.blk_mat.push_back(an.mat_total);
+    an.mat_total += (long long)N * N;
+    const long long L = (long long)N * (N + 1) / 2;
+    for (long long q0 = 0; q0 < L; q0 += POS_PER_CTA) {
+      an.cta_blk.push_back(b);
+      an.cta_q0.push_back(q0);
+    }
+    col += L;
+    if (N <= JAC_MAXN) {
+      an.small_blk.push_back(b);
+      an.max_small_N = std::max(an.max_small_N, N);
+    } else {
+      an.large_blk.push_back(b);
+    }
+  }
+  return SOSADMM_OK;
+}
+
+// Dense SPD inverse on the host (t' x t', row-major): Cholesky K = L L^T, then K^{-1} = L^{-T} L^{-1}.
+bool spd_inverse(std::vector<double>& K, int t) {
+  std::vector<double>& L = K;  // in place, lower triangle
+  for (int j = 0; j < t; ++j) {
+    double d = L[(size_t)j * t + j];
+    for (int k = 0; k < j; ++k) d -= L[(size_t)j * t + k] * L[(size_t)j * t + k];
+    if (!(d > 0.0)) return false;
+    d = std::sqrt(d);
+    L[(size_t)j * t + j] = d;
+    for (int i = j + 1; i < t; ++i) {
+      double s = L[(size_t)i * t + j];
+      const double* li = &L[(size_t)i * t];
+      const double* lj = &L[(size_t)j * t];
+      for (int k = 0; k < j; ++k) s -= li[k] * lj[k];
+      L[(size_t)i * t + j] = s / d;
+    }
+  }
+  // W = L^{-1} (lower), row-major
+  std::vector<double> W((size_t)t * t, 0.0);
+  for (int i = 0; i < t; ++i) {
+    W[(size_t)i * t + i] = 1.0 / L[(size_t)i * t + i];
+    for (int j = 0; j < i; ++j) {
+      double s = 0.0;
+      for (int k = j; k < i; ++k) s += L[(size_t)i * t + k] * W[(size_t)k * t + j];
+      W[(size_t)i * t + j] = -s / L[(size_t)i * t + i];
+    }
+  }
+  // K^{-1} = W^T W
+  for (int i = 0; i < t; ++i)
+    for (int j = 0; j <= i; ++j) {
+      double s = 0.0;
+      for (int k = i; k < t; ++k) s += W[(size_t)k * t + i] * W[(size_t)k * t + j];
+      K[(size_t)i * t + j] = s;
+      K[(size_t)j * t + i] = s;
+    }
+  return true;
+}
+
+}  // namespace
+
+struct sosadmm_ctx {
+  Analysis an;
+  sosadmm_err err = SOSADMM_OK;
+  std::string msg;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  void* own_mem = nullptr;
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  AffineArgs aa{};
+  JacobiArgs ja{};
+  LargeEig le;
+  double* d_tmp = nullptr;  // n-length scratch for unit entry points
+  cudaGraphExec_t graph = nullptr;
+  cudaGraph_t graph_raw = nullptr;
+  int gather_blocks = 1;
+  double tol = 1e-4;
+  long long max_iters = 2000;
+  long long launches = 0;
+  // host mirrors for get_structure
+  std::vector<int> row_of;
+};
+
+namespace {
+
+#define CK_CTX(ctx, call)                                                              \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess) {                                                           \
+      (ctx)->err = SOSADMM_E_CUDA;                                                     \
+      (ctx)->msg = std::string(#call) + ": " + cudaGetErrorString(e_);                 \
+      return (ctx)->err;                                                               \
+    }                                                                                  \
+  } while (0)
+
+// Device buffer layout (identical in the dry run and the real carve).
+template <class F>
+void layout(const Analysis& an, Arena& ar, F&& bind) {
+  bind(ar);
+}
+
+struct DevPtrs {
+  int *seg_ptr, *seg_col, *low_col, *lr_ptr, *lr_idx, *lc_ptr, *lc_row, *empty_cols, *code;
+  double *seg_val, *lr_val, *lc_val, *c_low, *h1_low, *beta_low, *Kinv, *b, *Pinv, *h2, *aval;
+  double *xi, *z, *y, *s, *x, *uhat2, *yt, *zt, *ulow, *aty, *part, *asvec, *mats, *tmp;
+  DevState* st;
+  IterScal* is;
+  long long *blk_col, *blk_mat, *cta_q0;
+  int *blk_N, *cta_blk, *small_blk;
+};
+
+void carve(const Analysis& an, Arena& ar, DevPtrs& d, int gather_blocks) {
+  const size_t m = an.m, n = an.n, tl = an.tl;
+  d.seg_ptr = ar.take<int>(m + 1);
+  d.seg_col = ar.take<int>(an.seg_col.size());
+  d.seg_val = ar.take<double>(an.seg_val.size());
+  d.low_col = ar.take<int>(tl);
+  d.lr_ptr = ar.take<int>(m + 1);
+  d.lr_idx = ar.take<int>(an.lr_idx.size());
+  d.lr_val = ar.take<double>(an.lr_val.size());
+  d.lc_ptr = ar.take<int>(tl + 1);
+  d.lc_row = ar.take<int>(an.lc_row.size());
+  d.lc_val = ar.take<double>(an.lc_val.size());
+  d.c_low = ar.take<double>(tl);
+  d.h1_low = ar.take<double>(tl);
+  d.beta_low = ar.take<double>(tl);
+  d.Kinv = ar.take<double>(tl * tl);
+  d.empty_cols = ar.take<int>(an.empty_cols.size());
+  d.b = ar.take<double>(m);
+  d.Pinv = ar.take<double>(m);
+  d.h2 = ar.take<double>(m);
+  d.code = ar.take<int>(n);
+  d.aval = ar.take<double>(n);
+  d.xi = ar.take<double>(n);
+  d.z = ar.take<double>(n);
+  d.y = ar.take<double>(m);
+  d.s = ar.take<double>(m);
+  d.x = ar.take<double>(m);
+  d.uhat2 = ar.take<double>(m);
+  d.yt = ar.take<double>(tl);
+  d.zt = ar.take<double>(tl);
+  d.ulow = ar.take<double>(tl);
+  d.aty = ar.take<double>(tl);
+  d.part = ar.take<double>((size_t)NPART * gather_blocks);
+  d.asvec = ar.take<double>(an.npsd);
+  d.mats = ar.take<double>((size_t)an.mat_total);
+  d.tmp = ar.take<double>(std::max<size_t>(n, 1));
+  d.st = ar.take<DevState>(1);
+  d.is = ar.take<IterScal>(1);
+  d.blk_col = ar.take<long long>(an.nblk);
+  d.blk_mat = ar.take<long long>(an.nblk);
+  d.blk_N = ar.take<int>(an.nblk);
+  d.cta_blk = ar.take<int>(an.cta_blk.size());
+  d.cta_q0 = ar.take<long long>(an.cta_q0.size());
+  d.small_blk = ar.take<int>(an.small_blk.size());
+}
+
+size_t total_bytes(const Analysis& an) {
+  Arena ar;
+  DevPtrs d;
+  const int gb = std::max(1, (an.m + GATHER_NT - 1) / GATHER_NT);
+  carve(an, ar, d, gb);
+  ar.used += large_eig_bytes(an.blk_N, an.large_blk) + kAlign;
+  return ar.used + kAlign;
+}
+
+template <class T>
+cudaError_t h2d(T* dst, const std::vector<T>& src, cudaStream_t s) {
+  if (src.empty()) return cudaSuccess;
+  return cudaMemcpyAsync(dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, s);
+}
+
+sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev) {
+  AffineArgs& a = c->aa;
+  cudaStream_t s = c->stream;
+  const int tlw = std::max(1, (a.tl * 32 + 255) / 256);
+  if (ev) cudaEventRecord(ev[0], s);
+  k_gather<<<c->gather_blocks, GATHER_NT, 0, s>>>(a);
+  k_lowT<<<tlw, 256, 0, s>>>(a);
+  k_kinv<<<tlw, 256, 0, s>>>(a);
+  k_tphase<<<1, TP_NT, 0, s>>>(a, mode_full ? 0 : 1);
+  if (!mode_full) return SOSADMM_OK;
+  k_rowupdate<<<(a.m + 255) / 256, 256, 0, s>>>(a, 1);
+  if (ev) cudaEventRecord(ev[1], s);
+  if (a.pos_ctas > 0) k_scatter<<<a.pos_ctas, POS_NT, 0, s>>>(a, 0);
+  if (ev) cudaEventRecord(ev[2], s);
+  if (!c->an.small_blk.empty())
+    k_psd_jacobi<<<(int)c->an.small_blk.size(), JAC_NT, jacobi_smem_bytes(c->an.max_small_N), s>>>(c->ja);
+  if (!c->an.large_blk.empty()) large_eig_launch(c->le, s, true);
+  if (ev) cudaEventRecord(ev[3], s);
+  if (a.pos_ctas > 0) k_pack<<<a.pos_ctas, POS_NT, 0, s>>>(a, nullptr, 1);
+  else k_commit<<<1, 1, 0, s>>>(a);
+  if (ev) cudaEventRecord(ev[4], s);
+  return SOSADMM_OK;
+}
+
+int64_t count_launches(const sosadmm_ctx* c) {
+  int64_t k = 6;  // gather, lowT, kinv, tphase, rowupdate, pack/commit
+  if (c->aa.pos_ctas > 0) k += 1;
+  if (!c->an.small_blk.empty()) k += 1;
+  if (!c->an.large_blk.empty()) k += large_eig_launches(c->le);
+  return k;
+}
+
+sosadmm_err check_async(sosadmm_ctx* c) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    c->err = SOSADMM_E_CUDA;
+    c->msg = std::string("kernel launch: ") + cudaGetErrorString(e);
+  }
+  return c->err;
+}
+
+sosadmm_err read_info(sosadmm_ctx* c, sosadmm_info* out) {
+  DevState st;
+  CK_CTX(c, cudaMemcpyAsync(&st, c->aa.st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+  CK_CTX(c, cudaStreamSynchronize(c->stream));
+  if (st.nonfinite) {
+    c->err = SOSADMM_E_NONFINITE;
+    c->msg = "non-finite iterate at iteration " + std::to_string(st.nonfinite_iter);
+  }
+  if (out) {
+    out->iter = st.iter;
+    out->status = st.status;
+    out->res_pri = st.res_pri;
+    out->res_dual = st.res_dual;
+    out->res_gap = st.res_gap;
+    out->pobj = st.pobj;
+    out->dobj = st.dobj;
+    out->tau = st.tau;
+    out->kappa = st.kappa;
+    out->pinf = st.pinf;
+    out->dinf = st.dinf;
+  }
+  return c->err;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t sosadmm_workspace_size(const sosadmm_problem* prob) {
+  Analysis an;
+  std::string msg;
+  if (analyse(prob, an, msg) != SOSADMM_OK) return 0;
+  return total_bytes(an);
+}
+
+sosadmm_err sosadmm_setup(const sosadmm_problem* prob, const sosadmm_settings* settings, sosadmm_ctx** out) {
+  if (!out) return SOSADMM_E_ARG;
+  *out = nullptr;
+  sosadmm_ctx* c = new sosadmm_ctx();
+  *out = c;
+  Analysis& an = c->an;
+  c->err = analyse(prob, an, c->msg);
+  if (c->err != SOSADMM_OK) return c->err;
+  if (settings) {
+    c->tol = settings->tol > 0 ? settings->tol : 1e-4;
+    c->max_iters = settings->max_iters > 0 ? settings->max_iters : 2000;
+    c->device = settings->device;
+  }
+  CK_CTX(c, cudaSetDevice(c->device));
+  if (settings && settings->stream) {
+    c->stream = (cudaStream_t)settings->stream;
+  } else {
+    CK_CTX(c, cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  const size_t need = total_bytes(an);
+  if (settings && settings->workspace) {
+    if (settings->workspace_bytes < need) {
+      c->err = SOSADMM_E_OOM;
+      c->msg = "workspace too small: need " + std::to_string(need) + " bytes";
+      return c->err;
+    }
+    c->ws = (char*)settings->workspace;
+    c->ws_bytes = settings->workspace_bytes;
+  } else {
+    CK_CTX(c, cudaMalloc(&c->own_mem, need));
+    c->ws = (char*)c->own_mem;
+    c->ws_bytes = need;
+  }
+  c->gather_blocks = std::max(1, (an.m + GATHER_NT - 1) / GATHER_NT);
+  Arena ar;
+  ar.base = (char*)(((uintptr_t)c->ws + kAlign - 1) / kAlign * kAlign);
+  DevPtrs d;
+  carve(an, ar, d, c->gather_blocks);
+  char* large_base = ar.take<char>(large_eig_bytes(an.blk_N, an.large_blk));
+
+  // ---- cache (row a0): K = I + A_low^T P^{-1} A_low, K^{-1}, h = M^{-1} zeta, denom --------
+  const int tl = an.tl, m = an.m;
+  std::vector<double> K((size_t)tl * tl, 0.0);
+  for (int j = 0; j < tl; ++j) K[(size_t)j * tl + j] = 1.0;
+  for (int r = 0; r < m; ++r) {
+    const double pi = an.Pinv[r];
+    for (int e = an.lr_ptr[r]; e < an.lr_ptr[r + 1]; ++e)
+      for (int f = an.lr_ptr[r]; f < an.lr_ptr[r + 1]; ++f)
+        K[(size_t)an.lr_idx[e] * tl + an.lr_idx[f]] += an.lr_val[e] * pi * an.lr_val[f];
+  }
+  if (!spd_inverse(K, tl)) {
+    c->err = SOSADMM_E_FACTOR;
+    c->msg = "I + A_low^T P^{-1} A_low is not numerically positive definite";
+    return c->err;
+  }
+  std::vector<double> c_low(tl), beta_low(tl, 0.0), h1_low(tl), h2(m);
+  for (int j = 0; j < tl; ++j) c_low[j] = an.c[an.low_col[j]];
+  // M^{-1} zeta with zeta = (c, -b):  r1 = c, r2 = -b;  A r1 = A_low c_low (c = 0 on orth cols)
+  {
+    std::vector<double> x(m), yt(tl, 0.0), zt(tl, 0.0);
+    for (int r = 0; r < m; ++r) {
+      double g = 0.0;
+      for (int e = an.lr_ptr[r]; e < an.lr_ptr[r + 1]; ++e) g += an.lr_val[e] * c_low[an.lr_idx[e]];
+      x[r] = (-an.b[r] - g) * an.Pinv[r];
+    }
+    for (int j = 0; j < tl; ++j) {
+      double s = 0.0, sb = 0.0;
+      for (int e = an.lc_ptr[j]; e < an.lc_ptr[j + 1]; ++e) {
+        s += an.lc_val[e] * x[an.lc_row[e]];
+        sb += an.lc_val[e] * an.Pinv[an.lc_row[e]] * an.b[an.lc_row[e]];
+      }
+      yt[j] = s;
+      beta_low[j] = sb;
+    }
+    for (int i = 0; i < tl; ++i) {
+      double s = 0.0;
+      for (int j = 0; j < tl; ++j) s += K[(size_t)i * tl + j] * yt[j];
+      zt[i] = s;
+    }
+    for (int r = 0; r < m; ++r) {
+      double v = 0.0;
+      for (int e = an.lr_ptr[r]; e < an.lr_ptr[r + 1]; ++e) v += an.lr_val[e] * zt[an.lr_idx[e]];
+      h2[r] = x[r] - an.Pinv[r] * v;
+    }
+    for (int j = 0; j < tl; ++j) {
+      double s = 0.0;
+      for (int e = an.lc_ptr[j]; e < an.lc_ptr[j + 1]; ++e) s += an.lc_val[e] * h2[an.lc_row[e]];
+      h1_low[j] = c_low[j] + s;
+    }
+  }
+  double ch = 0.0, bh = 0.0, nb = 0.0, nc = 0.0;
+  for (int j = 0; j < tl; ++j) ch += c_low[j] * h1_low[j];
+  for (int r = 0; r < m; ++r) {
+    bh += an.b[r] * h2[r];
+    nb += an.b[r] * an.b[r];
+  }
+  for (int j = 0; j < an.n; ++j) nc += an.c[j] * an.c[j];
+  const double denom = 1.0 + ch - bh;  // 1 + zeta^T M^{-1} zeta
+
+  // ---- upload -----------------------------------------------------------------------------
+  cudaStream_t s = c->stream;
+  CK_CTX(c, h2d(d.seg_ptr, an.seg_ptr, s));
+  CK_CTX(c, h2d(d.seg_col, an.seg_col, s));
+  CK_CTX(c, h2d(d.seg_val, an.seg_val, s));
+  CK_CTX(c, h2d(d.low_col, an.low_col, s));
+  CK_CTX(c, h2d(d.lr_ptr, an.lr_ptr, s));
+  CK_CTX(c, h2d(d.lr_idx, an.lr_idx, s));
+  CK_CTX(c, h2d(d.lr_val, an.lr_val, s));
+  CK_CTX(c, h2d(d.lc_ptr, an.lc_ptr, s));
+  CK_CTX(c, h2d(d.lc_row, an.lc_row, s));
+  CK_CTX(c, h2d(d.lc_val, an.lc_val, s));
+  CK_CTX(c, h2d(d.c_low, c_low, s));
+  CK_CTX(c, h2d(d.h1_low, h1_low, s));
+  CK_CTX(c, h2d(d.beta_low, beta_low, s));
+  CK_CTX(c, h2d(d.Kinv, K, s));
+  CK_CTX(c, h2d(d.empty_cols, an.empty_cols, s));
+  CK_CTX(c, h2d(d.b, an.b, s));
+  CK_CTX(c, h2d(d.Pinv, an.Pinv, s));
+  CK_CTX(c, h2d(d.h2, h2, s));
+  CK_CTX(c, h2d(d.code, an.code, s));
+  CK_CTX(c, h2d(d.aval, an.aval, s));
+  CK_CTX(c, h2d(d.blk_col, an.blk_col, s));
+  CK_CTX(c, h2d(d.blk_mat, an.blk_mat, s));
+  CK_CTX(c, h2d(d.blk_N, an.blk_N, s));
+  CK_CTX(c, h2d(d.cta_blk, an.cta_blk, s));
+  CK_CTX(c, h2d(d.cta_q0, an.cta_q0, s));
+  CK_CTX(c, h2d(d.small_blk, an.small_blk, s));
+  CK_CTX(c, cudaMemsetAsync(d.xi, 0, sizeof(double) * an.n, s));
+  CK_CTX(c, cudaMemsetAsync(d.z, 0, sizeof(double) * an.n, s));
+  CK_CTX(c, cudaMemsetAsync(d.y, 0, sizeof(double) * an.m, s));
+  CK_CTX(c, cudaMemsetAsync(d.s, 0, sizeof(double) * an.m, s));
+  CK_CTX(c, cudaMemsetAsync(d.mats, 0, sizeof(double) * std::max<long long>(an.mat_total, 1), s));
+  DevState st0{};
+  st0.tau = 1.0;  // reading C7: u0 = (0, 0, 1), v0 = 0
+  st0.kappa = 0.0;
+  st0.max_iters = c->max_iters;
+  st0.tol = c->tol;
+  st0.res_pri = st0.res_dual = st0.res_gap = INFINITY;
+  CK_CTX(c, cudaMemcpyAsync(d.st, &st0, sizeof(DevState), cudaMemcpyHostToDevice, s));
+  CK_CTX(c, cudaMemsetAsync(d.is, 0, sizeof(IterScal), s));
+
+  AffineArgs& a = c->aa;
+  a.m = an.m; a.n = an.n; a.t_free = an.t; a.tl = an.tl; a.npsd = an.npsd;
+  a.seg_ptr = d.seg_ptr; a.seg_col = d.seg_col; a.seg_val = d.seg_val;
+  a.low_col = d.low_col; a.lr_ptr = d.lr_ptr; a.lr_idx = d.lr_idx; a.lr_val = d.lr_val;
+  a.lc_ptr = d.lc_ptr; a.lc_row = d.lc_row; a.lc_val = d.lc_val;
+  a.c_low = d.c_low; a.h1_low = d.h1_low; a.beta_low = d.beta_low; a.Kinv = d.Kinv;
+  a.empty_cols = d.empty_cols; a.n_empty = (int)an.empty_cols.size();
+  a.b = d.b; a.Pinv = d.Pinv; a.h2 = d.h2;
+  a.denom = denom; a.bh2 = bh; a.nb = std::sqrt(nb); a.nc = std::sqrt(nc);
+  a.code = d.code; a.aval = d.aval;
+  a.xi = d.xi; a.z = d.z; a.y = d.y; a.s = d.s; a.st = d.st; a.is = d.is;
+  a.x = d.x; a.uhat2 = d.uhat2; a.yt = d.yt; a.zt = d.zt; a.ulow = d.ulow; a.aty = d.aty;
+  a.part = d.part; a.gather_blocks = c->gather_blocks; a.asvec = d.asvec;
+  a.nblk = an.nblk; a.blk_col = d.blk_col; a.blk_N = d.blk_N; a.blk_mat = d.blk_mat; a.mats = d.mats;
+  a.cta_blk = d.cta_blk; a.cta_q0 = d.cta_q0; a.pos_ctas = (int)an.cta_blk.size();
+  c->d_tmp = d.tmp;
+  JacobiArgs& ja = c->ja;
+  ja.mats = d.mats; ja.blk_mat = d.blk_mat; ja.blk_N = d.blk_N; ja.small_blk = d.small_blk;
+  ja.st = d.st; ja.is = d.is; ja.check_state = 1;
+  if (!an.small_blk.empty()) {
+    CK_CTX(c, cudaFuncSetAttribute(k_psd_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)jacobi_smem_bytes(JAC_MAXN)));
+  }
+  {
+    std::string lmsg;
+    if (large_eig_init(c->le, an.blk_N, an.blk_mat, an.large_blk, d.mats, large_base, d.st, d.is, s, lmsg) !=
+        0) {
+      c->err = SOSADMM_E_CUDA;
+      c->msg = "large-block eigensolver setup: " + lmsg;
+      return c->err;
+    }
+  }
+  // host mirror of the structure
+  c->row_of.assign(an.n, -2);
+  for (int j = an.t; j < an.n; ++j)
+    if (an.code[j] >= -1) c->row_of[j] = an.code[j];
+  c->launches = count_launches(c);
+  CK_CTX(c, cudaStreamSynchronize(s));
+  return SOSADMM_OK;
+}
+
+static sosadmm_err build_graph(sosadmm_ctx* c) {
+  if (c->graph) return SOSADMM_OK;
+  CK_CTX(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  launch_iteration(c, 1, nullptr);
+  cudaGraph_t g;
+  CK_CTX(c, cudaStreamEndCapture(c->stream, &g));
+  CK_CTX(c, cudaGraphInstantiate(&c->graph, g, 0));
+  c->graph_raw = g;
+  return SOSADMM_OK;
+}
+
+sosadmm_err sosadmm_iterate(sosadmm_ctx* c, int64_t k, sosadmm_info* out) {
+  if (!c) return SOSADMM_E_ARG;
+  if (c->err) return c->err;
+  if (k < 0) return SOSADMM_E_ARG;
+  CK_CTX(c, cudaSetDevice(c->device));
+  if (build_graph(c)) return c->err;
+  for (int64_t i = 0; i < k; ++i) CK_CTX(c, cudaGraphLaunch(c->graph, c->stream));
+  launch_iteration(c, 0, nullptr);  // residual check of the final iterate
+  if (check_async(c)) return c->err;
+  return read_info(c, out);
+}
+
+sosadmm_err sosadmm_iterate_profiled(sosadmm_ctx* c, int64_t k, sosadmm_info* out, double* ms_phase) {
+  if (!c) return SOSADMM_E_ARG;
+  if (c->err) return c->err;
+  CK_CTX(c, cudaSetDevice(c->device));
+  std::vector<cudaEvent_t> ev((size_t)5 * std::max<int64_t>(k, 1));
+  for (auto& e : ev) CK_CTX(c, cudaEventCreate(&e));
+  for (int64_t i = 0; i < k; ++i) launch_iteration(c, 1, &ev[5 * i]);
+  launch_iteration(c, 0, nullptr);
+  if (check_async(c)) return c->err;
+  CK_CTX(c, cudaStreamSynchronize(c->stream));
+  double acc[4] = {0, 0, 0, 0};
+  for (int64_t i = 0; i < k; ++i)
+    for (int p = 0; p < 4; ++p) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[5 * i + p], ev[5 * i + p + 1]);
+      acc[p] += ms;
+    }
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (ms_phase)
+    for (int p = 0; p < 4; ++p) ms_phase[p] += acc[p];
+  return read_info(c, out);
+}
+
+sosadmm_err sosadmm_get_info(sosadmm_ctx* c, sosadmm_info* out) {
+  if (!c) return SOSADMM_E_ARG;
+  if (c->err) return c->err;
+  CK_CTX(c, cudaSetDevice(c->device));
+  launch_iteration(c, 0, nullptr);
+  if (check_async(c)) return c->err;
+  return read_info(c, out);
+}
+
+sosadmm_err sosadmm_get_iterate(sosadmm_ctx* c, double* xi, double* y, double* z, double* s, double* tau,
+                                double* kappa, int64_t* iter) {
+  if (!c) return SOSADMM_E_ARG;
+  if (c->err) return c->err;
+  CK_CTX(c, cudaSetDevice(c->device));
+  const AffineArgs& a = c->aa;
+  if (xi) CK_CTX(c, cudaMemcpyAsync(xi, a.xi, sizeof(double) * a.n, cudaMemcpyDeviceToHost, c->stream));
+  if (z) CK_CTX(c, cudaMemcpyAsync(z, a.z, sizeof(double) * a.n, cudaMemcpyDeviceToHost, c->stream));
+  if (y) CK_CTX(c, cudaMemcpyAsync(y, a.y, sizeof(double) * a.m, cudaMemcpyDeviceToHost, c->stream));
+  if (s) CK_CTX(c, cudaMemcpyAsync(s, a.s, sizeof(double) * a.m, cudaMemcpyDeviceToHost, c->stream));
+  DevState st;
+  CK_CTX(c, cudaMemcpyAsync(&st, a.st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+  CK_CTX(c, cudaStreamSynchronize(c->stream));
+  if (tau) *tau = st.tau;
+  if (kappa) *kappa = st.kappa;
+  if (iter) *iter = st.iter;
+  return SOSADMM_OK;
+}
+
+sosadmm_err sosadmm_set_iterate(sosadmm_ctx* c, const double* xi, const double* y, const double* z,
+                                const double* s, double tau, double kappa, int64_t iter) {
+  if (!c) return SOSADMM_E_ARG;
+  if (c->err) return c->err;
+  if (!xi || !y || !z) return SOSADMM_E_ARG;
+  CK_CTX(c, cudaSetDevice(c->device));
+  const AffineArgs& a = c->aa;
+  CK_CTX(c, cudaMemcpyAsync(a.xi, xi, sizeof(double) * a.n, cudaMemcpyHostToDevice, c->stream));
+  CK_CTX(c, cudaMemcpyAsync(a.z, z, sizeof(double) * a.n, cudaMemcpyHostToDevice, c->stream));
+  CK_CTX(c, cudaMemcpyAsync(a.y, y, sizeof(double) * a.m, cudaMemcpyHostToDevice, c->stream));
+  if (s) CK_CTX(c, cudaMemcpyAsync(a.s, s, sizeof(double) * a.m, cudaMemcpyHostToDevice, c->stream));
+  else CK_CTX(c, cudaMemsetAsync(a.s, 0, sizeof(double) * a.m, c->stream));
+  DevState st{};
+  st.tau = tau;
+  st.kappa = kappa;
+  st.iter = iter;
+  st.max_iters = c->max_iters;
+  st.tol = c->tol;
+  st.res_pri = st.res_dual = st.res_gap = INFINITY;
+  CK_CTX(c, cudaMemcpyAsync(a.st, &st, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
+  CK_CTX(c, cudaStreamSynchronize(c->stream));
+  return SOSADMM_OK;
+}
+
+sosadmm_err sosadmm_get_structure(sosadmm_ctx* c, int32_t* row_of, double* D, int64_t* t_low) {
+  if (!c) return SOSADMM_E_ARG;
+  if (c->err) return c->err;
+  if (row_of) std::memcpy(row_of, c->row_of.data(), sizeof(int32_t) * c->an.n);
+  if (D) std::memcpy(D, c->an.D.data(), sizeof(double) * c->an.m);
+  if (t_low) *t_low = c->an.tl;
+  return SOSADMM_OK;
+}
+
+// Unit entry point: u_hat = (I + Q)^{-1} w through the production kernels (mode 2 of k_tphase).
+sosadmm_err sosadmm_project_affine(sosadmm_ctx* c, const double* w1, const double* w2, double w3, double* u1,
+                                   double* u2, double* u3) {
+  if (!c) return SOSADMM_E_ARG;
+  if (c->err) return c->err;
+  CK_CTX(c, cudaSetDevice(c->device));
+  const AffineArgs& a = c->aa;
+  const int n = a.n, m = a.m;
+  // save the iterate, load (xi, y, tau) = w and (z, s, kappa) = 0
+  std::vector<double> sxi(n), sz(n), sy(m), ss(m);
+  double stau, skap;
+  int64_t sit;
+  if (sosadmm_get_iterate(c, sxi.data(), sy.data(), sz.data(), ss.data(), &stau, &skap, &sit)) return c->err;
+  std::vector<double> zero_n(n, 0.0), zero_m(m, 0.0);
+  if (sosadmm_set_iterate(c, w1, w2, zero_n.data(), zero_m.data(), w3, 0.0, 0)) return c->err;
+  cudaStream_t s = c->stream;
+  const int tlw = std::max(1, (a.tl * 32 + 255) / 256);
+  k_gather<<<c->gather_blocks, GATHER_NT, 0, s>>>(a);
+  k_lowT<<<tlw, 256, 0, s>>>(a);
+  k_kinv<<<tlw, 256, 0, s>>>(a);
+  k_tphase<<<1, TP_NT, 0, s>>>(a, 2);
+  k_rowupdate<<<(m + 255) / 256, 256, 0, s>>>(a, 0);
+  if (a.pos_ctas > 0) k_scatter<<<a.pos_ctas, POS_NT, 0, s>>>(a, 1);
+  if (check_async(c)) return c->err;
+  std::vector<double> asv(std::max(a.npsd, 1)), ulow(std::max(a.tl, 1));
+  IterScal is;
+  CK_CTX(c, cudaMemcpyAsync(u2, a.uhat2, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+  if (a.npsd) CK_CTX(c, cudaMemcpyAsync(asv.data(), a.asvec, sizeof(double) * a.npsd, cudaMemcpyDeviceToHost, s));
+  if (a.tl) CK_CTX(c, cudaMemcpyAsync(ulow.data(), a.ulow, sizeof(double) * a.tl, cudaMemcpyDeviceToHost, s));
+  CK_CTX(c, cudaMemcpyAsync(&is, a.is, sizeof(IterScal), cudaMemcpyDeviceToHost, s));
+  CK_CTX(c, cudaStreamSynchronize(s));
+  for (int j = 0; j < c->an.t; ++j) u1[j] = 0.0;
+  for (int j = c->an.t; j < n; ++j) u1[j] = asv[j - c->an.t];
+  for (int jl = 0; jl < a.tl; ++jl) u1[c->an.low_col[jl]] = ulow[jl];
+  *u3 = is.u3;
+  return sosadmm_set_iterate(c, sxi.data(), sy.data(), sz.data(), ss.data(), stau, skap, sit);
+}
+
+// Unit entry point: Pi_{S+} of one block given in svec coordinates.
+sosadmm_err sosadmm_project_psd(sosadmm_ctx* c, int32_t block, const double* a_svec, double* out_svec) {
+  if (!c) return SOSADMM_E_ARG;
+  if (c->err) return c->err;
+  if (block < 0 || block >= c->an.nblk) return SOSADMM_E_ARG;
+  CK_CTX(c, cudaSetDevice(c->device));
+  const AffineArgs& a = c->aa;
+  const int N = c->an.blk_N[block];
+  const long long L = (long long)N * (N + 1) / 2;
+  const long long off = c->an.blk_col[block] - c->an.t;
+  cudaStream_t s = c->stream;
+  DevState sst;
+  IterScal sis;
+  CK_CTX(c, cudaMemcpyAsync(&sst, a.st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+  CK_CTX(c, cudaMemcpyAsync(&sis, a.is, sizeof(IterScal), cudaMemcpyDeviceToHost, s));
+  CK_CTX(c, cudaStreamSynchronize(s));
+  DevState st = sst;
+  st.done = 0;
+  IterScal is = sis;
+  is.proceed = 1;
+  CK_CTX(c, cudaMemcpyAsync(a.st, &st, sizeof(DevState), cudaMemcpyHostToDevice, s));
+  CK_CTX(c, cudaMemcpyAsync(a.is, &is, sizeof(IterScal), cudaMemcpyHostToDevice, s));
+  CK_CTX(c, cudaMemcpyAsync(c->d_tmp + off, a_svec, sizeof(double) * L, cudaMemcpyHostToDevice, s));
+  k_unpack_block<<<(int)((L + 255) / 256), 256, 0, s>>>(a, block, c->d_tmp + off);
+  if (!c->an.small_blk.empty())
+    k_psd_jacobi<<<(int)c->an.small_blk.size(), JAC_NT, jacobi_smem_bytes(c->an.max_small_N), s>>>(c->ja);
+  if (!c->an.large_blk.empty()) large_eig_launch(c->le, s, true);
+  if (a.pos_ctas > 0) k_pack<<<a.pos_ctas, POS_NT, 0, s>>>(a, c->d_tmp, 0);
+  if (check_async(c)) return c->err;
+  CK_CTX(c, cudaMemcpyAsync(out_svec, c->d_tmp + off, sizeof(double) * L, cudaMemcpyDeviceToHost, s));
+  CK_CTX(c, cudaMemcpyAsync(a.st, &sst, sizeof(DevState), cudaMemcpyHostToDevice, s));
+  CK_CTX(c, cudaMemcpyAsync(a.is, &sis, sizeof(IterScal), cudaMemcpyHostToDevice, s));
+  CK_CTX(c, cudaStreamSynchronize(s));
+  return SOSADMM_OK;
+}
+
+int64_t sosadmm_launches_per_iter(const sosadmm_ctx* c) { return c ? c->launches : 0; }
+
+void sosadmm_destroy(sosadmm_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  if (c->graph_raw) cudaGraphDestroy(c->graph_raw);
+  large_eig_free(c->le);
+  if (c->own_mem) cudaFree(c->own_mem);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* sosadmm_strerror(sosadmm_err e) {
+  switch (e) {
+    case SOSADMM_OK: return "ok";
+    case SOSADMM_E_ARG: return "invalid argument";
+    case SOSADMM_E_STRUCT: return "unsupported structure";
+    case SOSADMM_E_FACTOR: return "factorisation failed";
+    case SOSADMM_E_CUDA: return "CUDA error";
+    case SOSADMM_E_NCCL: return "NCCL error";
+    case SOSADMM_E_NONFINITE: return "non-finite iterate";
+    case SOSADMM_E_OOM: return "out of memory";
+  }
+  return "unknown error";
+}
+
+const char* sosadmm_last_error_message(const sosadmm_ctx* c) { return c ? c->msg.c_str() : "null context"; }
+
+}  // extern "C"

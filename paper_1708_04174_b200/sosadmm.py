@@ -1,0 +1,218 @@
+"""Thin ctypes binding of the C ABI in include/sosadmm.h (argument marshalling only).
+
+Every step of the ADMM iteration runs in the CUDA kernels of `libsosadmm.so`; this module only
+converts arrays to pointers, allocates the device workspace with PyTorch (device memory and a
+dedicated stream are the only things PyTorch provides) and decodes results.  There is no CPU
+fallback: if the library or a CUDA device is missing, construction raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsosadmm.so")
+
+STATUS = {0: "RUNNING", 1: "OPTIMAL", 2: "PRIMAL_INFEASIBLE", 3: "DUAL_INFEASIBLE", 4: "MAX_ITERS",
+          5: "INCONCLUSIVE"}
+
+EXPORTS = ["sosadmm_workspace_size", "sosadmm_setup", "sosadmm_iterate", "sosadmm_iterate_profiled",
+           "sosadmm_get_info", "sosadmm_get_iterate", "sosadmm_set_iterate", "sosadmm_get_structure",
+           "sosadmm_project_affine", "sosadmm_project_psd", "sosadmm_launches_per_iter", "sosadmm_destroy",
+           "sosadmm_strerror", "sosadmm_last_error_message"]
+
+
+class _Problem(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int64), ("n_free", ctypes.c_int64), ("n_psd", ctypes.c_int32),
+                ("psd_dim", ctypes.POINTER(ctypes.c_int32)), ("A_colptr", ctypes.POINTER(ctypes.c_int64)),
+                ("A_rowidx", ctypes.POINTER(ctypes.c_int32)), ("A_val", ctypes.POINTER(ctypes.c_double)),
+                ("b", ctypes.POINTER(ctypes.c_double)), ("c", ctypes.POINTER(ctypes.c_double))]
+
+
+class _Settings(ctypes.Structure):
+    _fields_ = [("tol", ctypes.c_double), ("max_iters", ctypes.c_int64), ("check_every", ctypes.c_int32),
+                ("device", ctypes.c_int32), ("stream", ctypes.c_void_p), ("workspace", ctypes.c_void_p),
+                ("workspace_bytes", ctypes.c_size_t)]
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [("iter", ctypes.c_int64), ("status", ctypes.c_int32), ("res_pri", ctypes.c_double),
+                ("res_dual", ctypes.c_double), ("res_gap", ctypes.c_double), ("pobj", ctypes.c_double),
+                ("dobj", ctypes.c_double), ("tau", ctypes.c_double), ("kappa", ctypes.c_double),
+                ("pinf", ctypes.c_double), ("dinf", ctypes.c_double)]
+
+    def as_dict(self) -> dict:
+        d = {f: getattr(self, f) for f, _ in self._fields_}
+        d["status_name"] = STATUS.get(self.status, str(self.status))
+        return d
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libsosadmm.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} not found: build it with `python -m paper_1708_04174_b200.build` "
+                           "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    P, D, I32, I64, V = (ctypes.POINTER(ctypes.c_double), ctypes.c_double, ctypes.c_int32, ctypes.c_int64,
+                         ctypes.c_void_p)
+    lib.sosadmm_workspace_size.argtypes = [ctypes.POINTER(_Problem)]
+    lib.sosadmm_workspace_size.restype = ctypes.c_size_t
+    lib.sosadmm_setup.argtypes = [ctypes.POINTER(_Problem), ctypes.POINTER(_Settings), ctypes.POINTER(V)]
+    lib.sosadmm_iterate.argtypes = [V, I64, ctypes.POINTER(_Info)]
+    lib.sosadmm_iterate_profiled.argtypes = [V, I64, ctypes.POINTER(_Info), P]
+    lib.sosadmm_get_info.argtypes = [V, ctypes.POINTER(_Info)]
+    lib.sosadmm_get_iterate.argtypes = [V, P, P, P, P, P, P, ctypes.POINTER(I64)]
+    lib.sosadmm_set_iterate.argtypes = [V, P, P, P, P, D, D, I64]
+    lib.sosadmm_get_structure.argtypes = [V, ctypes.POINTER(I32), P, ctypes.POINTER(I64)]
+    lib.sosadmm_project_affine.argtypes = [V, P, P, D, P, P, P]
+    lib.sosadmm_project_psd.argtypes = [V, I32, P, P]
+    lib.sosadmm_launches_per_iter.argtypes = [V]
+    lib.sosadmm_launches_per_iter.restype = I64
+    lib.sosadmm_destroy.argtypes = [V]
+    lib.sosadmm_destroy.restype = None
+    lib.sosadmm_strerror.argtypes = [ctypes.c_int]
+    lib.sosadmm_strerror.restype = ctypes.c_char_p
+    lib.sosadmm_last_error_message.argtypes = [V]
+    lib.sosadmm_last_error_message.restype = ctypes.c_char_p
+    for f in ["sosadmm_setup", "sosadmm_iterate", "sosadmm_iterate_profiled", "sosadmm_get_info",
+              "sosadmm_get_iterate", "sosadmm_set_iterate", "sosadmm_get_structure", "sosadmm_project_affine",
+              "sosadmm_project_psd"]:
+        getattr(lib, f).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+class SosAdmm:
+    """One SOS-derived SDP on one GPU: setup(A, b, c, cone dims) once, then iterate(k)."""
+
+    def __init__(self, A, b, c, n_free: int, psd_dims, tol: float = 1e-4, max_iters: int = 2000,
+                 device: int = 0):
+        import torch  # device memory + stream only
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("SosAdmm needs a CUDA device (no CPU fallback)")
+        self.lib = load_library()
+        self._A = A.tocsc() if hasattr(A, "tocsc") else A
+        self._A.sort_indices()
+        self.m, self.n = self._A.shape
+        self._colptr = np.ascontiguousarray(self._A.indptr, dtype=np.int64)
+        self._rowidx = np.ascontiguousarray(self._A.indices, dtype=np.int32)
+        self._val = np.ascontiguousarray(self._A.data, dtype=np.float64)
+        self._b = np.ascontiguousarray(b, dtype=np.float64)
+        self._c = np.ascontiguousarray(c, dtype=np.float64)
+        self._dims = np.ascontiguousarray(psd_dims, dtype=np.int32)
+        self.n_free = int(n_free)
+        self.psd_dims = [int(d) for d in psd_dims]
+        self._prob = _Problem(self.m, self.n_free, len(self._dims),
+                              self._dims.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                              self._colptr.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                              self._rowidx.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                              _dptr(self._val), _dptr(self._b), _dptr(self._c))
+        nbytes = self.lib.sosadmm_workspace_size(ctypes.byref(self._prob))
+        if nbytes == 0:
+            raise ValueError("malformed problem (sosadmm_workspace_size returned 0)")
+        self.device = device
+        self._torch_dev = torch.device("cuda", device)
+        self._ws = torch.empty(int(nbytes), dtype=torch.uint8, device=self._torch_dev)
+        self.stream = torch.cuda.Stream(device=self._torch_dev)
+        st = _Settings(tol, max_iters, 1, device, ctypes.c_void_p(self.stream.cuda_stream),
+                       ctypes.c_void_p(self._ws.data_ptr()), int(nbytes))
+        self._ctx = ctypes.c_void_p()
+        err = self.lib.sosadmm_setup(ctypes.byref(self._prob), ctypes.byref(st), ctypes.byref(self._ctx))
+        self._check(err, "setup")
+        self.workspace_bytes = int(nbytes)
+
+    @staticmethod
+    def from_problem(prob, **kw) -> "SosAdmm":
+        return SosAdmm(prob.A, prob.b, prob.c, prob.n_free, prob.psd_dims, **kw)
+
+    def _check(self, err: int, what: str):
+        if err != 0:
+            msg = self.lib.sosadmm_last_error_message(self._ctx).decode() if self._ctx else ""
+            raise RuntimeError(f"sosadmm_{what}: {self.lib.sosadmm_strerror(err).decode()} ({err}): {msg}")
+
+    def iterate(self, k: int) -> dict:
+        info = _Info()
+        self._check(self.lib.sosadmm_iterate(self._ctx, int(k), ctypes.byref(info)), "iterate")
+        return info.as_dict()
+
+    def iterate_profiled(self, k: int):
+        info = _Info()
+        ms = np.zeros(4)
+        self._check(self.lib.sosadmm_iterate_profiled(self._ctx, int(k), ctypes.byref(info), _dptr(ms)),
+                    "iterate_profiled")
+        return info.as_dict(), ms
+
+    def info(self) -> dict:
+        info = _Info()
+        self._check(self.lib.sosadmm_get_info(self._ctx, ctypes.byref(info)), "get_info")
+        return info.as_dict()
+
+    def get_iterate(self):
+        xi, z = np.empty(self.n), np.empty(self.n)
+        y, s = np.empty(self.m), np.empty(self.m)
+        tau, kappa, it = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        self._check(self.lib.sosadmm_get_iterate(self._ctx, _dptr(xi), _dptr(y), _dptr(z), _dptr(s),
+                                                 ctypes.byref(tau), ctypes.byref(kappa), ctypes.byref(it)),
+                    "get_iterate")
+        return dict(xi=xi, y=y, z=z, s=s, tau=tau.value, kappa=kappa.value, iter=it.value)
+
+    def set_iterate(self, xi, y, z, s=None, tau=1.0, kappa=0.0, iter=0):
+        xi = np.ascontiguousarray(xi, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        z = np.ascontiguousarray(z, dtype=np.float64)
+        sp_ = None if s is None else _dptr(np.ascontiguousarray(s, dtype=np.float64))
+        if s is not None:
+            s = np.ascontiguousarray(s, dtype=np.float64)
+            sp_ = _dptr(s)
+        self._check(self.lib.sosadmm_set_iterate(self._ctx, _dptr(xi), _dptr(y), _dptr(z), sp_, float(tau),
+                                                 float(kappa), int(iter)), "set_iterate")
+
+    def get_structure(self):
+        row_of = np.empty(self.n, dtype=np.int32)
+        D = np.empty(self.m)
+        t = ctypes.c_int64()
+        self._check(self.lib.sosadmm_get_structure(self._ctx, row_of.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                                   _dptr(D), ctypes.byref(t)), "get_structure")
+        return row_of, D, t.value
+
+    def project_affine(self, w1, w2, w3: float):
+        w1 = np.ascontiguousarray(w1, dtype=np.float64)
+        w2 = np.ascontiguousarray(w2, dtype=np.float64)
+        u1, u2, u3 = np.empty(self.n), np.empty(self.m), ctypes.c_double()
+        self._check(self.lib.sosadmm_project_affine(self._ctx, _dptr(w1), _dptr(w2), float(w3), _dptr(u1),
+                                                    _dptr(u2), ctypes.byref(u3)), "project_affine")
+        return u1, u2, u3.value
+
+    def project_psd(self, block: int, a_svec):
+        a = np.ascontiguousarray(a_svec, dtype=np.float64)
+        out = np.empty_like(a)
+        self._check(self.lib.sosadmm_project_psd(self._ctx, int(block), _dptr(a), _dptr(out)), "project_psd")
+        return out
+
+    @property
+    def launches_per_iter(self) -> int:
+        return int(self.lib.sosadmm_launches_per_iter(self._ctx))
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            self.lib.sosadmm_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,66 @@
+"""CPU checks of the boundary: the C-ABI library builds, loads and exports every symbol that
+include/sosadmm.h declares; workspace sizing works without a GPU."""
+import ctypes
+import os
+import re
+
+import numpy as np
+
+from paper_1708_04174_b200 import EXPORTS, load_library
+from paper_1708_04174_b200.build import build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "sosadmm.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)  # declarations only, not the comments
+    return sorted(set(re.findall(r"\b(sosadmm_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    build()
+    lib = load_library()
+    decl = declared_symbols()
+    assert len(decl) >= 14
+    for name in decl:
+        assert hasattr(lib, name), name
+    assert set(decl) == set(EXPORTS)
+
+
+def test_workspace_size_cpu():
+    from paper_1708_04174_b200.sosadmm import _Problem, _dptr
+    from sosgen import make_config
+
+    lib = load_library()
+    prob = make_config("pop6")
+    A = prob.A.tocsc()
+    cp = np.ascontiguousarray(A.indptr, dtype=np.int64)
+    ri = np.ascontiguousarray(A.indices, dtype=np.int32)
+    va = np.ascontiguousarray(A.data, dtype=np.float64)
+    dims = np.array(prob.psd_dims, dtype=np.int32)
+    p = _Problem(prob.m, prob.n_free, len(dims), dims.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                 cp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), ri.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                 _dptr(va), _dptr(prob.b), _dptr(prob.c))
+    nb = lib.sosadmm_workspace_size(ctypes.byref(p))
+    assert nb > 8 * (2 * prob.n + 2 * prob.m)
+    # malformed input: decreasing column pointers
+    bad = cp.copy()
+    bad[3] = bad[2] - 1
+    p.A_colptr = bad.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+    assert lib.sosadmm_workspace_size(ctypes.byref(p)) == 0
+
+
+def test_strerror():
+    lib = load_library()
+    assert lib.sosadmm_strerror(0) == b"ok"
+    assert lib.sosadmm_strerror(-6) == b"non-finite iterate"
+
+
+def test_product_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_1708_04174_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dp, f)).read()
+                assert not re.search(r"^\s*(from|import)\s+(oracle|sosgen)\b", txt, re.M), f

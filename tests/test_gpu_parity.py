@@ -1,0 +1,154 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Criteria (BASELINE.json north_star; readings C9, C13):
+* alpha-map and D bit-exact against brute-force enumeration (Proposition 1);
+* affine projection and PSD projection against the oracle's routines on identical inputs;
+* per-iterate relative error <= 1e-9 over the first 20 iterations, normalised by ||(u, v)|| of the
+  oracle iterate (reading C13);
+* residual-stop iteration counts within +-2% and the converged objective within 1e-6 relative.
+"""
+import numpy as np
+import pytest
+
+from oracle import HsdeOracle, Status, brute_force_structure, proj_psd_svec, svec
+from sosgen import ball_pop, make_config, planted_kkt, univariate_feasibility
+from sosgen.configs import planted_pop
+
+pytestmark = pytest.mark.gpu
+
+SMALL = ["pop6", "sq", "neg", "pop3k2", "ball4"]
+LARGE = ["pop20", "lyap10", "box24", "pop40"]
+
+
+def make(name):
+    if name == "sq":
+        return univariate_feasibility("sq", [1.0, 2.0, 1.0])
+    if name == "neg":
+        return univariate_feasibility("neg", [-1.0, 0.0, -1.0])
+    if name == "pop3k2":
+        return planted_pop("pop3k2", 3, 2, seed=5)
+    if name == "ball4":
+        return ball_pop(4)
+    return make_config(name)
+
+
+@pytest.fixture(scope="module")
+def solvers():
+    from paper_1708_04174_b200 import SosAdmm
+
+    cache = {}
+
+    def get(name, **kw):
+        key = (name, tuple(sorted(kw.items())))
+        if key not in cache:
+            prob = make(name)
+            cache[key] = (prob, SosAdmm.from_problem(prob, **kw), HsdeOracle.from_problem(prob))
+        return cache[key]
+
+    yield get
+    for _, s, _ in cache.values():
+        s.close()
+
+
+@pytest.mark.parametrize("name", SMALL + LARGE)
+def test_structure_bit_exact(name, solvers):
+    prob, gpu, _ = solvers(name)
+    row_of, D, tl = gpu.get_structure()
+    maps, n_alpha = brute_force_structure(prob.row_expo, prob.block_info, prob.m)
+    assert np.array_equal(D, n_alpha.astype(np.float64))  # exact integers
+    off = prob.n_free
+    n_weighted = 0
+    for N, amap, info in zip(prob.psd_dims, maps, prob.block_info):
+        L = N * (N + 1) // 2
+        if amap is None:
+            assert np.all(row_of[off:off + L] == -2)
+            n_weighted += L
+        else:
+            assert np.array_equal(row_of[off:off + L].astype(np.int64), amap)
+        off += L
+    assert tl == prob.n_free + n_weighted
+
+
+@pytest.mark.parametrize("name", SMALL + LARGE)
+def test_affine_projection_parity(name, solvers):
+    prob, gpu, orc = solvers(name)
+    rng = np.random.default_rng(11)
+    for _ in range(3):
+        w1, w2, w3 = rng.standard_normal(prob.n), rng.standard_normal(prob.m), float(rng.standard_normal())
+        g1, g2, g3 = gpu.project_affine(w1, w2, w3)
+        o1, o2, o3 = orc.affine(w1, w2, w3)
+        ref = np.concatenate([o1, o2, [o3]])
+        got = np.concatenate([g1, g2, [g3]])
+        # both sides round the same cancellations: relative 1e-10 of |w| + |u|
+        assert np.linalg.norm(got - ref) <= 1e-10 * (np.linalg.norm(ref) + np.linalg.norm(w1) + np.linalg.norm(w2))
+
+
+@pytest.mark.parametrize("name", SMALL + LARGE)
+def test_psd_projection_parity(name, solvers):
+    prob, gpu, _ = solvers(name)
+    rng = np.random.default_rng(3)
+    nb = len(prob.psd_dims)
+    for bidx in sorted({0, 1, 2, nb - 1} & set(range(nb))):
+        N = prob.psd_dims[bidx]
+        L = N * (N + 1) // 2
+        for kind in ["gauss", "lowrank"]:
+            if kind == "gauss":
+                a = rng.standard_normal(L)
+            else:  # clustered spectrum: rank-3 PSD minus rank-2 PSD plus tiny noise
+                G = rng.standard_normal((N, 3))
+                H = rng.standard_normal((N, 2))
+                X = G @ G.T - H @ H.T + 1e-10 * np.eye(N)
+                a = svec(X)
+            got = gpu.project_psd(bidx, a)
+            ref = proj_psd_svec(a, N)
+            assert np.linalg.norm(got - ref) <= 1e-11 * np.linalg.norm(a), (bidx, N, kind)
+
+
+def _rel(a, b, scale):
+    return np.linalg.norm(a - b) / scale
+
+
+@pytest.mark.parametrize("name", SMALL + LARGE)
+def test_first_20_iterates(name, solvers):
+    prob, gpu, orc = solvers(name)
+    gpu.set_iterate(np.zeros(prob.n), np.zeros(prob.m), np.zeros(prob.n), None, 1.0, 0.0, 0)
+    st = orc.initial_state()
+    worst_u = worst_v = 0.0
+    for k in range(1, 21):
+        st = orc.step(st)
+        gpu.iterate(1)
+        g = gpu.get_iterate()
+        if g["iter"] != k:  # terminated early (tiny problems); test_convergence_parity covers status
+            break
+        ug = np.concatenate([g["xi"], g["y"], [g["tau"]]])
+        vg = np.concatenate([g["z"], g["s"], [g["kappa"]]])
+        scale = np.linalg.norm(np.concatenate([st.u(), st.v()]))
+        worst_u = max(worst_u, _rel(ug, st.u(), scale))
+        worst_v = max(worst_v, _rel(vg, st.v(), scale))
+    assert worst_u <= 1e-9 and worst_v <= 1e-9, (worst_u, worst_v)
+
+
+@pytest.mark.parametrize("name", ["pop6", "sq", "neg", "pop3k2", "ball4"])
+def test_convergence_parity(name, solvers):
+    prob, gpu, orc = solvers(name, tol=1e-4, max_iters=5000)
+    st, status, hist = orc.solve(tol=1e-4, max_iters=5000)
+    gpu.set_iterate(np.zeros(prob.n), np.zeros(prob.m), np.zeros(prob.n), None, 1.0, 0.0, 0)
+    info = gpu.iterate(5000)
+    assert info["status"] == int(status)
+    assert abs(info["iter"] - st.k) <= max(1, int(0.02 * st.k))
+    if status == Status.OPTIMAL and np.isfinite(hist[-1][3]) and hist[-1][3] != 0:
+        assert abs(info["pobj"] - hist[-1][3]) <= 1e-6 * abs(hist[-1][3])
+
+
+@pytest.mark.parametrize("name", ["pop6", "pop20", "box24", "pop40"])
+def test_planted_fixed_point(name, solvers):
+    prob, gpu, _ = solvers(name)
+    xi, y, z = planted_kkt(prob)
+    gpu.set_iterate(xi, y, z, None, 1.0, 0.0, 0)
+    gpu.iterate(1)
+    g = gpu.get_iterate()
+    scale = np.linalg.norm(np.concatenate([xi, y, [1.0], z]))
+    assert np.linalg.norm(g["xi"] - xi) <= 1e-12 * scale
+    assert np.linalg.norm(g["z"] - z) <= 1e-12 * scale
+    assert np.linalg.norm(g["y"] - y) <= 1e-12 * scale
+    assert abs(g["tau"] - 1.0) <= 1e-12 and abs(g["kappa"]) <= 1e-12
