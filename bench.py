@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""Benchmark of the HSDE-ADMM hot path (BASELINE.json metric: "ADMM iters/s + time-to-1e-4 (n=40
+quartic POP); affine-proj HBM GB/s; eigh FP64 TF/s").
+
+One step = one full ADMM iteration (`eq:ADMMSteps`: affine projection, PSD projection,
+dual update, residual check) of config 4 (`pop40`: planted quartic POP, n = 40, N = 861,
+m = 135,751), the largest single-GPU config; inputs are resident in HBM when timing starts.
+Timing: W warm-up steps, then K timed steps; before every timed step an L2 flush (a 512 MB
+buffer, > 126 MB L2) runs on the same stream outside the timed window; each step is bracketed by
+CUDA events on the library's stream; barrier + synchronize around the region; max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config pop40]
+
+`--impl reference` times the CPU oracle (oracle/, plain FP64, generic KKT LU + LAPACK eigh) on
+the same workload.  For N > 1 every rank solves its own independent
+replica (single-block programs do not shard; weak scaling, no collective).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+# roofline denominators: measured on this pool's B200s
+DMMA_PEAK_TFLOPS = 74.3   # profiles/r01_probe_fp64.log: mma.sync m8n8k4 f64 (SASS DMMA), measured
+DFMA_PEAK_TFLOPS = 34.2   # same probe, scalar DFMA
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md recipe)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def eig_flops(N: int) -> float:
+    """Algorithmic FP64 flops of one N x N PSD projection: 4/3 N^3 tridiagonalisation
+    + 2 N^3 back-transform + N^3 symmetric reconstruction = 4.33 N^3 (dense eigh count)."""
+    return (4.0 / 3.0 + 2.0 + 1.0) * N ** 3
+
+
+def affine_bytes(prob, tl: int) -> float:
+    """Algorithmic HBM bytes of the affine projection per iteration:
+    36 L + 68 m + 24 nnz(A_low) + 8 t'^2 (dense K^{-1} apply), L = PSD svec entries."""
+    L = prob.n - prob.n_free
+    A = prob.A.tocsc()
+    nnz_low = 0
+    off = prob.n_free
+    nnz_low += A[:, :prob.n_free].nnz
+    col_nnz = np.diff(A.indptr)[prob.n_free:]
+    nnz_low += int(col_nnz[col_nnz > 1].sum())
+    return 36.0 * L + 68.0 * prob.m + 24.0 * nnz_low + 8.0 * tl * tl
+
+
+def run_ours(args):
+    import torch
+
+    world, rank, local = dist_init()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    from paper_1708_04174_b200 import SosAdmm
+    from sosgen import make_config
+
+    prob = make_config(args.config, seed=args.seed + rank)
+    # timing solver: tol 0 never stops, so every step is a full iteration
+    gpu = SosAdmm.from_problem(prob, tol=1e-300, max_iters=1 << 40, device=local)
+    st = gpu.stream
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    launches_per_iter = gpu.launches_per_iter
+    gpu.iterate(args.warmup)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed region: K steps, L2 flushed before each, CUDA events on the library stream ----
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            with torch.cuda.stream(st):
+                flush.fill_(float(i))
+                evs[i][0].record(st)
+            gpu.iterate(1)
+            with torch.cuda.stream(st):
+                evs[i][1].record(st)
+        barrier()
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    clocks = clk.summary()
+    # ---- warm (no flush) graph replay of K iterations, for context ----
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(st)
+    gpu.iterate(args.steps)
+    e1.record(st)
+    barrier()
+    ms_warm = e0.elapsed_time(e1)
+    # ---- per-phase device time (CUDA events around each kernel class, same iterations) ----
+    info, ph = gpu.iterate_profiled(args.steps)
+    ph_ms = [float(x) / args.steps for x in ph]  # per iteration: [affine gather..t-phase, scatter, psd, pack]
+    # ---- end-to-end through the C ABI with host buffers: H2D state, iterate, D2H state --------
+    it = gpu.get_iterate()
+    pin = {k: torch.from_numpy(np.ascontiguousarray(it[k])).pin_memory() for k in ("xi", "y", "z", "s")}
+    h2d = 8 * (2 * prob.n + 2 * prob.m) + 16
+    d2h = 8 * (2 * prob.n + 2 * prob.m) + 24
+    barrier()
+    t0 = time.perf_counter()
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ea.record(st)
+    for i in range(args.steps):
+        gpu.set_iterate(pin["xi"].numpy(), pin["y"].numpy(), pin["z"].numpy(), pin["s"].numpy(), it["tau"],
+                        it["kappa"], it["iter"])
+        gpu.iterate(1)
+        g = gpu.get_iterate()
+    eb.record(st)
+    barrier()
+    e2e_ms = ea.elapsed_time(eb)
+    e2e_wall = time.perf_counter() - t0
+    # max over ranks
+    vals = torch.tensor([ms, ms_warm, e2e_ms, ph_ms[2], ph_ms[0] + ph_ms[1] + ph_ms[3]], dtype=torch.float64,
+                        device=f"cuda:{local}")
+    if world > 1:
+        torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
+    ms, ms_warm, e2e_ms, psd_ms, aff_ms = [float(v) for v in vals.cpu()]
+    # time to 1e-4 (harness-side rule, C9): fresh solver, chunks of 25 iterations
+    ttt = None
+    if rank == 0 and not args.no_ttt:
+        ttt = time_to_tol(prob, local, args)
+    if rank != 0:
+        return
+    N = max(prob.psd_dims)
+    hbm, hbm_src = hbm_peak()
+    flops = eig_flops(N)
+    ach = flops / (psd_ms * 1e-3) / 1e12
+    _, _, tl = gpu.get_structure()
+    abytes = affine_bytes(prob, tl)
+    aff_gbs = abytes / (aff_ms * 1e-3) / 1e9
+    cpu = cpu_baseline(args) if not args.no_cpu else None
+    total_steps = args.steps * world
+    line = {
+        "metric": "ADMM iters/s (n=40 quartic POP, config 4)",
+        "value": total_steps / (ms * 1e-3),
+        "unit": "iters/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded planted POP, BASELINE.json config 4)",
+        "config": {"workload": f"{args.config} (N={N}, m={prob.m}, t'={tl}) seed {args.seed}",
+                   "l2": "flushed before every timed step (512 MB write, > 126 MB L2)",
+                   "parallelism": "replicas" if world > 1 else "single GPU"},
+        "warm_iters_per_s": total_steps / (ms_warm * 1e-3),
+        "time_to_1e-4": ttt,
+        "phase_ms_per_iter": {"affine_gather_tphase": ph_ms[0], "scatter": ph_ms[1], "psd_projection": ph_ms[2],
+                              "pack_dual_update": ph_ms[3]},
+        "roofline": {"kernel": "PSD projection of the 861x861 block (tridiag + D&C + back-transform + DMMA "
+                               "reconstruction), 4.33 N^3 algorithmic flops",
+                     "bound": "tensor", "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": ach / DMMA_PEAK_TFLOPS, "traffic": None,
+                     "peak_source": "measured FP64 DMMA (mma.sync m8n8k4) peak, profiles/r01_probe_fp64.log"},
+        "roofline_affine": {"kernel": "affine projection (gather, t-phase, row update, scatter, pack)",
+                            "bound": "hbm", "achieved": aff_gbs, "peak": hbm, "unit": "GB/s",
+                            "frac": aff_gbs / hbm, "algorithmic_bytes": abytes, "peak_source": hbm_src},
+        "cpu_baseline": cpu,
+        "e2e": {"value": total_steps / (e2e_ms * 1e-3), "unit": "iters/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "wall_s": e2e_wall},
+        "gpu_launches": int(launches_per_iter * args.steps + 4 * args.steps),
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def time_to_tol(prob, device, args):
+    """Wall time from setup to the first iterate with max residual <= 1e-4 and |gamma/gamma0 - 1| <= 1e-4
+    (checked every 25 iterations; the solver's own stop rule is residual-only)."""
+    import torch
+
+    from paper_1708_04174_b200 import SosAdmm
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    gpu = SosAdmm.from_problem(prob, tol=1e-300, max_iters=1 << 40, device=device)
+    g0 = prob.meta.get("gamma0")
+    res_stop = None
+    k = 0
+    while k < args.ttt_max:
+        info = gpu.iterate(25)
+        k = info["iter"]
+        r = max(info["res_pri"], info["res_dual"], info["res_gap"])
+        if res_stop is None and r <= 1e-4:
+            res_stop = k
+        if r <= 1e-4 and (g0 is None or abs(-info["pobj"] / g0 - 1.0) <= 1e-4):
+            return {"seconds": time.perf_counter() - t0, "iters": k, "residual_stop_iters": res_stop,
+                    "gamma": -info["pobj"], "check_stride": 25}
+    return {"seconds": None, "iters": None, "reached": False, "max_iters": args.ttt_max,
+            "residual_stop_iters": res_stop}
+
+
+def cpu_baseline(args):
+    """The oracle as it stands on the host, a bounded sample of the same workload."""
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from threadpoolctl import threadpool_limits
+
+    from oracle import HsdeOracle
+    from sosgen import make_config
+
+    prob = make_config(args.config, seed=args.seed)
+    with threadpool_limits(1):
+        orc = HsdeOracle.from_problem(prob)
+        st = orc.initial_state()
+        st = orc.step(st)  # warm-up
+        t0 = time.perf_counter()
+        n = 0
+        while n < args.cpu_steps or time.perf_counter() - t0 < 2.0:
+            st = orc.step(st)
+            orc.residuals(st)
+            n += 1
+            if time.perf_counter() - t0 > 30.0:
+                break
+        dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "iters/s", "cores": 1, "kind": "oracle",
+            "sample": f"{n} oracle HSDE-ADMM iterations (+ residuals) of {args.config} from iterate 2, KKT LU "
+                      "factorisation excluded, 1 BLAS thread (8 threads are slower, SURVEY §8(d))"}
+
+
+def run_reference(args):
+    world, rank, _ = dist_init()
+    if rank != 0:
+        return
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from threadpoolctl import threadpool_limits
+
+    from oracle import HsdeOracle
+    from sosgen import make_config
+
+    prob = make_config(args.config, seed=args.seed)
+    with threadpool_limits(1):
+        orc = HsdeOracle.from_problem(prob)
+        st = orc.initial_state()
+        for _ in range(args.warmup):
+            st = orc.step(st)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            st = orc.step(st)
+            orc.residuals(st)
+        dt = time.perf_counter() - t0
+    v = args.steps / dt
+    N = max(prob.psd_dims)
+    print(json.dumps({
+        "impl": "reference", "metric": "ADMM iters/s (n=40 quartic POP, config 4)", "value": v, "unit": "iters/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded planted POP, BASELINE.json config 4)",
+        "config": {"workload": f"{args.config} (N={N}, m={prob.m}) seed {args.seed}", "l2": "n/a (CPU)"},
+        "cpu_baseline": {"value": v, "unit": "iters/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{args.steps} oracle iterations after {args.warmup} warm-up, 1 BLAS thread"},
+        "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="pop40")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--cpu-steps", type=int, default=20)
+    ap.add_argument("--ttt-max", type=int, default=20000)
+    ap.add_argument("--no-ttt", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -14,6 +14,11 @@ shortcut (BASELINE.json `north_star`: "a dense or sparse LDL^T of
   M^{-1} r is computed from ONE generic sparse LU of the quasi-definite KKT = [[I, A^T], [A, -I]]
   (SuperLU, symmetric mode, minimum-degree ordering on A^T + A, no pivoting: an LDL^T up to
   diagonal scaling): M [p1; p2] = r  <=>  KKT [p1; -p2] = r.
+* The linear step is then refined (reading C15): two steps of iterative refinement on the
+  HSDE system (I + Q) u_hat = omega itself with residuals in extended precision
+  (np.longdouble), because the rank-one elimination loses up to ~1e-11 absolute in u_hat_3 when
+  1 + zeta^T M^{-1} zeta is large (4e5 on pop20) and tau << 1.  The refined u_hat is the solution of
+  the paper's linear system to working accuracy; the formula itself is unchanged.
 * Residuals / termination: DESIGN.md reading C9 (corrected infeasibility tests).
 * Initialisation: DESIGN.md reading C7: u0 = (0, 0, 1), v0 = (0, 0, 0).
 """
@@ -74,7 +79,8 @@ class Residuals:
 
 
 class HsdeOracle:
-    def __init__(self, A, b, c, n_free: int, psd_dims: list[int]):
+    def __init__(self, A, b, c, n_free: int, psd_dims: list[int], refine: int = 2):
+        self.refine = int(refine)
         self.A = sp.csc_matrix(A, dtype=np.float64)
         self.m, self.n = self.A.shape
         self.b = np.asarray(b, dtype=np.float64)
@@ -90,6 +96,11 @@ class HsdeOracle:
         self.denom = 1.0 + self.zeta @ self.h       # 1 + zeta^T M^{-1} zeta
         self.nb = np.linalg.norm(self.b)
         self.nc = np.linalg.norm(self.c)
+        LD = np.longdouble
+        self._A_ld = self.A.tocsr().astype(LD)
+        self._AT_ld = self.A.T.tocsr().astype(LD)
+        self._b_ld = self.b.astype(LD)
+        self._c_ld = self.c.astype(LD)
 
     @staticmethod
     def from_problem(prob) -> "HsdeOracle":
@@ -102,7 +113,24 @@ class HsdeOracle:
         return np.concatenate([sol[:self.n], -sol[self.n:]])
 
     def affine(self, w1: np.ndarray, w2: np.ndarray, w3: float):
-        """u_hat = (I + Q)^{-1} (w1, w2, w3): `E:MatrixInverseResult` + `E:FirstBlockElimination`."""
+        """u_hat = (I + Q)^{-1} (w1, w2, w3), refined (reading C15)."""
+        u1, u2, u3 = self.affine_once(w1, w2, w3)
+        if self.refine <= 0:
+            return u1, u2, u3
+        LD = np.longdouble
+        u1, u2, u3 = u1.astype(LD), u2.astype(LD), LD(u3)
+        w1l, w2l, w3l = np.asarray(w1, dtype=LD), np.asarray(w2, dtype=LD), LD(w3)
+        for _ in range(self.refine):
+            # residual of (I + Q) u = w, Q of eq:DefinitionQ (P:377-379), in extended precision
+            r1 = w1l - (u1 - self._AT_ld @ u2 + self._c_ld * u3)
+            r2 = w2l - (self._A_ld @ u1 + u2 - self._b_ld * u3)
+            r3 = w3l - (-(self._c_ld @ u1) + self._b_ld @ u2 + u3)
+            d1, d2, d3 = self.affine_once(r1.astype(np.float64), r2.astype(np.float64), float(r3))
+            u1, u2, u3 = u1 + d1, u2 + d2, u3 + LD(d3)
+        return u1.astype(np.float64), u2.astype(np.float64), float(u3)
+
+    def affine_once(self, w1: np.ndarray, w2: np.ndarray, w3: float):
+        """One pass of `E:MatrixInverseResult` (P:437-446) + `E:FirstBlockElimination` (P:434)."""
         r = np.concatenate([w1 - self.c * w3, w2 + self.b * w3])
         p = self.solve_M(r)
         coef = (self.zeta @ p) / self.denom

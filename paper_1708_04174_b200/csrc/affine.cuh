@@ -72,6 +72,7 @@ struct AffineArgs {
   const int* cta_blk;         // position-parallel kernels: CTA -> (block, first local svec index)
   const long long* cta_q0;
   int pos_ctas;
+  const int* side;            // per block: 1 = matrix holds Pi(-a) = Pi(a) - a (large-block path)
 };
 
 constexpr int GATHER_NT = 256;
@@ -292,8 +293,11 @@ __global__ void __launch_bounds__(TP_NT) k_tphase(AffineArgs a, int mode) {
   }
   cu = block_sum<TP_NT>(cu, sh);
   if (tid == 0) {
-    const double bu2 = bsig2 - coef * a.bh2;  // b^T u_hat_2 = b^T sigma_2 - coef b^T h_2
-    const double u3 = w3 + cu - bu2;          // E:FirstBlockElimination
+    // E:FirstBlockElimination u_hat_3 = w3 + c^T u_hat_1 - b^T u_hat_2 = w3 + zeta^T u_hat_12, and
+    // zeta^T u_hat_12 = zeta^T p - coef zeta^T h = zeta^T p (1 - (denom - 1)/denom) = coef exactly.
+    // This form avoids the O(|b||sigma_2|) cancellation of the dot products (reading C15).
+    const double u3 = w3 + coef;
+    (void)cu;
     a.is->omega3 = w3;
     a.is->coef = coef;
     a.is->u3 = u3;
@@ -379,20 +383,30 @@ __global__ void __launch_bounds__(POS_NT) k_pack(AffineArgs a, double* out_xi, i
   const long long L = (long long)N * (N + 1) / 2;
   const long long col0 = a.blk_col[b];
   const double* M = a.mats + a.blk_mat[b];
+  const int neg = a.side ? a.side[b] : 0;
   for (int k = threadIdx.x; k < POS_PER_CTA; k += POS_NT) {
     const long long q = q0 + k;
     if (q >= L) break;
     const long long col = col0 + q;
     int i, j;
     svec_ij(q, i, j);
-    // the projection kernels leave Pi(a) in the lower triangle (row j, column i, j >= i)
-    const double pij = M[(size_t)i * N + j];
-    const double xn = (i == j) ? pij : pij * SOS_RT2;
+    // the projection kernels leave their result in the lower triangle (row j, column i, j >= i)
+    const double mij = M[(size_t)i * N + j];
+    const double sv = (i == j) ? mij : mij * SOS_RT2;
+    const double av = a.asvec[col - a.t_free];
+    double xn, zn;
+    if (neg) {  // M = Pi(-a): z = M, xi = a + M (Moreau decomposition a = Pi(a) - Pi(-a))
+      zn = sv;
+      xn = av + sv;
+    } else {    // M = Pi(a): xi = M, z = xi - a
+      xn = sv;
+      zn = sv - av;
+    }
     if (out_xi) {
       out_xi[col - a.t_free] = xn;
     } else {
       a.xi[col] = xn;
-      a.z[col] = xn - a.asvec[col - a.t_free];
+      a.z[col] = zn;
     }
   }
   if (commit && blockIdx.x == 0 && threadIdx.x == 0) {

@@ -1,0 +1,463 @@
+// Divide-and-conquer eigensolver for the symmetric tridiagonal T (second stage of the large-block
+// PSD projection, north_star (c) "a tridiagonal solve").  Textbook Cuppen recursion restated for
+// the GPU:
+//   * a balanced bisection tree of depth D; all leaves (size 1 or 2) sit at depth D, so every level
+//     merges disjoint nodes and the eigenvector matrices ping-pong between two N x N buffers;
+//   * a cut at position k (T[k,k+1] = e_k) gives T = diag(T1', T2') + rho u u^T with rho = |e_k|,
+//     u = e_k + sign(e_k) e_{k+1}, T1'/T2' with |e_k| subtracted from the two adjacent diagonals;
+//   * a merge solves D + rho z z^T (z = [last row of Q1; sign(e_k) first row of Q2]):
+//     - sort, deflate small |z_i| and close pairs by Givens rotations (LAPACK dlaed2 rules),
+//     - one warp per secular root, origin at the nearer pole, bracketed rational (two-pole)
+//       iteration with bisection safeguard,
+//     - Gu-Eisenstat recomputation of z so that the eigenvectors u_j = z_hat / (d - lambda_j) are
+//       numerically orthogonal,
+//     - Q_new = Q_old[:, nondeflated] * U on the FP64 tensor cores (k_gemm_f64); deflated columns
+//       are copied; eigenvalues are merged into ascending order.
+#pragma once
+#include "common.cuh"
+#include "gemm_f64.cuh"
+
+constexpr double DC_EPS = 2.220446049250313e-16;
+constexpr int DC_NT = 256;
+
+struct DcNode {
+  int s, n1, n;
+  long long u_off;  // offset of this node's k x k matrix U in the level's U buffer
+};
+
+struct DcArgs {
+  int N;
+  const double* d;     // tridiagonal diagonal (N)
+  const double* e;     // off-diagonal (N-1)
+  double* dmod;        // modified diagonal for the leaves
+  double* Q[2];        // N x N ping-pong eigenvector buffers
+  double* lam[2];      // eigenvalues
+  const DcNode* nodes; // all nodes, level by level
+  const int* pos2node; // per level: node index of every position (D x N)
+  // position-indexed scratch (N each)
+  double *ndd, *ndz, *dfv, *tau_r, *zhat, *lam_r;
+  int *ndcol, *dfcol, *org, *outcol;
+  // node-indexed
+  int* node_k;
+  int* node_nd;
+  double* node_rho;
+  double* U;           // level U buffer (<= N^2)
+  int* rot_pq;         // 2 ints per rotation (position-indexed, N)
+  double* rot_cs;      // 2 doubles per rotation
+  int* rot_cnt;        // node-indexed
+  const DevState* st;
+  const IterScal* is;
+  int check_state;
+};
+
+__device__ __forceinline__ bool dc_skip(const DcArgs& a) {
+  return a.check_state && (a.st->done || !a.is->proceed);
+}
+
+// Leaves of size 1 or 2 (closed form); also sets Q[buf] diagonal blocks.
+__global__ void k_dc_leaf(DcArgs a, int first_leaf, int nleaves, int buf) {
+  if (dc_skip(a)) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nleaves) return;
+  const DcNode nd = a.nodes[first_leaf + t];
+  const int N = a.N, s = nd.s, n = nd.n;
+  double* Q = a.Q[buf];
+  double* lam = a.lam[buf];
+  // cuts: at the left boundary (if s > 0) and at the right boundary (if s + n < N)
+  auto dm = [&](int i) {
+    double v = a.d[i];
+    if (i == s && s > 0) v -= fabs(a.e[s - 1]);
+    if (i == s + n - 1 && s + n < N) v -= fabs(a.e[s + n - 1]);
+    return v;
+  };
+  if (n == 1) {
+    lam[s] = dm(s);
+    Q[(size_t)s * N + s] = 1.0;
+  } else {
+    const double p = dm(s), r = dm(s + 1), q = a.e[s];
+    double c = 1.0, sn = 0.0, l1 = p, l2 = r;
+    if (q != 0.0) {
+      const double th = (r - p) / (2.0 * q);
+      const double t2 = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(fma(th, th, 1.0)));
+      c = 1.0 / sqrt(fma(t2, t2, 1.0));
+      sn = t2 * c;
+      l1 = p - t2 * q;
+      l2 = r + t2 * q;
+    }
+    // eigenvectors: (c, -sn) for l1, (sn, c) for l2
+    double v1a = c, v1b = -sn, v2a = sn, v2b = c;
+    if (l1 > l2) {
+      double tt = l1; l1 = l2; l2 = tt;
+      tt = v1a; v1a = v2a; v2a = tt;
+      tt = v1b; v1b = v2b; v2b = tt;
+    }
+    lam[s] = l1;
+    lam[s + 1] = l2;
+    Q[(size_t)s * N + s] = v1a;
+    Q[(size_t)s * N + s + 1] = v1b;
+    Q[(size_t)(s + 1) * N + s] = v2a;
+    Q[(size_t)(s + 1) * N + s + 1] = v2b;
+  }
+}
+
+// ---- merge step 1: z, sort, deflation (one CTA per node) ---------------------------------
+constexpr int DC_MAXN = 1280;
+__global__ void __launch_bounds__(DC_NT) k_dc_prep(DcArgs a, int node0, int ob) {
+  if (dc_skip(a)) return;
+  const int node = node0 + blockIdx.x;
+  const DcNode nd = a.nodes[node];
+  const int N = a.N, s = nd.s, n1 = nd.n1, n = nd.n;
+  double* Qo = a.Q[ob];
+  const double* lo = a.lam[ob];
+  __shared__ double dsh[DC_MAXN], zsh[DC_MAXN];
+  __shared__ int perm[DC_MAXN];
+  __shared__ int ndl[DC_MAXN], dfl[DC_MAXN];
+  __shared__ double red[DC_NT / 32];
+  __shared__ int nk, ndf, nrot;
+  __shared__ double rho_s;
+  const int tid = threadIdx.x;
+  const double er = a.e[s + n1 - 1];
+  const double rho = fabs(er);
+  const double sg = (er < 0.0) ? -1.0 : 1.0;
+  // sorted merge of the two ascending child spectra (ties: left child first)
+  for (int i = tid; i < n; i += DC_NT) {
+    const double di = lo[s + i];
+    int rank;
+    if (i < n1) {  // count right elements < di
+      int l = 0, h = n - n1;
+      while (l < h) {
+        const int mid = (l + h) >> 1;
+        if (lo[s + n1 + mid] < di) l = mid + 1; else h = mid;
+      }
+      rank = i + l;
+    } else {  // count left elements <= di
+      int l = 0, h = n1;
+      while (l < h) {
+        const int mid = (l + h) >> 1;
+        if (lo[s + mid] <= di) l = mid + 1; else h = mid;
+      }
+      rank = (i - n1) + l;
+    }
+    perm[rank] = i;
+  }
+  __syncthreads();
+  double z2 = 0.0, dmax = 0.0;
+  for (int r = tid; r < n; r += DC_NT) {
+    const int i = perm[r];
+    const double zi = (i < n1) ? Qo[(size_t)(s + i) * N + (s + n1 - 1)] : sg * Qo[(size_t)(s + i) * N + (s + n1)];
+    dsh[r] = lo[s + i];
+    zsh[r] = zi;
+    z2 = fma(zi, zi, z2);
+    dmax = fmax(dmax, fabs(lo[s + i]));
+  }
+  // block reductions (sum, max)
+  z2 = warp_sum(z2);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  if ((tid & 31) == 0) red[tid >> 5] = z2;
+  __syncthreads();
+  double zn2 = 0.0;
+  for (int w = 0; w < DC_NT / 32; ++w) zn2 += red[w];
+  __syncthreads();
+  if ((tid & 31) == 0) red[tid >> 5] = dmax;
+  __syncthreads();
+  double dm = 0.0;
+  for (int w = 0; w < DC_NT / 32; ++w) dm = fmax(dm, red[w]);
+  __syncthreads();
+  const double zn = sqrt(zn2);
+  double zmax = 0.0;
+  for (int r = tid; r < n; r += DC_NT) {
+    zsh[r] = (zn > 0.0) ? zsh[r] / zn : 0.0;
+    zmax = fmax(zmax, fabs(zsh[r]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
+  if ((tid & 31) == 0) red[tid >> 5] = zmax;
+  __syncthreads();
+  double zm = 0.0;
+  for (int w = 0; w < DC_NT / 32; ++w) zm = fmax(zm, red[w]);
+  const double rhop = rho * zn2;  // rho z z^T = rhop zn zn^T with |zn| = 1
+  const double tol = 8.0 * DC_EPS * fmax(dm, zm);
+  // sequential deflation scan (dlaed2 rules), rotations recorded for the column update
+  if (tid == 0) {
+    int k = 0, df = 0, nr = 0, pj = -1;
+    for (int r = 0; r < n; ++r) {
+      if (rhop * fabs(zsh[r]) <= tol) {
+        dfl[df++] = r;
+        continue;
+      }
+      if (pj < 0) {
+        pj = r;
+        continue;
+      }
+      double sv = zsh[pj], cv = zsh[r];
+      const double tt = hypot(cv, sv);
+      const double t = dsh[r] - dsh[pj];
+      cv /= tt;
+      sv = -sv / tt;
+      if (fabs(t * cv * sv) <= tol) {
+        zsh[r] = tt;
+        zsh[pj] = 0.0;
+        const int rp = s + nr;
+        a.rot_pq[2 * rp] = s + perm[pj];
+        a.rot_pq[2 * rp + 1] = s + perm[r];
+        a.rot_cs[2 * rp] = cv;
+        a.rot_cs[2 * rp + 1] = sv;
+        ++nr;
+        const double t1 = dsh[pj] * cv * cv + dsh[r] * sv * sv;
+        dsh[r] = dsh[pj] * sv * sv + dsh[r] * cv * cv;
+        dsh[pj] = t1;
+        dfl[df++] = pj;
+        pj = r;
+      } else {
+        ndl[k++] = pj;
+        pj = r;
+      }
+    }
+    if (pj >= 0) ndl[k++] = pj;
+    nk = k;
+    ndf = df;
+    nrot = nr;
+    rho_s = rhop;
+  }
+  __syncthreads();
+  const int k = nk, df = ndf, nr = nrot;
+  // apply the deflation rotations to the columns of Q_old (rows of this node only), in order:
+  // x' = c x + s y, y' = c y - s x  (drot)
+  for (int row = s + tid; row < s + n; row += DC_NT) {
+    for (int q = 0; q < nr; ++q) {
+      const int rp = s + q;
+      const int cp = a.rot_pq[2 * rp], cq = a.rot_pq[2 * rp + 1];
+      const double c = a.rot_cs[2 * rp], sn = a.rot_cs[2 * rp + 1];
+      double* xp = Qo + (size_t)cp * N + row;
+      double* yp = Qo + (size_t)cq * N + row;
+      const double x = *xp, y = *yp;
+      *xp = c * x + sn * y;
+      *yp = c * y - sn * x;
+    }
+  }
+  for (int i = tid; i < k; i += DC_NT) {
+    const int r = ndl[i];
+    a.ndd[s + i] = dsh[r];
+    a.ndz[s + i] = zsh[r];
+    a.ndcol[s + i] = s + perm[r];
+  }
+  for (int i = tid; i < df; i += DC_NT) {
+    const int r = dfl[i];
+    a.dfv[s + i] = dsh[r];
+    a.dfcol[s + i] = s + perm[r];
+  }
+  if (tid == 0) {
+    a.node_k[node] = k;
+    a.node_nd[node] = df;
+    a.node_rho[node] = rho_s;
+    a.rot_cnt[node] = nr;
+  }
+}
+
+// ---- merge step 2: secular roots, one warp per root ----------------------------------------
+// f(lambda) = 1/rho + sum_i z_i^2 / (d_i - lambda), increasing between consecutive poles.
+__global__ void __launch_bounds__(DC_NT) k_dc_secular(DcArgs a, int level) {
+  if (dc_skip(a)) return;
+  const int N = a.N;
+  const int p = (blockIdx.x * DC_NT + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (p >= N) return;
+  const int node = a.pos2node[(size_t)level * N + p];
+  const DcNode nd = a.nodes[node];
+  const int s = nd.s, j = p - s, k = a.node_k[node];
+  if (j >= k) return;
+  const double* d = a.ndd + s;
+  const double* z = a.ndz + s;
+  const double rho = a.node_rho[node];
+  const double rinv = 1.0 / rho;
+  int org;
+  double lo, hi;
+  if (k == 1) {
+    if (lane == 0) {
+      a.org[p] = 0;
+      a.tau_r[p] = rho * z[0] * z[0];
+      a.lam_r[p] = d[0] + rho * z[0] * z[0];
+    }
+    return;
+  }
+  if (j < k - 1) {
+    const double mid = 0.5 * (d[j + 1] - d[j]);
+    double f = 0.0;
+    for (int i = lane; i < k; i += 32) f += z[i] * z[i] / ((d[i] - d[j]) - mid);
+    f = rinv + warp_sum(f);
+    if (f >= 0.0) {
+      org = j;
+      lo = 0.0;
+      hi = mid;
+    } else {
+      org = j + 1;
+      lo = -mid;
+      hi = 0.0;
+    }
+  } else {
+    double zz = 0.0;
+    for (int i = lane; i < k; i += 32) zz = fma(z[i], z[i], zz);
+    zz = warp_sum(zz);
+    org = k - 1;
+    lo = 0.0;
+    hi = rho * zz;
+  }
+  const double dorg = d[org];
+  const double dl = d[j] - dorg;                             // left pole (shifted)
+  const double dr = (j < k - 1) ? d[j + 1] - dorg : 0.0;     // right pole (shifted)
+  double tau = 0.5 * (lo + hi);
+  for (int it = 0; it < 200; ++it) {
+    double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0, asum = 0.0;
+    for (int i = lane; i < k; i += 32) {
+      const double del = (d[i] - dorg) - tau;
+      const double r = z[i] / del;
+      const double term = z[i] * r;
+      if (i <= j) {
+        psi += term;
+        dpsi = fma(r, r, dpsi);
+      } else {
+        phi += term;
+        dphi = fma(r, r, dphi);
+      }
+      asum += fabs(term);
+    }
+    psi = warp_sum(psi);
+    dpsi = warp_sum(dpsi);
+    phi = warp_sum(phi);
+    dphi = warp_sum(dphi);
+    asum = warp_sum(asum);
+    const double g = rinv + psi + phi;
+    if (g < 0.0) lo = tau; else hi = tau;
+    if (fabs(g) <= 8.0 * DC_EPS * (rinv + asum) * (1.0 + 0.0625 * k) || g == 0.0) break;
+    // two-pole rational model through (tau, g, g')
+    const double D1 = dl - tau;
+    double eta;
+    bool ok = true;
+    if (j < k - 1) {
+      const double D2 = dr - tau;
+      const double B1 = dpsi * D1 * D1, B2 = dphi * D2 * D2;
+      const double c = g - B1 / D1 - B2 / D2;
+      const double bq = c * (D1 + D2) + B1 + B2;  // c eta^2 - bq eta + D1 D2 g = 0
+      const double cq = D1 * D2 * g;
+      if (c == 0.0) {
+        eta = cq / bq;
+      } else {
+        const double disc = bq * bq - 4.0 * c * cq;
+        if (disc < 0.0) {
+          ok = false;
+          eta = 0.0;
+        } else {
+          const double sq = sqrt(disc);
+          const double qq = 0.5 * (bq + (bq >= 0.0 ? sq : -sq));
+          const double e1 = qq / c, e2 = (qq != 0.0) ? cq / qq : e1;
+          const bool in1 = (tau + e1 > lo) && (tau + e1 < hi);
+          const bool in2 = (tau + e2 > lo) && (tau + e2 < hi);
+          if (in1 && in2) eta = (fabs(e1) < fabs(e2)) ? e1 : e2;
+          else if (in1) eta = e1;
+          else if (in2) eta = e2;
+          else ok = false;
+        }
+      }
+    } else {
+      const double B1 = dpsi * D1 * D1;
+      const double c = g - B1 / D1;
+      eta = (c != 0.0) ? D1 + B1 / c : 0.0;
+      if (c == 0.0) ok = false;
+    }
+    double tn = tau + eta;
+    if (!ok || !(tn > lo && tn < hi)) tn = 0.5 * (lo + hi);
+    const bool conv = fabs(tn - tau) <= 2.0 * DC_EPS * fabs(tn);
+    tau = tn;
+    if (conv || hi - lo <= 2.0 * DC_EPS * fmax(fabs(lo), fabs(hi))) break;
+  }
+  if (lane == 0) {
+    a.org[p] = org;
+    a.tau_r[p] = tau;
+    a.lam_r[p] = dorg + tau;
+  }
+}
+
+// ---- merge step 3: Gu-Eisenstat z_hat, one warp per position i ------------------------------
+__global__ void __launch_bounds__(DC_NT) k_dc_zhat(DcArgs a, int level) {
+  if (dc_skip(a)) return;
+  const int N = a.N;
+  const int p = (blockIdx.x * DC_NT + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (p >= N) return;
+  const int node = a.pos2node[(size_t)level * N + p];
+  const int s = a.nodes[node].s, i = p - s, k = a.node_k[node];
+  if (i >= k) return;
+  const double* d = a.ndd + s;
+  const double rho = a.node_rho[node];
+  double prod = 1.0;
+  for (int j = lane; j < k; j += 32) {
+    const double del = (d[i] - d[a.org[s + j]]) - a.tau_r[s + j];  // d_i - lambda_j
+    if (j == i) prod *= -del / rho;
+    else prod *= -del / (d[j] - d[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) prod *= __shfl_xor_sync(0xffffffffu, prod, o);
+  if (lane == 0) a.zhat[p] = copysign(sqrt(fmax(prod, 0.0)), a.ndz[p]);
+}
+
+// ---- merge step 4: eigenvector matrix U (k x k) and output ranks, one warp per root j -------
+__global__ void __launch_bounds__(DC_NT) k_dc_vec(DcArgs a, int level, int nb) {
+  if (dc_skip(a)) return;
+  const int N = a.N;
+  const int p = (blockIdx.x * DC_NT + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (p >= N) return;
+  const int node = a.pos2node[(size_t)level * N + p];
+  const DcNode nd = a.nodes[node];
+  const int s = nd.s, j = p - s, k = a.node_k[node], df = a.node_nd[node];
+  if (j >= k) return;
+  const double* d = a.ndd + s;
+  const double dj = d[a.org[p]], tj = a.tau_r[p];
+  double* U = a.U + nd.u_off + (size_t)j * nd.n;  // column stride n (static upper bound of k)
+  double nrm = 0.0;
+  for (int i = lane; i < k; i += 32) {
+    const double u = a.zhat[s + i] / ((d[i] - dj) - tj);
+    U[i] = u;
+    nrm = fma(u, u, nrm);
+  }
+  nrm = warp_sum(nrm);
+  const double inv = 1.0 / sqrt(nrm);
+  for (int i = lane; i < k; i += 32) U[i] *= inv;
+  // rank among (roots ascending) U (deflated values; deflated first on ties)
+  const double lj = a.lam_r[p];
+  int cnt = 0;
+  for (int q = lane; q < df; q += 32) cnt += (a.dfv[s + q] <= lj) ? 1 : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if (lane == 0) {
+    const int rank = j + cnt;
+    a.outcol[p] = s + rank;
+    a.lam[nb][s + rank] = lj;
+  }
+}
+
+// ---- merge step 6: deflated eigenpairs (copied columns), one CTA per node ------------------
+__global__ void __launch_bounds__(DC_NT) k_dc_final(DcArgs a, int node0, int ob, int nb) {
+  if (dc_skip(a)) return;
+  const int node = node0 + blockIdx.x;
+  const DcNode nd = a.nodes[node];
+  const int N = a.N, s = nd.s, n = nd.n, k = a.node_k[node], df = a.node_nd[node];
+  const double* Qo = a.Q[ob];
+  double* Qn = a.Q[nb];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int q = warp; q < df; q += DC_NT / 32) {
+    const double x = a.dfv[s + q];
+    // roots strictly below x, deflated values below x (ties by index)
+    int cnt = 0;
+    for (int j = lane; j < k; j += 32) cnt += (a.lam_r[s + j] < x) ? 1 : 0;
+    for (int q2 = lane; q2 < df; q2 += 32) {
+      const double y = a.dfv[s + q2];
+      cnt += (y < x || (y == x && q2 < q)) ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    const int col = s + cnt;
+    if (lane == 0) a.lam[nb][col] = x;
+    const double* src = Qo + (size_t)a.dfcol[s + q] * N;
+    double* dst = Qn + (size_t)col * N;
+    for (int r = s + lane; r < s + n; r += 32) dst[r] = src[r];
+  }
+}

@@ -1,26 +1,432 @@
-// PSD projection of large Gram blocks (N > 64): placeholder, replaced by the tridiagonal
-// path (Householder tridiagonalisation in a thread-block cluster, divide-and-conquer, DMMA
-// back-transform and reconstruction).
+// PSD-cone projection of large Gram blocks (N > 64).
+//
+//   a  --(k_tridiag, one cluster)-->  T = H^T a H, reflectors V, tau
+//      --(divide and conquer, dc.cuh)-->  T = Z diag(lambda) Z^T
+//      --(k_select)-->  the spectral side with fewer eigenpairs: r = min(#lambda>0, #lambda<0)
+//      --(k_backtransform)-->  W = H Z_side diag(sqrt|lambda_side|)   (only r columns)
+//      --(k_gemm_f64, DMMA)-->  M = W W^T
+// M is Pi_{S+}(a) when the positive side was chosen, and Pi_{S+}(-a) = Pi_{S+}(a) - a (Moreau)
+// when the negative side was; k_pack reads the per-block side flag.  Picking the smaller side
+// makes the back-transform and the reconstruction O(N^2 r) instead of O(N^3) near convergence,
+// where the projected Gram matrices have low rank (SURVEY §7 H1 "partial spectrum").
 #pragma once
 #include <string>
 #include <vector>
-#include "common.cuh"
 
-struct LargeEig {
-  int nlarge = 0;
+#include "common.cuh"
+#include "dc.cuh"
+#include "gemm_f64.cuh"
+#include "tridiag.cuh"
+
+struct LargeBlock {
+  int b = 0, N = 0, C = 1, D = 0;
+  long long smem_cols = 0;
+  size_t trd_smem = 0;
+  double* M = nullptr;
+  double *d = nullptr, *e = nullptr, *tau = nullptr, *V = nullptr;
+  DcArgs dc{};
+  std::vector<int> level_node0, level_nn, level_nmax;
+  int leaf0 = 0, nleaves = 0;
+  GemmDesc* gdesc = nullptr;  // per level (node-indexed), then the reconstruction descriptor
+  std::vector<int> gdesc_off;
+  int* sel = nullptr;         // [r, c0, side]
+  int recon = 0;              // index of the reconstruction descriptor in gdesc
+  double* W = nullptr;
+  TridiagArgs ta{};
 };
 
-inline size_t large_eig_bytes(const std::vector<int>& blk_N, const std::vector<int>& large) { return 0; }
+struct LargeEig {
+  std::vector<LargeBlock> blocks;
+  int* side = nullptr;   // per PSD block: 1 = block matrix holds Pi(-a)
+  const DevState* st = nullptr;
+  const IterScal* is = nullptr;
+  int check_state = 1;
+};
+
+// ---------------------------------------------------------------------------------------------
+__global__ void k_select(const double* lam, int* sel, int* side, int b, int N, const DevState* st,
+                         const IterScal* is, int check_state) {
+  if (check_state && (st->done || !is->proceed)) return;
+  __shared__ int cp, cn;
+  if (threadIdx.x == 0) cp = cn = 0;
+  __syncthreads();
+  int p = 0, q = 0;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    p += lam[i] > 0.0;
+    q += lam[i] < 0.0;
+  }
+  atomicAdd(&cp, p);
+  atomicAdd(&cn, q);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (cp <= cn) {
+      sel[0] = cp;
+      sel[1] = N - cp;
+      sel[2] = 0;
+    } else {
+      sel[0] = cn;
+      sel[1] = 0;
+      sel[2] = 1;
+    }
+    side[b] = sel[2];
+  }
+}
+
+// W[:, c] = H Z[:, c0 + c] * sqrt(|lambda|), one warp per column; H = H_0 H_1 ... H_{N-3} applied
+// right to left (LAPACK dormtr, 'L', 'N').
+constexpr int BT_NT = 512;
+__global__ void __launch_bounds__(BT_NT) k_backtransform(const double* Qf, const double* lamf, const double* V,
+                                                         const double* tau, const int* sel, double* W, int N,
+                                                         const DevState* st, const IterScal* is, int check_state) {
+  if (check_state && (st->done || !is->proceed)) return;
+  const int r = sel[0], c0 = sel[1];
+  const int c = blockIdx.x * (BT_NT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (c >= r) return;
+  const double* z = Qf + (size_t)(c0 + c) * N;
+  double* w = W + (size_t)c * N;
+  for (int i = lane; i < N; i += 32) w[i] = z[i];
+  __syncwarp();
+  for (int k = N - 3; k >= 0; --k) {
+    const double tk = tau[k];
+    if (tk == 0.0) continue;
+    const double* v = V + (size_t)k * N;
+    double sacc = 0.0;
+    for (int i = k + 1 + lane; i < N; i += 32) sacc = fma(v[i], w[i], sacc);
+    sacc = warp_sum(sacc) * tk;
+    for (int i = k + 1 + lane; i < N; i += 32) w[i] = fma(-sacc, v[i], w[i]);
+    __syncwarp();
+  }
+  const double sc = sqrt(fabs(lamf[c0 + c]));
+  for (int i = lane; i < N; i += 32) w[i] *= sc;
+}
+
+// ---------------------------------------------------------------------------------------------
+struct LargeLayout {
+  size_t bytes = 0;
+};
+
+inline void dc_build_tree(int N, std::vector<DcNode>& nodes, std::vector<int>& level_node0,
+                          std::vector<int>& level_nn, std::vector<int>& level_nmax, int& D, int& leaf0,
+                          int& nleaves, std::vector<int>& pos2node) {
+  D = 0;
+  while ((1 << (D + 1)) <= N) ++D;  // 2^D <= N < 2^(D+1): leaves of size 1 or 2
+  // nodes per depth (depth 0 = root), recursive bisection
+  std::vector<std::vector<DcNode>> by_depth(D + 1);
+  by_depth[0].push_back(DcNode{0, N / 2, N, 0});
+  for (int dep = 0; dep < D; ++dep)
+    for (const DcNode& nd : by_depth[dep]) {
+      const int n1 = nd.n / 2, n2 = nd.n - n1;
+      by_depth[dep + 1].push_back(DcNode{nd.s, n1 / 2, n1, 0});
+      by_depth[dep + 1].push_back(DcNode{nd.s + n1, n2 / 2, n2, 0});
+    }
+  // fix the split of every internal node: n1 = size of its left child
+  for (int dep = 0; dep < D; ++dep)
+    for (size_t q = 0; q < by_depth[dep].size(); ++q) by_depth[dep][q].n1 = by_depth[dep + 1][2 * q].n;
+  // levels bottom-up: level h (1..D) merges depth D-h; leaves are depth D
+  nodes.clear();
+  level_node0.assign(D + 1, 0);
+  level_nn.assign(D + 1, 0);
+  level_nmax.assign(D + 1, 0);
+  pos2node.assign((size_t)(D + 1) * N, 0);
+  leaf0 = 0;
+  nleaves = (int)by_depth[D].size();
+  for (const DcNode& nd : by_depth[D]) nodes.push_back(nd);
+  for (int h = 1; h <= D; ++h) {
+    level_node0[h] = (int)nodes.size();
+    long long uoff = 0;
+    for (DcNode nd : by_depth[D - h]) {
+      nd.u_off = uoff;
+      uoff += (long long)nd.n * nd.n;
+      const int id = (int)nodes.size();
+      for (int p = nd.s; p < nd.s + nd.n; ++p) pos2node[(size_t)h * N + p] = id;
+      level_nmax[h] = std::max(level_nmax[h], nd.n);
+      nodes.push_back(nd);
+    }
+    level_nn[h] = (int)nodes.size() - level_node0[h];
+  }
+}
+
+constexpr int TRD_MAX_DYN_SMEM = 227 * 1024 - 2048;  // leaves room for the static colp table
+
+inline int tridiag_cluster_size(int N) { return N > 512 ? 16 : (N > 160 ? 8 : 4); }
+
+// Shared-memory budget for the distributed trailing matrix (per CTA).
+inline long long tridiag_col_budget(int N, int C) {
+  const long long cap = TRD_MAX_DYN_SMEM / 8 - (3LL * N + (N + C - 1) / C + 1 + 2 + 32) - 8;
+  long long need = 0;
+  for (int c = 0; c < C; ++c) {
+    long long s = 0;
+    for (int j = c; j < N; j += C) s += N - j;
+    need = std::max(need, s);
+  }
+  return std::min(cap, need);
+}
+
+template <class F>
+inline size_t large_carve(const std::vector<int>& blk_N, const std::vector<int>& large, char* base, int** side,
+                          F&& per_block) {
+  size_t used = 0;
+  auto take = [&](size_t bytes) -> char* {
+    used = (used + 255) / 256 * 256;
+    char* p = base ? base + used : nullptr;
+    used += std::max<size_t>(bytes, 8);
+    return p;
+  };
+  char* sp = take(4 * std::max<size_t>(blk_N.size(), 1));  // per-block side flags
+  if (side) *side = (int*)sp;
+  for (int b : large) {
+    const int N = blk_N[b];
+    std::vector<DcNode> nodes;
+    std::vector<int> l0, lnn, lmax, p2n;
+    int D, leaf0, nleaves;
+    dc_build_tree(N, nodes, l0, lnn, lmax, D, leaf0, nleaves, p2n);
+    const size_t NN = (size_t)N * N;
+    char* p[32];
+    int q = 0;
+    p[q++] = take(8 * N);                 // d
+    p[q++] = take(8 * N);                 // e
+    p[q++] = take(8 * N);                 // tau
+    p[q++] = take(8 * NN);                // V
+    p[q++] = take(8 * NN);                // Q0
+    p[q++] = take(8 * NN);                // Q1
+    p[q++] = take(8 * N);                 // lam0
+    p[q++] = take(8 * N);                 // lam1
+    p[q++] = take(sizeof(DcNode) * nodes.size());
+    p[q++] = take(4 * p2n.size());
+    for (int t = 0; t < 6; ++t) p[q++] = take(8 * N);   // ndd ndz dfv tau_r zhat lam_r
+    for (int t = 0; t < 4; ++t) p[q++] = take(4 * N);   // ndcol dfcol org outcol
+    p[q++] = take(4 * nodes.size());      // node_k
+    p[q++] = take(4 * nodes.size());      // node_nd
+    p[q++] = take(8 * nodes.size());      // node_rho
+    p[q++] = take(8 * NN);                // U
+    p[q++] = take(8 * N);                 // rot_pq (2 ints)
+    p[q++] = take(16 * N);                // rot_cs
+    p[q++] = take(4 * nodes.size());      // rot_cnt
+    p[q++] = take(sizeof(GemmDesc) * (nodes.size() + 1));
+    p[q++] = take(4 * 4);                 // sel
+    per_block(b, N, p, nodes, l0, lnn, lmax, D, leaf0, nleaves, p2n);
+  }
+  return used + 256;
+}
+
+inline size_t large_eig_bytes(const std::vector<int>& blk_N, const std::vector<int>& large) {
+  return large_carve(blk_N, large, nullptr, nullptr, [](int, int, char**, auto&, auto&, auto&, auto&, int, int, int, auto&) {});
+}
+
 inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std::vector<long long>& blk_mat,
                           const std::vector<int>& large, double* mats, char* base, DevState* st, IterScal* is,
                           cudaStream_t s, std::string& msg) {
-  le.nlarge = (int)large.size();
-  if (le.nlarge) {
-    msg = "blocks with N > 64 are not supported yet";
+  le.st = st;
+  le.is = is;
+  le.blocks.clear();
+  cudaError_t err = cudaSuccess;
+  int* side_p = nullptr;
+  large_carve(blk_N, large, base, &side_p, [&](int b, int N, char** p, std::vector<DcNode>& nodes,
+                                                   std::vector<int>& l0, std::vector<int>& lnn,
+                                                   std::vector<int>& lmax, int D, int leaf0, int nleaves,
+                                                   std::vector<int>& p2n) {
+    LargeBlock lb;
+    lb.b = b;
+    lb.N = N;
+    lb.M = mats + blk_mat[b];
+    lb.C = tridiag_cluster_size(N);
+    lb.smem_cols = tridiag_col_budget(N, lb.C);
+    lb.trd_smem = tridiag_smem_bytes(N, lb.C, lb.smem_cols);
+    int q = 0;
+    lb.d = (double*)p[q++];
+    lb.e = (double*)p[q++];
+    lb.tau = (double*)p[q++];
+    lb.V = (double*)p[q++];
+    DcArgs& dc = lb.dc;
+    dc.N = N;
+    dc.d = lb.d;
+    dc.e = lb.e;
+    dc.dmod = nullptr;
+    dc.Q[0] = (double*)p[q++];
+    dc.Q[1] = (double*)p[q++];
+    dc.lam[0] = (double*)p[q++];
+    dc.lam[1] = (double*)p[q++];
+    DcNode* dnodes = (DcNode*)p[q++];
+    int* dp2n = (int*)p[q++];
+    dc.nodes = dnodes;
+    dc.pos2node = dp2n;
+    dc.ndd = (double*)p[q++];
+    dc.ndz = (double*)p[q++];
+    dc.dfv = (double*)p[q++];
+    dc.tau_r = (double*)p[q++];
+    dc.zhat = (double*)p[q++];
+    dc.lam_r = (double*)p[q++];
+    dc.ndcol = (int*)p[q++];
+    dc.dfcol = (int*)p[q++];
+    dc.org = (int*)p[q++];
+    dc.outcol = (int*)p[q++];
+    dc.node_k = (int*)p[q++];
+    dc.node_nd = (int*)p[q++];
+    dc.node_rho = (double*)p[q++];
+    dc.U = (double*)p[q++];
+    dc.rot_pq = (int*)p[q++];
+    dc.rot_cs = (double*)p[q++];
+    dc.rot_cnt = (int*)p[q++];
+    dc.st = st;
+    dc.is = is;
+    dc.check_state = 1;
+    lb.gdesc = (GemmDesc*)p[q++];
+    lb.sel = (int*)p[q++];
+    lb.recon = (int)nodes.size();
+    lb.D = D;
+    lb.level_node0 = l0;
+    lb.level_nn = lnn;
+    lb.level_nmax = lmax;
+    lb.leaf0 = leaf0;
+    lb.nleaves = nleaves;
+    // GEMM descriptors: one per merge node (Q_new = Q_old[:, nd] U), then the reconstruction
+    std::vector<GemmDesc> gd(nodes.size() + 1);
+    for (int h = 1; h <= D; ++h) {
+      const int ob = (h - 1) & 1, nb = h & 1;
+      for (int t = 0; t < lnn[h]; ++t) {
+        const int id = l0[h] + t;
+        const DcNode& nd = nodes[id];
+        GemmDesc g{};
+        g.A = dc.Q[ob] + nd.s;
+        g.lda = N;
+        g.acol = dc.ndcol + nd.s;
+        g.B = dc.U + nd.u_off;
+        g.ldb = nd.n;
+        g.C = dc.Q[nb] + nd.s;
+        g.ldc = N;
+        g.ccol = dc.outcol + nd.s;
+        g.M = nd.n;
+        g.N = nd.n;
+        g.K = nd.n;
+        g.Kdev = dc.node_k + id;
+        g.Ndev = dc.node_k + id;
+        g.alpha = 1.0;
+        g.beta = 0.0;
+        gd[id] = g;
+      }
+    }
+    const int fb = D & 1;  // buffer holding the final eigenpairs
+    lb.W = dc.Q[1 - fb];
+    {
+      GemmDesc g{};
+      g.A = lb.W;
+      g.lda = N;
+      g.B = lb.W;
+      g.ldb = N;
+      g.transB = 1;
+      g.C = lb.M;
+      g.ldc = N;
+      g.M = N;
+      g.N = N;
+      g.K = N;
+      g.Kdev = lb.sel;
+      g.alpha = 1.0;
+      g.beta = 0.0;
+      gd[nodes.size()] = g;
+    }
+    if (err == cudaSuccess) err = cudaMemcpyAsync(dnodes, nodes.data(), sizeof(DcNode) * nodes.size(), cudaMemcpyHostToDevice, s);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(dp2n, p2n.data(), 4 * p2n.size(), cudaMemcpyHostToDevice, s);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(lb.gdesc, gd.data(), sizeof(GemmDesc) * gd.size(), cudaMemcpyHostToDevice, s);
+    // tridiagonalisation arguments
+    TridiagArgs& ta = lb.ta;
+    ta.M = lb.M;
+    ta.N = N;
+    ta.C = lb.C;
+    ta.smem_cols_doubles = lb.smem_cols;
+    ta.d = lb.d;
+    ta.e = lb.e;
+    ta.tau = lb.tau;
+    ta.V = lb.V;
+    ta.st = st;
+    ta.is = is;
+    ta.check_state = 1;
+    le.blocks.push_back(lb);
+  });
+  le.side = side_p;
+  if (err != cudaSuccess) {
+    msg = cudaGetErrorString(err);
     return 1;
+  }
+  if (le.side) {
+    err = cudaMemsetAsync(le.side, 0, 4 * std::max<size_t>(blk_N.size(), 1), s);
+    if (err != cudaSuccess) {
+      msg = cudaGetErrorString(err);
+      return 1;
+    }
+  }
+  if (!le.blocks.empty()) {
+    err = cudaFuncSetAttribute(k_tridiag, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(k_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, TRD_MAX_DYN_SMEM);
+    if (err != cudaSuccess) {
+      msg = std::string("k_tridiag attributes: ") + cudaGetErrorString(err);
+      return 1;
+    }
   }
   return 0;
 }
-inline void large_eig_launch(LargeEig& le, cudaStream_t s, bool check) {}
-inline int large_eig_launches(const LargeEig& le) { return 0; }
-inline void large_eig_free(LargeEig& le) {}
+
+inline void large_block_tridiag(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool check) {
+  lb.ta.check_state = check;
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(lb.C, 1, 1);
+    cfg.blockDim = dim3(TRD_NT, 1, 1);
+    cfg.dynamicSmemBytes = lb.trd_smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = lb.C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_tridiag, lb.ta);
+  }
+}
+
+inline void large_block_dc(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool check) {
+  const int N = lb.N;
+  lb.dc.check_state = check;
+  cudaMemsetAsync(lb.dc.Q[0], 0, sizeof(double) * N * N, s);
+  cudaMemsetAsync(lb.dc.Q[1], 0, sizeof(double) * N * N, s);
+  k_dc_leaf<<<(lb.nleaves + 127) / 128, 128, 0, s>>>(lb.dc, lb.leaf0, lb.nleaves, 0);
+  const int wblocks = (N * 32 + DC_NT - 1) / DC_NT;
+  for (int h = 1; h <= lb.D; ++h) {
+    const int ob = (h - 1) & 1, nb = h & 1;
+    const int n0 = lb.level_node0[h], nn = lb.level_nn[h], nmax = lb.level_nmax[h];
+    k_dc_prep<<<nn, DC_NT, 0, s>>>(lb.dc, n0, ob);
+    k_dc_secular<<<wblocks, DC_NT, 0, s>>>(lb.dc, h);
+    k_dc_zhat<<<wblocks, DC_NT, 0, s>>>(lb.dc, h);
+    k_dc_vec<<<wblocks, DC_NT, 0, s>>>(lb.dc, h, nb);
+    dim3 gg((nmax + GM_BM - 1) / GM_BM, (nmax + GM_BN - 1) / GM_BN, nn);
+    k_gemm_f64<<<gg, GM_NT, 0, s>>>(lb.gdesc + n0, le.st, le.is, check);
+    k_dc_final<<<nn, DC_NT, 0, s>>>(lb.dc, n0, ob, nb);
+  }
+}
+
+inline void large_block_recon(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool check) {
+  const int N = lb.N;
+  const int fb = lb.D & 1;
+  k_select<<<1, 256, 0, s>>>(lb.dc.lam[fb], lb.sel, le.side, lb.b, N, le.st, le.is, check);
+  k_backtransform<<<(N + BT_NT / 32 - 1) / (BT_NT / 32), BT_NT, 0, s>>>(lb.dc.Q[fb], lb.dc.lam[fb], lb.V, lb.tau,
+                                                                        lb.sel, lb.W, N, le.st, le.is, check);
+  dim3 gr((N + GM_BM - 1) / GM_BM, (N + GM_BN - 1) / GM_BN, 1);
+  k_gemm_f64<<<gr, GM_NT, 0, s>>>(lb.gdesc + lb.recon, le.st, le.is, check);
+}
+
+inline void large_eig_launch(LargeEig& le, cudaStream_t s, bool check) {
+  for (auto& lb : le.blocks) {
+    large_block_tridiag(le, lb, s, check);
+    large_block_dc(le, lb, s, check);
+    large_block_recon(le, lb, s, check);
+  }
+}
+
+inline int large_eig_launches(const LargeEig& le) {
+  int k = 0;
+  for (const auto& lb : le.blocks) k += 1 + 2 + 1 + 6 * lb.D + 3;
+  return k;
+}
+
+inline void large_eig_free(LargeEig& le) { le.blocks.clear(); }

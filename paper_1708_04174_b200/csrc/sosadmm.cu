@@ -20,6 +20,7 @@
 #include "affine.cuh"
 #include "psd_jacobi.cuh"
 #include "psd_large.cuh"
+#include "spdinv.cuh"
 
 namespace {
 
@@ -496,7 +497,22 @@ sosadmm_err sosadmm_setup(const sosadmm_problem* prob, const sosadmm_settings* s
       for (int f = an.lr_ptr[r]; f < an.lr_ptr[r + 1]; ++f)
         K[(size_t)an.lr_idx[e] * tl + an.lr_idx[f]] += an.lr_val[e] * pi * an.lr_val[f];
   }
-  if (!spd_inverse(K, tl)) {
+  bool spd_ok;
+  if (tl <= 256) {
+    spd_ok = spd_inverse(K, tl);
+  } else {  // large t' (weighted SOS, config 3): blocked Cholesky + inverse on the DMMA GEMM
+    CK_CTX(c, cudaMemcpyAsync(d.Kinv, K.data(), sizeof(double) * K.size(), cudaMemcpyHostToDevice, c->stream));
+    const int rc = gpu_spd_inverse(d.Kinv, tl, c->stream);
+    if (rc == 2) {
+      c->err = SOSADMM_E_CUDA;
+      c->msg = "GPU inverse of I + A_low^T P^{-1} A_low failed";
+      return c->err;
+    }
+    spd_ok = rc == 0;
+    CK_CTX(c, cudaMemcpyAsync(K.data(), d.Kinv, sizeof(double) * K.size(), cudaMemcpyDeviceToHost, c->stream));
+    CK_CTX(c, cudaStreamSynchronize(c->stream));
+  }
+  if (!spd_ok) {
     c->err = SOSADMM_E_FACTOR;
     c->msg = "I + A_low^T P^{-1} A_low is not numerically positive definite";
     return c->err;
@@ -603,6 +619,7 @@ sosadmm_err sosadmm_setup(const sosadmm_problem* prob, const sosadmm_settings* s
   a.nblk = an.nblk; a.blk_col = d.blk_col; a.blk_N = d.blk_N; a.blk_mat = d.blk_mat; a.mats = d.mats;
   a.cta_blk = d.cta_blk; a.cta_q0 = d.cta_q0; a.pos_ctas = (int)an.cta_blk.size();
   c->d_tmp = d.tmp;
+  a.side = nullptr;
   JacobiArgs& ja = c->ja;
   ja.mats = d.mats; ja.blk_mat = d.blk_mat; ja.blk_N = d.blk_N; ja.small_blk = d.small_blk;
   ja.st = d.st; ja.is = d.is; ja.check_state = 1;
@@ -619,6 +636,7 @@ sosadmm_err sosadmm_setup(const sosadmm_problem* prob, const sosadmm_settings* s
       return c->err;
     }
   }
+  c->aa.side = c->le.side;
   // host mirror of the structure
   c->row_of.assign(an.n, -2);
   for (int j = an.t; j < an.n; ++j)
@@ -840,3 +858,111 @@ const char* sosadmm_strerror(sosadmm_err e) {
 const char* sosadmm_last_error_message(const sosadmm_ctx* c) { return c ? c->msg.c_str() : "null context"; }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------------------------
+// Stage-level debug entry points (include/sosadmm_debug.h).
+#include "../../include/sosadmm_debug.h"
+
+namespace {
+struct DebugLarge {
+  LargeEig le;
+  DevState* st = nullptr;
+  IterScal* is = nullptr;
+  double* mats = nullptr;
+  char* base = nullptr;
+  cudaStream_t s = nullptr;
+  int init(int N) {
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) return -4;
+    std::vector<int> blk_N{N}, large{0};
+    std::vector<long long> blk_mat{0};
+    const size_t bytes = large_eig_bytes(blk_N, large);
+    if (cudaMalloc(&base, bytes + 1024)) return -7;
+    if (cudaMalloc(&mats, sizeof(double) * N * N)) return -7;
+    if (cudaMalloc(&st, sizeof(DevState))) return -7;
+    if (cudaMalloc(&is, sizeof(IterScal))) return -7;
+    cudaMemset(st, 0, sizeof(DevState));
+    IterScal h{};
+    h.proceed = 1;
+    cudaMemcpy(is, &h, sizeof(h), cudaMemcpyHostToDevice);
+    std::string msg;
+    if (large_eig_init(le, blk_N, blk_mat, large, mats, base, st, is, s, msg)) return -4;
+    return cudaStreamSynchronize(s) ? -4 : 0;
+  }
+  ~DebugLarge() {
+    if (s) cudaStreamSynchronize(s);
+    cudaFree(base);
+    cudaFree(mats);
+    cudaFree(st);
+    cudaFree(is);
+    if (s) cudaStreamDestroy(s);
+  }
+};
+}  // namespace
+
+extern "C" int sosadmm_debug_gemm(int M, int N, int K, const double* A, const double* B, int transB, double* C) {
+  double *dA, *dB, *dC;
+  GemmDesc* dg;
+  if (cudaMalloc(&dA, 8ull * M * std::max(K, 1)) || cudaMalloc(&dB, 8ull * N * std::max(K, 1)) ||
+      cudaMalloc(&dC, 8ull * M * N) || cudaMalloc(&dg, sizeof(GemmDesc)))
+    return -7;
+  cudaMemcpy(dA, A, 8ull * M * K, cudaMemcpyHostToDevice);
+  cudaMemcpy(dB, B, 8ull * N * K, cudaMemcpyHostToDevice);
+  GemmDesc g{};
+  g.A = dA; g.lda = M; g.B = dB; g.ldb = transB ? N : K; g.transB = transB;
+  g.C = dC; g.ldc = M; g.M = M; g.N = N; g.K = K; g.alpha = 1.0; g.beta = 0.0;
+  cudaMemcpy(dg, &g, sizeof(g), cudaMemcpyHostToDevice);
+  dim3 gr((M + GM_BM - 1) / GM_BM, (N + GM_BN - 1) / GM_BN, 1);
+  k_gemm_f64<<<gr, GM_NT>>>(dg, nullptr, nullptr, 0);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) cudaMemcpy(C, dC, 8ull * M * N, cudaMemcpyDeviceToHost);
+  cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(dg);
+  return e == cudaSuccess ? 0 : -4;
+}
+
+extern "C" int sosadmm_debug_tridiag(int N, const double* A, double* d, double* e, double* tau, double* V) {
+  if (N < 3) return -1;
+  DebugLarge dl;
+  int rc = dl.init(N);
+  if (rc) return rc;
+  LargeBlock& lb = dl.le.blocks[0];
+  cudaMemcpyAsync(lb.M, A, 8ull * N * N, cudaMemcpyHostToDevice, dl.s);
+  cudaMemsetAsync(lb.V, 0, 8ull * N * N, dl.s);
+  large_block_tridiag(dl.le, lb, dl.s, false);
+  cudaError_t err = cudaStreamSynchronize(dl.s);
+  if (err != cudaSuccess) return -4;
+  cudaMemcpy(d, lb.d, 8ull * N, cudaMemcpyDeviceToHost);
+  cudaMemcpy(e, lb.e, 8ull * (N - 1), cudaMemcpyDeviceToHost);
+  cudaMemcpy(tau, lb.tau, 8ull * (N - 1), cudaMemcpyDeviceToHost);
+  cudaMemcpy(V, lb.V, 8ull * N * N, cudaMemcpyDeviceToHost);
+  return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
+extern "C" int sosadmm_debug_stedc(int N, const double* d, const double* e, double* lam, double* Z) {
+  if (N < 2) return -1;
+  DebugLarge dl;
+  int rc = dl.init(N);
+  if (rc) return rc;
+  LargeBlock& lb = dl.le.blocks[0];
+  cudaMemcpyAsync(lb.d, d, 8ull * N, cudaMemcpyHostToDevice, dl.s);
+  cudaMemcpyAsync(lb.e, e, 8ull * (N - 1), cudaMemcpyHostToDevice, dl.s);
+  large_block_dc(dl.le, lb, dl.s, false);
+  cudaError_t err = cudaStreamSynchronize(dl.s);
+  if (err != cudaSuccess) return -4;
+  const int fb = lb.D & 1;
+  cudaMemcpy(lam, lb.dc.lam[fb], 8ull * N, cudaMemcpyDeviceToHost);
+  cudaMemcpy(Z, lb.dc.Q[fb], 8ull * N * N, cudaMemcpyDeviceToHost);
+  return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
+extern "C" int sosadmm_debug_spdinv(int t, double* K) {
+  double* dK;
+  cudaStream_t s;
+  if (cudaStreamCreate(&s)) return -4;
+  if (cudaMalloc(&dK, 8ull * t * t)) return -7;
+  cudaMemcpy(dK, K, 8ull * t * t, cudaMemcpyHostToDevice);
+  const int rc = gpu_spd_inverse(dK, t, s);
+  cudaMemcpy(K, dK, 8ull * t * t, cudaMemcpyDeviceToHost);
+  cudaFree(dK);
+  cudaStreamDestroy(s);
+  return rc == 0 ? 0 : (rc == 1 ? -3 : -4);
+}

@@ -1,0 +1,120 @@
+"""GPU unit tests of the large-block PSD-projection stages (include/sosadmm_debug.h) against plain
+numpy / LAPACK definitions: the DMMA GEMM, the cluster Householder tridiagonalisation (checked
+through the similarity H T H^T = A it defines) and the divide-and-conquer tridiagonal
+eigensolver (eigenvalues vs LAPACK, residual and orthogonality of the eigenvectors)."""
+import ctypes
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+pytestmark = pytest.mark.gpu
+
+P = ctypes.POINTER(ctypes.c_double)
+
+
+def lib():
+    from paper_1708_04174_b200 import load_library
+
+    L = load_library()
+    L.sosadmm_debug_gemm.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, ctypes.c_int, P]
+    L.sosadmm_debug_tridiag.argtypes = [ctypes.c_int, P, P, P, P, P]
+    L.sosadmm_debug_stedc.argtypes = [ctypes.c_int, P, P, P, P]
+    L.sosadmm_debug_spdinv.argtypes = [ctypes.c_int, P]
+    return L
+
+
+def dp(a):
+    return a.ctypes.data_as(P)
+
+
+@pytest.mark.parametrize("M,N,K,tb", [(64, 64, 16, 0), (100, 37, 53, 0), (861, 861, 40, 1), (7, 130, 300, 1),
+                                      (300, 5, 1, 0), (33, 33, 0, 0)])
+def test_dmma_gemm(M, N, K, tb):
+    rng = np.random.default_rng(M + N + K)
+    A = np.asfortranarray(rng.standard_normal((M, K)))
+    B = np.asfortranarray(rng.standard_normal((N, K) if tb else (K, N)))
+    C = np.zeros((M, N), order="F")
+    assert lib().sosadmm_debug_gemm(M, N, K, dp(A), dp(B), tb, dp(C)) == 0
+    ref = A @ (B.T if tb else B)
+    if K == 0:
+        assert not C.any()
+        return
+    assert np.max(np.abs(C - ref)) <= 1e-14 * max(1, K) * (np.abs(A).max() * np.abs(B).max())
+
+
+def _householder_Q(V, tau, N):
+    Q = np.eye(N)
+    for k in range(N - 2):
+        v = V[:, k].copy()
+        v[:k + 1] = 0.0
+        Q = Q @ (np.eye(N) - tau[k] * np.outer(v, v))
+    return Q
+
+
+@pytest.mark.parametrize("N", [65, 100, 231, 285, 325, 861])
+def test_tridiag(N):
+    rng = np.random.default_rng(N)
+    G = rng.standard_normal((N, N))
+    A = np.asfortranarray(G + G.T)
+    d, e, tau = np.zeros(N), np.zeros(N - 1), np.zeros(N - 1)
+    V = np.zeros((N, N), order="F")
+    assert lib().sosadmm_debug_tridiag(N, dp(A), dp(d), dp(e), dp(tau), dp(V)) == 0
+    T = np.diag(d) + np.diag(e, 1) + np.diag(e, -1)
+    lam_T = sla.eigh_tridiagonal(d, e, eigvals_only=True)
+    lam_A = np.linalg.eigvalsh(A)
+    assert np.max(np.abs(lam_T - lam_A)) <= 1e-12 * np.abs(lam_A).max() * np.sqrt(N)
+    if N <= 325:
+        Q = _householder_Q(V, tau, N)
+        assert np.linalg.norm(Q @ T @ Q.T - A) <= 1e-13 * np.linalg.norm(A) * np.sqrt(N)
+
+
+def _stedc(d, e):
+    N = len(d)
+    lam = np.zeros(N)
+    Z = np.zeros((N, N), order="F")
+    assert lib().sosadmm_debug_stedc(N, dp(np.ascontiguousarray(d)), dp(np.ascontiguousarray(e)), dp(lam), dp(Z)) == 0
+    return lam, Z
+
+
+@pytest.mark.parametrize("N,kind", [(2, "rand"), (3, "rand"), (17, "rand"), (65, "rand"), (231, "rand"),
+                                    (861, "rand"), (300, "glued"), (200, "zero_e"), (129, "equal_d"),
+                                    (500, "wilkinson"), (861, "clustered")])
+def test_stedc(N, kind):
+    rng = np.random.default_rng(N + len(kind))
+    if kind == "rand":
+        d, e = rng.standard_normal(N), rng.standard_normal(N - 1)
+    elif kind == "glued":  # nearly decoupled blocks: tiny couplings
+        d, e = rng.standard_normal(N), rng.standard_normal(N - 1)
+        e[::25] = 1e-14
+    elif kind == "zero_e":
+        d, e = rng.standard_normal(N), rng.standard_normal(N - 1)
+        e[::7] = 0.0
+    elif kind == "equal_d":
+        d, e = np.ones(N), 1e-3 * rng.standard_normal(N - 1)
+    elif kind == "wilkinson":
+        m = (N - 1) / 2
+        d, e = np.abs(np.arange(N) - m), np.ones(N - 1)
+    else:  # a low-rank-plus-noise spectrum tridiagonalised (many eigenvalues near 0)
+        G = rng.standard_normal((N, 5))
+        X = G @ G.T + 1e-12 * np.diag(rng.standard_normal(N))
+        Tm = sla.hessenberg(X)
+        d, e = np.diag(Tm).copy(), np.diag(Tm, 1).copy()
+    lam, Z = _stedc(d, e)
+    T = np.diag(d) + np.diag(e, 1) + np.diag(e, -1)
+    ref = sla.eigh_tridiagonal(d, e, eigvals_only=True)
+    nrm = max(np.abs(ref).max(), 1e-300)
+    assert np.all(np.diff(lam) >= 0)
+    assert np.max(np.abs(lam - ref)) <= 1e-13 * nrm * np.sqrt(N)
+    assert np.linalg.norm(T @ Z - Z * lam) <= 1e-13 * nrm * N
+    assert np.linalg.norm(Z.T @ Z - np.eye(N)) <= 1e-13 * N
+
+
+@pytest.mark.parametrize("t", [65, 130, 300, 1000, 2001])
+def test_spd_inverse(t):
+    rng = np.random.default_rng(t)
+    G = rng.standard_normal((t, 3 * t // 2)) / np.sqrt(t)
+    K = np.asfortranarray(np.eye(t) + G @ G.T)
+    X = K.copy(order="F")
+    assert lib().sosadmm_debug_spdinv(t, dp(X)) == 0
+    assert np.linalg.norm(X @ K - np.eye(t)) <= 1e-12 * np.sqrt(t) * np.linalg.cond(K)
