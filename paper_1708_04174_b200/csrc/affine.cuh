@@ -4,8 +4,15 @@
 // (sigma_1 elimination: (I + A A^T) sigma_2 = w2 - A w1), P:469-480 (Woodbury with P = I + D
 // diagonal, D = A_orth A_orth^T, Proposition 1) and the Appendix op list P:870-877.
 //
+// Elimination order (reading C15): the linear system is solved as
+//   q = M^{-1} w_12 (partial orthogonality + Woodbury, with r = w_12),
+//   u_hat_3 = (w3 + zeta^T q) / (1 + zeta^T h),   u_hat_12 = q - u_hat_3 h,   h = M^{-1} zeta cached,
+// which is E:MatrixInverse / E:MatrixInverseResult reassociated: rows 1-2 of (I+Q)u = w
+// read M u_12 + zeta u_3 = w_12 and row 3 reads u_3 - zeta^T u_12 = w3.  It avoids subtracting two
+// vectors ~1/tau larger than the result (p - coef h) when tau << 1.
+//
 // Data flow per iteration:
-//   k_gather   (rows)     : g = A r1, x = P^{-1}(r2 - g), partial b^T x; residual partials of u^k
+//   k_gather   (rows)     : g = A w1, x = P^{-1}(w2 - g), partial b^T x; residual partials of u^k
 //   k_lowT     (t' cols)  : y_t = A_low^T x, A_low^T y
 //   k_kinv     (t' rows)  : z_t = K^{-1} y_t         (K = I + A_low^T P^{-1} A_low)
 //   k_tphase   (1 CTA)    : residuals/termination of u^k (reading C9); coef, u_hat_low, u_hat_3,
@@ -86,11 +93,12 @@ constexpr int POS_PER_CTA = 1024;
 //   x_alpha  = (y_alpha + s_alpha + b_alpha w3 - g_alpha) / P_alpha
 // and, for the residuals of u^k (reading C9), (A xi)_alpha and sum_{j in seg(alpha)} (A^T y + z)_j^2.
 __global__ void __launch_bounds__(GATHER_NT) k_gather(AffineArgs a) {
-  __shared__ double sh[GATHER_NT / 32];
+  __shared__ double sh[2 * (GATHER_NT / 32)];
   if (a.st->done) return;
-  const double tau = a.st->tau, w3 = tau + a.st->kappa;
+  const double tau = a.st->tau;
   const int r = blockIdx.x * GATHER_NT + threadIdx.x;
-  double p_bx = 0, p_pres = 0, p_axi = 0, p_dres = 0, p_by = 0;
+  double p_pres = 0, p_axi = 0, p_dres = 0, p_by = 0;
+  dd bxd{0.0, 0.0};
   if (r < a.m) {
     const double yr = a.y[r];
     double gx = 0.0, gz = 0.0, dres = 0.0;
@@ -111,25 +119,28 @@ __global__ void __launch_bounds__(GATHER_NT) k_gather(AffineArgs a) {
       const int j = a.low_col[jl];
       const double v = a.lr_val[e];
       const double xj = a.xi[j];
-      const double r1 = (xj + a.z[j]) - a.c_low[jl] * w3;
+      const double r1 = xj + a.z[j];  // w1 on the low columns (q = M^{-1} w_12, reading C15)
       gl = fma(v, r1, gl);
       axl = fma(v, xj, axl);
     }
     const double g = (gx + gz) + gl;
-    const double r2 = (yr + a.s[r]) + a.b[r] * w3;
+    const double r2 = yr + a.s[r];  // w2
     const double xr = (r2 - g) * a.Pinv[r];
     a.x[r] = xr;
     const double axi = gx + axl;
     const double pr = axi - a.b[r] * tau;
-    p_bx = a.b[r] * xr;
+    bxd = dd_prod(a.b[r], xr);
     p_pres = pr * pr;
     p_axi = axi * axi;
     p_dres = dres;
     p_by = a.b[r] * yr;
   }
   double v;
-  v = block_sum<GATHER_NT>(p_bx, sh);
-  if (threadIdx.x == 0) a.part[PART_BX * a.gather_blocks + blockIdx.x] = v;
+  const dd bxs = dd_block_sum<GATHER_NT>(bxd, sh);
+  if (threadIdx.x == 0) {
+    a.part[PART_BX * a.gather_blocks + blockIdx.x] = bxs.hi;
+    a.part[PART_BXLO * a.gather_blocks + blockIdx.x] = bxs.lo;
+  }
   v = block_sum<GATHER_NT>(p_pres, sh);
   if (threadIdx.x == 0) a.part[PART_PRES * a.gather_blocks + blockIdx.x] = v;
   v = block_sum<GATHER_NT>(p_axi, sh);
@@ -177,19 +188,29 @@ __global__ void __launch_bounds__(256) k_kinv(AffineArgs a) {
 // 2 = affine-only (unit entry point: no termination logic, no writes to xi/z).
 constexpr int TP_NT = 512;
 __global__ void __launch_bounds__(TP_NT) k_tphase(AffineArgs a, int mode) {
-  __shared__ double sh[TP_NT / 32];
-  __shared__ double bc[8];
+  __shared__ double sh[2 * (TP_NT / 32)];
+  __shared__ double bc[10];
   DevState* st = a.st;
   if (st->done) return;
   const int tid = threadIdx.x;
-  // 1. fixed-order reductions of the gather partials
+  // 1. fixed-order reductions of the gather partials (b^T x in double-double)
   double sums[NPART];
-#pragma unroll
   for (int k = 0; k < NPART; ++k) {
+    if (k == PART_BX || k == PART_BXLO) continue;
     double v = 0.0;
     for (int i = tid; i < a.gather_blocks; i += TP_NT) v += a.part[k * a.gather_blocks + i];
     v = block_sum<TP_NT>(v, sh);
     if (tid == 0) bc[k] = v;
+  }
+  {
+    dd v{0.0, 0.0};
+    for (int i = tid; i < a.gather_blocks; i += TP_NT)
+      v = dd_add(v, dd{a.part[PART_BX * a.gather_blocks + i], a.part[PART_BXLO * a.gather_blocks + i]});
+    v = dd_block_sum<TP_NT>(v, sh);
+    if (tid == 0) {
+      bc[PART_BX] = v.hi;
+      bc[PART_BXLO] = v.lo;
+    }
   }
   // low / free columns: c^T xi, dual residual of low columns, (A_low xi part already in gather)
   const double tau = st->tau, kappa = st->kappa, w3 = tau + kappa;
@@ -209,16 +230,16 @@ __global__ void __launch_bounds__(TP_NT) k_tphase(AffineArgs a, int mode) {
     dl0 = fma(zj, zj, dl0);
   }
   cx = block_sum<TP_NT>(cx, sh);
-  if (tid == 0) bc[5] = cx;
+  if (tid == 0) bc[7] = cx;
   dl = block_sum<TP_NT>(dl, sh);
-  if (tid == 0) bc[6] = dl;
+  if (tid == 0) bc[8] = dl;
   dl0 = block_sum<TP_NT>(dl0, sh);
-  if (tid == 0) bc[7] = dl0;
+  if (tid == 0) bc[9] = dl0;
   __syncthreads();
   for (int k = 0; k < NPART; ++k) sums[k] = bc[k];
-  cx = bc[5];
-  dl = bc[6];
-  dl0 = bc[7];
+  cx = bc[7];
+  dl = bc[8];
+  dl0 = bc[9];
 
   // 2. residuals of u^k and the termination rule (reading C9)
   if (mode != 2 && tid == 0) {
@@ -266,46 +287,40 @@ __global__ void __launch_bounds__(TP_NT) k_tphase(AffineArgs a, int mode) {
   if (mode == 1) return;
   if (!a.is->proceed) return;
 
-  // 3. rank-one HSDE correction and tau-elimination
-  //    p1_low = r1_low + A_low^T sigma_2 = r1_low + z_t;  b^T sigma_2 = b^T x - beta_low^T z_t
-  double bz = 0.0, cp = 0.0;
+  // 3. tau elimination by the Schur complement on u_hat_3 (reading C15):
+  //    q_low = w1_low + A_low^T sigma_2 = w1_low + z_t;  b^T q_2 = b^T x - beta_low^T z_t
+  //    u_hat_3 = (w3 + c^T q_1 - b^T q_2) / (1 + zeta^T h);  u_hat_12 = q - u_hat_3 h
+  dd bz{0.0, 0.0}, cq{0.0, 0.0};
   for (int j = tid; j < a.tl; j += TP_NT) {
     const int col = a.low_col[j];
-    const double cj = a.c_low[j];
-    const double p1 = ((a.xi[col] + a.z[col]) - cj * w3) + a.zt[j];
-    a.ulow[j] = p1;  // temporarily p1_low
-    bz = fma(a.beta_low[j], a.zt[j], bz);
-    cp = fma(cj, p1, cp);
+    const double q1 = (a.xi[col] + a.z[col]) + a.zt[j];
+    a.ulow[j] = q1;  // temporarily q_low
+    bz = dd_add(bz, dd_prod(a.beta_low[j], a.zt[j]));
+    cq = dd_add(cq, dd_prod(a.c_low[j], q1));
   }
-  bz = block_sum<TP_NT>(bz, sh);
-  if (tid == 0) bc[0] = bz;
-  cp = block_sum<TP_NT>(cp, sh);
-  if (tid == 0) bc[1] = cp;
-  __syncthreads();
-  const double bsig2 = sums[PART_BX] - bc[0];
-  const double zp = bc[1] - bsig2;            // zeta^T p = c^T p1 - b^T p2
-  const double coef = zp / a.denom;           // (M^{-1}zeta)zeta^T / (1 + zeta^T M^{-1} zeta)
-  double cu = 0.0;
-  for (int j = tid; j < a.tl; j += TP_NT) {
-    const double u = a.ulow[j] - coef * a.h1_low[j];
-    a.ulow[j] = u;
-    cu = fma(a.c_low[j], u, cu);
-  }
-  cu = block_sum<TP_NT>(cu, sh);
+  bz = dd_block_sum<TP_NT>(bz, sh);
   if (tid == 0) {
-    // E:FirstBlockElimination u_hat_3 = w3 + c^T u_hat_1 - b^T u_hat_2 = w3 + zeta^T u_hat_12, and
-    // zeta^T u_hat_12 = zeta^T p - coef zeta^T h = zeta^T p (1 - (denom - 1)/denom) = coef exactly.
-    // This form avoids the O(|b||sigma_2|) cancellation of the dot products (reading C15).
-    const double u3 = w3 + coef;
-    (void)cu;
+    bc[0] = bz.hi;
+    bc[1] = bz.lo;
+  }
+  cq = dd_block_sum<TP_NT>(cq, sh);
+  if (tid == 0) {
+    // zeta^T q = c^T q_1 - b^T q_2 = cq - (bx - bz), all in double-double
+    dd bq2 = dd_add(dd{sums[PART_BX], sums[PART_BXLO]}, dd{-bc[0], -bc[1]});
+    dd zq = dd_add(cq, dd{-bq2.hi, -bq2.lo});
+    dd num = dd_add(dd{w3, 0.0}, zq);
+    const double u3 = (num.hi + num.lo) / a.denom;
     a.is->omega3 = w3;
-    a.is->coef = coef;
+    a.is->coef = u3;
     a.is->u3 = u3;
-    a.is->bsig2 = bsig2;
+    a.is->bsig2 = bq2.hi;
     const double tn = fmax(0.0, u3 - kappa);  // P_{R+}
     a.is->tau_new = tn;
     a.is->kappa_new = kappa - u3 + tn;
   }
+  __syncthreads();
+  const double u3 = a.is->u3;
+  for (int j = tid; j < a.tl; j += TP_NT) a.ulow[j] = a.ulow[j] - u3 * a.h1_low[j];
   __syncthreads();
   if (mode == 2) return;
   // 4. free columns: cone R^t -> identity; xi = u_hat - z, z = z - u_hat + xi
@@ -321,7 +336,7 @@ __global__ void __launch_bounds__(TP_NT) k_tphase(AffineArgs a, int mode) {
   }
 }
 
-// k_rowupdate: sigma_2 = x - P^{-1} A_low z_t; u_hat_2 = sigma_2 - coef h_2;
+// k_rowupdate: sigma_2 = q_2 = x - P^{-1} A_low z_t; u_hat_2 = q_2 - u_hat_3 h_2;
 // y = u_hat_2 - s (R^m cone: identity); s = s - u_hat_2 + y.
 __global__ void __launch_bounds__(256) k_rowupdate(AffineArgs a, int write_state) {
   if (a.st->done || !a.is->proceed) return;

@@ -21,15 +21,15 @@ struct DevState {
 // Per-iteration scratch scalars written by the t-phase kernel.
 struct IterScal {
   double omega3;   // tau + kappa
-  double coef;     // zeta^T p / (1 + zeta^T h)   (E:MatrixInverseResult)
-  double u3;       // u_hat_3 (E:FirstBlockElimination)
+  double coef;     // multiplier of h in u_hat_12 = q - coef h; equals u_hat_3 (reading C15)
+  double u3;       // u_hat_3 = (w3 + zeta^T q) / (1 + zeta^T h)
   double tau_new, kappa_new;
   double bsig2;    // b^T sigma_2
   int proceed;     // 1 if this iteration continues past the t-phase
 };
 
 // Number of per-CTA partial sums the gather kernel produces.
-enum { PART_BX = 0, PART_PRES, PART_AXI, PART_DRES, PART_BY, NPART };
+enum { PART_BX = 0, PART_PRES, PART_AXI, PART_DRES, PART_BY, PART_BXLO, NPART };
 
 template <int NT>
 __device__ __forceinline__ double block_sum(double v, double* sh) {
@@ -67,4 +67,48 @@ __device__ __forceinline__ void svec_ij(long long q, int& i, int& j) {
   while ((jj + 1) * (jj + 2) / 2 <= q) ++jj;
   j = (int)jj;
   i = (int)(q - jj * (jj + 1) / 2);
+}
+
+// ---- double-double helpers (error-free transformations) for the few dot products whose
+// accuracy decides u_hat_3 (reading C15) ----
+struct dd {
+  double hi, lo;
+};
+__device__ __forceinline__ dd dd_two_sum(double a, double b) {
+  const double s = a + b;
+  const double bb = s - a;
+  return dd{s, (a - (s - bb)) + (b - bb)};
+}
+__device__ __forceinline__ dd dd_add(dd a, dd b) {
+  dd s = dd_two_sum(a.hi, b.hi);
+  const double e = s.lo + a.lo + b.lo;
+  const double hi = s.hi + e;
+  return dd{hi, e - (hi - s.hi)};
+}
+__device__ __forceinline__ dd dd_prod(double a, double b) {
+  const double p = a * b;
+  return dd{p, fma(a, b, -p)};
+}
+__device__ __forceinline__ dd dd_warp_sum(dd v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dd w{__shfl_xor_sync(0xffffffffu, v.hi, o), __shfl_xor_sync(0xffffffffu, v.lo, o)};
+    v = dd_add(v, w);
+  }
+  return v;
+}
+template <int NT>
+__device__ __forceinline__ dd dd_block_sum(dd v, double* sh) {  // sh: 2 * NT/32 doubles
+  v = dd_warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) {
+    sh[2 * w] = v.hi;
+    sh[2 * w + 1] = v.lo;
+  }
+  __syncthreads();
+  dd r{0.0, 0.0};
+  if (threadIdx.x == 0)
+    for (int i = 0; i < NT / 32; ++i) r = dd_add(r, dd{sh[2 * i], sh[2 * i + 1]});
+  return r;  // valid in thread 0
 }

@@ -552,14 +552,16 @@ sosadmm_err sosadmm_setup(const sosadmm_problem* prob, const sosadmm_settings* s
       h1_low[j] = c_low[j] + s;
     }
   }
-  double ch = 0.0, bh = 0.0, nb = 0.0, nc = 0.0;
-  for (int j = 0; j < tl; ++j) ch += c_low[j] * h1_low[j];
+  // 1 + zeta^T M^{-1} zeta, accumulated in extended precision (it divides u_hat_3, reading C15)
+  long double ch = 0.0L, bhl = 0.0L, nbl = 0.0L, ncl = 0.0L;
+  for (int j = 0; j < tl; ++j) ch += (long double)c_low[j] * h1_low[j];
   for (int r = 0; r < m; ++r) {
-    bh += an.b[r] * h2[r];
-    nb += an.b[r] * an.b[r];
+    bhl += (long double)an.b[r] * h2[r];
+    nbl += (long double)an.b[r] * an.b[r];
   }
-  for (int j = 0; j < an.n; ++j) nc += an.c[j] * an.c[j];
-  const double denom = 1.0 + ch - bh;  // 1 + zeta^T M^{-1} zeta
+  for (int j = 0; j < an.n; ++j) ncl += (long double)an.c[j] * an.c[j];
+  const double denom = (double)(1.0L + ch - bhl);
+  const double bh = (double)bhl, nb = (double)nbl, nc = (double)ncl;
 
   // ---- upload -----------------------------------------------------------------------------
   cudaStream_t s = c->stream;
