@@ -1,0 +1,7 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+timeout 600 python bench.py --steps 20 --warmup 5 --no-ttt > gpurun_out/bench_nottt.log 2>&1; echo bench=$?
+timeout 900 python bench.py --steps 20 --warmup 5 --no-cpu > gpurun_out/bench_ttt.log 2>&1; echo bench2=$?
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-ttt --no-cpu > gpurun_out/ncu.log 2>&1; echo ncu=$?
