@@ -9,8 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsosadmm.so")
 SOURCES = ["sosadmm.cu"]
-HEADERS = ["common.cuh", "affine.cuh", "psd_jacobi.cuh", "psd_large.cuh", "gemm_f64.cuh", "tridiag.cuh",
-           "dc.cuh"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith(".cuh"))
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
 

@@ -3,7 +3,8 @@
 //   a  --(k_tridiag, one cluster)-->  T = H^T a H, reflectors V, tau
 //      --(divide and conquer, dc.cuh)-->  T = Z diag(lambda) Z^T
 //      --(k_select)-->  the spectral side with fewer eigenpairs: r = min(#lambda>0, #lambda<0)
-//      --(k_backtransform)-->  W = H Z_side diag(sqrt|lambda_side|)   (only r columns)
+//      --(k_bt_larft, k_bt_apply: compact-WY blocks on DMMA)-->  W = H Z_side diag(sqrt|lambda_side|)
+//                                                              (only r columns)
 //      --(k_gemm_f64, DMMA)-->  M = W W^T
 // M is Pi_{S+}(a) when the positive side was chosen, and Pi_{S+}(-a) = Pi_{S+}(a) - a (Moreau)
 // when the negative side was; k_pack reads the per-block side flag.  Picking the smaller side
@@ -17,6 +18,7 @@
 #include "dc.cuh"
 #include "gemm_f64.cuh"
 #include "tridiag.cuh"
+#include "backtransform.cuh"
 
 struct LargeBlock {
   int b = 0, N = 0, C = 1, D = 0;
@@ -30,6 +32,8 @@ struct LargeBlock {
   GemmDesc* gdesc = nullptr;  // per level (node-indexed), then the reconstruction descriptor
   std::vector<int> gdesc_off;
   int* sel = nullptr;         // [r, c0, side]
+  double* Twy = nullptr;      // compact-WY T factors of the reflector blocks (backtransform.cuh)
+  double* Gwy = nullptr;      // their Gram partials per row chunk
   int recon = 0;              // index of the reconstruction descriptor in gdesc
   double* W = nullptr;
   TridiagArgs ta{};
@@ -70,34 +74,6 @@ __global__ void k_select(const double* lam, int* sel, int* side, int b, int N, c
     }
     side[b] = sel[2];
   }
-}
-
-// W[:, c] = H Z[:, c0 + c] * sqrt(|lambda|), one warp per column; H = H_0 H_1 ... H_{N-3} applied
-// right to left (LAPACK dormtr, 'L', 'N').
-constexpr int BT_NT = 512;
-__global__ void __launch_bounds__(BT_NT) k_backtransform(const double* Qf, const double* lamf, const double* V,
-                                                         const double* tau, const int* sel, double* W, int N,
-                                                         const DevState* st, const IterScal* is, int check_state) {
-  if (check_state && (st->done || !is->proceed)) return;
-  const int r = sel[0], c0 = sel[1];
-  const int c = blockIdx.x * (BT_NT / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (c >= r) return;
-  const double* z = Qf + (size_t)(c0 + c) * N;
-  double* w = W + (size_t)c * N;
-  for (int i = lane; i < N; i += 32) w[i] = z[i];
-  __syncwarp();
-  for (int k = N - 3; k >= 0; --k) {
-    const double tk = tau[k];
-    if (tk == 0.0) continue;
-    const double* v = V + (size_t)k * N;
-    double sacc = 0.0;
-    for (int i = k + 1 + lane; i < N; i += 32) sacc = fma(v[i], w[i], sacc);
-    sacc = warp_sum(sacc) * tk;
-    for (int i = k + 1 + lane; i < N; i += 32) w[i] = fma(-sacc, v[i], w[i]);
-    __syncwarp();
-  }
-  const double sc = sqrt(fabs(lamf[c0 + c]));
-  for (int i = lane; i < N; i += 32) w[i] *= sc;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -146,17 +122,17 @@ inline void dc_build_tree(int N, std::vector<DcNode>& nodes, std::vector<int>& l
   }
 }
 
-constexpr int TRD_MAX_DYN_SMEM = 227 * 1024 - 2048;  // leaves room for the static colp table
+constexpr int TRD_MAX_DYN_SMEM = 227 * 1024 - 1024;  // leaves room for the static tables
 
 inline int tridiag_cluster_size(int N) { return N > 512 ? 16 : (N > 160 ? 8 : 4); }
 
-// Shared-memory budget for the distributed trailing matrix (per CTA).
-inline long long tridiag_col_budget(int N, int C) {
-  const long long cap = TRD_MAX_DYN_SMEM / 8 - (3LL * N + (N + C - 1) / C + 1 + 2 + 32) - 8;
+// Shared-memory budget (doubles) for the row storage of the distributed lower triangle (per CTA).
+inline long long tridiag_row_budget(int N, int C) {
+  const long long cap = TRD_MAX_DYN_SMEM / 8 - trd_fixed_doubles(N, C);
   long long need = 0;
   for (int c = 0; c < C; ++c) {
     long long s = 0;
-    for (int j = c; j < N; j += C) s += N - j;
+    for (int i = c; i < N; i += C) s += i + 1;
     need = std::max(need, s);
   }
   return std::min(cap, need);
@@ -204,6 +180,8 @@ inline size_t large_carve(const std::vector<int>& blk_N, const std::vector<int>&
     p[q++] = take(4 * nodes.size());      // rot_cnt
     p[q++] = take(sizeof(GemmDesc) * (nodes.size() + 1));
     p[q++] = take(4 * 4);                 // sel
+    p[q++] = take(8 * (size_t)BTW_NB * BTW_NB * ((N - 2 + BTW_NB - 1) / BTW_NB));  // Twy
+    p[q++] = take(8 * (size_t)BTW_NB * BTW_NB * ((N - 2 + BTW_NB - 1) / BTW_NB) * bt_gram_chunks(N));  // Gwy
     per_block(b, N, p, nodes, l0, lnn, lmax, D, leaf0, nleaves, p2n);
   }
   return used + 256;
@@ -230,7 +208,7 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     lb.N = N;
     lb.M = mats + blk_mat[b];
     lb.C = tridiag_cluster_size(N);
-    lb.smem_cols = tridiag_col_budget(N, lb.C);
+    lb.smem_cols = tridiag_row_budget(N, lb.C);
     lb.trd_smem = tridiag_smem_bytes(N, lb.C, lb.smem_cols);
     int q = 0;
     lb.d = (double*)p[q++];
@@ -272,6 +250,8 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     dc.check_state = 1;
     lb.gdesc = (GemmDesc*)p[q++];
     lb.sel = (int*)p[q++];
+    lb.Twy = (double*)p[q++];
+    lb.Gwy = (double*)p[q++];
     lb.recon = (int)nodes.size();
     lb.D = D;
     lb.level_node0 = l0;
@@ -332,7 +312,7 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     ta.M = lb.M;
     ta.N = N;
     ta.C = lb.C;
-    ta.smem_cols_doubles = lb.smem_cols;
+    ta.smem_rows_doubles = lb.smem_cols;
     ta.d = lb.d;
     ta.e = lb.e;
     ta.tau = lb.tau;
@@ -340,6 +320,7 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     ta.st = st;
     ta.is = is;
     ta.check_state = 1;
+    ta.prof = nullptr;
     le.blocks.push_back(lb);
   });
   le.side = side_p;
@@ -355,9 +336,14 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     }
   }
   if (!le.blocks.empty()) {
-    err = cudaFuncSetAttribute(k_tridiag, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    for (TridiagKernel kt : {k_tridiag<2>, k_tridiag<4>, k_tridiag<7>, k_tridiag<10>}) {
+      if (err == cudaSuccess) err = cudaFuncSetAttribute(kt, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (err == cudaSuccess)
+        err = cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, TRD_MAX_DYN_SMEM);
+    }
     if (err == cudaSuccess)
-      err = cudaFuncSetAttribute(k_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, TRD_MAX_DYN_SMEM);
+      err = cudaFuncSetAttribute(k_bt_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)bt_apply_smem_bytes(DC_MAXN));
     if (err != cudaSuccess) {
       msg = std::string("k_tridiag attributes: ") + cudaGetErrorString(err);
       return 1;
@@ -381,7 +367,7 @@ inline void large_block_tridiag(LargeEig& le, LargeBlock& lb, cudaStream_t s, bo
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_tridiag, lb.ta);
+    cudaLaunchKernelEx(&cfg, tridiag_kernel(lb.N), lb.ta);
   }
 }
 
@@ -408,9 +394,28 @@ inline void large_block_dc(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool ch
 inline void large_block_recon(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool check) {
   const int N = lb.N;
   const int fb = lb.D & 1;
+  const int nref = N - 2;
   k_select<<<1, 256, 0, s>>>(lb.dc.lam[fb], lb.sel, le.side, lb.b, N, le.st, le.is, check);
-  k_backtransform<<<(N + BT_NT / 32 - 1) / (BT_NT / 32), BT_NT, 0, s>>>(lb.dc.Q[fb], lb.dc.lam[fb], lb.V, lb.tau,
-                                                                        lb.sel, lb.W, N, le.st, le.is, check);
+  const int nbw = (nref + BTW_NB - 1) / BTW_NB;
+  k_bt_gram<<<dim3(nbw, bt_gram_chunks(N)), BTW_NT, 0, s>>>(lb.V, lb.Gwy, N, nref, le.st, le.is, check);
+  k_bt_larft<<<nbw, BTW_NT, 0, s>>>(lb.Gwy, bt_gram_chunks(N), lb.tau, lb.Twy, nref, le.st, le.is, check);
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(BTC_P * ((N / 2 + BTW_NC - 1) / BTW_NC), 1, 1);
+    cfg.blockDim = dim3(BTC_NT, 1, 1);
+    cfg.dynamicSmemBytes = bt_apply_smem_bytes(N);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = BTC_P;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_bt_apply, (const double*)lb.dc.Q[fb], (const double*)lb.dc.lam[fb],
+                       (const double*)lb.V, (const double*)lb.Twy, (const int*)lb.sel, lb.W, N, nref, le.st,
+                       le.is, (int)check);
+  }
   dim3 gr((N + GM_BM - 1) / GM_BM, (N + GM_BN - 1) / GM_BN, 1);
   k_gemm_f64<<<gr, GM_NT, 0, s>>>(lb.gdesc + lb.recon, le.st, le.is, check);
 }
@@ -425,7 +430,7 @@ inline void large_eig_launch(LargeEig& le, cudaStream_t s, bool check) {
 
 inline int large_eig_launches(const LargeEig& le) {
   int k = 0;
-  for (const auto& lb : le.blocks) k += 1 + 2 + 1 + 6 * lb.D + 3;
+  for (const auto& lb : le.blocks) k += 1 + 2 + 1 + 6 * lb.D + 5;
   return k;
 }
 

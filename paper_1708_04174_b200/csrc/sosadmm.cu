@@ -968,3 +968,36 @@ extern "C" int sosadmm_debug_spdinv(int t, double* K) {
   cudaStreamDestroy(s);
   return rc == 0 ? 0 : (rc == 1 ? -3 : -4);
 }
+
+// Timing probe of the cluster tridiagonalisation: prof receives 8 clock64 stamps per step of CTA 0
+// ((N - 2) x 8), ms the CUDA-event time of one launch (after a warm-up launch).
+extern "C" int sosadmm_debug_tridiag_prof(int N, const double* A, long long* prof, float* ms) {
+  if (N < 3) return -1;
+  DebugLarge dl;
+  int rc = dl.init(N);
+  if (rc) return rc;
+  LargeBlock& lb = dl.le.blocks[0];
+  long long* dprof;
+  if (cudaMalloc(&dprof, sizeof(long long) * 8 * N)) return -7;
+  cudaMemsetAsync(dprof, 0, sizeof(long long) * 8 * N, dl.s);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int rep = 0; rep < 2; ++rep) {
+    cudaMemcpyAsync(lb.M, A, 8ull * N * N, cudaMemcpyHostToDevice, dl.s);
+    lb.ta.prof = rep ? dprof : nullptr;
+    if (rep) cudaEventRecord(e0, dl.s);
+    large_block_tridiag(dl.le, lb, dl.s, false);
+    if (rep) cudaEventRecord(e1, dl.s);
+  }
+  lb.ta.prof = nullptr;
+  cudaError_t err = cudaStreamSynchronize(dl.s);
+  if (err == cudaSuccess) {
+    cudaEventElapsedTime(ms, e0, e1);
+    cudaMemcpy(prof, dprof, sizeof(long long) * 8 * (N - 2), cudaMemcpyDeviceToHost);
+  }
+  cudaFree(dprof);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return err == cudaSuccess ? 0 : -4;
+}
