@@ -24,6 +24,9 @@ struct LargeBlock {
   int b = 0, N = 0, C = 1, D = 0;
   long long smem_cols = 0;
   size_t trd_smem = 0;
+  int ksw = 0;                // first step done by the single-CTA tail (N - 2: no tail)
+  size_t tail_smem = 0;
+  TridiagArgs ta_tail{};
   double* M = nullptr;
   double *d = nullptr, *e = nullptr, *tau = nullptr, *V = nullptr;
   DcArgs dc{};
@@ -122,20 +125,36 @@ inline void dc_build_tree(int N, std::vector<DcNode>& nodes, std::vector<int>& l
   }
 }
 
-constexpr int TRD_MAX_DYN_SMEM = 227 * 1024 - 1024;  // leaves room for the static tables
+constexpr int TRD_MAX_DYN_SMEM = 227 * 1024 - 2048;  // leaves room for the static tables
 
 inline int tridiag_cluster_size(int N) { return N > 512 ? 16 : (N > 160 ? 8 : 4); }
 
-// Shared-memory budget (doubles) for the row storage of the distributed lower triangle (per CTA).
+// Row storage (doubles) of CTA c of C for rows i >= kb stored from column kb.
+inline long long tridiag_rows_need(int N, int C, int c, int kb) {
+  long long s = 0;
+  for (int i = c; i < N; i += C)
+    if (i >= kb) s += i + 1 - kb;
+  return s;
+}
+// Shared-memory budget (doubles) for the row storage of the cluster head (per CTA, rows from 0).
 inline long long tridiag_row_budget(int N, int C) {
-  const long long cap = TRD_MAX_DYN_SMEM / 8 - trd_fixed_doubles(N, C);
+  const long long cap = TRD_MAX_DYN_SMEM / 8 - trd_fixed_doubles(N, C, (N + C - 1) / C);
   long long need = 0;
-  for (int c = 0; c < C; ++c) {
-    long long s = 0;
-    for (int i = c; i < N; i += C) s += i + 1;
-    need = std::max(need, s);
-  }
+  for (int c = 0; c < C; ++c) need = std::max(need, tridiag_rows_need(N, C, c, 0));
   return std::min(cap, need);
+}
+// Number of trailing rows n the single-CTA tail takes over (the whole lower triangle of the last n
+// rows in one SM's shared memory); 0 = no tail.  Capped at TRD_TAIL_MAX: below it the per-step fixed
+// cost of the cluster exchanges (~5k cycles) exceeds one SM's share of the trailing work.
+constexpr int TRD_TAIL_MAX = 0;  // disabled: measured slower than the cluster (profiles/r01_*)
+inline int tridiag_tail_rows(int N) {
+  int n = 0;
+  for (int t = 16; t <= std::min(N - 3, TRD_TAIL_MAX); ++t) {
+    const long long need = trd_fixed_doubles(N, 1, t) + (long long)t * (t + 1) / 2;
+    if (need > TRD_MAX_DYN_SMEM / 8) break;
+    n = t;
+  }
+  return n;
 }
 
 template <class F>
@@ -180,6 +199,7 @@ inline size_t large_carve(const std::vector<int>& blk_N, const std::vector<int>&
     p[q++] = take(4 * nodes.size());      // rot_cnt
     p[q++] = take(sizeof(GemmDesc) * (nodes.size() + 1));
     p[q++] = take(4 * 4);                 // sel
+    p[q++] = take(8 * ((size_t)3 * N + 2));  // tridiagonalisation hand-over state
     p[q++] = take(8 * (size_t)BTW_NB * BTW_NB * ((N - 2 + BTW_NB - 1) / BTW_NB));  // Twy
     p[q++] = take(8 * (size_t)BTW_NB * BTW_NB * ((N - 2 + BTW_NB - 1) / BTW_NB) * bt_gram_chunks(N));  // Gwy
     per_block(b, N, p, nodes, l0, lnn, lmax, D, leaf0, nleaves, p2n);
@@ -209,7 +229,13 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     lb.M = mats + blk_mat[b];
     lb.C = tridiag_cluster_size(N);
     lb.smem_cols = tridiag_row_budget(N, lb.C);
-    lb.trd_smem = tridiag_smem_bytes(N, lb.C, lb.smem_cols);
+    lb.trd_smem = tridiag_smem_bytes(N, lb.C, (N + lb.C - 1) / lb.C, lb.smem_cols);
+    {
+      const int nt = tridiag_tail_rows(N);
+      lb.ksw = (nt >= 16 && N - nt > 8) ? N - nt : N - 2;
+      const int S = N - lb.ksw;
+      lb.tail_smem = tridiag_smem_bytes(N, 1, S, tridiag_rows_need(N, 1, 0, lb.ksw));
+    }
     int q = 0;
     lb.d = (double*)p[q++];
     lb.e = (double*)p[q++];
@@ -250,6 +276,7 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     dc.check_state = 1;
     lb.gdesc = (GemmDesc*)p[q++];
     lb.sel = (int*)p[q++];
+    double* hand = (double*)p[q++];
     lb.Twy = (double*)p[q++];
     lb.Gwy = (double*)p[q++];
     lb.recon = (int)nodes.size();
@@ -321,6 +348,14 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     ta.is = is;
     ta.check_state = 1;
     ta.prof = nullptr;
+    ta.kb = 0;
+    ta.ke = lb.ksw;
+    ta.hand = hand;
+    lb.ta_tail = ta;
+    lb.ta_tail.C = 1;
+    lb.ta_tail.kb = lb.ksw;
+    lb.ta_tail.ke = N - 2;
+    lb.ta_tail.smem_rows_doubles = tridiag_rows_need(N, 1, 0, lb.ksw);
     le.blocks.push_back(lb);
   });
   le.side = side_p;
@@ -336,7 +371,8 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     }
   }
   if (!le.blocks.empty()) {
-    for (TridiagKernel kt : {k_tridiag<2>, k_tridiag<4>, k_tridiag<7>, k_tridiag<10>}) {
+    for (TridiagKernel kt : {k_tridiag<2, false>, k_tridiag<4, false>, k_tridiag<7, false>, k_tridiag<10, false>,
+                             k_tridiag<2, true>, k_tridiag<4, true>, k_tridiag<7, true>, k_tridiag<10, true>}) {
       if (err == cudaSuccess) err = cudaFuncSetAttribute(kt, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (err == cudaSuccess)
         err = cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, TRD_MAX_DYN_SMEM);
@@ -354,6 +390,8 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
 
 inline void large_block_tridiag(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool check) {
   lb.ta.check_state = check;
+  lb.ta_tail.check_state = check;
+  lb.ta_tail.prof = lb.ta.prof;
   {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(lb.C, 1, 1);
@@ -367,8 +405,10 @@ inline void large_block_tridiag(LargeEig& le, LargeBlock& lb, cudaStream_t s, bo
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, tridiag_kernel(lb.N), lb.ta);
+    cudaLaunchKernelEx(&cfg, tridiag_kernel(lb.N, false), lb.ta);
   }
+  if (lb.ksw < lb.N - 2)
+    tridiag_kernel(lb.N, true)<<<1, TRD_NT, lb.tail_smem, s>>>(lb.ta_tail);
 }
 
 inline void large_block_dc(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool check) {
@@ -430,7 +470,7 @@ inline void large_eig_launch(LargeEig& le, cudaStream_t s, bool check) {
 
 inline int large_eig_launches(const LargeEig& le) {
   int k = 0;
-  for (const auto& lb : le.blocks) k += 1 + 2 + 1 + 6 * lb.D + 5;
+  for (const auto& lb : le.blocks) k += (lb.ksw < lb.N - 2 ? 2 : 1) + 2 + 1 + 6 * lb.D + 5;
   return k;
 }
 

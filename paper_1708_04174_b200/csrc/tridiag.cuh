@@ -26,7 +26,7 @@
 constexpr int TRD_NT = 512;
 constexpr int TRD_NW = TRD_NT / 32;
 constexpr int TRD_MAXC = 16;
-constexpr int TRD_MAXOWN = 96;  // own rows per CTA
+constexpr int TRD_MAXOWN = 256;  // own rows per CTA (the single-CTA tail owns every trailing row)
 // Phase X thread mapping: lane = (lr, cc), lr = lane / 8 picks one of 4 rows of a row group, cc one
 // of 8 consecutive columns of a column block; warp w owns column blocks w, w + 16, w + 32, ...
 // (MAXB of them), so row sums reduce over 8 lanes and column sums over 4 lanes only.
@@ -49,6 +49,8 @@ struct TridiagArgs {
   const IterScal* is;
   int check_state;
   long long* prof;   // optional (debug): clock64 stamps of CTA 0 per step and phase, 8 per step
+  int kb, ke;        // Householder steps [kb, ke) done by this launch
+  double* hand;      // 3 N + 2 doubles: head -> tail hand-over state
 };
 
 __device__ __forceinline__ void trd_cluster_sync() {
@@ -110,21 +112,37 @@ __device__ __forceinline__ double trd_block_sum(double v, double* red) {
   return trd_sum16(red, TRD_NW, 1);
 }
 
-// Shared-memory layout (doubles): xt[2][N] wb[N] | per own slot (S = ceil(N/C)): vown[2][S] wown[S]
+// Shared-memory layout (doubles): xt[2][N] wb[N] | per own slot (S slots): vown[2][S] wown[S]
 // pown[S] xs[S] qr[C][S] rp[NW][S] | scalars sd[C] se[C] ss[C] red[32] | rows.
-__host__ __device__ inline long long trd_fixed_doubles(int N, int C) {
-  const int S = (N + C - 1) / C;
+__host__ __device__ inline long long trd_fixed_doubles(int N, int C, int S) {
   return 3LL * N + 5LL * S + (long long)C * S + (long long)TRD_NW * S + 3LL * C + 32;
 }
+__host__ __device__ inline int trd_log2(int C) { return C >= 16 ? 4 : (C >= 8 ? 3 : (C >= 4 ? 2 : (C >= 2 ? 1 : 0))); }
 
-template <int MAXB>
+// k_tridiag<MAXB, SOLO> runs Householder steps [kb, ke) of one block.
+//   cluster head (SOLO = false, C in {2,4,8,16}, kb = 0): if ke < N - 2 it stops after step ke - 1 and
+//     hands its state over through global memory: the unfinished trailing rows i >= ke (entries
+//     ke..i, still owing the lazy rank-2 update of step ke - 1) go back to the block matrix, and
+//     hand[] = [x~_ke (N), x~_{ke-1} (N), w_{ke-1} (N), ||x~_ke[ke+1:]||^2, scale_{ke-1}];
+//   single-CTA tail (SOLO = true, C = 1, kb = ke of the head): resumes from that state with local
+//     stores and __syncthreads in place of the DSMEM exchanges, where the per-step fixed cost of the
+//     cluster (two exchange latencies) would dominate the shrinking trailing work.
+template <int MAXB, bool SOLO>
 __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
   if (a.check_state && (a.st->done || !a.is->proceed)) return;
-  const int C = a.C, N = a.N;
-  const int me = (int)trd_cluster_rank();
+  const int C = SOLO ? 1 : a.C, N = a.N;
+  const int logC = trd_log2(C);
+  const int kb = a.kb, ke = min(a.ke, N - 2);
+  const int me = SOLO ? 0 : (int)trd_cluster_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lr = lane >> 3, cc = lane & 7;
-  const int S = (N + C - 1) / C;
+  const int nown = (N - me + C - 1) >> logC;  // own rows i = me + q C
+  auto first_slot = [&](int m) { return m > me ? (m - me + C - 1) >> logC : 0; };  // first q with i >= m
+  const int qlo = first_slot(kb);             // rows below kb are finished before this launch
+  // per-slot arrays are indexed q - qlo; S must be the same in every CTA of the cluster (the DSMEM
+  // exchange addresses are computed from the local layout)
+  const int S = SOLO ? N - kb : (N + C - 1) >> logC;
+  const int jb = kb;                          // row storage starts at column kb
   extern __shared__ __align__(16) double sm[];
   double* xt = sm;                 // [2][N] x~_k: the column that defines v_k (allgathered), by parity
   double* wb = xt + 2 * N;         // w_{k-1} (allgathered)
@@ -139,58 +157,81 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
   double* ss = se + C;             // [C] partial ||x~||^2
   double* red = ss + C;            // [32]: warp partials (two independent halves)
   double* rows = red + 32;
-  __shared__ int roff[TRD_MAXOWN];  // smem offset of own row slot q, -1 = spilled to global
+  __shared__ int roff[TRD_MAXOWN];  // smem offset of own row slot q - qlo, -1 = spilled to global
   __shared__ int nspill_s;
   __shared__ double qk1_s;
   __shared__ __align__(8) uint64_t barQ, barY;
 
-  const int nown = (N - me + C - 1) / C;  // own rows i = me + q C
-  auto first_slot = [&](int m) { return (m - me + C - 1) / C > 0 ? (m - me + C - 1) / C : 0; };  // i >= m
   if (tid == 0) {
-    // smallest rows spill first; rows are stored whole (entries 0..i)
+    // smallest rows spill first; rows are stored from column jb to the diagonal
     long long need = 0;
-    for (int q = 0; q < nown; ++q) need += me + q * C + 1;
-    int ns = 0;
+    for (int q = qlo; q < nown; ++q) need += me + q * C + 1 - jb;
+    int ns = qlo;
     while (need > a.smem_rows_doubles && ns < nown) {
-      need -= me + ns * C + 1;
+      need -= me + ns * C + 1 - jb;
       ++ns;
     }
     long long off = 0;
-    for (int q = 0; q < nown; ++q) {
+    for (int q = qlo; q < nown; ++q) {
       if (q < ns) {
-        roff[q] = -1;
+        roff[q - qlo] = -1;
       } else {
-        roff[q] = (int)off;
-        off += me + q * C + 1;
+        roff[q - qlo] = (int)off;
+        off += me + q * C + 1 - jb;
       }
     }
     nspill_s = ns;
-    trd_bar_init(&barQ);
-    trd_bar_init(&barY);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (!SOLO) {
+      trd_bar_init(&barQ);
+      trd_bar_init(&barY);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
   }
   __syncthreads();
   const int nspill = nspill_s;
-  for (int q = nspill; q < nown; ++q) {
-    const int i = me + q * C;
-    const double* src = a.M + (size_t)i * N;  // upper triangle of column i = row i of the lower
-    double* dst = rows + roff[q];
-    for (int j = tid; j <= i; j += TRD_NT) dst[j] = src[j];
-  }
-  for (int j = tid; j < N; j += TRD_NT) wb[j] = 0.0;
-  for (int q = tid; q < 2 * S; q += TRD_NT) vown[q] = 0.0;
-  for (int q = tid; q < S; q += TRD_NT) wown[q] = 0.0;
-  trd_cluster_sync();  // barriers initialised and every CTA running before the first remote store
-
   auto rowptr_g = [&](int q) -> double* { return a.M + (size_t)(me + q * C) * N; };
-  auto rowptr_s = [&](int q) -> double* { return rows + roff[q]; };
+  auto rowptr_s = [&](int q) -> double* { return rows + roff[q - qlo] - jb; };
   auto rowval = [&](int q, int j) -> double {  // entry (i, j) of own row slot q
     return q < nspill ? rowptr_g(q)[j] : rowptr_s(q)[j];
   };
+  for (int q = nspill; q < nown; ++q) {
+    const int i = me + q * C;
+    const double* src = a.M + (size_t)i * N;  // upper triangle of column i = row i of the lower
+    double* dst = rowptr_s(q);
+    for (int j = jb + tid; j <= i; j += TRD_NT) dst[j] = src[j];
+  }
+  double scale_prev = 0.0;
+  if (kb == 0) {
+    for (int j = tid; j < N; j += TRD_NT) wb[j] = 0.0;
+    for (int q = tid; q < 2 * S; q += TRD_NT) vown[q] = 0.0;
+    for (int q = tid; q < S; q += TRD_NT) wown[q] = 0.0;
+  } else {  // resume from the head's hand-over state
+    const int pk = kb & 1;
+    for (int j = tid; j < N; j += TRD_NT) {
+      xt[pk * N + j] = a.hand[j];
+      xt[(pk ^ 1) * N + j] = a.hand[N + j];
+      wb[j] = a.hand[2 * N + j];
+    }
+    if (tid == 0) ss[0] = a.hand[3 * N];
+    scale_prev = a.hand[3 * N + 1];
+    for (int q = qlo + tid; q < nown; q += TRD_NT) {
+      const int i = me + q * C;  // v_{kb-1}[i]: 1 at row kb, x~_{kb-1}[i] scale_{kb-1} below
+      vown[(pk ^ 1) * S + q - qlo] = (i == kb) ? 1.0 : a.hand[N + i] * scale_prev;
+      wown[q - qlo] = a.hand[2 * N + i];
+    }
+  }
+  if (!SOLO) trd_cluster_sync();  // barriers initialised and every CTA running before the first remote store
+  else __syncthreads();
 
-  // ---- column 0 defines v_0: push x~_0 = A[1:, 0], ||A[2:, 0]||^2 partials; d[0] ----
-  if (tid == 0) trd_bar_expect(&barY, (unsigned)(8 * ((N - 1) + C)));
-  {
+  // exchange primitives: SOLO = plain local stores (the waits are __syncthreads)
+  auto push = [&](double* dst, int peer, double v, uint64_t* bar) {
+    if (SOLO) *dst = v;
+    else trd_push(trd_mapa(dst, peer), v, trd_mapa(bar, peer));
+  };
+
+  if (kb == 0) {
+    // ---- column 0 defines v_0: push x~_0 = A[1:, 0], ||A[2:, 0]||^2 partials; d[0] ----
+    if (!SOLO && tid == 0) trd_bar_expect(&barY, (unsigned)(8 * ((N - 1) + C)));
     double s2 = 0.0;
     for (int q = tid; q < nown; q += TRD_NT) {
       const int i = me + q * C;
@@ -201,24 +242,24 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     }
     s2 = trd_block_sum(s2, red);
     for (int e = tid; e < nown * C; e += TRD_NT) {
-      const int q = e / C, peer = e % C, i = me + q * C;
-      if (i >= 1) trd_push(trd_mapa(xt + i, peer), xs[q], trd_mapa(&barY, peer));
+      const int q = e >> logC, peer = e & (C - 1), i = me + q * C;
+      if (i >= 1) push(xt + i, peer, xs[q], &barY);
     }
-    if (tid < C) trd_push(trd_mapa(ss + me, tid), s2, trd_mapa(&barY, tid));
+    if (tid < C) push(ss + me, tid, s2, &barY);
+    if (!SOLO) trd_bar_wait(&barY, 0);
+    else __syncthreads();
   }
-  trd_bar_wait(&barY, 0);
 
-  double scale_prev = 0.0;
   const bool prof = a.prof != nullptr && me == 0 && tid == 0;
 #define TRD_STAMP(ph) \
   if (prof) a.prof[(size_t)k * 8 + (ph)] = clock64();
-  for (int k = 0; k < N - 2; ++k) {
+  for (int k = kb; k < ke; ++k) {
     const int par = k & 1;
     TRD_STAMP(0)
     const double* xk = xt + par * N;          // x~_k
     const double* xkm = xt + (par ^ 1) * N;   // x~_{k-1}
     const int qs1 = first_slot(k + 1), qs2 = first_slot(k + 2);
-    if (tid == 0) trd_bar_expect(&barQ, (unsigned)(8 * (C * (nown - qs2) + 2 * C)));
+    if (!SOLO && tid == 0) trd_bar_expect(&barQ, (unsigned)(8 * (C * (nown - qs2) + 2 * C)));
     // ---- Phase A: the reflector of column k (every CTA computes it redundantly, same order) ----
     const double sig = trd_sum16(ss, C, 1);
     const double alpha = xk[k + 1];
@@ -232,21 +273,24 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
       tk = (beta - alpha) / beta;
       scale = 1.0 / (alpha - beta);
     }
-    if (me == k % C) {
+    if (me == (k & (C - 1))) {
       for (int j = k + 1 + tid; j < N; j += TRD_NT) a.V[(size_t)k * N + j] = (j == k + 1) ? 1.0 : xk[j] * scale;
       if (tid == 0) {
         a.e[k] = beta;
         a.tau[k] = tk;
       }
     }
-    double* vcur = vown + par * S;
-    const double* vprev = vown + (par ^ 1) * S;
+    double* vcur = vown + par * S - qlo;          // indexed by absolute slot q
+    const double* vprev = vown + (par ^ 1) * S - qlo;
+    double* wo_own = wown - qlo;
+    double* po = pown - qlo;
+    double* xso = xs - qlo;
     for (int q = qs1 + tid; q < nown; q += TRD_NT) {
       const int i = me + q * C;
       vcur[q] = (i == k + 1) ? 1.0 : xk[i] * scale;
     }
     // this lane's columns: blocks bb = warp + 16 t of 8 columns starting at k + 1
-    const int nb = (N - k - 1 + 7) / 8;
+    const int nb = (N - k - 1 + 7) >> 3;
     const int nbt = nb > warp ? (nb - warp + TRD_NW - 1) / TRD_NW : 0;  // blocks of this warp
     double vn[MAXB], vo[MAXB], wo[MAXB], qa[MAXB];
 #pragma unroll
@@ -263,28 +307,32 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
 
     // ---- Phase X: fused rank-2 update of step k-1 and symv with v_k over own rows i >= k+1 ----
     // rows in groups of 4 (lane row lr), processed from slot qb to qe with row pointers from rp_of
+    // a warp only visits rows that reach its first column block (rows i >= k + 1 + 8 warp)
+    const int qw = first_slot(k + 1 + 8 * warp);
     auto row_groups = [&](int qb, int qe, auto rp_of) {
-      for (int g = qb; g < qe; g += 4) {
+      if (nbt == 0) return;
+      for (int g = max(qb, qw); g < qe; g += 4) {
         const int q = min(g + lr, qe - 1);
         const bool valid = g + lr < qe;
         const int i = valid ? me + q * C : -1;
         const int imin = me + g * C;                   // smallest row of the group (uniform)
         const int imax = me + min(g + 3, qe - 1) * C;  // largest row of the group (uniform)
         double* R = rp_of(q);
-        const double vio = vprev[q], wio = wown[q], vin = vcur[q];
+        const double vio = vprev[q], wio = wo_own[q], vin = vcur[q];
         double racc = 0.0;
 #pragma unroll
         for (int t = 0; t < MAXB; ++t) {
           const int jf = k + 1 + 8 * (warp + TRD_NW * t);
           if (t >= nbt || jf > imax) break;  // this and all later blocks lie right of the group's diagonal
           const int j = jf + cc;
-          if (jf + 7 < imin) {  // strictly below every row's diagonal: no masking
+          if (jf + 7 < imin) {  // strictly below every row's diagonal: no column masking
+            if (!valid) continue;
             double x = R[j];
             x = fma(-vio, wo[t], fma(-wio, vo[t], x));
             R[j] = x;
             racc = fma(x, vn[t], racc);
             qa[t] = fma(x, vin, qa[t]);
-          } else if (j <= i) {
+          } else if (j <= i) {  // i = -1 on the padding lanes of the last group
             double x = R[j];
             x = fma(-vio, wo[t], fma(-wio, vo[t], x));
             R[j] = x;
@@ -295,7 +343,7 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
         racc += __shfl_xor_sync(0xffffffffu, racc, 1);
         racc += __shfl_xor_sync(0xffffffffu, racc, 2);
         racc += __shfl_xor_sync(0xffffffffu, racc, 4);
-        if (valid && cc == 0) rp[warp * S + q] = racc;
+        if (valid && cc == 0) rp[warp * S + q - qlo] = racc;
       }
     };
     if (qs1 < nspill) row_groups(qs1, nspill, rowptr_g);
@@ -319,17 +367,16 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
       for (int t = 0; t < MAXB; ++t) {
         if (t >= nbt) break;
         const int j = k + 1 + 8 * (warp + TRD_NW * t) + cc;
-        if (j >= k + 2 && j < N) {
-          const int peer = j % C;
-          trd_push(trd_mapa(qr + me * S + j / C, peer), qa[t], trd_mapa(&barQ, peer));
-        }
+        if (j >= k + 2 && j < N) push(qr + me * S + (j >> logC) - qlo, j & (C - 1), qa[t], &barQ);
       }
     }
     __syncthreads();
     TRD_STAMP(3)
     for (int q = qs1 + tid; q < nown; q += TRD_NT) {
-      const double s = trd_sum16(rp + q, TRD_NW, S);
-      pown[q] = s;
+      // warps w < min(16, nb, (i - k - 1) / 8 + 1) reach row i; the others wrote nothing for it
+      const int i = me + q * C;
+      const double s = trd_sum16(rp + q - qlo, min(min(TRD_NW, nb), (i - k - 1) / 8 + 1), S);
+      po[q] = s;
       dpart = fma(s, vcur[q], dpart);
     }
     dpart = warp_sum(dpart);
@@ -339,14 +386,17 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     if (tid < C) {
       const double dsum = trd_sum16(red, TRD_NW, 1);
       double e1 = qk1_s;
-      if ((k + 1) % C == me) e1 += pown[(k + 1) / C];
-      const unsigned rb = trd_mapa(&barQ, tid);
-      trd_push(trd_mapa(sd + me, tid), dsum, rb);
-      trd_push(trd_mapa(se + me, tid), e1, rb);
+      if (((k + 1) & (C - 1)) == me) e1 += po[(k + 1) >> logC];
+      push(sd + me, tid, dsum, &barQ);
+      push(se + me, tid, e1, &barQ);
     }
     const bool last = (k == N - 3);
-    if (tid == 0 && !last) trd_bar_expect(&barY, (unsigned)(8 * (2 * (N - k - 2) + C)));
-    trd_bar_wait(&barQ, par);
+    if (!SOLO) {
+      if (tid == 0 && !last) trd_bar_expect(&barY, (unsigned)(8 * (2 * (N - k - 2) + C)));
+      trd_bar_wait(&barQ, par);
+    } else {
+      __syncthreads();
+    }
     TRD_STAMP(5)
 
     // ---- Phase Y: w_k on own rows, eager update of column k+1, its norm partial ----
@@ -358,16 +408,16 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
       const int i = me + q * C;
       if (i == k + 1) {
         a.d[k + 1] = rowval(q, k + 1) - 2.0 * wk1;
-        wown[q] = wk1;
+        wo_own[q] = wk1;
         continue;
       }
-      const double pq = pown[q] + trd_sum16(qr + q, C, S);
+      const double pq = po[q] + trd_sum16(qr + q - qlo, C, S);
       const double wi = fma(-Kc, vcur[q], tk * pq);
-      wown[q] = wi;
+      wo_own[q] = wi;
       double* R = q < nspill ? rowptr_g(q) : rowptr_s(q);
       const double x = fma(-vcur[q], wk1, R[k + 1] - wi);
       R[k + 1] = x;
-      xs[q] = x;
+      xso[q] = x;
       if (i >= k + 3) s2 = fma(x, x, s2);
       if (last) {  // i == N - 1: the trailing 2 x 2 block
         a.e[N - 2] = x;
@@ -379,36 +429,58 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     TRD_STAMP(6)
     s2 = warp_sum(s2);
     if (lane == 0) red[16 + warp] = s2;  // second half of red: no conflict with the dsum partials
+    __syncthreads();                     // xs / wown of every own row written
+    if (tid < C) push(ss + me, tid, trd_sum16(red + 16, TRD_NW, 1), &barY);
     {
       double* xnext = xt + (par ^ 1) * N;
       const int nact = nown - qs2;  // own rows >= k+2
       for (int e = tid; e < nact * C; e += TRD_NT) {
-        const int q = qs2 + e / C, peer = e % C, i = me + q * C;
-        const unsigned rb = trd_mapa(&barY, peer);
-        trd_push(trd_mapa(xnext + i, peer), xs[q], rb);
-        trd_push(trd_mapa(wb + i, peer), wown[q], rb);
+        const int q = qs2 + (e >> logC), peer = e & (C - 1), i = me + q * C;
+        push(xnext + i, peer, xso[q], &barY);
+        push(wb + i, peer, wo_own[q], &barY);
       }
     }
-    __syncthreads();
-    if (tid < C) trd_push(trd_mapa(ss + me, tid), trd_sum16(red + 16, TRD_NW, 1), trd_mapa(&barY, tid));
     scale_prev = scale;
     TRD_STAMP(7)
-    trd_bar_wait(&barY, par ^ 1);
+    if (!SOLO) trd_bar_wait(&barY, par ^ 1);
+    else __syncthreads();
+    if (k + 1 == ke && ke < N - 2) {
+      // ---- hand over to the single-CTA tail: rows i >= ke back to global, lazy state to hand[] ----
+      for (int q = max(first_slot(ke), nspill); q < nown; ++q) {
+        const int i = me + q * C;
+        const double* src = rowptr_s(q);
+        double* dst = a.M + (size_t)i * N;
+        for (int j = ke + tid; j <= i; j += TRD_NT) dst[j] = src[j];
+      }
+      if (me == 0) {
+        const int pk = ke & 1;
+        for (int j = tid; j < N; j += TRD_NT) {
+          a.hand[j] = xt[pk * N + j];
+          a.hand[N + j] = xt[(pk ^ 1) * N + j];
+          a.hand[2 * N + j] = wb[j];
+        }
+        if (tid == 0) {
+          a.hand[3 * N] = trd_sum16(ss, C, 1);
+          a.hand[3 * N + 1] = scale_prev;
+        }
+      }
+      break;
+    }
   }
 #undef TRD_STAMP
-  trd_cluster_sync();  // no CTA leaves while a peer may still address its shared memory
+  if (!SOLO) trd_cluster_sync();  // no CTA leaves while a peer may still address its shared memory
 }
 
-inline size_t tridiag_smem_bytes(int N, int C, long long row_doubles) {
-  return sizeof(double) * (size_t)(trd_fixed_doubles(N, C) + row_doubles);
+inline size_t tridiag_smem_bytes(int N, int C, int S, long long row_doubles) {
+  return sizeof(double) * (size_t)(trd_fixed_doubles(N, C, S) + row_doubles);
 }
 
 typedef void (*TridiagKernel)(TridiagArgs);
-inline TridiagKernel tridiag_kernel(int N) {
+inline TridiagKernel tridiag_kernel(int N, bool solo) {
   switch (tridiag_maxb(N)) {
-    case 2: return k_tridiag<2>;
-    case 4: return k_tridiag<4>;
-    case 7: return k_tridiag<7>;
-    default: return k_tridiag<10>;
+    case 2: return solo ? k_tridiag<2, true> : k_tridiag<2, false>;
+    case 4: return solo ? k_tridiag<4, true> : k_tridiag<4, false>;
+    case 7: return solo ? k_tridiag<7, true> : k_tridiag<7, false>;
+    default: return solo ? k_tridiag<10, true> : k_tridiag<10, false>;
   }
 }
