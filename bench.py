@@ -30,6 +30,11 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
+CONFIG_INDEX = {"pop6": 0, "pop20": 1, "lyap10": 2, "box24": 3, "pop40": 4}
+CONFIG_DESC = {"pop6": "n=6 quartic POP, config 0", "pop20": "n=20 quartic POP, config 1",
+               "lyap10": "n=10 Lyapunov program, config 2", "box24": "n=24 box-constrained POP, config 3",
+               "pop40": "n=40 quartic POP, config 4"}
+
 # roofline denominators: measured on this pool's B200s
 DMMA_PEAK_TFLOPS = 74.3   # profiles/r01_probe_fp64.log: mma.sync m8n8k4 f64 (SASS DMMA), measured
 DFMA_PEAK_TFLOPS = 34.2   # same probe, scalar DFMA
@@ -116,6 +121,58 @@ def affine_bytes(prob, tl: int) -> float:
     return 36.0 * L + 68.0 * prob.m + 24.0 * nnz_low + 8.0 * tl * tl
 
 
+def roofline_table(prob, tl, phase, large, hbm, hbm_src):
+    """Per-kernel-class rooflines.  achieved = algorithmic work per iteration /
+    measured phase time per iteration (CUDA events on the library stream)."""
+    out = []
+    aff_ms = phase["affine"] + phase["scatter"] + phase["pack"]
+    abytes = affine_bytes(prob, tl)
+    out.append({"kernel": "affine projection: k_gather, k_lowT, k_kinv, k_tphase, k_rowupdate, k_scatter, k_pack "
+                          "(36 L + 68 m + 24 nnz(A_low) + 8 t'^2 algorithmic bytes)",
+                "bound": "hbm", "achieved": abytes / (aff_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                "frac": abytes / (aff_ms * 1e-3) / 1e9 / hbm, "traffic": None, "algorithmic_per_launch": abytes,
+                "peak_source": hbm_src, "ms_per_iter": aff_ms})
+    if large:
+        fl = sum(4.0 / 3.0 * N ** 3 for N in large)
+        tms = phase["tridiag"]
+        out.append({"kernel": f"k_tridiag (Householder tridiagonalisation, one {TRD_CLUSTER(max(large))}-CTA cluster per "
+                              f"block, N={'+'.join(map(str, large))}: 4/3 N^3 FP64 flops on CUDA-core DFMA)",
+                    "bound": "alu", "achieved": fl / (tms * 1e-3) / 1e12, "peak": DFMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": fl / (tms * 1e-3) / 1e12 / DFMA_PEAK_TFLOPS, "traffic": None, "algorithmic_per_launch": fl,
+                    "peak_source": "measured FP64 DFMA peak of this pool's B200 (profiles/r01_probe_fp64.log); "
+                                   "MEASURED_PEAKS.json has no FP64 entry", "ms_per_iter": tms})
+        fd = sum(4.0 / 3.0 * N ** 3 for N in large)
+        out.append({"kernel": "divide-and-conquer tridiagonal eigensolver (k_dc_*, merge GEMMs on DMMA; 4/3 N^3 "
+                              "dense-count flops, deflation lowers the real count)",
+                    "bound": "tensor", "achieved": fd / (phase["dc"] * 1e-3) / 1e12, "peak": DMMA_PEAK_TFLOPS,
+                    "unit": "TFLOP/s", "frac": fd / (phase["dc"] * 1e-3) / 1e12 / DMMA_PEAK_TFLOPS, "traffic": None,
+                    "algorithmic_per_launch": fd,
+                    "peak_source": "measured FP64 DMMA (mma.sync m8n8k4) peak, profiles/r01_probe_fp64.log",
+                    "ms_per_iter": phase["dc"]})
+        fb = sum(2.0 * N ** 3 for N in large)  # back-transform 2 N^2 r + reconstruction 2 N^2 r at r = N / 2
+        out.append({"kernel": "back-transform + reconstruction (k_bt_gram, k_bt_larft, k_bt_apply, k_gemm_f64 on "
+                              "DMMA; 4 N^2 r flops, counted at the r = N/2 upper bound)",
+                    "bound": "tensor", "achieved": fb / (phase["backtransform_recon"] * 1e-3) / 1e12,
+                    "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": fb / (phase["backtransform_recon"] * 1e-3) / 1e12 / DMMA_PEAK_TFLOPS, "traffic": None,
+                    "algorithmic_per_launch": fb,
+                    "peak_source": "measured FP64 DMMA (mma.sync m8n8k4) peak, profiles/r01_probe_fp64.log",
+                    "ms_per_iter": phase["backtransform_recon"]})
+    if phase["jacobi"] > 0:
+        small = [d for d in prob.psd_dims if d <= 64]
+        fj = sum(10.0 * N ** 3 for N in small)  # ~ 3 Jacobi sweeps x (3 N^3 rotations) + reconstruction
+        out.append({"kernel": f"k_psd_jacobi ({len(small)} blocks N<=64, one CTA each; ~10 N^3 flops)",
+                    "bound": "alu", "achieved": fj / (phase["jacobi"] * 1e-3) / 1e12, "peak": DFMA_PEAK_TFLOPS,
+                    "unit": "TFLOP/s", "frac": fj / (phase["jacobi"] * 1e-3) / 1e12 / DFMA_PEAK_TFLOPS,
+                    "traffic": None, "algorithmic_per_launch": fj,
+                    "peak_source": "measured FP64 DFMA peak, profiles/r01_probe_fp64.log", "ms_per_iter": phase["jacobi"]})
+    return out
+
+
+def TRD_CLUSTER(N):
+    return 16 if N > 512 else (8 if N > 160 else 4)
+
+
 def run_ours(args):
     import torch
 
@@ -128,9 +185,19 @@ def run_ours(args):
     from paper_1708_04174_b200 import SosAdmm
     from sosgen import make_config
 
-    prob = make_config(args.config, seed=args.seed + rank)
-    # timing solver: tol 0 never stops, so every step is a full iteration
-    gpu = SosAdmm.from_problem(prob, tol=1e-300, max_iters=1 << 40, device=local)
+    sharded = world > 1 and len(make_config(args.config, seed=args.seed).psd_dims) > 1
+    if sharded:
+        # multi-block program: ONE problem, its PSD blocks sharded over the ranks;
+        # every iteration all-reduces the length-m partial sums over NCCL/NVLink inside the library
+        from paper_1708_04174_b200.parallel import sharded_solver
+
+        prob = make_config(args.config, seed=args.seed)
+        gpu, owner = sharded_solver(prob, rank, world, local, tol=1e-300, max_iters=1 << 40)
+    else:
+        # single-block program: independent replicas, one per GPU (no collective)
+        prob = make_config(args.config, seed=args.seed + rank)
+        # timing solver: tol 0 never stops, so every step is a full iteration
+        gpu = SosAdmm.from_problem(prob, tol=1e-300, max_iters=1 << 40, device=local)
     st = gpu.stream
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
     launches_per_iter = gpu.launches_per_iter
@@ -164,9 +231,12 @@ def run_ours(args):
     e1.record(st)
     barrier()
     ms_warm = e0.elapsed_time(e1)
-    # ---- per-phase device time (CUDA events around each kernel class, same iterations) ----
+    # ---- per-phase device time: the same iterations launched un-graphed with CUDA events on the
+    # library's stream around each kernel class (include/sosadmm.h SOSADMM_NPHASE) ----
+    from paper_1708_04174_b200.sosadmm import PHASES
+
     info, ph = gpu.iterate_profiled(args.steps)
-    ph_ms = [float(x) / args.steps for x in ph]  # per iteration: [affine gather..t-phase, scatter, psd, pack]
+    ph_ms = [float(x) / args.steps for x in ph]  # ms per iteration per phase
     # ---- end-to-end through the C ABI with host buffers: H2D state, iterate, D2H state --------
     it = gpu.get_iterate()
     pin = {k: torch.from_numpy(np.ascontiguousarray(it[k])).pin_memory() for k in ("xi", "y", "z", "s")}
@@ -186,28 +256,27 @@ def run_ours(args):
     e2e_ms = ea.elapsed_time(eb)
     e2e_wall = time.perf_counter() - t0
     # max over ranks
-    vals = torch.tensor([ms, ms_warm, e2e_ms, ph_ms[2], ph_ms[0] + ph_ms[1] + ph_ms[3]], dtype=torch.float64,
-                        device=f"cuda:{local}")
+    vals = torch.tensor([ms, ms_warm, e2e_ms] + ph_ms, dtype=torch.float64, device=f"cuda:{local}")
     if world > 1:
         torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
-    ms, ms_warm, e2e_ms, psd_ms, aff_ms = [float(v) for v in vals.cpu()]
+    vals = [float(v) for v in vals.cpu()]
+    ms, ms_warm, e2e_ms, ph_ms = vals[0], vals[1], vals[2], vals[3:]
+    phase = dict(zip(PHASES, ph_ms))
     # time to 1e-4 (harness-side rule, C9): fresh solver, chunks of 25 iterations
     ttt = None
-    if rank == 0 and not args.no_ttt:
+    if rank == 0 and not args.no_ttt and not sharded:
         ttt = time_to_tol(prob, local, args)
     if rank != 0:
         return
-    N = max(prob.psd_dims)
     hbm, hbm_src = hbm_peak()
-    flops = eig_flops(N)
-    ach = flops / (psd_ms * 1e-3) / 1e12
     _, _, tl = gpu.get_structure()
-    abytes = affine_bytes(prob, tl)
-    aff_gbs = abytes / (aff_ms * 1e-3) / 1e9
+    large = [d for d in prob.psd_dims if d > 64]
+    rooflines = roofline_table(prob, tl, phase, large, hbm, hbm_src)
+    dominant = max(rooflines, key=lambda r: r["ms_per_iter"])
     cpu = cpu_baseline(args) if not args.no_cpu else None
-    total_steps = args.steps * world
+    total_steps = args.steps * (1 if sharded else world)  # sharded: all ranks advance ONE problem
     line = {
-        "metric": "ADMM iters/s (n=40 quartic POP, config 4)",
+        "metric": f"ADMM iters/s ({CONFIG_DESC.get(args.config, args.config)})",
         "value": total_steps / (ms * 1e-3),
         "unit": "iters/s",
         "n_gpus": world,
@@ -215,29 +284,26 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": ms / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (seeded planted POP, BASELINE.json config 4)",
-        "config": {"workload": f"{args.config} (N={N}, m={prob.m}, t'={tl}) seed {args.seed}",
+        "data": f"synthetic (seeded, BASELINE.json config {CONFIG_INDEX.get(args.config, '?')})",
+        "config": {"workload": f"{args.config} (N={'+'.join(str(d) for d in sorted(set(prob.psd_dims), reverse=True))}, "
+                               f"{len(prob.psd_dims)} PSD blocks, m={prob.m}, t'={tl}) seed {args.seed}",
                    "l2": "flushed before every timed step (512 MB write, > 126 MB L2)",
-                   "parallelism": "replicas" if world > 1 else "single GPU"},
+                   "parallelism": (f"block-sharded over {world} GPUs, owners {list(map(int, owner))}, one NCCL "
+                                   f"allreduce of 2m+3 partial sums per iteration") if sharded else
+                                  (f"{world} independent replicas" if world > 1 else "single GPU")},
         "warm_iters_per_s": total_steps / (ms_warm * 1e-3),
         "time_to_1e-4": ttt,
-        "phase_ms_per_iter": {"affine_gather_tphase": ph_ms[0], "scatter": ph_ms[1], "psd_projection": ph_ms[2],
-                              "pack_dual_update": ph_ms[3]},
-        "roofline": {"kernel": "PSD projection of the 861x861 block (tridiag + D&C + back-transform + DMMA "
-                               "reconstruction), 4.33 N^3 algorithmic flops",
-                     "bound": "tensor", "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": ach / DMMA_PEAK_TFLOPS, "traffic": None,
-                     "peak_source": "measured FP64 DMMA (mma.sync m8n8k4) peak, profiles/r01_probe_fp64.log"},
-        "roofline_affine": {"kernel": "affine projection (gather, t-phase, row update, scatter, pack)",
-                            "bound": "hbm", "achieved": aff_gbs, "peak": hbm, "unit": "GB/s",
-                            "frac": aff_gbs / hbm, "algorithmic_bytes": abytes, "peak_source": hbm_src},
+        "phase_ms_per_iter": phase,
+        "roofline": {k: dominant[k] for k in ("kernel", "bound", "achieved", "peak", "unit", "frac", "traffic",
+                                              "algorithmic_per_launch", "peak_source", "ms_per_iter")},
+        "roofline_kernels": rooflines,
         "cpu_baseline": cpu,
         "e2e": {"value": total_steps / (e2e_ms * 1e-3), "unit": "iters/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "wall_s": e2e_wall},
-        "gpu_launches": int(launches_per_iter * args.steps + 4 * args.steps),
+        "gpu_launches": int((launches_per_iter + (7 if sharded else 4)) * args.steps),
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)
@@ -320,11 +386,13 @@ def run_reference(args):
     v = args.steps / dt
     N = max(prob.psd_dims)
     print(json.dumps({
-        "impl": "reference", "metric": "ADMM iters/s (n=40 quartic POP, config 4)", "value": v, "unit": "iters/s",
+        "impl": "reference", "metric": f"ADMM iters/s ({CONFIG_DESC.get(args.config, args.config)})", "value": v,
+        "unit": "iters/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded planted POP, BASELINE.json config 4)",
-        "config": {"workload": f"{args.config} (N={N}, m={prob.m}) seed {args.seed}", "l2": "n/a (CPU)"},
+        "data": f"synthetic (seeded, BASELINE.json config {CONFIG_INDEX.get(args.config, '?')})",
+        "config": {"workload": f"{args.config} (N={'+'.join(str(d) for d in sorted(set(prob.psd_dims), reverse=True))}, "
+                               f"{len(prob.psd_dims)} PSD blocks, m={prob.m}) seed {args.seed}", "l2": "n/a (CPU)"},
         "cpu_baseline": {"value": v, "unit": "iters/s", "cores": 1, "kind": "oracle",
                          "sample": f"{args.steps} oracle iterations after {args.warmup} warm-up, 1 BLAS thread"},
         "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

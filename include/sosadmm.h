@@ -46,7 +46,7 @@ typedef enum {
   SOSADMM_E_STRUCT = -2,    /* unsupported structure (e.g. low-rank width too large) */
   SOSADMM_E_FACTOR = -3,    /* I + A_low^T P^{-1} A_low not numerically SPD (impossible in exact arithmetic) */
   SOSADMM_E_CUDA = -4,      /* CUDA runtime error (message has the detail) */
-  SOSADMM_E_NCCL = -5,      /* reserved for the sharded mode */
+  SOSADMM_E_NCCL = -5,      /* NCCL unavailable or failed (sharded mode) */
   SOSADMM_E_NONFINITE = -6, /* non-finite iterate; message names the iteration */
   SOSADMM_E_OOM = -7        /* workspace too small / allocation failed */
 } sosadmm_err;
@@ -105,14 +105,35 @@ size_t sosadmm_workspace_size(const sosadmm_problem* prob);
  * h = M^{-1} zeta (zeta = (c, -b)) and 1 + zeta^T h; copy the data to the device; set u0, v0. */
 sosadmm_err sosadmm_setup(const sosadmm_problem* prob, const sosadmm_settings* settings, sosadmm_ctx** out);
 
+/* ---- Multi-GPU block sharding (north_star: "partition the blocks across the GPUs of
+ * one 8xB200 box and NCCL-allreduce the length-m A2 x partial sums over NVLink each iteration").
+ * Rank r owns the PSD blocks with block_owner[b] == r (the free columns are accounted by rank 0);
+ * every iteration each rank forms the partial gather sums over its columns and one
+ * ncclAllReduce(sum, FP64, 2m + 3) completes them; the Woodbury / HSDE scalar work is replicated and
+ * bit-identical on all ranks, the scatter / PSD projection / dual update touch owned blocks only.
+ * NCCL is resolved at run time from the process's libnccl.so.2 (E_NCCL if it cannot be loaded).
+ * sosadmm_nccl_unique_id writes SOSADMM_NCCL_ID_BYTES bytes (call on rank 0, broadcast with any
+ * transport, e.g. torch.distributed); every rank then calls sosadmm_setup_sharded with the same
+ * problem, settings.device = its GPU, the same id and the same block_owner (n_psd entries in
+ * [0, world)).  sosadmm_iterate / sosadmm_get_info / sosadmm_get_iterate are collectives on a
+ * sharded context (every rank must call them in the same order); sosadmm_get_iterate returns the
+ * full iterate on every rank.  The unit entry points return E_ARG on a sharded context. */
+#define SOSADMM_NCCL_ID_BYTES 128
+sosadmm_err sosadmm_nccl_unique_id(void* id);
+sosadmm_err sosadmm_setup_sharded(const sosadmm_problem* prob, const sosadmm_settings* settings, const void* nccl_id,
+                                  int32_t rank, int32_t world, const int32_t* block_owner, sosadmm_ctx** out);
+
 /* Run up to k ADMM iterations (`eq:ADMMSteps`) on the device, stopping early when the C9 rule
  * fires or max_iters is reached; every iteration's residuals are checked.  Asynchronous work is
  * completed before return; *out (may be NULL) receives the state after the last iteration. */
 sosadmm_err sosadmm_iterate(sosadmm_ctx* ctx, int64_t k, sosadmm_info* out);
 
-/* Same iterations launched without the CUDA graph, with CUDA events around each phase; adds the
- * phase durations (ms) to ms_phase[0..3] = {affine gather+t-phase, scatter, PSD projection,
- * pack/dual update}.  Used by bench.py for the per-kernel-class roofline. */
+/* Same iterations launched without the CUDA graph, with CUDA events (on the library's stream)
+ * around each phase; adds the phase durations (ms) to ms_phase[0..SOSADMM_NPHASE-1] = {affine
+ * gather..row update, scatter, small-block Jacobi projections, large-block tridiagonalisation,
+ * divide-and-conquer tridiagonal eigensolver, back-transform + reconstruction, pack / dual
+ * update}.  Used by bench.py for the per-kernel-class rooflines. */
+#define SOSADMM_NPHASE 7
 sosadmm_err sosadmm_iterate_profiled(sosadmm_ctx* ctx, int64_t k, sosadmm_info* out, double* ms_phase);
 
 /* Current info without iterating (residuals of u^k are computed on demand). */

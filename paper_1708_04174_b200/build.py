@@ -29,10 +29,24 @@ def stale() -> bool:
     return any(os.path.exists(d) and os.path.getmtime(d) > t for d in deps)
 
 
+def _nccl_include() -> list:
+    """nccl.h of the NCCL that torch loads (the nvidia-nccl wheel); only types are used at compile
+    time, the library is resolved at run time with dlopen (csrc/sosadmm.cu)."""
+    try:
+        import nvidia.nccl  # noqa: F401
+
+        d = os.path.join(list(nvidia.nccl.__path__)[0], "include")
+        if os.path.exists(os.path.join(d, "nccl.h")):
+            return ["-I", d]
+    except Exception:
+        pass
+    return []
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
-    cmd = [_nvcc()] + NVCC_FLAGS + ["-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES]
+    cmd = [_nvcc()] + NVCC_FLAGS + _nccl_include() + ["-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES] + ["-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -80,6 +80,7 @@ struct AffineArgs {
   const long long* cta_q0;
   int pos_ctas;
   const int* side;            // per block: 1 = matrix holds Pi(-a) = Pi(a) - a (large-block path)
+  const double* shard_scal;   // sharded mode (shard.cuh): all-reduced [orth dual, low dual, low dual0]
 };
 
 constexpr int GATHER_NT = 256;
@@ -215,26 +216,30 @@ __global__ void __launch_bounds__(TP_NT) k_tphase(AffineArgs a, int mode) {
   // low / free columns: c^T xi, dual residual of low columns, (A_low xi part already in gather)
   const double tau = st->tau, kappa = st->kappa, w3 = tau + kappa;
   double cx = 0.0, dl = 0.0, dl0 = 0.0;
+  const bool sharded = a.shard_scal != nullptr;  // low-column dual sums arrive all-reduced
   for (int j = tid; j < a.tl; j += TP_NT) {
     const int col = a.low_col[j];
     const double cj = a.c_low[j];
-    cx = fma(cj, a.xi[col], cx);
-    const double d0 = a.aty[j] + a.z[col];
-    const double d = d0 - cj * tau;
-    dl = fma(d, d, dl);
-    dl0 = fma(d0, d0, dl0);
+    cx = fma(cj, a.xi[col], cx);  // c vanishes off the (replicated) free columns
+    if (!sharded) {
+      const double d0 = a.aty[j] + a.z[col];
+      const double d = d0 - cj * tau;
+      dl = fma(d, d, dl);
+      dl0 = fma(d0, d0, dl0);
+    }
   }
-  for (int j = tid; j < a.n_empty; j += TP_NT) {
-    const double zj = a.z[a.empty_cols[j]];
-    dl = fma(zj, zj, dl);
-    dl0 = fma(zj, zj, dl0);
-  }
+  if (!sharded)
+    for (int j = tid; j < a.n_empty; j += TP_NT) {
+      const double zj = a.z[a.empty_cols[j]];
+      dl = fma(zj, zj, dl);
+      dl0 = fma(zj, zj, dl0);
+    }
   cx = block_sum<TP_NT>(cx, sh);
   if (tid == 0) bc[7] = cx;
   dl = block_sum<TP_NT>(dl, sh);
-  if (tid == 0) bc[8] = dl;
+  if (tid == 0) bc[8] = sharded ? a.shard_scal[1] : dl;
   dl0 = block_sum<TP_NT>(dl0, sh);
-  if (tid == 0) bc[9] = dl0;
+  if (tid == 0) bc[9] = sharded ? a.shard_scal[2] : dl0;
   __syncthreads();
   for (int k = 0; k < NPART; ++k) sums[k] = bc[k];
   cx = bc[7];

@@ -460,12 +460,15 @@ inline void large_block_recon(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool
   k_gemm_f64<<<gr, GM_NT, 0, s>>>(lb.gdesc + lb.recon, le.st, le.is, check);
 }
 
-inline void large_eig_launch(LargeEig& le, cudaStream_t s, bool check) {
-  for (auto& lb : le.blocks) {
-    large_block_tridiag(le, lb, s, check);
-    large_block_dc(le, lb, s, check);
-    large_block_recon(le, lb, s, check);
-  }
+// Stage-major over the large blocks; ev (optional, 3 events) is recorded after the
+// tridiagonalisations, after the divide-and-conquer solves and after the reconstructions.
+inline void large_eig_launch(LargeEig& le, cudaStream_t s, bool check, cudaEvent_t* ev = nullptr) {
+  for (auto& lb : le.blocks) large_block_tridiag(le, lb, s, check);
+  if (ev) cudaEventRecord(ev[0], s);
+  for (auto& lb : le.blocks) large_block_dc(le, lb, s, check);
+  if (ev) cudaEventRecord(ev[1], s);
+  for (auto& lb : le.blocks) large_block_recon(le, lb, s, check);
+  if (ev) cudaEventRecord(ev[2], s);
 }
 
 inline int large_eig_launches(const LargeEig& le) {

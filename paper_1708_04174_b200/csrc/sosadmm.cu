@@ -8,6 +8,8 @@
 #include "../../include/sosadmm.h"
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -20,11 +22,47 @@
 #include "affine.cuh"
 #include "psd_jacobi.cuh"
 #include "psd_large.cuh"
+#include "shard.cuh"
 #include "spdinv.cuh"
 
 namespace {
 
 constexpr size_t kAlign = 256;
+
+// NCCL is resolved at run time from the libnccl.so.2 already loaded by the process (torch's), so the
+// library itself loads without NCCL and there is a single NCCL copy per process.
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  if (!api.tried) {
+    api.tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+      api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
+      api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+      api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
+      api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.commDestroy && api.getErrorString;
+    }
+  }
+  return api;
+}
+
+struct ShardSpec {
+  int rank = 0, world = 1;
+  const int32_t* block_owner = nullptr;  // nullptr: every block on this rank
+  bool sharded = false;                  // true: NCCL partial-sum allreduce in the loop
+};
 
 struct Arena {
   char* base = nullptr;  // nullptr = dry run (size accounting only)
@@ -55,11 +93,12 @@ struct Analysis {
   std::vector<int> small_blk, large_blk;
   long long mat_total = 0;
   int max_small_N = 0;
+  std::vector<int> colown;  // 1: this rank accounts for the column in the sharded partial sums
 };
 
 // Column classification and the orthogonal / low-rank split (Proposition 1, P:302-311;
 // Proposition 3): a PSD column with at most one nonzero and c_j = 0 is orthogonal.
-sosadmm_err analyse(const sosadmm_problem* p, Analysis& an, std::string& msg) {
+sosadmm_err analyse(const sosadmm_problem* p, Analysis& an, std::string& msg, const ShardSpec& sp = ShardSpec()) {
   if (!p || p->m <= 0 || p->n_free < 0 || p->n_psd < 0 || !p->A_colptr || !p->b || !p->c) {
     msg = "null pointer or negative size in sosadmm_problem";
     return SOSADMM_E_ARG;
@@ -192,27 +231,38 @@ sosadmm_err analyse(const sosadmm_problem* p, Analysis& an, std::string& msg) {
         fill[r]++;
       }
   }
-  // PSD blocks
+  // PSD blocks (only the blocks this rank owns are scattered, projected and packed)
   long long col = an.t;
   an.mat_total = 0;
+  an.colown.assign(an.n, 0);
+  for (int j = 0; j < an.t; ++j) an.colown[j] = sp.rank == 0 ? 1 : 0;
   for (int b = 0; b < an.nblk; ++b) {
     const int N = p->psd_dim[b];
+    const int owner = sp.block_owner ? sp.block_owner[b] : sp.rank;
+    if (owner < 0 || owner >= sp.world) {
+      msg = "block_owner[" + std::to_string(b) + "] out of range";
+      return SOSADMM_E_ARG;
+    }
+    const bool mine = owner == sp.rank;
     an.blk_col.push_back(col);
     an.blk_N.push_back(N);
     an.blk_mat.push_back(an.mat_total);
     an.mat_total += (long long)N * N;
     const long long L = (long long)N * (N + 1) / 2;
-    for (long long q0 = 0; q0 < L; q0 += POS_PER_CTA) {
-      an.cta_blk.push_back(b);
-      an.cta_q0.push_back(q0);
+    if (mine) {
+      for (long long q = 0; q < L; ++q) an.colown[col + q] = 1;
+      for (long long q0 = 0; q0 < L; q0 += POS_PER_CTA) {
+        an.cta_blk.push_back(b);
+        an.cta_q0.push_back(q0);
+      }
+      if (N <= JAC_MAXN) {
+        an.small_blk.push_back(b);
+        an.max_small_N = std::max(an.max_small_N, N);
+      } else {
+        an.large_blk.push_back(b);
+      }
     }
     col += L;
-    if (N <= JAC_MAXN) {
-      an.small_blk.push_back(b);
-      an.max_small_N = std::max(an.max_small_N, N);
-    } else {
-      an.large_blk.push_back(b);
-    }
   }
   return SOSADMM_OK;
 }
@@ -279,6 +329,11 @@ struct sosadmm_ctx {
   long long launches = 0;
   // host mirrors for get_structure
   std::vector<int> row_of;
+  // sharded mode (shard.cuh)
+  ShardSpec sp;
+  ncclComm_t comm = nullptr;
+  ShardArgs sh{};
+  int nb_low = 1;
 };
 
 namespace {
@@ -307,7 +362,13 @@ struct DevPtrs {
   IterScal* is;
   long long *blk_col, *blk_mat, *cta_q0;
   int *blk_N, *cta_blk, *small_blk;
+  int* colown;
+  double *shbuf, *shpart;
 };
+
+int low_blocks(const Analysis& an) {
+  return std::max(1, std::max((an.tl + SH_NT / 32 - 1) / (SH_NT / 32), ((int)an.empty_cols.size() + SH_NT - 1) / SH_NT));
+}
 
 void carve(const Analysis& an, Arena& ar, DevPtrs& d, int gather_blocks) {
   const size_t m = an.m, n = an.n, tl = an.tl;
@@ -353,6 +414,9 @@ void carve(const Analysis& an, Arena& ar, DevPtrs& d, int gather_blocks) {
   d.cta_blk = ar.take<int>(an.cta_blk.size());
   d.cta_q0 = ar.take<long long>(an.cta_q0.size());
   d.small_blk = ar.take<int>(an.small_blk.size());
+  d.colown = ar.take<int>(n);
+  d.shbuf = ar.take<double>(2 * m + 3);
+  d.shpart = ar.take<double>(3 * (size_t)std::max(gather_blocks, low_blocks(an)));
 }
 
 size_t total_bytes(const Analysis& an) {
@@ -375,7 +439,21 @@ sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev) {
   cudaStream_t s = c->stream;
   const int tlw = std::max(1, (a.tl * 32 + 255) / 256);
   if (ev) cudaEventRecord(ev[0], s);
-  k_gather<<<c->gather_blocks, GATHER_NT, 0, s>>>(a);
+  if (c->sp.sharded) {
+    k_lowdual_part<<<c->nb_low, SH_NT, 0, s>>>(a, c->sh);
+    k_gather_part<<<c->gather_blocks, SH_NT, 0, s>>>(a, c->sh);
+    k_shard_scalars<<<1, SH_NT, 0, s>>>(a, c->sh, c->gather_blocks, c->nb_low);
+    const ncclResult_t nr = nccl().allReduce(c->sh.buf, c->sh.buf, 2 * (size_t)a.m + 3, ncclFloat64, ncclSum,
+                                             c->comm, s);
+    if (nr != ncclSuccess) {
+      c->err = SOSADMM_E_NCCL;
+      c->msg = std::string("ncclAllReduce: ") + nccl().getErrorString(nr);
+      return c->err;
+    }
+    k_gather_fin<<<c->gather_blocks, GATHER_NT, 0, s>>>(a, c->sh);
+  } else {
+    k_gather<<<c->gather_blocks, GATHER_NT, 0, s>>>(a);
+  }
   k_lowT<<<tlw, 256, 0, s>>>(a);
   k_kinv<<<tlw, 256, 0, s>>>(a);
   k_tphase<<<1, TP_NT, 0, s>>>(a, mode_full ? 0 : 1);
@@ -386,16 +464,20 @@ sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev) {
   if (ev) cudaEventRecord(ev[2], s);
   if (!c->an.small_blk.empty())
     k_psd_jacobi<<<(int)c->an.small_blk.size(), JAC_NT, jacobi_smem_bytes(c->an.max_small_N), s>>>(c->ja);
-  if (!c->an.large_blk.empty()) large_eig_launch(c->le, s, true);
   if (ev) cudaEventRecord(ev[3], s);
+  if (!c->an.large_blk.empty()) {
+    large_eig_launch(c->le, s, true, ev ? ev + 4 : nullptr);
+  } else if (ev) {
+    for (int q = 4; q < 7; ++q) cudaEventRecord(ev[q], s);
+  }
   if (a.pos_ctas > 0) k_pack<<<a.pos_ctas, POS_NT, 0, s>>>(a, nullptr, 1);
   else k_commit<<<1, 1, 0, s>>>(a);
-  if (ev) cudaEventRecord(ev[4], s);
+  if (ev) cudaEventRecord(ev[7], s);
   return SOSADMM_OK;
 }
 
 int64_t count_launches(const sosadmm_ctx* c) {
-  int64_t k = 6;  // gather, lowT, kinv, tphase, rowupdate, pack/commit
+  int64_t k = c->sp.sharded ? 9 : 6;  // gather (sharded: 4 kernels + allreduce), lowT, kinv, tphase, rowupdate, pack
   if (c->aa.pos_ctas > 0) k += 1;
   if (!c->an.small_blk.empty()) k += 1;
   if (!c->an.large_blk.empty()) k += large_eig_launches(c->le);
@@ -446,13 +528,15 @@ size_t sosadmm_workspace_size(const sosadmm_problem* prob) {
   return total_bytes(an);
 }
 
-sosadmm_err sosadmm_setup(const sosadmm_problem* prob, const sosadmm_settings* settings, sosadmm_ctx** out) {
+static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_settings* settings, const ShardSpec& sp,
+                              const void* nccl_id, sosadmm_ctx** out) {
   if (!out) return SOSADMM_E_ARG;
   *out = nullptr;
   sosadmm_ctx* c = new sosadmm_ctx();
   *out = c;
+  c->sp = sp;
   Analysis& an = c->an;
-  c->err = analyse(prob, an, c->msg);
+  c->err = analyse(prob, an, c->msg, sp);
   if (c->err != SOSADMM_OK) return c->err;
   if (settings) {
     c->tol = settings->tol > 0 ? settings->tol : 1e-4;
@@ -460,6 +544,21 @@ sosadmm_err sosadmm_setup(const sosadmm_problem* prob, const sosadmm_settings* s
     c->device = settings->device;
   }
   CK_CTX(c, cudaSetDevice(c->device));
+  if (sp.sharded) {
+    if (!nccl().ok) {
+      c->err = SOSADMM_E_NCCL;
+      c->msg = "libnccl.so.2 could not be loaded";
+      return c->err;
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    const ncclResult_t nr = nccl().commInitRank(&c->comm, sp.world, id, sp.rank);
+    if (nr != ncclSuccess) {
+      c->err = SOSADMM_E_NCCL;
+      c->msg = std::string("ncclCommInitRank: ") + nccl().getErrorString(nr);
+      return c->err;
+    }
+  }
   if (settings && settings->stream) {
     c->stream = (cudaStream_t)settings->stream;
   } else {
@@ -591,6 +690,8 @@ sosadmm_err sosadmm_setup(const sosadmm_problem* prob, const sosadmm_settings* s
   CK_CTX(c, h2d(d.cta_blk, an.cta_blk, s));
   CK_CTX(c, h2d(d.cta_q0, an.cta_q0, s));
   CK_CTX(c, h2d(d.small_blk, an.small_blk, s));
+  CK_CTX(c, h2d(d.colown, an.colown, s));
+  CK_CTX(c, cudaMemsetAsync(d.shbuf, 0, sizeof(double) * (2 * (size_t)an.m + 3), s));
   CK_CTX(c, cudaMemsetAsync(d.xi, 0, sizeof(double) * an.n, s));
   CK_CTX(c, cudaMemsetAsync(d.z, 0, sizeof(double) * an.n, s));
   CK_CTX(c, cudaMemsetAsync(d.y, 0, sizeof(double) * an.m, s));
@@ -622,6 +723,12 @@ sosadmm_err sosadmm_setup(const sosadmm_problem* prob, const sosadmm_settings* s
   a.cta_blk = d.cta_blk; a.cta_q0 = d.cta_q0; a.pos_ctas = (int)an.cta_blk.size();
   c->d_tmp = d.tmp;
   a.side = nullptr;
+  a.shard_scal = sp.sharded ? d.shbuf + 2 * (size_t)an.m : nullptr;
+  c->nb_low = low_blocks(an);
+  c->sh.colown = d.colown;
+  c->sh.buf = d.shbuf;
+  c->sh.part = d.shpart;
+  c->sh.nparts = std::max(c->gather_blocks, c->nb_low);
   JacobiArgs& ja = c->ja;
   ja.mats = d.mats; ja.blk_mat = d.blk_mat; ja.blk_N = d.blk_N; ja.small_blk = d.small_blk;
   ja.st = d.st; ja.is = d.is; ja.check_state = 1;
@@ -646,6 +753,34 @@ sosadmm_err sosadmm_setup(const sosadmm_problem* prob, const sosadmm_settings* s
   c->launches = count_launches(c);
   CK_CTX(c, cudaStreamSynchronize(s));
   return SOSADMM_OK;
+}
+
+sosadmm_err sosadmm_setup(const sosadmm_problem* prob, const sosadmm_settings* settings, sosadmm_ctx** out) {
+  return setup_impl(prob, settings, ShardSpec(), nullptr, out);
+}
+
+sosadmm_err sosadmm_nccl_unique_id(void* id) {
+  if (!id) return SOSADMM_E_ARG;
+  if (!nccl().ok) return SOSADMM_E_NCCL;
+  ncclUniqueId u;
+  if (nccl().getUniqueId(&u) != ncclSuccess) return SOSADMM_E_NCCL;
+  std::memcpy(id, &u, sizeof(u));
+  return SOSADMM_OK;
+}
+
+sosadmm_err sosadmm_setup_sharded(const sosadmm_problem* prob, const sosadmm_settings* settings, const void* nccl_id,
+                                  int32_t rank, int32_t world, const int32_t* block_owner, sosadmm_ctx** out) {
+  if (!out) return SOSADMM_E_ARG;
+  if (!nccl_id || world < 1 || rank < 0 || rank >= world || !block_owner) {
+    *out = nullptr;
+    return SOSADMM_E_ARG;
+  }
+  ShardSpec sp;
+  sp.rank = rank;
+  sp.world = world;
+  sp.block_owner = block_owner;
+  sp.sharded = true;
+  return setup_impl(prob, settings, sp, nccl_id, out);
 }
 
 static sosadmm_err build_graph(sosadmm_ctx* c) {
@@ -675,22 +810,24 @@ sosadmm_err sosadmm_iterate_profiled(sosadmm_ctx* c, int64_t k, sosadmm_info* ou
   if (!c) return SOSADMM_E_ARG;
   if (c->err) return c->err;
   CK_CTX(c, cudaSetDevice(c->device));
-  std::vector<cudaEvent_t> ev((size_t)5 * std::max<int64_t>(k, 1));
+  constexpr int NE = SOSADMM_NPHASE + 1;
+  std::vector<cudaEvent_t> ev((size_t)NE * std::max<int64_t>(k, 1));
   for (auto& e : ev) CK_CTX(c, cudaEventCreate(&e));
-  for (int64_t i = 0; i < k; ++i) launch_iteration(c, 1, &ev[5 * i]);
+  for (int64_t i = 0; i < k; ++i)
+    if (launch_iteration(c, 1, &ev[NE * i])) return c->err;
   launch_iteration(c, 0, nullptr);
   if (check_async(c)) return c->err;
   CK_CTX(c, cudaStreamSynchronize(c->stream));
-  double acc[4] = {0, 0, 0, 0};
+  double acc[SOSADMM_NPHASE] = {};
   for (int64_t i = 0; i < k; ++i)
-    for (int p = 0; p < 4; ++p) {
+    for (int p = 0; p < SOSADMM_NPHASE; ++p) {
       float ms = 0;
-      cudaEventElapsedTime(&ms, ev[5 * i + p], ev[5 * i + p + 1]);
+      cudaEventElapsedTime(&ms, ev[NE * i + p], ev[NE * i + p + 1]);
       acc[p] += ms;
     }
   for (auto& e : ev) cudaEventDestroy(e);
   if (ms_phase)
-    for (int p = 0; p < 4; ++p) ms_phase[p] += acc[p];
+    for (int p = 0; p < SOSADMM_NPHASE; ++p) ms_phase[p] += acc[p];
   return read_info(c, out);
 }
 
@@ -709,6 +846,24 @@ sosadmm_err sosadmm_get_iterate(sosadmm_ctx* c, double* xi, double* y, double* z
   if (c->err) return c->err;
   CK_CTX(c, cudaSetDevice(c->device));
   const AffineArgs& a = c->aa;
+  if (c->sp.sharded) {  // collective: assemble the owned entries of every rank (exact: x + 0 = x)
+    for (int v = 0; v < 2; ++v) {
+      double* host = v == 0 ? xi : z;
+      const double* src = v == 0 ? a.xi : a.z;
+      k_mask_owned<<<(a.n + 255) / 256, 256, 0, c->stream>>>(src, c->sh.colown, c->d_tmp, a.n);
+      const ncclResult_t nr = nccl().allReduce(c->d_tmp, c->d_tmp, (size_t)a.n, ncclFloat64, ncclSum, c->comm,
+                                               c->stream);
+      if (nr != ncclSuccess) {
+        c->err = SOSADMM_E_NCCL;
+        c->msg = std::string("ncclAllReduce: ") + nccl().getErrorString(nr);
+        return c->err;
+      }
+      if (host) CK_CTX(c, cudaMemcpyAsync(host, c->d_tmp, sizeof(double) * a.n, cudaMemcpyDeviceToHost, c->stream));
+      CK_CTX(c, cudaStreamSynchronize(c->stream));
+    }
+    xi = nullptr;
+    z = nullptr;
+  }
   if (xi) CK_CTX(c, cudaMemcpyAsync(xi, a.xi, sizeof(double) * a.n, cudaMemcpyDeviceToHost, c->stream));
   if (z) CK_CTX(c, cudaMemcpyAsync(z, a.z, sizeof(double) * a.n, cudaMemcpyDeviceToHost, c->stream));
   if (y) CK_CTX(c, cudaMemcpyAsync(y, a.y, sizeof(double) * a.m, cudaMemcpyDeviceToHost, c->stream));
@@ -760,6 +915,7 @@ sosadmm_err sosadmm_project_affine(sosadmm_ctx* c, const double* w1, const doubl
                                    double* u2, double* u3) {
   if (!c) return SOSADMM_E_ARG;
   if (c->err) return c->err;
+  if (c->sp.sharded) return SOSADMM_E_ARG;  // unit entry points are single-GPU only
   CK_CTX(c, cudaSetDevice(c->device));
   const AffineArgs& a = c->aa;
   const int n = a.n, m = a.m;
@@ -797,6 +953,7 @@ sosadmm_err sosadmm_project_affine(sosadmm_ctx* c, const double* w1, const doubl
 sosadmm_err sosadmm_project_psd(sosadmm_ctx* c, int32_t block, const double* a_svec, double* out_svec) {
   if (!c) return SOSADMM_E_ARG;
   if (c->err) return c->err;
+  if (c->sp.sharded) return SOSADMM_E_ARG;  // unit entry points are single-GPU only
   if (block < 0 || block >= c->an.nblk) return SOSADMM_E_ARG;
   CK_CTX(c, cudaSetDevice(c->device));
   const AffineArgs& a = c->aa;
@@ -838,6 +995,7 @@ void sosadmm_destroy(sosadmm_ctx* c) {
   if (c->graph) cudaGraphExecDestroy(c->graph);
   if (c->graph_raw) cudaGraphDestroy(c->graph_raw);
   large_eig_free(c->le);
+  if (c->comm) nccl().commDestroy(c->comm);
   if (c->own_mem) cudaFree(c->own_mem);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;

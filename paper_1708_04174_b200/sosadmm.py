@@ -18,7 +18,8 @@ LIB_PATH = os.path.join(_HERE, "libsosadmm.so")
 STATUS = {0: "RUNNING", 1: "OPTIMAL", 2: "PRIMAL_INFEASIBLE", 3: "DUAL_INFEASIBLE", 4: "MAX_ITERS",
           5: "INCONCLUSIVE"}
 
-EXPORTS = ["sosadmm_workspace_size", "sosadmm_setup", "sosadmm_iterate", "sosadmm_iterate_profiled",
+EXPORTS = ["sosadmm_workspace_size", "sosadmm_setup", "sosadmm_setup_sharded", "sosadmm_nccl_unique_id",
+           "sosadmm_iterate", "sosadmm_iterate_profiled",
            "sosadmm_get_info", "sosadmm_get_iterate", "sosadmm_set_iterate", "sosadmm_get_structure",
            "sosadmm_project_affine", "sosadmm_project_psd", "sosadmm_launches_per_iter", "sosadmm_destroy",
            "sosadmm_strerror", "sosadmm_last_error_message"]
@@ -66,6 +67,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.sosadmm_workspace_size.argtypes = [ctypes.POINTER(_Problem)]
     lib.sosadmm_workspace_size.restype = ctypes.c_size_t
     lib.sosadmm_setup.argtypes = [ctypes.POINTER(_Problem), ctypes.POINTER(_Settings), ctypes.POINTER(V)]
+    lib.sosadmm_setup_sharded.argtypes = [ctypes.POINTER(_Problem), ctypes.POINTER(_Settings), ctypes.c_char_p, I32,
+                                          I32, ctypes.POINTER(I32), ctypes.POINTER(V)]
+    lib.sosadmm_nccl_unique_id.argtypes = [ctypes.c_char_p]
     lib.sosadmm_iterate.argtypes = [V, I64, ctypes.POINTER(_Info)]
     lib.sosadmm_iterate_profiled.argtypes = [V, I64, ctypes.POINTER(_Info), P]
     lib.sosadmm_get_info.argtypes = [V, ctypes.POINTER(_Info)]
@@ -82,7 +86,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.sosadmm_strerror.restype = ctypes.c_char_p
     lib.sosadmm_last_error_message.argtypes = [V]
     lib.sosadmm_last_error_message.restype = ctypes.c_char_p
-    for f in ["sosadmm_setup", "sosadmm_iterate", "sosadmm_iterate_profiled", "sosadmm_get_info",
+    for f in ["sosadmm_setup", "sosadmm_setup_sharded", "sosadmm_nccl_unique_id", "sosadmm_iterate", "sosadmm_iterate_profiled", "sosadmm_get_info",
               "sosadmm_get_iterate", "sosadmm_set_iterate", "sosadmm_get_structure", "sosadmm_project_affine",
               "sosadmm_project_psd"]:
         getattr(lib, f).restype = ctypes.c_int
@@ -94,11 +98,30 @@ def _dptr(a: np.ndarray):
     return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
 
 
+NCCL_ID_BYTES = 128
+NPHASE = 7  # SOSADMM_NPHASE
+PHASES = ["affine", "scatter", "jacobi", "tridiag", "dc", "backtransform_recon", "pack"]
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (rank 0 of a sharded solve creates it; the caller broadcasts it)."""
+    import torch  # noqa: F401  (loads torch's libnccl.so.2 first, so the library resolves the same NCCL)
+
+    lib = load_library()
+    buf = ctypes.create_string_buffer(NCCL_ID_BYTES)
+    err = lib.sosadmm_nccl_unique_id(buf)
+    if err != 0:
+        raise RuntimeError(f"sosadmm_nccl_unique_id: {lib.sosadmm_strerror(err).decode()} ({err})")
+    return buf.raw
+
+
 class SosAdmm:
     """One SOS-derived SDP on one GPU: setup(A, b, c, cone dims) once, then iterate(k)."""
 
     def __init__(self, A, b, c, n_free: int, psd_dims, tol: float = 1e-4, max_iters: int = 2000,
-                 device: int = 0):
+                 device: int = 0, shard=None):
+        """shard = (rank, world, nccl_id, block_owner) runs the multi-GPU block-sharded mode
+        (sosadmm_setup_sharded); iterate / info / get_iterate are then collectives."""
         import torch  # device memory + stream only
 
         if not torch.cuda.is_available():
@@ -130,7 +153,18 @@ class SosAdmm:
         st = _Settings(tol, max_iters, 1, device, ctypes.c_void_p(self.stream.cuda_stream),
                        ctypes.c_void_p(self._ws.data_ptr()), int(nbytes))
         self._ctx = ctypes.c_void_p()
-        err = self.lib.sosadmm_setup(ctypes.byref(self._prob), ctypes.byref(st), ctypes.byref(self._ctx))
+        self.shard = shard
+        if shard is None:
+            err = self.lib.sosadmm_setup(ctypes.byref(self._prob), ctypes.byref(st), ctypes.byref(self._ctx))
+        else:
+            rank, world, nccl_id, owner = shard
+            self._owner = np.ascontiguousarray(owner, dtype=np.int32)
+            if len(self._owner) != len(self._dims) or len(nccl_id) != NCCL_ID_BYTES:
+                raise ValueError("shard: block_owner needs one entry per PSD block and a 128-byte NCCL id")
+            err = self.lib.sosadmm_setup_sharded(ctypes.byref(self._prob), ctypes.byref(st), bytes(nccl_id),
+                                                 int(rank), int(world),
+                                                 self._owner.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                                 ctypes.byref(self._ctx))
         self._check(err, "setup")
         self.workspace_bytes = int(nbytes)
 
@@ -150,7 +184,7 @@ class SosAdmm:
 
     def iterate_profiled(self, k: int):
         info = _Info()
-        ms = np.zeros(4)
+        ms = np.zeros(NPHASE)
         self._check(self.lib.sosadmm_iterate_profiled(self._ctx, int(k), ctypes.byref(info), _dptr(ms)),
                     "iterate_profiled")
         return info.as_dict(), ms
