@@ -20,7 +20,7 @@ int sosadmm_debug_tridiag(int N, const double* A, double* d, double* e, double* 
 int sosadmm_debug_stedc(int N, const double* d, const double* e, double* lam, double* Z);
 /* In-place inverse of the SPD t x t matrix K (setup-time cache of I + A_low^T P^{-1} A_low). */
 int sosadmm_debug_spdinv(int t, double* K);
-/* Timing probe of the tridiagonalisation: prof ((N-2) x 8 clock64 stamps of CTA 0 at the phase
+/* Timing probe of the tridiagonalisation: prof ((N-2) x 16 clock64 stamp slots of CTA 0 at the phase
  * boundaries of every Householder step), ms = CUDA-event time of one launch after a warm-up. */
 int sosadmm_debug_tridiag_prof(int N, const double* A, long long* prof, float* ms);
 #ifdef __cplusplus

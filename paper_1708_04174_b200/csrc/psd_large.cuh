@@ -371,8 +371,9 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     }
   }
   if (!le.blocks.empty()) {
-    for (TridiagKernel kt : {k_tridiag<2, false>, k_tridiag<4, false>, k_tridiag<7, false>, k_tridiag<10, false>,
-                             k_tridiag<2, true>, k_tridiag<4, true>, k_tridiag<7, true>, k_tridiag<10, true>}) {
+#define TRD_PTR(MB, CCX) k_tridiag<MB, CCX>,
+    for (TridiagKernel kt : {TRD_KERNELS(TRD_PTR)}) {
+#undef TRD_PTR
       if (err == cudaSuccess) err = cudaFuncSetAttribute(kt, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (err == cudaSuccess)
         err = cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, TRD_MAX_DYN_SMEM);
@@ -405,10 +406,10 @@ inline void large_block_tridiag(LargeEig& le, LargeBlock& lb, cudaStream_t s, bo
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, tridiag_kernel(lb.N, false), lb.ta);
+    cudaLaunchKernelEx(&cfg, tridiag_kernel_mc(tridiag_maxb(lb.N), lb.C), lb.ta);
   }
   if (lb.ksw < lb.N - 2)
-    tridiag_kernel(lb.N, true)<<<1, TRD_NT, lb.tail_smem, s>>>(lb.ta_tail);
+    tridiag_kernel_mc(tridiag_maxb(lb.N), 1)<<<1, TRD_NT, lb.tail_smem, s>>>(lb.ta_tail);
 }
 
 inline void large_block_dc(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool check) {

@@ -1127,8 +1127,8 @@ extern "C" int sosadmm_debug_spdinv(int t, double* K) {
   return rc == 0 ? 0 : (rc == 1 ? -3 : -4);
 }
 
-// Timing probe of the cluster tridiagonalisation: prof receives 8 clock64 stamps per step of CTA 0
-// ((N - 2) x 8), ms the CUDA-event time of one launch (after a warm-up launch).
+// Timing probe of the cluster tridiagonalisation: prof receives 16 clock64 stamp slots per step of
+// CTA 0 ((N - 2) x 16), ms the CUDA-event time of one launch (after a warm-up launch).
 extern "C" int sosadmm_debug_tridiag_prof(int N, const double* A, long long* prof, float* ms) {
   if (N < 3) return -1;
   DebugLarge dl;
@@ -1136,8 +1136,8 @@ extern "C" int sosadmm_debug_tridiag_prof(int N, const double* A, long long* pro
   if (rc) return rc;
   LargeBlock& lb = dl.le.blocks[0];
   long long* dprof;
-  if (cudaMalloc(&dprof, sizeof(long long) * 8 * N)) return -7;
-  cudaMemsetAsync(dprof, 0, sizeof(long long) * 8 * N, dl.s);
+  if (cudaMalloc(&dprof, sizeof(long long) * 16 * N)) return -7;
+  cudaMemsetAsync(dprof, 0, sizeof(long long) * 16 * N, dl.s);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -1152,7 +1152,7 @@ extern "C" int sosadmm_debug_tridiag_prof(int N, const double* A, long long* pro
   cudaError_t err = cudaStreamSynchronize(dl.s);
   if (err == cudaSuccess) {
     cudaEventElapsedTime(ms, e0, e1);
-    cudaMemcpy(prof, dprof, sizeof(long long) * 8 * (N - 2), cudaMemcpyDeviceToHost);
+    cudaMemcpy(prof, dprof, sizeof(long long) * 16 * (N - 2), cudaMemcpyDeviceToHost);
   }
   cudaFree(dprof);
   cudaEventDestroy(e0);

@@ -102,6 +102,35 @@ __device__ __forceinline__ double trd_sum16(const double* p, int n, int stride) 
   return v[0];
 }
 
+// Column block of warp w's t-th slot: a "snake" order (w, 31 - w, 32 + w, 63 - w, ...) so that the
+// triangular work (block bb covers rows >= 8 bb) is balanced over the warps; increasing in t.
+__device__ __forceinline__ int trd_block(int w, int t) { return TRD_NW * t + ((t & 1) ? TRD_NW - 1 - w : w); }
+
+// fixed-order sum of p[0..n), n <= 16, over the lanes of a warp (xor tree within each half-warp;
+// every lane gets the result, the same value in every warp and CTA)
+__device__ __forceinline__ double trd_lane_sum16(const double* p, int n) {
+  const int l = threadIdx.x & 15;  // both half-warps compute the same sum
+  double v = (l < n) ? p[l] : 0.0;
+  v += __shfl_xor_sync(0xffffffffu, v, 8);
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  return v;
+}
+
+// fixed-order sum of p[0..CC) (compile-time count: unrolled, unpredicated loads and a balanced tree)
+template <int CC>
+__device__ __forceinline__ double trd_sumc(const double* p) {
+  double v[CC];
+#pragma unroll
+  for (int c = 0; c < CC; ++c) v[c] = p[c];
+#pragma unroll
+  for (int h = CC / 2; h >= 1; h >>= 1)
+#pragma unroll
+    for (int c = 0; c < h; ++c) v[c] += v[c + h];
+  return v[0];
+}
+
 // fixed-order block sum over TRD_NT threads; result valid in every thread
 __device__ __forceinline__ double trd_block_sum(double v, double* red) {
   v = warp_sum(v);
@@ -112,26 +141,31 @@ __device__ __forceinline__ double trd_block_sum(double v, double* red) {
   return trd_sum16(red, TRD_NW, 1);
 }
 
-// Shared-memory layout (doubles): xt[2][N] wb[N] | per own slot (S slots): vown[2][S] wown[S]
-// pown[S] xs[S] qr[C][S] rp[NW][S] | scalars sd[C] se[C] ss[C] red[32] | rows.
+// Shared-memory layout (doubles): xt[2][N] wb[N] | per own slot (S slots): wown[S] xs[S] qr[C][S]
+// rp[NW][S] | scalars sd[C] se[C] ss[C] red[32] | rows.
 __host__ __device__ inline long long trd_fixed_doubles(int N, int C, int S) {
-  return 3LL * N + 5LL * S + (long long)C * S + (long long)TRD_NW * S + 3LL * C + 32;
+  return 3LL * N + 2LL * S + (long long)C * S + (long long)TRD_NW * S + 3LL * C + 32;
 }
 __host__ __device__ inline int trd_log2(int C) { return C >= 16 ? 4 : (C >= 8 ? 3 : (C >= 4 ? 2 : (C >= 2 ? 1 : 0))); }
 
-// k_tridiag<MAXB, SOLO> runs Householder steps [kb, ke) of one block.
-//   cluster head (SOLO = false, C in {2,4,8,16}, kb = 0): if ke < N - 2 it stops after step ke - 1 and
+// k_tridiag<MAXB, CC> runs Householder steps [kb, ke) of one block; CC is the cluster size (compile
+// time, so every fixed-order C-term sum is an unrolled tree), CC = 1 the single-CTA variant (SOLO).
+//   cluster head (SOLO = false, C in {4,8,16}, kb = 0): if ke < N - 2 it stops after step ke - 1 and
 //     hands its state over through global memory: the unfinished trailing rows i >= ke (entries
 //     ke..i, still owing the lazy rank-2 update of step ke - 1) go back to the block matrix, and
 //     hand[] = [x~_ke (N), x~_{ke-1} (N), w_{ke-1} (N), ||x~_ke[ke+1:]||^2, scale_{ke-1}];
 //   single-CTA tail (SOLO = true, C = 1, kb = ke of the head): resumes from that state with local
-//     stores and __syncthreads in place of the DSMEM exchanges, where the per-step fixed cost of the
-//     cluster (two exchange latencies) would dominate the shrinking trailing work.
-template <int MAXB, bool SOLO>
+//     stores and __syncthreads in place of the DSMEM exchanges.
+// Scalar work is done by one warp (reflector) or by the own-row threads (Phase Y) only; the other
+// warps only run the fused pass and the exchanges (redundant FP64 div/sqrt in 16 warps cost issue
+// slots, measured).  v_k on a row is recomputed as x~_k[i] * scale_k (1 at row k+1).
+template <int MAXB, int CC>
 __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
   if (a.check_state && (a.st->done || !a.is->proceed)) return;
-  const int C = SOLO ? 1 : a.C, N = a.N;
-  const int logC = trd_log2(C);
+  constexpr bool SOLO = CC == 1;
+  constexpr int C = CC;
+  constexpr int logC = CC >= 16 ? 4 : (CC >= 8 ? 3 : (CC >= 4 ? 2 : (CC >= 2 ? 1 : 0)));
+  const int N = a.N;
   const int kb = a.kb, ke = min(a.ke, N - 2);
   const int me = SOLO ? 0 : (int)trd_cluster_rank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -146,10 +180,8 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
   extern __shared__ __align__(16) double sm[];
   double* xt = sm;                 // [2][N] x~_k: the column that defines v_k (allgathered), by parity
   double* wb = xt + 2 * N;         // w_{k-1} (allgathered)
-  double* vown = wb + N;           // [2][S] v_k on own rows, by step parity
-  double* wown = vown + 2 * S;     // w on own rows
-  double* pown = wown + S;         // own row dots
-  double* xs = pown + S;           // updated column on own rows (Phase Y)
+  double* wown = wb + N;           // w on own rows
+  double* xs = wown + S;           // updated column on own rows (Phase Y)
   double* qr = xs + S;             // [C][S] reduce-scatter receive
   double* rp = qr + C * S;         // [NW][S] per-warp row partials
   double* sd = rp + TRD_NW * S;    // [C] partial v^T A v
@@ -159,7 +191,7 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
   double* rows = red + 32;
   __shared__ int roff[TRD_MAXOWN];  // smem offset of own row slot q - qlo, -1 = spilled to global
   __shared__ int nspill_s;
-  __shared__ double qk1_s;
+  __shared__ double qk1_s, scal_s[2];
   __shared__ __align__(8) uint64_t barQ, barY;
 
   if (tid == 0) {
@@ -200,10 +232,14 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     double* dst = rowptr_s(q);
     for (int j = jb + tid; j <= i; j += TRD_NT) dst[j] = src[j];
   }
+  double* wo_own = wown - qlo;  // indexed by absolute slot q
+  double* xso = xs - qlo;
   double scale_prev = 0.0;
   if (kb == 0) {
-    for (int j = tid; j < N; j += TRD_NT) wb[j] = 0.0;
-    for (int q = tid; q < 2 * S; q += TRD_NT) vown[q] = 0.0;
+    for (int j = tid; j < N; j += TRD_NT) {
+      wb[j] = 0.0;
+      xt[N + j] = 0.0;  // x~_{-1}: read (times scale_{-1} = 0) by step 0
+    }
     for (int q = tid; q < S; q += TRD_NT) wown[q] = 0.0;
   } else {  // resume from the head's hand-over state
     const int pk = kb & 1;
@@ -214,11 +250,7 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     }
     if (tid == 0) ss[0] = a.hand[3 * N];
     scale_prev = a.hand[3 * N + 1];
-    for (int q = qlo + tid; q < nown; q += TRD_NT) {
-      const int i = me + q * C;  // v_{kb-1}[i]: 1 at row kb, x~_{kb-1}[i] scale_{kb-1} below
-      vown[(pk ^ 1) * S + q - qlo] = (i == kb) ? 1.0 : a.hand[N + i] * scale_prev;
-      wown[q - qlo] = a.hand[2 * N + i];
-    }
+    for (int q = qlo + tid; q < nown; q += TRD_NT) wo_own[q] = a.hand[2 * N + me + q * C];
   }
   if (!SOLO) trd_cluster_sync();  // barriers initialised and every CTA running before the first remote store
   else __syncthreads();
@@ -252,77 +284,77 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
 
   const bool prof = a.prof != nullptr && me == 0 && tid == 0;
 #define TRD_STAMP(ph) \
-  if (prof) a.prof[(size_t)k * 8 + (ph)] = clock64();
+  if (prof) a.prof[(size_t)k * 16 + (ph)] = clock64();
   for (int k = kb; k < ke; ++k) {
     const int par = k & 1;
     TRD_STAMP(0)
     const double* xk = xt + par * N;          // x~_k
     const double* xkm = xt + (par ^ 1) * N;   // x~_{k-1}
     const int qs1 = first_slot(k + 1), qs2 = first_slot(k + 2);
-    if (!SOLO && tid == 0) trd_bar_expect(&barQ, (unsigned)(8 * (C * (nown - qs2) + 2 * C)));
-    // ---- Phase A: the reflector of column k (every CTA computes it redundantly, same order) ----
-    const double sig = trd_sum16(ss, C, 1);
-    const double alpha = xk[k + 1];
-    double tk, beta, scale;
-    if (sig == 0.0) {
-      tk = 0.0;
-      beta = alpha;
-      scale = 0.0;
-    } else {
-      beta = -copysign(sqrt(fma(alpha, alpha, sig)), alpha);
-      tk = (beta - alpha) / beta;
-      scale = 1.0 / (alpha - beta);
-    }
-    if (me == (k & (C - 1))) {
-      for (int j = k + 1 + tid; j < N; j += TRD_NT) a.V[(size_t)k * N + j] = (j == k + 1) ? 1.0 : xk[j] * scale;
-      if (tid == 0) {
-        a.e[k] = beta;
-        a.tau[k] = tk;
+    const int nb = (N - k - 1 + 7) >> 3;      // 8-column blocks of the trailing matrix
+    auto nwarps_of_row = [&](int i) { return min(min(TRD_NW, nb), (i - k - 1) / 8 + 1); };  // warps reaching row i
+    // ---- Phase A: the reflector of column k, by warp 0 (same order in every CTA) ----
+    if (warp == 0) {
+      if (!SOLO && lane == 0) trd_bar_expect(&barQ, (unsigned)(8 * (C * (nown - qs2) + 2 * C)));
+      const double sig = trd_lane_sum16(ss, C);
+      const double alpha = xk[k + 1];
+      double tk = 0.0, beta = alpha, scale = 0.0;
+      if (sig != 0.0) {
+        beta = -copysign(sqrt(fma(alpha, alpha, sig)), alpha);
+        tk = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      TRD_STAMP(8)
+      if (lane == 0) {
+        scal_s[0] = tk;
+        scal_s[1] = scale;
+        if (me == (k & (C - 1))) {
+          a.e[k] = beta;
+          a.tau[k] = tk;
+        }
       }
     }
-    double* vcur = vown + par * S - qlo;          // indexed by absolute slot q
-    const double* vprev = vown + (par ^ 1) * S - qlo;
-    double* wo_own = wown - qlo;
-    double* po = pown - qlo;
-    double* xso = xs - qlo;
-    for (int q = qs1 + tid; q < nown; q += TRD_NT) {
-      const int i = me + q * C;
-      vcur[q] = (i == k + 1) ? 1.0 : xk[i] * scale;
-    }
+    __syncthreads();
+    TRD_STAMP(9)
+    const double tk = scal_s[0], scale = scal_s[1];
+    if (me == (k & (C - 1)))
+      for (int j = k + 1 + tid; j < N; j += TRD_NT) a.V[(size_t)k * N + j] = (j == k + 1) ? 1.0 : xk[j] * scale;
     // this lane's columns: blocks bb = warp + 16 t of 8 columns starting at k + 1
-    const int nb = (N - k - 1 + 7) >> 3;
-    const int nbt = nb > warp ? (nb - warp + TRD_NW - 1) / TRD_NW : 0;  // blocks of this warp
+    int nbt = 0;  // blocks of this warp (trd_block is increasing in t)
+#pragma unroll
+    for (int t = 0; t < MAXB; ++t) nbt += trd_block(warp, t) < nb ? 1 : 0;
     double vn[MAXB], vo[MAXB], wo[MAXB], qa[MAXB];
 #pragma unroll
     for (int t = 0; t < MAXB; ++t) {
-      const int j = k + 1 + 8 * (warp + TRD_NW * t) + cc;
+      const int j = k + 1 + 8 * trd_block(warp, t) + cc;
       const bool ok = t < nbt && j < N;
       vn[t] = !ok ? 0.0 : (j == k + 1 ? 1.0 : xk[j] * scale);
       vo[t] = ok ? xkm[j] * scale_prev : 0.0;  // scale_prev = 0 at k = 0: no pending update
       wo[t] = ok ? wb[j] : 0.0;
       qa[t] = 0.0;
     }
-    __syncthreads();
     TRD_STAMP(1)
 
     // ---- Phase X: fused rank-2 update of step k-1 and symv with v_k over own rows i >= k+1 ----
-    // rows in groups of 4 (lane row lr), processed from slot qb to qe with row pointers from rp_of
-    // a warp only visits rows that reach its first column block (rows i >= k + 1 + 8 warp)
-    const int qw = first_slot(k + 1 + 8 * warp);
+    double dpart = 0.0;  // this thread's share of v^T A v (row part: racc v_i; column part: q_j v_j)
+    const int qw = first_slot(k + 1 + 8 * warp);  // a warp only visits rows reaching its first block
     auto row_groups = [&](int qb, int qe, auto rp_of) {
       if (nbt == 0) return;
       for (int g = max(qb, qw); g < qe; g += 4) {
         const int q = min(g + lr, qe - 1);
         const bool valid = g + lr < qe;
-        const int i = valid ? me + q * C : -1;
+        const int ic = me + q * C;                     // row (clamped on the padding lanes)
+        const int i = valid ? ic : -1;
         const int imin = me + g * C;                   // smallest row of the group (uniform)
         const int imax = me + min(g + 3, qe - 1) * C;  // largest row of the group (uniform)
         double* R = rp_of(q);
-        const double vio = vprev[q], wio = wo_own[q], vin = vcur[q];
+        const double vio = xkm[ic] * scale_prev;       // v_{k-1}[i], i >= k + 1
+        const double vin = (ic == k + 1) ? 1.0 : xk[ic] * scale;
+        const double wio = wo_own[q];
         double racc = 0.0;
 #pragma unroll
         for (int t = 0; t < MAXB; ++t) {
-          const int jf = k + 1 + 8 * (warp + TRD_NW * t);
+          const int jf = k + 1 + 8 * trd_block(warp, t);
           if (t >= nbt || jf > imax) break;  // this and all later blocks lie right of the group's diagonal
           const int j = jf + cc;
           if (jf + 7 < imin) {  // strictly below every row's diagonal: no column masking
@@ -343,14 +375,16 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
         racc += __shfl_xor_sync(0xffffffffu, racc, 1);
         racc += __shfl_xor_sync(0xffffffffu, racc, 2);
         racc += __shfl_xor_sync(0xffffffffu, racc, 4);
-        if (valid && cc == 0) rp[warp * S + q - qlo] = racc;
+        if (valid && cc == 0) {
+          rp[warp * S + q - qlo] = racc;
+          dpart = fma(racc, vin, dpart);
+        }
       }
     };
     if (qs1 < nspill) row_groups(qs1, nspill, rowptr_g);
     row_groups(max(qs1, nspill), nown, rowptr_s);
     TRD_STAMP(2)
     // column sums over the 4 row lanes; lanes with lr == 0 hold q[j] for their 8-column blocks
-    double dpart = 0.0;
 #pragma unroll
     for (int t = 0; t < MAXB; ++t) {
       if (t >= nbt) break;
@@ -366,30 +400,25 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
 #pragma unroll
       for (int t = 0; t < MAXB; ++t) {
         if (t >= nbt) break;
-        const int j = k + 1 + 8 * (warp + TRD_NW * t) + cc;
+        const int j = k + 1 + 8 * trd_block(warp, t) + cc;
         if (j >= k + 2 && j < N) push(qr + me * S + (j >> logC) - qlo, j & (C - 1), qa[t], &barQ);
       }
-    }
-    __syncthreads();
-    TRD_STAMP(3)
-    for (int q = qs1 + tid; q < nown; q += TRD_NT) {
-      // warps w < min(16, nb, (i - k - 1) / 8 + 1) reach row i; the others wrote nothing for it
-      const int i = me + q * C;
-      const double s = trd_sum16(rp + q - qlo, min(min(TRD_NW, nb), (i - k - 1) / 8 + 1), S);
-      po[q] = s;
-      dpart = fma(s, vcur[q], dpart);
     }
     dpart = warp_sum(dpart);
     if (lane == 0) red[warp] = dpart;
     __syncthreads();
-    TRD_STAMP(4)
+    TRD_STAMP(3)
     if (tid < C) {
-      const double dsum = trd_sum16(red, TRD_NW, 1);
+      const double dsum = trd_sumc<TRD_NW>(red);
       double e1 = qk1_s;
-      if (((k + 1) & (C - 1)) == me) e1 += po[(k + 1) >> logC];
+      if (((k + 1) & (C - 1)) == me) {
+        const int q1 = (k + 1) >> logC;
+        e1 += trd_sum16(rp + q1 - qlo, nwarps_of_row(k + 1), S);
+      }
       push(sd + me, tid, dsum, &barQ);
       push(se + me, tid, e1, &barQ);
     }
+    TRD_STAMP(4)
     const bool last = (k == N - 3);
     if (!SOLO) {
       if (tid == 0 && !last) trd_bar_expect(&barY, (unsigned)(8 * (2 * (N - k - 2) + C)));
@@ -399,38 +428,54 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     }
     TRD_STAMP(5)
 
-    // ---- Phase Y: w_k on own rows, eager update of column k+1, its norm partial ----
-    const double sdv = trd_sum16(sd, C, 1), sev = trd_sum16(se, C, 1);
-    const double Kc = 0.5 * tk * tk * sdv;   // (tau/2) p^T v with p = tau A v
-    const double wk1 = tk * sev - Kc;       // w_k[k+1] (v_k[k+1] = 1)
+    // ---- Phase Y (own-row threads): w_k, eager update of column k+1, its norm partial ----
+    const int nslot = nown - qs1;
+    const int nslotw = (nslot + 31) >> 5;
     double s2 = 0.0;
-    for (int q = qs1 + tid; q < nown; q += TRD_NT) {
-      const int i = me + q * C;
-      if (i == k + 1) {
-        a.d[k + 1] = rowval(q, k + 1) - 2.0 * wk1;
-        wo_own[q] = wk1;
-        continue;
-      }
-      const double pq = po[q] + trd_sum16(qr + q - qlo, C, S);
-      const double wi = fma(-Kc, vcur[q], tk * pq);
-      wo_own[q] = wi;
-      double* R = q < nspill ? rowptr_g(q) : rowptr_s(q);
-      const double x = fma(-vcur[q], wk1, R[k + 1] - wi);
-      R[k + 1] = x;
-      xso[q] = x;
-      if (i >= k + 3) s2 = fma(x, x, s2);
-      if (last) {  // i == N - 1: the trailing 2 x 2 block
-        a.e[N - 2] = x;
-        a.d[N - 1] = R[N - 1] - 2.0 * vcur[q] * wi;
-        a.tau[N - 2] = 0.0;
-      }
+    double sdv = 0.0, sev = 0.0;
+    if (warp < nslotw) {
+      sdv = trd_lane_sum16(sd, C);
+      sev = trd_lane_sum16(se, C);
     }
+    TRD_STAMP(10)
+    auto phase_y = [&](int q, double* R) {
+      const int i = me + q * C;
+      const double Kc = 0.5 * tk * tk * sdv;   // (tau/2) p^T v with p = tau A v
+      const double wk1 = tk * sev - Kc;       // w_k[k+1] (v_k[k+1] = 1)
+      if (i == k + 1) {
+        a.d[k + 1] = R[k + 1] - 2.0 * wk1;
+        wo_own[q] = wk1;
+      } else {
+        const double vin = xk[i] * scale;
+        const double pq = trd_sum16(rp + q - qlo, nwarps_of_row(i), S) + trd_sum16(qr + q - qlo, C, S);
+        const double wi = fma(-Kc, vin, tk * pq);
+        wo_own[q] = wi;
+        const double x = fma(-vin, wk1, R[k + 1] - wi);
+        R[k + 1] = x;
+        xso[q] = x;
+        if (i >= k + 3) s2 = x * x;
+        if (last) {  // i == N - 1: the trailing 2 x 2 block
+          a.e[N - 2] = x;
+          a.d[N - 1] = R[N - 1] - 2.0 * vin * wi;
+          a.tau[N - 2] = 0.0;
+        }
+      }
+    };
+    if (tid < nslot) {
+      const int q = qs1 + tid;
+      if (q < nspill) phase_y(q, rowptr_g(q));
+      else phase_y(q, rowptr_s(q));
+    }
+    TRD_STAMP(11)
     if (last) break;
+    if (warp < nslotw) {
+      s2 = warp_sum(s2);
+      if (lane == 0) red[16 + warp] = s2;  // second half of red: no conflict with the dsum partials
+    }
     TRD_STAMP(6)
-    s2 = warp_sum(s2);
-    if (lane == 0) red[16 + warp] = s2;  // second half of red: no conflict with the dsum partials
-    __syncthreads();                     // xs / wown of every own row written
-    if (tid < C) push(ss + me, tid, trd_sum16(red + 16, TRD_NW, 1), &barY);
+    __syncthreads();  // xs / wown of every own row written
+    TRD_STAMP(12)
+    if (tid < C) push(ss + me, tid, trd_sum16(red + 16, nslotw, 1), &barY);
     {
       double* xnext = xt + (par ^ 1) * N;
       const int nact = nown - qs2;  // own rows >= k+2
@@ -460,7 +505,7 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
           a.hand[2 * N + j] = wb[j];
         }
         if (tid == 0) {
-          a.hand[3 * N] = trd_sum16(ss, C, 1);
+          a.hand[3 * N] = trd_sumc<CC>(ss);
           a.hand[3 * N + 1] = scale_prev;
         }
       }
@@ -476,11 +521,12 @@ inline size_t tridiag_smem_bytes(int N, int C, int S, long long row_doubles) {
 }
 
 typedef void (*TridiagKernel)(TridiagArgs);
-inline TridiagKernel tridiag_kernel(int N, bool solo) {
-  switch (tridiag_maxb(N)) {
-    case 2: return solo ? k_tridiag<2, true> : k_tridiag<2, false>;
-    case 4: return solo ? k_tridiag<4, true> : k_tridiag<4, false>;
-    case 7: return solo ? k_tridiag<7, true> : k_tridiag<7, false>;
-    default: return solo ? k_tridiag<10, true> : k_tridiag<10, false>;
-  }
+// (MAXB, C) pairs reachable from tridiag_maxb / tridiag_cluster_size, plus the single-CTA tails.
+#define TRD_KERNELS(X) X(2, 4) X(2, 8) X(4, 8) X(4, 16) X(7, 16) X(10, 16) X(2, 1) X(4, 1) X(7, 1) X(10, 1)
+inline TridiagKernel tridiag_kernel_mc(int maxb, int C) {
+#define TRD_CASE(MB, CCX) \
+  if (maxb == MB && C == CCX) return k_tridiag<MB, CCX>;
+  TRD_KERNELS(TRD_CASE)
+#undef TRD_CASE
+  return nullptr;
 }

@@ -14,19 +14,22 @@ for N in [int(x) for x in (sys.argv[1:] or ["861"])]:
     rng = np.random.default_rng(N)
     G = rng.standard_normal((N, N))
     A = np.asfortranarray(G + G.T)
-    prof = np.zeros((N - 2) * 8, dtype=np.int64)
+    prof = np.zeros((N - 2) * 16, dtype=np.int64)
     ms = ctypes.c_float(0)
     rc = L.sosadmm_debug_tridiag_prof(N, A.ctypes.data_as(P), prof.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong)),
                                       ctypes.byref(ms))
     assert rc == 0, rc
-    pr = prof.reshape(N - 2, 8).astype(np.float64)
-    step = np.diff(pr[:, 0])  # cycles per step
-    names = ["A:reflector+setup", "X:fused pass", "X:col sums+push+rowsum", "blocksum(d)", "push sd/se + wait Q",
-             "Y:w,x", "Y:blocksum+push", "wait Y"]
-    d = np.zeros((N - 3, 8))
-    for p in range(7):
-        d[:, p] = pr[:-1, p + 1] - pr[:-1, p]
-    d[:, 7] = pr[1:, 0] - pr[:-1, 7]
-    print(f"N={N}: launch {ms.value:.3f} ms, {ms.value * 1e3 / (N - 2):.2f} us/step, mean {step.mean():.0f} cycles/step")
+    pr = prof.reshape(N - 2, 16).astype(np.float64)
+    # stamp order within a step: 0, 8 (warp 0 scalars done), 9 (after sync), 1, 2, 3, 4, 5, 10, 11, 6, 12, 7
+    order = [0, 8, 9, 1, 2, 3, 4, 5, 10, 11, 6, 12, 7]
+    names = ["A:scalars(w0)", "A:sync", "A:V+regs", "X:fused", "X:colsum+push+sync", "tid<C push", "wait Q",
+             "Y:lane sums", "Y:slot work", "Y:s2 warpsum", "Y:sync", "Y:push", "wait Y"]
+    n = N - 3
+    d = np.zeros((n, len(order)))
+    for p in range(len(order) - 1):
+        d[:, p] = pr[:n, order[p + 1]] - pr[:n, order[p]]
+    d[:, -1] = pr[1:n + 1, 0] - pr[:n, 7]
+    step = np.diff(pr[:, 0])
+    print(f"N={N}: launch {ms.value:.3f} ms, {ms.value * 1e3 / (N - 2):.2f} us/step, median {np.median(step):.0f} cycles/step")
     for lo, hi in [(0, 50), (N // 3, N // 3 + 50), (2 * N // 3, 2 * N // 3 + 50), (N - 60, N - 10)]:
-        print(f"  k in [{lo},{hi}):", " ".join(f"{names[p]}={d[lo:hi, p].mean():.0f}" for p in range(8)))
+        print(f"  k in [{lo},{hi}):", " ".join(f"{names[p]}={np.median(d[lo:hi, p]):.0f}" for p in range(len(order))))
