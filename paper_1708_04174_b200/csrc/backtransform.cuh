@@ -27,18 +27,6 @@ constexpr int BTW_RC = 128;  // V rows per streamed chunk
 constexpr int BTW_LD = BTW_RC + 4;  // padded chunk row stride (conflict-free DMMA fragment reads)
 constexpr int BTG_RC = 128;  // rows per Gram partial
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
 // v_k[row] as stored by k_tridiag: 0 above row k+1, 1 at row k+1, V[k N + row] below; reflectors
 // k >= nref do not exist (zero).
 __device__ __forceinline__ double btw_v(const double* __restrict__ V, int N, int nref, int k, int row) {

@@ -178,24 +178,30 @@ __global__ void __launch_bounds__(DC_NT) k_dc_prep(DcArgs a, int node0, int ob) 
   for (int w = 0; w < DC_NT / 32; ++w) zm = fmax(zm, red[w]);
   const double rhop = rho * zn2;  // rho z z^T = rhop zn zn^T with |zn| = 1
   const double tol = 8.0 * DC_EPS * fmax(dm, zm);
-  // sequential deflation scan (dlaed2 rules), rotations recorded for the column update
+  // sequential deflation scan (dlaed2 rules), rotations recorded for the column update (applied by
+  // k_dc_rot).  The close-pair test |t c s| <= tol is evaluated as |t z_r z_pj| <= tol (z_r^2 + z_pj^2)
+  // (c s = -z_r z_pj / (z_r^2 + z_pj^2)), so the hypot and the divisions run only when a rotation
+  // actually happens; z_pj, d_pj are carried in registers.
   if (tid == 0) {
     int k = 0, df = 0, nr = 0, pj = -1;
+    double zp = 0.0, dp = 0.0;
     for (int r = 0; r < n; ++r) {
-      if (rhop * fabs(zsh[r]) <= tol) {
+      const double zr = zsh[r], dr = dsh[r];
+      if (rhop * fabs(zr) <= tol) {
         dfl[df++] = r;
         continue;
       }
       if (pj < 0) {
         pj = r;
+        zp = zr;
+        dp = dr;
         continue;
       }
-      double sv = zsh[pj], cv = zsh[r];
-      const double tt = hypot(cv, sv);
-      const double t = dsh[r] - dsh[pj];
-      cv /= tt;
-      sv = -sv / tt;
-      if (fabs(t * cv * sv) <= tol) {
+      const double t = dr - dp;
+      const double nn = fma(zr, zr, zp * zp);
+      if (fabs(t * zr * zp) <= tol * nn) {
+        const double tt = sqrt(nn);
+        const double cv = zr / tt, sv = -zp / tt;
         zsh[r] = tt;
         zsh[pj] = 0.0;
         const int rp = s + nr;
@@ -204,14 +210,19 @@ __global__ void __launch_bounds__(DC_NT) k_dc_prep(DcArgs a, int node0, int ob) 
         a.rot_cs[2 * rp] = cv;
         a.rot_cs[2 * rp + 1] = sv;
         ++nr;
-        const double t1 = dsh[pj] * cv * cv + dsh[r] * sv * sv;
-        dsh[r] = dsh[pj] * sv * sv + dsh[r] * cv * cv;
+        const double t1 = dp * cv * cv + dr * sv * sv;
+        const double dnew = dp * sv * sv + dr * cv * cv;
+        dsh[r] = dnew;
         dsh[pj] = t1;
         dfl[df++] = pj;
         pj = r;
+        zp = tt;
+        dp = dnew;
       } else {
         ndl[k++] = pj;
         pj = r;
+        zp = zr;
+        dp = dr;
       }
     }
     if (pj >= 0) ndl[k++] = pj;
@@ -222,20 +233,6 @@ __global__ void __launch_bounds__(DC_NT) k_dc_prep(DcArgs a, int node0, int ob) 
   }
   __syncthreads();
   const int k = nk, df = ndf, nr = nrot;
-  // apply the deflation rotations to the columns of Q_old (rows of this node only), in order:
-  // x' = c x + s y, y' = c y - s x  (drot)
-  for (int row = s + tid; row < s + n; row += DC_NT) {
-    for (int q = 0; q < nr; ++q) {
-      const int rp = s + q;
-      const int cp = a.rot_pq[2 * rp], cq = a.rot_pq[2 * rp + 1];
-      const double c = a.rot_cs[2 * rp], sn = a.rot_cs[2 * rp + 1];
-      double* xp = Qo + (size_t)cp * N + row;
-      double* yp = Qo + (size_t)cq * N + row;
-      const double x = *xp, y = *yp;
-      *xp = c * x + sn * y;
-      *yp = c * y - sn * x;
-    }
-  }
   for (int i = tid; i < k; i += DC_NT) {
     const int r = ndl[i];
     a.ndd[s + i] = dsh[r];
@@ -434,7 +431,45 @@ __global__ void __launch_bounds__(DC_NT) k_dc_vec(DcArgs a, int level, int nb) {
   }
 }
 
-// ---- merge step 6: deflated eigenpairs (copied columns), one CTA per node ------------------
+// ---- merge step 1b: the deflation rotations applied to the columns of Q_old (drot:
+// x' = c x + s y, y' = c y - s x), one thread per row.  In dlaed2's scan every rotation pairs the
+// running column pj with a fresh column r, and r becomes the next pj, so the rotated r column is
+// carried in a register (only the fresh column is loaded; it does not depend on earlier rotations,
+// so those loads overlap) and the finished pj column is stored at once. ----
+constexpr int DCR_NT = 128;
+__global__ void __launch_bounds__(DCR_NT) k_dc_rot(DcArgs a, int level, int ob) {
+  if (dc_skip(a)) return;
+  const int N = a.N;
+  const int row = blockIdx.x * DCR_NT + threadIdx.x;
+  if (row >= N) return;
+  const int node = a.pos2node[(size_t)level * N + row];
+  const int s = a.nodes[node].s;
+  const int nr = a.rot_cnt[node];
+  if (nr == 0) return;
+  double* Qo = a.Q[ob];
+  int ccol = -1;
+  double cval = 0.0;
+  for (int q = 0; q < nr; ++q) {
+    const int cp = a.rot_pq[2 * (s + q)], cq = a.rot_pq[2 * (s + q) + 1];
+    const double c = a.rot_cs[2 * (s + q)], sn = a.rot_cs[2 * (s + q) + 1];
+    const double y = Qo[(size_t)cq * N + row];
+    double x;
+    if (cp == ccol) {
+      x = cval;
+    } else {
+      if (ccol >= 0) Qo[(size_t)ccol * N + row] = cval;  // chain ended: flush
+      x = Qo[(size_t)cp * N + row];
+    }
+    Qo[(size_t)cp * N + row] = fma(c, x, sn * y);
+    ccol = cq;
+    cval = fma(c, y, -sn * x);
+  }
+  Qo[(size_t)ccol * N + row] = cval;
+}
+
+// ---- merge step 6: deflated eigenpairs (copied columns).  grid (node, column chunk): one warp per
+// deflated column computes its rank among the merged spectrum, then copies the column. ----
+constexpr int DCF_COLS = DC_NT / 32;  // deflated columns per CTA (one per warp)
 __global__ void __launch_bounds__(DC_NT) k_dc_final(DcArgs a, int node0, int ob, int nb) {
   if (dc_skip(a)) return;
   const int node = node0 + blockIdx.x;
@@ -443,21 +478,21 @@ __global__ void __launch_bounds__(DC_NT) k_dc_final(DcArgs a, int node0, int ob,
   const double* Qo = a.Q[ob];
   double* Qn = a.Q[nb];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int q = warp; q < df; q += DC_NT / 32) {
-    const double x = a.dfv[s + q];
-    // roots strictly below x, deflated values below x (ties by index)
-    int cnt = 0;
-    for (int j = lane; j < k; j += 32) cnt += (a.lam_r[s + j] < x) ? 1 : 0;
-    for (int q2 = lane; q2 < df; q2 += 32) {
-      const double y = a.dfv[s + q2];
-      cnt += (y < x || (y == x && q2 < q)) ? 1 : 0;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    const int col = s + cnt;
-    if (lane == 0) a.lam[nb][col] = x;
-    const double* src = Qo + (size_t)a.dfcol[s + q] * N;
-    double* dst = Qn + (size_t)col * N;
-    for (int r = s + lane; r < s + n; r += 32) dst[r] = src[r];
+  const int q = blockIdx.y * DCF_COLS + warp;
+  if (q >= df) return;
+  const double x = a.dfv[s + q];
+  // roots strictly below x, deflated values below x (ties by index)
+  int cnt = 0;
+  for (int j = lane; j < k; j += 32) cnt += (a.lam_r[s + j] < x) ? 1 : 0;
+  for (int q2 = lane; q2 < df; q2 += 32) {
+    const double y = a.dfv[s + q2];
+    cnt += (y < x || (y == x && q2 < q)) ? 1 : 0;
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  const int col = s + cnt;
+  if (lane == 0) a.lam[nb][col] = x;
+  const double* src = Qo + (size_t)a.dfcol[s + q] * N;
+  double* dst = Qn + (size_t)col * N;
+  for (int r = s + lane; r < s + n; r += 32) dst[r] = src[r];
 }

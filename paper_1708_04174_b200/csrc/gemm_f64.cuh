@@ -34,6 +34,9 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
 }
 
 // grid: (ceil(maxM/64), ceil(maxN/64), batch); 8 warps as 2 (M) x 4 (N), warp tile 32 x 16.
+// K is streamed in 16-deep slices through a cp.async double buffer (the copies of slice s+1, with the
+// column gather acol[] resolved by the copy engine's address, overlap the DMMAs of slice s);
+// out-of-range elements are zero-filled by the copy itself.
 __global__ void __launch_bounds__(GM_NT) k_gemm_f64(const GemmDesc* __restrict__ descs, const DevState* st,
                                                     const IterScal* is, int check_state) {
   if (check_state && (st->done || !is->proceed)) return;
@@ -44,8 +47,8 @@ __global__ void __launch_bounds__(GM_NT) k_gemm_f64(const GemmDesc* __restrict__
   const int K = g.Kdev ? *g.Kdev : g.K;
   const int i0 = blockIdx.x * GM_BM, j0 = blockIdx.y * GM_BN;
   if (i0 >= M || j0 >= N) return;
-  __shared__ double As[GM_BK][GM_BM + GM_PAD];
-  __shared__ double Bs[GM_BK][GM_BN + GM_PAD];
+  __shared__ __align__(16) double As[2][GM_BK][GM_BM + GM_PAD];
+  __shared__ __align__(16) double Bs[2][GM_BK][GM_BN + GM_PAD];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 1, wn = warp >> 1;  // warp tile origin (wm*32, wn*16)
   double acc[4][2][2];
@@ -54,52 +57,63 @@ __global__ void __launch_bounds__(GM_NT) k_gemm_f64(const GemmDesc* __restrict__
 #pragma unroll
     for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
-  for (int k0 = 0; k0 < K; k0 += GM_BK) {
-    // A tile (64 x 16): coalesced along rows
+  auto issue = [&](int k0, int buf) {
+    // A slice (64 x 16): each k column contiguous in the rows
 #pragma unroll
     for (int r = 0; r < (GM_BM * GM_BK) / GM_NT; ++r) {
       const int idx = tid + r * GM_NT;
       const int i = idx % GM_BM, k = idx / GM_BM;
       const int gi = i0 + i, gk = k0 + k;
-      double v = 0.0;
-      if (gi < M && gk < K) {
-        const int col = g.acol ? g.acol[gk] : gk;
-        v = g.A[(size_t)col * g.lda + gi];
-      }
-      As[k][i] = v;
+      const bool ok = gi < M && gk < K;
+      const int col = ok ? (g.acol ? g.acol[gk] : gk) : 0;
+      cp_async8z(&As[buf][k][i], g.A + (ok ? (size_t)col * g.lda + gi : 0), ok);
     }
-    // B tile (16 x 64)
-    if (!g.transB) {
+    if (!g.transB) {  // op(B)[k, j] = B[j * ldb + k]: contiguous in k
 #pragma unroll
       for (int r = 0; r < (GM_BK * GM_BN) / GM_NT; ++r) {
         const int idx = tid + r * GM_NT;
         const int k = idx % GM_BK, j = idx / GM_BK;
         const int gk = k0 + k, gj = j0 + j;
-        Bs[k][j] = (gk < K && gj < N) ? g.B[(size_t)gj * g.ldb + gk] : 0.0;
+        const bool ok = gk < K && gj < N;
+        cp_async8z(&Bs[buf][k][j], g.B + (ok ? (size_t)gj * g.ldb + gk : 0), ok);
       }
-    } else {  // op(B)[k, j] = B[j, k]
+    } else {  // op(B)[k, j] = B[k * ldb + j]: contiguous in j
 #pragma unroll
       for (int r = 0; r < (GM_BK * GM_BN) / GM_NT; ++r) {
         const int idx = tid + r * GM_NT;
         const int j = idx % GM_BN, k = idx / GM_BN;
         const int gk = k0 + k, gj = j0 + j;
-        Bs[k][j] = (gk < K && gj < N) ? g.B[(size_t)gk * g.ldb + gj] : 0.0;
+        const bool ok = gk < K && gj < N;
+        cp_async8z(&Bs[buf][k][j], g.B + (ok ? (size_t)gk * g.ldb + gj : 0), ok);
       }
+    }
+    cp_async_commit();
+  };
+
+  const int nslices = (K + GM_BK - 1) / GM_BK;
+  if (nslices > 0) issue(0, 0);
+  for (int sl = 0; sl < nslices; ++sl) {
+    const int buf = sl & 1;
+    if (sl + 1 < nslices) {
+      issue((sl + 1) * GM_BK, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < GM_BK; kk += 4) {
       double af[4], bf[2];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) af[a] = As[kk + (lane & 3)][wm * 32 + a * 8 + (lane >> 2)];
+      for (int a = 0; a < 4; ++a) af[a] = As[buf][kk + (lane & 3)][wm * 32 + a * 8 + (lane >> 2)];
 #pragma unroll
-      for (int b = 0; b < 2; ++b) bf[b] = Bs[kk + (lane & 3)][wn * 16 + b * 8 + (lane >> 2)];
+      for (int b = 0; b < 2; ++b) bf[b] = Bs[buf][kk + (lane & 3)][wn * 16 + b * 8 + (lane >> 2)];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 2; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
     }
-    __syncthreads();
+    __syncthreads();  // buffer `buf` is refilled by the issue of slice sl + 2
   }
   // epilogue: c0/c1 at (row = lane >> 2, col = 2 (lane & 3) + {0, 1}) of each 8 x 8 tile
 #pragma unroll

@@ -423,12 +423,13 @@ inline void large_block_dc(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool ch
     const int ob = (h - 1) & 1, nb = h & 1;
     const int n0 = lb.level_node0[h], nn = lb.level_nn[h], nmax = lb.level_nmax[h];
     k_dc_prep<<<nn, DC_NT, 0, s>>>(lb.dc, n0, ob);
+    k_dc_rot<<<(N + DCR_NT - 1) / DCR_NT, DCR_NT, 0, s>>>(lb.dc, h, ob);
     k_dc_secular<<<wblocks, DC_NT, 0, s>>>(lb.dc, h);
     k_dc_zhat<<<wblocks, DC_NT, 0, s>>>(lb.dc, h);
     k_dc_vec<<<wblocks, DC_NT, 0, s>>>(lb.dc, h, nb);
     dim3 gg((nmax + GM_BM - 1) / GM_BM, (nmax + GM_BN - 1) / GM_BN, nn);
     k_gemm_f64<<<gg, GM_NT, 0, s>>>(lb.gdesc + n0, le.st, le.is, check);
-    k_dc_final<<<nn, DC_NT, 0, s>>>(lb.dc, n0, ob, nb);
+    k_dc_final<<<dim3(nn, (nmax + DCF_COLS - 1) / DCF_COLS), DC_NT, 0, s>>>(lb.dc, n0, ob, nb);
   }
 }
 
@@ -474,7 +475,7 @@ inline void large_eig_launch(LargeEig& le, cudaStream_t s, bool check, cudaEvent
 
 inline int large_eig_launches(const LargeEig& le) {
   int k = 0;
-  for (const auto& lb : le.blocks) k += (lb.ksw < lb.N - 2 ? 2 : 1) + 2 + 1 + 6 * lb.D + 5;
+  for (const auto& lb : le.blocks) k += (lb.ksw < lb.N - 2 ? 2 : 1) + 2 + 1 + 7 * lb.D + 5;
   return k;
 }
 
