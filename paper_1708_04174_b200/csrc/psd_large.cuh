@@ -433,14 +433,20 @@ inline void large_block_dc(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool ch
   }
 }
 
-inline void large_block_recon(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool check) {
+// compact-WY T factors of the reflector blocks (depend on the tridiagonalisation only)
+inline void large_block_wy(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool check) {
+  const int N = lb.N, nref = N - 2;
+  const int nbw = (nref + BTW_NB - 1) / BTW_NB;
+  k_bt_gram<<<dim3(nbw, bt_gram_chunks(N)), BTW_NT, 0, s>>>(lb.V, lb.Gwy, N, nref, le.st, le.is, check);
+  k_bt_larft<<<nbw, BTW_NT, 0, s>>>(lb.Gwy, bt_gram_chunks(N), lb.tau, lb.Twy, nref, le.st, le.is, check);
+}
+
+inline void large_block_recon(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool check, bool with_wy = true) {
   const int N = lb.N;
   const int fb = lb.D & 1;
   const int nref = N - 2;
   k_select<<<1, 256, 0, s>>>(lb.dc.lam[fb], lb.sel, le.side, lb.b, N, le.st, le.is, check);
-  const int nbw = (nref + BTW_NB - 1) / BTW_NB;
-  k_bt_gram<<<dim3(nbw, bt_gram_chunks(N)), BTW_NT, 0, s>>>(lb.V, lb.Gwy, N, nref, le.st, le.is, check);
-  k_bt_larft<<<nbw, BTW_NT, 0, s>>>(lb.Gwy, bt_gram_chunks(N), lb.tau, lb.Twy, nref, le.st, le.is, check);
+  if (with_wy) large_block_wy(le, lb, s, check);
   {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(BTC_P * ((N / 2 + BTW_NC - 1) / BTW_NC), 1, 1);
@@ -471,6 +477,30 @@ inline void large_eig_launch(LargeEig& le, cudaStream_t s, bool check, cudaEvent
   if (ev) cudaEventRecord(ev[1], s);
   for (auto& lb : le.blocks) large_block_recon(le, lb, s, check);
   if (ev) cudaEventRecord(ev[2], s);
+}
+
+// Concurrent variant (graph path): every large block runs its chain on its own stream (block 0 on
+// s), and inside a chain the WY factors run on a side stream beside the divide-and-conquer solve.
+// fork: event already recorded on s; aux: >= 2 * nblocks streams; evs: >= 3 * nblocks events.
+inline void large_eig_launch_concurrent(LargeEig& le, cudaStream_t s, bool check, cudaEvent_t fork,
+                                        const cudaStream_t* aux, const cudaEvent_t* evs) {
+  const int nb = (int)le.blocks.size();
+  for (int b = 0; b < nb; ++b) {
+    LargeBlock& lb = le.blocks[b];
+    cudaStream_t sb = b == 0 ? s : aux[2 * b];
+    cudaStream_t sw = aux[2 * b + 1];
+    if (b > 0) cudaStreamWaitEvent(sb, fork, 0);
+    large_block_tridiag(le, lb, sb, check);
+    cudaEventRecord(evs[3 * b], sb);         // tridiagonal + reflectors ready
+    cudaStreamWaitEvent(sw, evs[3 * b], 0);
+    large_block_wy(le, lb, sw, check);
+    cudaEventRecord(evs[3 * b + 1], sw);
+    large_block_dc(le, lb, sb, check);
+    cudaStreamWaitEvent(sb, evs[3 * b + 1], 0);
+    large_block_recon(le, lb, sb, check, false);
+    if (b > 0) cudaEventRecord(evs[3 * b + 2], sb);
+  }
+  for (int b = 1; b < nb; ++b) cudaStreamWaitEvent(s, evs[3 * b + 2], 0);
 }
 
 inline int large_eig_launches(const LargeEig& le) {

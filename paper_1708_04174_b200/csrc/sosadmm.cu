@@ -334,6 +334,11 @@ struct sosadmm_ctx {
   ncclComm_t comm = nullptr;
   ShardArgs sh{};
   int nb_low = 1;
+  // parallel branches of the PSD projection inside the CUDA graph
+  static constexpr int kMaxAux = 1 + 2 * 8;
+  cudaStream_t aux[kMaxAux] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_blk[3 * 8] = {};
+  bool aux_ok = false;
 };
 
 namespace {
@@ -462,13 +467,27 @@ sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev) {
   if (ev) cudaEventRecord(ev[1], s);
   if (a.pos_ctas > 0) k_scatter<<<a.pos_ctas, POS_NT, 0, s>>>(a, 0);
   if (ev) cudaEventRecord(ev[2], s);
-  if (!c->an.small_blk.empty())
-    k_psd_jacobi<<<(int)c->an.small_blk.size(), JAC_NT, jacobi_smem_bytes(c->an.max_small_N), s>>>(c->ja);
-  if (ev) cudaEventRecord(ev[3], s);
-  if (!c->an.large_blk.empty()) {
-    large_eig_launch(c->le, s, true, ev ? ev + 4 : nullptr);
-  } else if (ev) {
-    for (int q = 4; q < 7; ++q) cudaEventRecord(ev[q], s);
+  const bool has_small = !c->an.small_blk.empty(), has_large = !c->an.large_blk.empty();
+  if (!ev && has_large && c->aux_ok) {
+    // graph path: Jacobi blocks, every large block's chain and its WY factors on parallel branches
+    cudaEventRecord(c->ev_fork, s);
+    if (has_small) {
+      cudaStreamWaitEvent(c->aux[0], c->ev_fork, 0);
+      k_psd_jacobi<<<(int)c->an.small_blk.size(), JAC_NT, jacobi_smem_bytes(c->an.max_small_N), c->aux[0]>>>(
+          c->ja);
+      cudaEventRecord(c->ev_join, c->aux[0]);
+    }
+    large_eig_launch_concurrent(c->le, s, true, c->ev_fork, c->aux + 1, c->ev_blk);
+    if (has_small) cudaStreamWaitEvent(s, c->ev_join, 0);
+  } else {
+    if (has_small)
+      k_psd_jacobi<<<(int)c->an.small_blk.size(), JAC_NT, jacobi_smem_bytes(c->an.max_small_N), s>>>(c->ja);
+    if (ev) cudaEventRecord(ev[3], s);
+    if (has_large) {
+      large_eig_launch(c->le, s, true, ev ? ev + 4 : nullptr);
+    } else if (ev) {
+      for (int q = 4; q < 7; ++q) cudaEventRecord(ev[q], s);
+    }
   }
   if (a.pos_ctas > 0) k_pack<<<a.pos_ctas, POS_NT, 0, s>>>(a, nullptr, 1);
   else k_commit<<<1, 1, 0, s>>>(a);
@@ -750,6 +769,15 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
   c->row_of.assign(an.n, -2);
   for (int j = an.t; j < an.n; ++j)
     if (an.code[j] >= -1) c->row_of[j] = an.code[j];
+  if (!an.large_blk.empty() && an.large_blk.size() <= 8) {
+    const int naux = 1 + 2 * (int)an.large_blk.size();
+    for (int q = 0; q < naux; ++q) CK_CTX(c, cudaStreamCreateWithFlags(&c->aux[q], cudaStreamNonBlocking));
+    CK_CTX(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CK_CTX(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    for (int q = 0; q < 3 * (int)an.large_blk.size(); ++q)
+      CK_CTX(c, cudaEventCreateWithFlags(&c->ev_blk[q], cudaEventDisableTiming));
+    c->aux_ok = true;
+  }
   c->launches = count_launches(c);
   CK_CTX(c, cudaStreamSynchronize(s));
   return SOSADMM_OK;
@@ -996,6 +1024,12 @@ void sosadmm_destroy(sosadmm_ctx* c) {
   if (c->graph_raw) cudaGraphDestroy(c->graph_raw);
   large_eig_free(c->le);
   if (c->comm) nccl().commDestroy(c->comm);
+  for (auto& a : c->aux)
+    if (a) cudaStreamDestroy(a);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  for (auto& e : c->ev_blk)
+    if (e) cudaEventDestroy(e);
   if (c->own_mem) cudaFree(c->own_mem);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
