@@ -67,6 +67,11 @@ __device__ __forceinline__ void trd_push(unsigned raddr, double v, unsigned rbar
                "r"(rbar)
                : "memory");
 }
+__device__ __forceinline__ void trd_push2(unsigned raddr, double v0, double v1, unsigned rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+               "d"(v0), "d"(v1), "r"(rbar)
+               : "memory");
+}
 __device__ __forceinline__ void trd_bar_init(uint64_t* bar) {
   const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(1) : "memory");
@@ -77,12 +82,14 @@ __device__ __forceinline__ void trd_bar_expect(uint64_t* bar, unsigned bytes) {
 }
 __device__ __forceinline__ void trd_bar_wait(uint64_t* bar, unsigned parity) {
   const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-  unsigned ok = 0;
-  while (!ok)
+  unsigned ok = 0, spins = 0;
+  while (!ok) {
     asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
                  : "=r"(ok)
                  : "r"(b), "r"(parity)
                  : "memory");
+    if (++spins == (1u << 26)) __trap();  // a lost exchange is a bug: fail loudly instead of hanging the GPU
+  }
 }
 __device__ __forceinline__ unsigned trd_cluster_rank() {
   unsigned r;
@@ -141,10 +148,10 @@ __device__ __forceinline__ double trd_block_sum(double v, double* red) {
   return trd_sum16(red, TRD_NW, 1);
 }
 
-// Shared-memory layout (doubles): xt[2][N] wb[N] | per own slot (S slots): wown[S] xs[S] qr[C][S]
-// rp[NW][S] | scalars sd[C] se[C] ss[C] red[32] | rows.
+// Shared-memory layout (doubles): xw[2][N] (double2: x~_k[j], w_{k-1}[j], by step parity) | per own
+// slot (S slots): wown[S] xs[S] qr[C][S] rp[NW][S] | scalars sd[C] se[C] ss[C] red[32] | rows.
 __host__ __device__ inline long long trd_fixed_doubles(int N, int C, int S) {
-  return 3LL * N + 2LL * S + (long long)C * S + (long long)TRD_NW * S + 3LL * C + 32;
+  return 4LL * N + 2LL * S + (long long)C * S + (long long)TRD_NW * S + 3LL * C + 32;
 }
 __host__ __device__ inline int trd_log2(int C) { return C >= 16 ? 4 : (C >= 8 ? 3 : (C >= 4 ? 2 : (C >= 2 ? 1 : 0))); }
 
@@ -178,9 +185,10 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
   const int S = SOLO ? N - kb : (N + C - 1) >> logC;
   const int jb = kb;                          // row storage starts at column kb
   extern __shared__ __align__(16) double sm[];
-  double* xt = sm;                 // [2][N] x~_k: the column that defines v_k (allgathered), by parity
-  double* wb = xt + 2 * N;         // w_{k-1} (allgathered)
-  double* wown = wb + N;           // w on own rows
+  // xw[par][j] = (x~_k[j], w_{k-1}[j]) for k of parity par: x~_k is the column that defines v_k,
+  // w_{k-1} the pending update; both allgathered in ONE 16-byte st.async per (row, peer)
+  double2* xw = reinterpret_cast<double2*>(sm);
+  double* wown = sm + 4 * (size_t)N;  // w on own rows
   double* xs = wown + S;           // updated column on own rows (Phase Y)
   double* qr = xs + S;             // [C][S] reduce-scatter receive
   double* rp = qr + C * S;         // [NW][S] per-warp row partials
@@ -236,17 +244,13 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
   double* xso = xs - qlo;
   double scale_prev = 0.0;
   if (kb == 0) {
-    for (int j = tid; j < N; j += TRD_NT) {
-      wb[j] = 0.0;
-      xt[N + j] = 0.0;  // x~_{-1}: read (times scale_{-1} = 0) by step 0
-    }
+    for (int j = tid; j < 2 * N; j += TRD_NT) xw[j] = make_double2(0.0, 0.0);  // x~_{-1}, w_{-1} = 0
     for (int q = tid; q < S; q += TRD_NT) wown[q] = 0.0;
   } else {  // resume from the head's hand-over state
     const int pk = kb & 1;
     for (int j = tid; j < N; j += TRD_NT) {
-      xt[pk * N + j] = a.hand[j];
-      xt[(pk ^ 1) * N + j] = a.hand[N + j];
-      wb[j] = a.hand[2 * N + j];
+      xw[pk * N + j] = make_double2(a.hand[j], a.hand[2 * N + j]);
+      xw[(pk ^ 1) * N + j] = make_double2(a.hand[N + j], 0.0);
     }
     if (tid == 0) ss[0] = a.hand[3 * N];
     scale_prev = a.hand[3 * N + 1];
@@ -260,10 +264,14 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     if (SOLO) *dst = v;
     else trd_push(trd_mapa(dst, peer), v, trd_mapa(bar, peer));
   };
+  auto push2 = [&](double2* dst, int peer, double v0, double v1, uint64_t* bar) {
+    if (SOLO) *dst = make_double2(v0, v1);
+    else trd_push2(trd_mapa(dst, peer), v0, v1, trd_mapa(bar, peer));
+  };
 
   if (kb == 0) {
     // ---- column 0 defines v_0: push x~_0 = A[1:, 0], ||A[2:, 0]||^2 partials; d[0] ----
-    if (!SOLO && tid == 0) trd_bar_expect(&barY, (unsigned)(8 * ((N - 1) + C)));
+    if (!SOLO && tid == 0) trd_bar_expect(&barY, (unsigned)(16 * (N - 1) + 8 * C));  // (x, 0) pairs + norms
     double s2 = 0.0;
     for (int q = tid; q < nown; q += TRD_NT) {
       const int i = me + q * C;
@@ -275,7 +283,7 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     s2 = trd_block_sum(s2, red);
     for (int e = tid; e < nown * C; e += TRD_NT) {
       const int q = e >> logC, peer = e & (C - 1), i = me + q * C;
-      if (i >= 1) push(xt + i, peer, xs[q], &barY);
+      if (i >= 1) push2(xw + i, peer, xs[q], 0.0, &barY);
     }
     if (tid < C) push(ss + me, tid, s2, &barY);
     if (!SOLO) trd_bar_wait(&barY, 0);
@@ -288,8 +296,10 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
   for (int k = kb; k < ke; ++k) {
     const int par = k & 1;
     TRD_STAMP(0)
-    const double* xk = xt + par * N;          // x~_k
-    const double* xkm = xt + (par ^ 1) * N;   // x~_{k-1}
+    const double2* xwk = xw + par * N;         // (x~_k, w_{k-1})
+    const double2* xwm = xw + (par ^ 1) * N;   // (x~_{k-1}, .)
+    auto xk = [&](int j) { return xwk[j].x; };
+    auto xkm = [&](int j) { return xwm[j].x; };
     const int qs1 = first_slot(k + 1), qs2 = first_slot(k + 2);
     const int nb = (N - k - 1 + 7) >> 3;      // 8-column blocks of the trailing matrix
     auto nwarps_of_row = [&](int i) { return min(min(TRD_NW, nb), (i - k - 1) / 8 + 1); };  // warps reaching row i
@@ -297,7 +307,7 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     if (warp == 0) {
       if (!SOLO && lane == 0) trd_bar_expect(&barQ, (unsigned)(8 * (C * (nown - qs2) + 2 * C)));
       const double sig = trd_lane_sum16(ss, C);
-      const double alpha = xk[k + 1];
+      const double alpha = xk(k + 1);
       double tk = 0.0, beta = alpha, scale = 0.0;
       if (sig != 0.0) {
         beta = -copysign(sqrt(fma(alpha, alpha, sig)), alpha);
@@ -318,7 +328,7 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     TRD_STAMP(9)
     const double tk = scal_s[0], scale = scal_s[1];
     if (me == (k & (C - 1)))
-      for (int j = k + 1 + tid; j < N; j += TRD_NT) a.V[(size_t)k * N + j] = (j == k + 1) ? 1.0 : xk[j] * scale;
+      for (int j = k + 1 + tid; j < N; j += TRD_NT) a.V[(size_t)k * N + j] = (j == k + 1) ? 1.0 : xk(j) * scale;
     // this lane's columns: blocks bb = warp + 16 t of 8 columns starting at k + 1
     int nbt = 0;  // blocks of this warp (trd_block is increasing in t)
 #pragma unroll
@@ -328,9 +338,10 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     for (int t = 0; t < MAXB; ++t) {
       const int j = k + 1 + 8 * trd_block(warp, t) + cc;
       const bool ok = t < nbt && j < N;
-      vn[t] = !ok ? 0.0 : (j == k + 1 ? 1.0 : xk[j] * scale);
-      vo[t] = ok ? xkm[j] * scale_prev : 0.0;  // scale_prev = 0 at k = 0: no pending update
-      wo[t] = ok ? wb[j] : 0.0;
+      const double2 cw = ok ? xwk[j] : make_double2(0.0, 0.0);
+      vn[t] = !ok ? 0.0 : (j == k + 1 ? 1.0 : cw.x * scale);
+      vo[t] = ok ? xkm(j) * scale_prev : 0.0;  // scale_prev = 0 at k = 0: no pending update
+      wo[t] = cw.y;
       qa[t] = 0.0;
     }
     TRD_STAMP(1)
@@ -348,8 +359,8 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
         const int imin = me + g * C;                   // smallest row of the group (uniform)
         const int imax = me + min(g + 3, qe - 1) * C;  // largest row of the group (uniform)
         double* R = rp_of(q);
-        const double vio = xkm[ic] * scale_prev;       // v_{k-1}[i], i >= k + 1
-        const double vin = (ic == k + 1) ? 1.0 : xk[ic] * scale;
+        const double vio = xkm(ic) * scale_prev;       // v_{k-1}[i], i >= k + 1
+        const double vin = (ic == k + 1) ? 1.0 : xk(ic) * scale;
         const double wio = wo_own[q];
         double racc = 0.0;
 #pragma unroll
@@ -446,7 +457,7 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
         a.d[k + 1] = R[k + 1] - 2.0 * wk1;
         wo_own[q] = wk1;
       } else {
-        const double vin = xk[i] * scale;
+        const double vin = xk(i) * scale;
         const double pq = trd_sum16(rp + q - qlo, nwarps_of_row(i), S) + trd_sum16(qr + q - qlo, C, S);
         const double wi = fma(-Kc, vin, tk * pq);
         wo_own[q] = wi;
@@ -477,12 +488,11 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     TRD_STAMP(12)
     if (tid < C) push(ss + me, tid, trd_sum16(red + 16, nslotw, 1), &barY);
     {
-      double* xnext = xt + (par ^ 1) * N;
-      const int nact = nown - qs2;  // own rows >= k+2
+      double2* xnext = xw + (par ^ 1) * N;  // (x~_{k+1}, w_k)
+      const int nact = nown - qs2;           // own rows >= k+2
       for (int e = tid; e < nact * C; e += TRD_NT) {
         const int q = qs2 + (e >> logC), peer = e & (C - 1), i = me + q * C;
-        push(xnext + i, peer, xso[q], &barY);
-        push(wb + i, peer, wo_own[q], &barY);
+        push2(xnext + i, peer, xso[q], wo_own[q], &barY);
       }
     }
     scale_prev = scale;
@@ -500,9 +510,9 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
       if (me == 0) {
         const int pk = ke & 1;
         for (int j = tid; j < N; j += TRD_NT) {
-          a.hand[j] = xt[pk * N + j];
-          a.hand[N + j] = xt[(pk ^ 1) * N + j];
-          a.hand[2 * N + j] = wb[j];
+          a.hand[j] = xw[pk * N + j].x;
+          a.hand[N + j] = xw[(pk ^ 1) * N + j].x;
+          a.hand[2 * N + j] = xw[pk * N + j].y;
         }
         if (tid == 0) {
           a.hand[3 * N] = trd_sumc<CC>(ss);
