@@ -121,10 +121,31 @@ def affine_bytes(prob, tl: int) -> float:
     return 36.0 * L + 68.0 * prob.m + 24.0 * nnz_low + 8.0 * tl * tl
 
 
-def roofline_table(prob, tl, phase, large, hbm, hbm_src):
+def kernel_traffic():
+    """DRAM bytes per launch from the committed ncu --set full capture (profiles/*_kernel_traffic.json),
+    keyed by kernel name; {} if none is committed."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_kernel_traffic.json")))
+    if not files:
+        return {}
+    with open(files[-1]) as f:
+        d = json.load(f)
+    return {k: v["dram_read_bytes"] + v["dram_write_bytes"] for k, v in d.get("kernels", {}).items()}
+
+
+def traffic_of(prefix, table):
+    for k, v in table.items():
+        if k.startswith(prefix):
+            return v
+    return None
+
+
+def roofline_table(prob, tl, phase, large, hbm, hbm_src, config="pop40"):
     """Per-kernel-class rooflines.  achieved = algorithmic work per iteration /
     measured phase time per iteration (CUDA events on the library stream)."""
     out = []
+    traffic = kernel_traffic() if config == "pop40" else {}  # the committed capture is of config 4
     aff_ms = phase["affine"] + phase["scatter"] + phase["pack"]
     abytes = affine_bytes(prob, tl)
     out.append({"kernel": "affine projection: k_gather, k_lowT, k_kinv, k_tphase, k_rowupdate, k_scatter, k_pack "
@@ -138,7 +159,9 @@ def roofline_table(prob, tl, phase, large, hbm, hbm_src):
         out.append({"kernel": f"k_tridiag (Householder tridiagonalisation, one {TRD_CLUSTER(max(large))}-CTA cluster per "
                               f"block, N={'+'.join(map(str, large))}: 4/3 N^3 FP64 flops on CUDA-core DFMA)",
                     "bound": "alu", "achieved": fl / (tms * 1e-3) / 1e12, "peak": DFMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                    "frac": fl / (tms * 1e-3) / 1e12 / DFMA_PEAK_TFLOPS, "traffic": None, "algorithmic_per_launch": fl,
+                    "frac": fl / (tms * 1e-3) / 1e12 / DFMA_PEAK_TFLOPS,
+                    "traffic": traffic_of("k_tridiag", traffic) if len(large) == 1 else None,
+                    "algorithmic_per_launch": fl,
                     "peak_source": "measured FP64 DFMA peak of this pool's B200 (profiles/r01_probe_fp64.log); "
                                    "MEASURED_PEAKS.json has no FP64 entry", "ms_per_iter": tms})
         fd = sum(4.0 / 3.0 * N ** 3 for N in large)
@@ -271,7 +294,7 @@ def run_ours(args):
     hbm, hbm_src = hbm_peak()
     _, _, tl = gpu.get_structure()
     large = [d for d in prob.psd_dims if d > 64]
-    rooflines = roofline_table(prob, tl, phase, large, hbm, hbm_src)
+    rooflines = roofline_table(prob, tl, phase, large, hbm, hbm_src, args.config)
     dominant = max(rooflines, key=lambda r: r["ms_per_iter"])
     cpu = cpu_baseline(args) if not args.no_cpu else None
     total_steps = args.steps * (1 if sharded else world)  # sharded: all ranks advance ONE problem
