@@ -21,6 +21,8 @@
 // Rows that do not fit in shared memory (smallest first) stay in the block matrix in global memory
 // (upper triangle of column i = row i of the lower triangle), L2-resident.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 constexpr int TRD_NT = 512;
@@ -303,10 +305,26 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     const int qs1 = first_slot(k + 1), qs2 = first_slot(k + 2);
     const int nb = (N - k - 1 + 7) >> 3;      // 8-column blocks of the trailing matrix
     auto nwarps_of_row = [&](int i) { return min(min(TRD_NW, nb), (i - k - 1) / 8 + 1); };  // warps reaching row i
+    // this lane's columns: blocks bb = warp + 16 t of 8 columns starting at k + 1; their unscaled
+    // x~_k, v_{k-1} and w_{k-1} are loaded BEFORE the reflector scalars are known (the loads overlap
+    // warp 0's sqrt / division chain), and scaled after the barrier
+    int nbt = 0;  // blocks of this warp (trd_block is increasing in t)
+#pragma unroll
+    for (int t = 0; t < MAXB; ++t) nbt += trd_block(warp, t) < nb ? 1 : 0;
+    double vn[MAXB], vo[MAXB], wo[MAXB], qa[MAXB];
+#pragma unroll
+    for (int t = 0; t < MAXB; ++t) {
+      const int j = k + 1 + 8 * trd_block(warp, t) + cc;
+      const bool ok = t < nbt && j < N;
+      const double2 cw = ok ? xwk[j] : make_double2(0.0, 0.0);
+      vn[t] = cw.x;                            // x~_k[j] (scaled below)
+      vo[t] = ok ? xkm(j) * scale_prev : 0.0;  // v_{k-1}[j]; scale_prev = 0 at k = 0: no pending update
+      wo[t] = cw.y;                            // w_{k-1}[j]
+      qa[t] = 0.0;
+    }
     // ---- Phase A: the reflector of column k, by warp 0 (same order in every CTA) ----
     if (warp == 0) {
-      if (!SOLO && lane == 0) trd_bar_expect(&barQ, (unsigned)(8 * (C * (nown - qs2) + 2 * C)));
-      const double sig = trd_lane_sum16(ss, C);
+      const double sig = trd_sumc<CC>(ss);
       const double alpha = xk(k + 1);
       double tk = 0.0, beta = alpha, scale = 0.0;
       if (sig != 0.0) {
@@ -323,74 +341,73 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
           a.tau[k] = tk;
         }
       }
+    } else if (warp == 1 && lane == 0 && !SOLO) {
+      trd_bar_expect(&barQ, (unsigned)(8 * (C * (nown - qs2) + 2 * C)));
     }
     __syncthreads();
     TRD_STAMP(9)
     const double tk = scal_s[0], scale = scal_s[1];
-    if (me == (k & (C - 1)))
-      for (int j = k + 1 + tid; j < N; j += TRD_NT) a.V[(size_t)k * N + j] = (j == k + 1) ? 1.0 : xk(j) * scale;
-    // this lane's columns: blocks bb = warp + 16 t of 8 columns starting at k + 1
-    int nbt = 0;  // blocks of this warp (trd_block is increasing in t)
-#pragma unroll
-    for (int t = 0; t < MAXB; ++t) nbt += trd_block(warp, t) < nb ? 1 : 0;
-    double vn[MAXB], vo[MAXB], wo[MAXB], qa[MAXB];
 #pragma unroll
     for (int t = 0; t < MAXB; ++t) {
       const int j = k + 1 + 8 * trd_block(warp, t) + cc;
-      const bool ok = t < nbt && j < N;
-      const double2 cw = ok ? xwk[j] : make_double2(0.0, 0.0);
-      vn[t] = !ok ? 0.0 : (j == k + 1 ? 1.0 : cw.x * scale);
-      vo[t] = ok ? xkm(j) * scale_prev : 0.0;  // scale_prev = 0 at k = 0: no pending update
-      wo[t] = cw.y;
-      qa[t] = 0.0;
+      vn[t] = (t < nbt && j < N) ? (j == k + 1 ? 1.0 : vn[t] * scale) : 0.0;
     }
+    if (me == (k & (C - 1)))
+      for (int j = k + 1 + tid; j < N; j += TRD_NT) a.V[(size_t)k * N + j] = (j == k + 1) ? 1.0 : xk(j) * scale;
     TRD_STAMP(1)
 
     // ---- Phase X: fused rank-2 update of step k-1 and symv with v_k over own rows i >= k+1 ----
     double dpart = 0.0;  // this thread's share of v^T A v (row part: racc v_i; column part: q_j v_j)
     const int qw = first_slot(k + 1 + 8 * warp);  // a warp only visits rows reaching its first block
-    auto row_groups = [&](int qb, int qe, auto rp_of) {
-      if (nbt == 0) return;
-      for (int g = max(qb, qw); g < qe; g += 4) {
-        const int q = min(g + lr, qe - 1);
-        const bool valid = g + lr < qe;
-        const int ic = me + q * C;                     // row (clamped on the padding lanes)
-        const int i = valid ? ic : -1;
-        const int imin = me + g * C;                   // smallest row of the group (uniform)
-        const int imax = me + min(g + 3, qe - 1) * C;  // largest row of the group (uniform)
-        double* R = rp_of(q);
-        const double vio = xkm(ic) * scale_prev;       // v_{k-1}[i], i >= k + 1
-        const double vin = (ic == k + 1) ? 1.0 : xk(ic) * scale;
-        const double wio = wo_own[q];
-        double racc = 0.0;
+    // one group of 4 rows (lane row lr); FULL = all four rows exist (every group but possibly the
+    // last), which removes every per-lane validity test from the unmasked path
+    auto row_group = [&](int g, int qe, auto rp_of, auto FULL) {
+      constexpr bool full = decltype(FULL)::value;
+      const int q = full ? g + lr : min(g + lr, qe - 1);
+      const bool valid = full || g + lr < qe;
+      const int ic = me + q * C;                     // row (clamped on the padding lanes)
+      const int i = valid ? ic : -1;
+      const int imin = me + g * C;                   // smallest row of the group (uniform)
+      const int imax = me + (full ? g + 3 : min(g + 3, qe - 1)) * C;  // largest row of the group (uniform)
+      double* R = rp_of(q);
+      const double vio = xkm(ic) * scale_prev;       // v_{k-1}[i], i >= k + 1
+      const double vin = (ic == k + 1) ? 1.0 : xk(ic) * scale;
+      const double wio = wo_own[q];
+      double racc = 0.0;
 #pragma unroll
-        for (int t = 0; t < MAXB; ++t) {
-          const int jf = k + 1 + 8 * trd_block(warp, t);
-          if (t >= nbt || jf > imax) break;  // this and all later blocks lie right of the group's diagonal
-          const int j = jf + cc;
-          if (jf + 7 < imin) {  // strictly below every row's diagonal: no column masking
-            if (!valid) continue;
+      for (int t = 0; t < MAXB; ++t) {
+        const int jf = k + 1 + 8 * trd_block(warp, t);
+        if (t >= nbt || jf > imax) break;  // this and all later blocks lie right of the group's diagonal
+        const int j = jf + cc;
+        if (jf + 7 < imin) {  // strictly below every row's diagonal: no column masking
+          if (full || valid) {
             double x = R[j];
             x = fma(-vio, wo[t], fma(-wio, vo[t], x));
             R[j] = x;
             racc = fma(x, vn[t], racc);
             qa[t] = fma(x, vin, qa[t]);
-          } else if (j <= i) {  // i = -1 on the padding lanes of the last group
-            double x = R[j];
-            x = fma(-vio, wo[t], fma(-wio, vo[t], x));
-            R[j] = x;
-            racc = fma(x, vn[t], racc);
-            qa[t] = fma(x, (j < i) ? vin : 0.0, qa[t]);
           }
-        }
-        racc += __shfl_xor_sync(0xffffffffu, racc, 1);
-        racc += __shfl_xor_sync(0xffffffffu, racc, 2);
-        racc += __shfl_xor_sync(0xffffffffu, racc, 4);
-        if (valid && cc == 0) {
-          rp[warp * S + q - qlo] = racc;
-          dpart = fma(racc, vin, dpart);
+        } else if (j <= i) {  // i = -1 on the padding lanes of the last group
+          double x = R[j];
+          x = fma(-vio, wo[t], fma(-wio, vo[t], x));
+          R[j] = x;
+          racc = fma(x, vn[t], racc);
+          qa[t] = fma(x, (j < i) ? vin : 0.0, qa[t]);
         }
       }
+      racc += __shfl_xor_sync(0xffffffffu, racc, 1);
+      racc += __shfl_xor_sync(0xffffffffu, racc, 2);
+      racc += __shfl_xor_sync(0xffffffffu, racc, 4);
+      if (valid && cc == 0) {
+        rp[warp * S + q - qlo] = racc;
+        dpart = fma(racc, vin, dpart);
+      }
+    };
+    auto row_groups = [&](int qb, int qe, auto rp_of) {
+      if (nbt == 0) return;
+      int g = max(qb, qw);
+      for (; g + 4 <= qe; g += 4) row_group(g, qe, rp_of, std::true_type());
+      if (g < qe) row_group(g, qe, rp_of, std::false_type());
     };
     if (qs1 < nspill) row_groups(qs1, nspill, rowptr_g);
     row_groups(max(qs1, nspill), nown, rowptr_s);
@@ -431,6 +448,13 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     }
     TRD_STAMP(4)
     const bool last = (k == N - 3);
+    const int nslot = nown - qs1;
+    const int nslotw = (nslot + 31) >> 5;
+    double prow_own = 0.0;  // this CTA's row dot of its own row (sum over the warps), before the wait
+    if (tid < nslot) {
+      const int i = me + (qs1 + tid) * C;
+      if (i > k + 1) prow_own = trd_sum16(rp + qs1 + tid - qlo, nwarps_of_row(i), S);
+    }
     if (!SOLO) {
       if (tid == 0 && !last) trd_bar_expect(&barY, (unsigned)(8 * (2 * (N - k - 2) + C)));
       trd_bar_wait(&barQ, par);
@@ -440,16 +464,14 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     TRD_STAMP(5)
 
     // ---- Phase Y (own-row threads): w_k, eager update of column k+1, its norm partial ----
-    const int nslot = nown - qs1;
-    const int nslotw = (nslot + 31) >> 5;
     double s2 = 0.0;
     double sdv = 0.0, sev = 0.0;
-    if (warp < nslotw) {
-      sdv = trd_lane_sum16(sd, C);
-      sev = trd_lane_sum16(se, C);
+    if (tid < nslot) {
+      sdv = trd_sumc<CC>(sd);
+      sev = trd_sumc<CC>(se);
     }
     TRD_STAMP(10)
-    auto phase_y = [&](int q, double* R) {
+    auto phase_y = [&](int q, double* R, double prow) {
       const int i = me + q * C;
       const double Kc = 0.5 * tk * tk * sdv;   // (tau/2) p^T v with p = tau A v
       const double wk1 = tk * sev - Kc;       // w_k[k+1] (v_k[k+1] = 1)
@@ -458,7 +480,7 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
         wo_own[q] = wk1;
       } else {
         const double vin = xk(i) * scale;
-        const double pq = trd_sum16(rp + q - qlo, nwarps_of_row(i), S) + trd_sum16(qr + q - qlo, C, S);
+        const double pq = prow + trd_sum16(qr + q - qlo, C, S);
         const double wi = fma(-Kc, vin, tk * pq);
         wo_own[q] = wi;
         const double x = fma(-vin, wk1, R[k + 1] - wi);
@@ -474,8 +496,8 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     };
     if (tid < nslot) {
       const int q = qs1 + tid;
-      if (q < nspill) phase_y(q, rowptr_g(q));
-      else phase_y(q, rowptr_s(q));
+      if (q < nspill) phase_y(q, rowptr_g(q), prow_own);
+      else phase_y(q, rowptr_s(q), prow_own);
     }
     TRD_STAMP(11)
     if (last) break;
