@@ -18,12 +18,16 @@
 #include "dc.cuh"
 #include "gemm_f64.cuh"
 #include "tridiag.cuh"
+#include "tridiag_blk.cuh"
 #include "backtransform.cuh"
 
 struct LargeBlock {
   int b = 0, N = 0, C = 1, D = 0;
   long long smem_cols = 0;
   size_t trd_smem = 0;
+  bool blk = true;            // blocked tridiagonalisation with DMMA panel updates (tridiag_blk.cuh)
+  size_t blk_smem = 0;
+  long long blk_rows = 0;
   int ksw = 0;                // first step done by the single-CTA tail (N - 2: no tail)
   size_t tail_smem = 0;
   TridiagArgs ta_tail{};
@@ -200,6 +204,7 @@ inline size_t large_carve(const std::vector<int>& blk_N, const std::vector<int>&
     p[q++] = take(sizeof(GemmDesc) * (nodes.size() + 1));
     p[q++] = take(4 * 4);                 // sel
     p[q++] = take(8 * ((size_t)3 * N + 2));  // tridiagonalisation hand-over state
+    p[q++] = take(8 * (size_t)2 * N * TRB_NB);  // blocked tridiagonalisation panels Vg, Wg
     p[q++] = take(8 * (size_t)BTW_NB * BTW_NB * ((N - 2 + BTW_NB - 1) / BTW_NB));  // Twy
     p[q++] = take(8 * (size_t)BTW_NB * BTW_NB * ((N - 2 + BTW_NB - 1) / BTW_NB) * bt_gram_chunks(N));  // Gwy
     per_block(b, N, p, nodes, l0, lnn, lmax, D, leaf0, nleaves, p2n);
@@ -230,6 +235,16 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     lb.C = tridiag_cluster_size(N);
     lb.smem_cols = tridiag_row_budget(N, lb.C);
     lb.trd_smem = tridiag_smem_bytes(N, lb.C, (N + lb.C - 1) / lb.C, lb.smem_cols);
+    {
+      const char* env = getenv("SOSADMM_TRIDIAG");
+      lb.blk = env && std::string(env) == "blocked";  // default: fused update+symv (faster at N <= ~900, measured)
+      const int S = (N + lb.C - 1) / lb.C;
+      const long long fixed = trb_fixed_doubles(N, lb.C, S, TRB_NB);
+      long long need = 0;
+      for (int c = 0; c < lb.C; ++c) need = std::max(need, tridiag_rows_need(N, lb.C, c, 0));
+      lb.blk_rows = std::min(need, (long long)TRD_MAX_DYN_SMEM / 8 - fixed);
+      lb.blk_smem = sizeof(double) * (size_t)(fixed + lb.blk_rows);
+    }
     {
       const int nt = tridiag_tail_rows(N);
       lb.ksw = (nt >= 16 && N - nt > 8) ? N - nt : N - 2;
@@ -277,6 +292,7 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     lb.gdesc = (GemmDesc*)p[q++];
     lb.sel = (int*)p[q++];
     double* hand = (double*)p[q++];
+    double* vwg = (double*)p[q++];
     lb.Twy = (double*)p[q++];
     lb.Gwy = (double*)p[q++];
     lb.recon = (int)nodes.size();
@@ -351,6 +367,8 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     ta.kb = 0;
     ta.ke = lb.ksw;
     ta.hand = hand;
+    ta.Vg = vwg;
+    ta.Wg = vwg + (size_t)N * TRB_NB;
     lb.ta_tail = ta;
     lb.ta_tail.C = 1;
     lb.ta_tail.kb = lb.ksw;
@@ -372,8 +390,10 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
   }
   if (!le.blocks.empty()) {
 #define TRD_PTR(MB, CCX) k_tridiag<MB, CCX>,
-    for (TridiagKernel kt : {TRD_KERNELS(TRD_PTR)}) {
+#define TRB_PTR(MB, CCX) k_tridiag_blk<MB, CCX, TRB_NB>,
+    for (TridiagKernel kt : {TRD_KERNELS(TRD_PTR) TRB_KERNELS(TRB_PTR)}) {
 #undef TRD_PTR
+#undef TRB_PTR
       if (err == cudaSuccess) err = cudaFuncSetAttribute(kt, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (err == cudaSuccess)
         err = cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, TRD_MAX_DYN_SMEM);
@@ -397,7 +417,7 @@ inline void large_block_tridiag(LargeEig& le, LargeBlock& lb, cudaStream_t s, bo
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(lb.C, 1, 1);
     cfg.blockDim = dim3(TRD_NT, 1, 1);
-    cfg.dynamicSmemBytes = lb.trd_smem;
+    cfg.dynamicSmemBytes = lb.blk ? lb.blk_smem : lb.trd_smem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -406,6 +426,12 @@ inline void large_block_tridiag(LargeEig& le, LargeBlock& lb, cudaStream_t s, bo
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    if (lb.blk) {
+      TridiagArgs tb = lb.ta;
+      tb.smem_rows_doubles = lb.blk_rows;
+      cudaLaunchKernelEx(&cfg, tridiag_blk_kernel_mc(tridiag_maxb(lb.N), lb.C), tb);
+      return;
+    }
     cudaLaunchKernelEx(&cfg, tridiag_kernel_mc(tridiag_maxb(lb.N), lb.C), lb.ta);
   }
   if (lb.ksw < lb.N - 2)
@@ -505,7 +531,7 @@ inline void large_eig_launch_concurrent(LargeEig& le, cudaStream_t s, bool check
 
 inline int large_eig_launches(const LargeEig& le) {
   int k = 0;
-  for (const auto& lb : le.blocks) k += (lb.ksw < lb.N - 2 ? 2 : 1) + 2 + 1 + 7 * lb.D + 5;
+  for (const auto& lb : le.blocks) k += (!lb.blk && lb.ksw < lb.N - 2 ? 2 : 1) + 2 + 1 + 7 * lb.D + 5;
   return k;
 }
 

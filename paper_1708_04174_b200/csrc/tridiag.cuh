@@ -53,6 +53,7 @@ struct TridiagArgs {
   long long* prof;   // optional (debug): clock64 stamps of CTA 0 per step and phase, 8 per step
   int kb, ke;        // Householder steps [kb, ke) done by this launch
   double* hand;      // 3 N + 2 doubles: head -> tail hand-over state
+  double *Vg, *Wg;   // k_tridiag_blk: N x NB panel buffers
 };
 
 __device__ __forceinline__ void trd_cluster_sync() {
@@ -406,6 +407,7 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     auto row_groups = [&](int qb, int qe, auto rp_of) {
       if (nbt == 0) return;
       int g = max(qb, qw);
+#pragma unroll 2
       for (; g + 4 <= qe; g += 4) row_group(g, qe, rp_of, std::true_type());
       if (g < qe) row_group(g, qe, rp_of, std::false_type());
     };
