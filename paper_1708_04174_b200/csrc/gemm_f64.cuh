@@ -24,7 +24,7 @@ struct GemmDesc {
   int skip;            // 1 = this batch entry does nothing
 };
 
-constexpr int GM_BM = 64, GM_BN = 64, GM_BK = 16, GM_NT = 256;
+constexpr int GM_BM = 32, GM_BN = 64, GM_BK = 16, GM_NT = 128;
 constexpr int GM_PAD = 8;
 
 __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
@@ -33,7 +33,8 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
                : "d"(a), "d"(b));
 }
 
-// grid: (ceil(maxM/64), ceil(maxN/64), batch); 8 warps as 2 (M) x 4 (N), warp tile 32 x 16.
+// grid: (ceil(maxM/32), ceil(maxN/64), batch); 4 warps as 1 (M) x 4 (N), warp tile 32 x 16 (small
+// tiles: the D&C merges and the reconstruction are N <= ~1000 GEMMs, so more CTAs per SM hide latency).
 // K is streamed in 16-deep slices through a cp.async double buffer (the copies of slice s+1, with the
 // column gather acol[] resolved by the copy engine's address, overlap the DMMAs of slice s);
 // out-of-range elements are zero-filled by the copy itself.
@@ -50,7 +51,7 @@ __global__ void __launch_bounds__(GM_NT) k_gemm_f64(const GemmDesc* __restrict__
   __shared__ __align__(16) double As[2][GM_BK][GM_BM + GM_PAD];
   __shared__ __align__(16) double Bs[2][GM_BK][GM_BN + GM_PAD];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 1, wn = warp >> 1;  // warp tile origin (wm*32, wn*16)
+  const int wm = 0, wn = warp;  // warp tile origin (wm*32, wn*16)
   double acc[4][2][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
