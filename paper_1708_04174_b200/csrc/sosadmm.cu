@@ -28,6 +28,7 @@
 namespace {
 
 constexpr size_t kAlign = 256;
+constexpr double SQRT2_HOST = 1.4142135623730951;  // fl(sqrt 2)
 
 // NCCL is resolved at run time from the libnccl.so.2 already loaded by the process (torch's), so the
 // library itself loads without NCCL and there is a single NCCL copy per process.
@@ -144,16 +145,6 @@ sosadmm_err analyse(const sosadmm_problem* p, Analysis& an, std::string& msg, co
   an.c.assign(p->c, p->c + an.n);
   an.code.assign(an.n, -2);
   an.aval.assign(an.n, 0.0);
-  // svec weight of each PSD column (1 on the diagonal, sqrt 2 off it)
-  std::vector<double> wsv(an.n, 1.0);
-  {
-    long long col = an.t;
-    for (int b = 0; b < an.nblk; ++b) {
-      const int N = p->psd_dim[b];
-      for (int j = 0; j < N; ++j)
-        for (int i = 0; i <= j; ++i) wsv[col++] = (i == j) ? 1.0 : std::sqrt(2.0);
-    }
-  }
   std::vector<int> cnt(an.m, 0);
   for (int j = an.t; j < an.n; ++j) {
     const long long e0 = p->A_colptr[j], e1 = p->A_colptr[j + 1];
@@ -193,8 +184,12 @@ sosadmm_err analyse(const sosadmm_problem* p, Analysis& an, std::string& msg, co
         an.seg_col[fill[r]] = j;
         an.seg_val[fill[r]] = an.aval[j];
         fill[r]++;
-        const double s = an.aval[j] / wsv[j];  // indicator coefficient (exactly 1 for B_alpha data)
-        an.D[r] += s * s * (wsv[j] == 1.0 ? 1.0 : 2.0);
+        // A_orth A_orth^T is diagonal with entries sum_j A_rj^2; for indicator data the entries are
+        // 1 or fl(sqrt 2) (scalar SOS, Proposition 1) or 1 on off-diagonal svec entries (off-diagonal
+        // blocks of a matrix SOS, Proposition 2), whose squares are the integers 1 and 2 — counted
+        // exactly (never fl(sqrt 2)^2 = 2.0000000000000004, reading C10)
+        const double v = an.aval[j];
+        an.D[r] += (v == 1.0 || v == -1.0) ? 1.0 : ((v == SQRT2_HOST || v == -SQRT2_HOST) ? 2.0 : v * v);
       }
   }
   an.Pinv.resize(an.m);

@@ -13,11 +13,12 @@ import pytest
 from oracle import HsdeOracle, Status, brute_force_structure, proj_psd_svec, svec
 from sosgen import ball_pop, make_config, planted_kkt, univariate_feasibility
 from sosgen.configs import planted_pop
+from sosgen.matrix_sos import brute_force_counts, matrix_planted_kkt, matrix_sos_pop
 
 pytestmark = pytest.mark.gpu
 
-SMALL = ["pop6", "sq", "neg", "pop3k2", "ball4"]
-LARGE = ["pop20", "lyap10", "box24", "pop40"]
+SMALL = ["pop6", "sq", "neg", "pop3k2", "ball4", "msos2"]
+LARGE = ["pop20", "lyap10", "box24", "pop40", "msos3"]
 
 
 def make(name):
@@ -29,6 +30,10 @@ def make(name):
         return planted_pop("pop3k2", 3, 2, seed=5)
     if name == "ball4":
         return ball_pop(4)
+    if name == "msos2":  # matrix-valued SOS (Proposition 2): Y in S^{2 * 10} (Jacobi path)
+        return matrix_sos_pop("msos2", 3, 2, 2, 2, seed=3)
+    if name == "msos3":  # Y in S^{3 * 28} (cluster tridiagonalisation path)
+        return matrix_sos_pop("msos3", 6, 3, 2, 3, seed=4)
     return make_config(name)
 
 
@@ -54,6 +59,10 @@ def solvers():
 def test_structure_bit_exact(name, solvers):
     prob, gpu, _ = solvers(name)
     row_of, D, tl = gpu.get_structure()
+    if name.startswith("msos"):  # Proposition 2: D = ordered-pair counts of every (alpha, i, j) row
+        assert np.array_equal(D, brute_force_counts(prob).astype(np.float64))
+        assert np.all(row_of[prob.n_free:] >= 0) and tl == prob.n_free
+        return
     maps, n_alpha = brute_force_structure(prob.row_expo, prob.block_info, prob.m)
     assert np.array_equal(D, n_alpha.astype(np.float64))  # exact integers
     off = prob.n_free
@@ -128,7 +137,7 @@ def test_first_20_iterates(name, solvers):
     assert worst_u <= 1e-9 and worst_v <= 1e-9, (worst_u, worst_v)
 
 
-@pytest.mark.parametrize("name", ["pop6", "sq", "neg", "pop3k2", "ball4"])
+@pytest.mark.parametrize("name", ["pop6", "sq", "neg", "pop3k2", "ball4", "msos2"])
 def test_convergence_parity(name, solvers):
     prob, gpu, orc = solvers(name, tol=1e-4, max_iters=5000)
     st, status, hist = orc.solve(tol=1e-4, max_iters=5000)
@@ -140,10 +149,10 @@ def test_convergence_parity(name, solvers):
         assert abs(info["pobj"] - hist[-1][3]) <= 1e-6 * abs(hist[-1][3])
 
 
-@pytest.mark.parametrize("name", ["pop6", "pop20", "box24", "pop40"])
+@pytest.mark.parametrize("name", ["pop6", "pop20", "box24", "pop40", "msos2", "msos3"])
 def test_planted_fixed_point(name, solvers):
     prob, gpu, _ = solvers(name)
-    xi, y, z = planted_kkt(prob)
+    xi, y, z = matrix_planted_kkt(prob) if name.startswith("msos") else planted_kkt(prob)
     gpu.set_iterate(xi, y, z, None, 1.0, 0.0, 0)
     gpu.iterate(1)
     g = gpu.get_iterate()
