@@ -43,7 +43,7 @@ extern "C" {
 typedef enum {
   SOSADMM_OK = 0,
   SOSADMM_E_ARG = -1,       /* malformed input (sizes, pointers, CSC structure) */
-  SOSADMM_E_STRUCT = -2,    /* unsupported structure (e.g. low-rank width too large) */
+  SOSADMM_E_STRUCT = -2,    /* unsupported structure (low-rank width > 16384, a block > SOSADMM_MAX_BLOCK) */
   SOSADMM_E_FACTOR = -3,    /* I + A_low^T P^{-1} A_low not numerically SPD (impossible in exact arithmetic) */
   SOSADMM_E_CUDA = -4,      /* CUDA runtime error (message has the detail) */
   SOSADMM_E_NCCL = -5,      /* NCCL unavailable or failed (sharded mode) */
@@ -59,6 +59,10 @@ typedef enum {
   SOSADMM_MAX_ITERS = 4,
   SOSADMM_INCONCLUSIVE = 5
 } sosadmm_status;
+
+/* Largest supported PSD block dimension (the cluster tridiagonalisation and the divide-and-conquer
+ * merge keep per-block state in shared memory); larger blocks make setup fail with E_STRUCT. */
+#define SOSADMM_MAX_BLOCK 1280
 
 /* Conic data of `eq:generalSDP`.  psd_dim[b] = N_b; block b owns N_b(N_b+1)/2 svec columns. */
 typedef struct {

@@ -117,6 +117,11 @@ sosadmm_err analyse(const sosadmm_problem* p, Analysis& an, std::string& msg, co
       msg = "PSD block dimension must be positive";
       return SOSADMM_E_ARG;
     }
+    if (N > SOSADMM_MAX_BLOCK) {
+      msg = "PSD block " + std::to_string(b) + " has dimension " + std::to_string(N) + " > " +
+            std::to_string(SOSADMM_MAX_BLOCK) + " (largest supported block)";
+      return SOSADMM_E_STRUCT;
+    }
     n += (long long)N * (N + 1) / 2;
   }
   if (n > (1LL << 30)) {

@@ -26,6 +26,12 @@ def test_library_exports_every_declared_symbol():
     for name in decl:
         assert hasattr(lib, name), name
     assert set(decl) == set(EXPORTS)
+    # the stage-level debug entry points of include/sosadmm_debug.h as well
+    src = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "sosadmm_debug.h")).read(), flags=re.S)
+    dbg = sorted(set(re.findall(r"\b(sosadmm_debug_[a-z_]+)\s*\(", src)))
+    assert len(dbg) >= 5
+    for name in dbg:
+        assert hasattr(lib, name), name
 
 
 def test_workspace_size_cpu():
@@ -44,6 +50,12 @@ def test_workspace_size_cpu():
                  _dptr(va), _dptr(prob.b), _dptr(prob.c))
     nb = lib.sosadmm_workspace_size(ctypes.byref(p))
     assert nb > 8 * (2 * prob.n + 2 * prob.m)
+    # a block larger than SOSADMM_MAX_BLOCK is refused (E_STRUCT at setup, 0 bytes here)
+    big = np.array([1281], dtype=np.int32)
+    pb = _Problem(prob.m, prob.n_free, 1, big.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                  cp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), ri.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                  _dptr(va), _dptr(prob.b), _dptr(prob.c))
+    assert lib.sosadmm_workspace_size(ctypes.byref(pb)) == 0
     # malformed input: decreasing column pointers
     bad = cp.copy()
     bad[3] = bad[2] - 1

@@ -17,7 +17,7 @@ from sosgen.matrix_sos import brute_force_counts, matrix_planted_kkt, matrix_sos
 
 pytestmark = pytest.mark.gpu
 
-SMALL = ["pop6", "sq", "neg", "pop3k2", "ball4", "msos2"]
+SMALL = ["pop6", "sq", "neg", "one", "pop3k2", "ball4", "msos2"]
 LARGE = ["pop20", "lyap10", "box24", "pop40", "msos3"]
 
 
@@ -26,6 +26,8 @@ def make(name):
         return univariate_feasibility("sq", [1.0, 2.0, 1.0])
     if name == "neg":
         return univariate_feasibility("neg", [-1.0, 0.0, -1.0])
+    if name == "one":  # degenerate: a 1 x 1 PSD block, t = 0, m = 1
+        return univariate_feasibility("one", [1.0])
     if name == "pop3k2":
         return planted_pop("pop3k2", 3, 2, seed=5)
     if name == "ball4":
@@ -100,9 +102,14 @@ def test_psd_projection_parity(name, solvers):
     for bidx in sorted({0, 1, 2, nb - 1} & set(range(nb))):
         N = prob.psd_dims[bidx]
         L = N * (N + 1) // 2
-        for kind in ["gauss", "lowrank"]:
+        for kind in ["gauss", "lowrank", "zero", "psd", "nsd"]:
             if kind == "gauss":
                 a = rng.standard_normal(L)
+            elif kind == "zero":  # degenerate: Pi(0) = 0
+                a = np.zeros(L)
+            elif kind in ("psd", "nsd"):  # already in the cone: Pi = identity / Pi = 0
+                G = rng.standard_normal((N, N))
+                a = svec((1.0 if kind == "psd" else -1.0) * (G @ G.T + np.eye(N)))
             else:  # clustered spectrum: rank-3 PSD minus rank-2 PSD plus tiny noise
                 G = rng.standard_normal((N, 3))
                 H = rng.standard_normal((N, 2))
@@ -110,7 +117,7 @@ def test_psd_projection_parity(name, solvers):
                 a = svec(X)
             got = gpu.project_psd(bidx, a)
             ref = proj_psd_svec(a, N)
-            assert np.linalg.norm(got - ref) <= 1e-11 * np.linalg.norm(a), (bidx, N, kind)
+            assert np.linalg.norm(got - ref) <= 1e-11 * max(np.linalg.norm(a), 1e-300), (bidx, N, kind)
 
 
 def _rel(a, b, scale):

@@ -52,7 +52,7 @@ def _householder_Q(V, tau, N):
     return Q
 
 
-@pytest.mark.parametrize("N", [65, 100, 231, 285, 325, 861])
+@pytest.mark.parametrize("N", [65, 100, 231, 285, 325, 513, 861, 1024, 1280])
 def test_tridiag(N):
     rng = np.random.default_rng(N)
     G = rng.standard_normal((N, N))
@@ -79,7 +79,7 @@ def _stedc(d, e):
 
 @pytest.mark.parametrize("N,kind", [(2, "rand"), (3, "rand"), (17, "rand"), (65, "rand"), (231, "rand"),
                                     (861, "rand"), (300, "glued"), (200, "zero_e"), (129, "equal_d"),
-                                    (500, "wilkinson"), (861, "clustered")])
+                                    (500, "wilkinson"), (861, "clustered"), (1280, "rand"), (1024, "clustered")])
 def test_stedc(N, kind):
     rng = np.random.default_rng(N + len(kind))
     if kind == "rand":
