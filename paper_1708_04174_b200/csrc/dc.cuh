@@ -178,19 +178,55 @@ __global__ void __launch_bounds__(DC_NT) k_dc_prep(DcArgs a, int node0, int ob) 
   for (int w = 0; w < DC_NT / 32; ++w) zm = fmax(zm, red[w]);
   const double rhop = rho * zn2;  // rho z z^T = rhop zn zn^T with |zn| = 1
   const double tol = 8.0 * DC_EPS * fmax(dm, zm);
-  // sequential deflation scan (dlaed2 rules), rotations recorded for the column update (applied by
-  // k_dc_rot).  The close-pair test |t c s| <= tol is evaluated as |t z_r z_pj| <= tol (z_r^2 + z_pj^2)
-  // (c s = -z_r z_pj / (z_r^2 + z_pj^2)), so the hypot and the divisions run only when a rotation
-  // actually happens; z_pj, d_pj are carried in registers.
-  if (tid == 0) {
-    int k = 0, df = 0, nr = 0, pj = -1;
-    double zp = 0.0, dp = 0.0;
-    for (int r = 0; r < n; ++r) {
-      const double zr = zsh[r], dr = dsh[r];
-      if (rhop * fabs(zr) <= tol) {
-        dfl[df++] = r;
-        continue;
+  // deflation (dlaed2 rules).  Type 1 (|z_r| small) is decided in parallel and compacted in order;
+  // the close-pair scan (type 2), whose rotations change z and d of the running pair, runs in one
+  // thread over the remaining candidates only.  Rotations are recorded for k_dc_rot.  The pair test
+  // |t c s| <= tol is evaluated as |t z_r z_pj| <= tol (z_r^2 + z_pj^2) (c s = -z_r z_pj /
+  // (z_r^2 + z_pj^2)), so hypot and divisions run only when a rotation happens.
+  __shared__ int cand[DC_MAXN];
+  __shared__ int wcnt[2][DC_NT / 32];
+  __shared__ int ncand_s, ndf1_s;
+  {
+    const int warp = tid >> 5, lane = tid & 31;
+    int base_c = 0, base_d = 0;
+    for (int r0 = 0; r0 < n; r0 += DC_NT) {
+      const int r = r0 + tid;
+      const bool valid = r < n;
+      const bool t1 = valid && rhop * fabs(zsh[r]) <= tol;
+      const bool cd = valid && !t1;
+      const unsigned mc = __ballot_sync(0xffffffffu, cd), md = __ballot_sync(0xffffffffu, t1);
+      if (lane == 0) {
+        wcnt[0][warp] = __popc(mc);
+        wcnt[1][warp] = __popc(md);
       }
+      __syncthreads();
+      int oc = base_c, od = base_d;
+      for (int w = 0; w < warp; ++w) {
+        oc += wcnt[0][w];
+        od += wcnt[1][w];
+      }
+      const unsigned below = (1u << lane) - 1u;
+      if (cd) cand[oc + __popc(mc & below)] = r;
+      if (t1) dfl[od + __popc(md & below)] = r;
+      for (int w = 0; w < DC_NT / 32; ++w) {
+        base_c += wcnt[0][w];
+        base_d += wcnt[1][w];
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      ncand_s = base_c;
+      ndf1_s = base_d;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const int nc = ncand_s;
+    int k = 0, df = ndf1_s, nr = 0, pj = -1;
+    double zp = 0.0, dp = 0.0;
+    for (int c = 0; c < nc; ++c) {
+      const int r = cand[c];
+      const double zr = zsh[r], dr = dsh[r];
       if (pj < 0) {
         pj = r;
         zp = zr;
