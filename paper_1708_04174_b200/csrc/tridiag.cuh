@@ -325,13 +325,21 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     }
     // ---- Phase A: the reflector of column k, by warp 0 (same order in every CTA) ----
     if (warp == 0) {
+      TRD_STAMP(13)
       const double sig = trd_sumc<CC>(ss);
       const double alpha = xk(k + 1);
+      if (prof) a.prof[(size_t)k * 16 + 14] = clock64() + (long long)(sig * 0.0) + (long long)(alpha * 0.0);
       double tk = 0.0, beta = alpha, scale = 0.0;
       if (sig != 0.0) {
-        beta = -copysign(sqrt(fma(alpha, alpha, sig)), alpha);
-        tk = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
+        // beta = -sign(alpha) sqrt(n2), tau = (beta - alpha) / beta = 1 + |alpha| / sqrt(n2),
+        // scale = 1 / (alpha - beta) = sign(alpha) / (|alpha| + sqrt(n2)): one rsqrt + one division
+        const double n2 = fma(alpha, alpha, sig);
+        const double rs = rsqrt(n2);
+        const double nrm = n2 * rs;
+        beta = -copysign(nrm, alpha);
+        if (prof) a.prof[(size_t)k * 16 + 15] = clock64() + (long long)(beta * 0.0);
+        tk = fma(fabs(alpha), rs, 1.0);
+        scale = copysign(1.0, alpha) / (fabs(alpha) + nrm);
       }
       TRD_STAMP(8)
       if (lane == 0) {
@@ -346,6 +354,9 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
       trd_bar_expect(&barQ, (unsigned)(8 * (C * (nown - qs2) + 2 * C)));
     }
     __syncthreads();
+    // compiler barrier: keep the column register set-up below from being hoisted into warp 0's
+    // reflector chain (measured: it delayed the sqrt / division chain by ~600 cycles per step)
+    asm volatile("" ::: "memory");
     TRD_STAMP(9)
     const double tk = scal_s[0], scale = scal_s[1];
 #pragma unroll

@@ -33,3 +33,7 @@ for N in [int(x) for x in (sys.argv[1:] or ["861"])]:
     print(f"N={N}: launch {ms.value:.3f} ms, {ms.value * 1e3 / (N - 2):.2f} us/step, median {np.median(step):.0f} cycles/step")
     for lo, hi in [(0, 50), (N // 3, N // 3 + 50), (2 * N // 3, 2 * N // 3 + 50), (N - 60, N - 10)]:
         print(f"  k in [{lo},{hi}):", " ".join(f"{names[p]}={np.median(d[lo:hi, p]):.0f}" for p in range(len(order))))
+        if pr[lo:hi, 13].any():
+            sub = [np.median(pr[lo:hi, 13] - pr[lo:hi, 0]), np.median(pr[lo:hi, 14] - pr[lo:hi, 13]),
+                   np.median(pr[lo:hi, 15] - pr[lo:hi, 14]), np.median(pr[lo:hi, 8] - pr[lo:hi, 15])]
+            print("     warp0: top->start %.0f  sum+alpha %.0f  sqrt %.0f  divs %.0f" % tuple(sub))
