@@ -139,10 +139,13 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag_blk(TridiagArgs a) {
       const double sig = trd_sumc<CC>(ss);
       const double alpha = xk[k + 1];
       double tk = 0.0, beta = alpha, scale = 0.0;
-      if (sig != 0.0) {
-        beta = -copysign(sqrt(fma(alpha, alpha, sig)), alpha);
-        tk = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
+      if (sig != 0.0) {  // one rsqrt + one division (see k_tridiag)
+        const double n2 = fma(alpha, alpha, sig);
+        const double rs = rsqrt(n2);
+        const double nrm = n2 * rs;
+        beta = -copysign(nrm, alpha);
+        tk = fma(fabs(alpha), rs, 1.0);
+        scale = copysign(1.0, alpha) / (fabs(alpha) + nrm);
       }
       TRB_STAMP(8)
       if (lane == 0) {
@@ -212,9 +215,54 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag_blk(TridiagArgs a) {
         dpart = fma(racc, vin, dpart);
       }
     };
+    // two full groups per iteration: independent load / FMA chains for latency hiding
+    auto row_group2 = [&](int g, auto rp_of) {
+      const int qA = g + lr, qB = g + 4 + lr;
+      const int iA = me + qA * C, iB = me + qB * C;
+      const int iminA = me + g * C, iminB = me + (g + 4) * C, imax = me + (g + 7) * C;
+      const double* RA = rp_of(qA);
+      const double* RB = rp_of(qB);
+      const double vA = vof(iA), vB = vof(iB);
+      double ra = 0.0, rb = 0.0;
+#pragma unroll
+      for (int tt = 0; tt < MAXB; ++tt) {
+        const int jf = k + 1 + 8 * trd_block(warp, tt);
+        if (tt >= nbt || jf > imax) break;
+        const int j = jf + cc;
+        if (jf + 7 < iminA) {  // both groups strictly below the diagonal
+          const double xa = RA[j], xb = RB[j];
+          ra = fma(xa, vn[tt], ra);
+          rb = fma(xb, vn[tt], rb);
+          qa[tt] = fma(xb, vB, fma(xa, vA, qa[tt]));
+        } else {
+          if (j <= iA) {
+            const double xa = RA[j];
+            ra = fma(xa, vn[tt], ra);
+            qa[tt] = fma(xa, (j < iA) ? vA : 0.0, qa[tt]);
+          }
+          if (j <= iB) {
+            const double xb = RB[j];
+            rb = fma(xb, vn[tt], rb);
+            qa[tt] = fma(xb, (j < iB) ? vB : 0.0, qa[tt]);
+          }
+        }
+      }
+      ra += __shfl_xor_sync(0xffffffffu, ra, 1);
+      rb += __shfl_xor_sync(0xffffffffu, rb, 1);
+      ra += __shfl_xor_sync(0xffffffffu, ra, 2);
+      rb += __shfl_xor_sync(0xffffffffu, rb, 2);
+      ra += __shfl_xor_sync(0xffffffffu, ra, 4);
+      rb += __shfl_xor_sync(0xffffffffu, rb, 4);
+      if (cc == 0) {
+        rp[warp * S + qA] = ra;
+        rp[warp * S + qB] = rb;
+        dpart = fma(ra, vA, fma(rb, vB, dpart));
+      }
+    };
     auto row_groups = [&](int qb, int qe, auto rp_of) {
       if (nbt == 0) return;
       int g = max(qb, qw);
+      for (; g + 8 <= qe; g += 8) row_group2(g, rp_of);
       for (; g + 4 <= qe; g += 4) row_group(g, qe, rp_of, std::true_type());
       if (g < qe) row_group(g, qe, rp_of, std::false_type());
     };
@@ -277,15 +325,18 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag_blk(TridiagArgs a) {
     // ---- Phase Y: corrected w_k on own rows, x~_{k+1}, its norm partial ----
     if (tid < 2 * t) ab[tid < t ? tid : NB + tid - t] = trd_sum16(pab + (tid < t ? tid : NB + tid - t), C, 2 * NB);
     __syncthreads();
-    double sab = 0.0;  // a . b
-    for (int u = 0; u < t; ++u) sab = fma(ab[u], ab[NB + u], sab);
-    const double sdv = trd_sumc<CC>(sd) - 2.0 * sab;  // v^T A v with the panel correction
-    const double Kc = 0.5 * tk * tk * sdv;
-    // p_{k+1} and w_k[k+1] (row k+1 is the panel row rr = t): every CTA, same order
-    double corr1 = 0.0;
-    for (int u = 0; u < t; ++u) corr1 = fma(Vd[t * NB + u], ab[NB + u], fma(Wd[t * NB + u], ab[u], corr1));
-    const double wk1 = tk * (trd_sumc<CC>(se) - corr1) - Kc;
-    if (tid == 0) Wd[t * NB + t] = wk1;
+    double Kc = 0.0, wk1 = 0.0;
+    if (tid < max(nslot, 1)) {  // only the own-row threads (and thread 0) need the scalars
+      double sab = 0.0;  // a . b
+      for (int u = 0; u < t; ++u) sab = fma(ab[u], ab[NB + u], sab);
+      const double sdv = trd_sumc<CC>(sd) - 2.0 * sab;  // v^T A v with the panel correction
+      Kc = 0.5 * tk * tk * sdv;
+      // p_{k+1} and w_k[k+1] (row k+1 is the panel row rr = t): every CTA, same order
+      double corr1 = 0.0;
+      for (int u = 0; u < t; ++u) corr1 = fma(Vd[t * NB + u], ab[NB + u], fma(Wd[t * NB + u], ab[u], corr1));
+      wk1 = tk * (trd_sumc<CC>(se) - corr1) - Kc;
+      if (tid == 0) Wd[t * NB + t] = wk1;
+    }
     TRB_STAMP(10)
     double s2 = 0.0;
     if (tid < nslot) {
