@@ -151,10 +151,10 @@ __device__ __forceinline__ double trd_block_sum(double v, double* red) {
   return trd_sum16(red, TRD_NW, 1);
 }
 
-// Shared-memory layout (doubles): xw[2][N] (double2: x~_k[j], w_{k-1}[j], by step parity) | per own
-// slot (S slots): wown[S] xs[S] qr[C][S] rp[NW][S] | scalars sd[C] se[C] ss[C] red[32] | rows.
+// Shared-memory layout (doubles): xw[2][N] (double2: x~_k[j], scale_{k-1} w_{k-1}[j], by step
+// parity) | per own slot (S slots): xs[S] qr[C][S] rp[NW][S] | scalars sd[C] se[C] sc[C] red[32] | rows.
 __host__ __device__ inline long long trd_fixed_doubles(int N, int C, int S) {
-  return 4LL * N + 2LL * S + (long long)C * S + (long long)TRD_NW * S + 3LL * C + 32;
+  return 4LL * N + (long long)S + (long long)C * S + (long long)TRD_NW * S + 3LL * C + 32;
 }
 __host__ __device__ inline int trd_log2(int C) { return C >= 16 ? 4 : (C >= 8 ? 3 : (C >= 4 ? 2 : (C >= 2 ? 1 : 0))); }
 
@@ -163,7 +163,7 @@ __host__ __device__ inline int trd_log2(int C) { return C >= 16 ? 4 : (C >= 8 ? 
 //   cluster head (SOLO = false, C in {4,8,16}, kb = 0): if ke < N - 2 it stops after step ke - 1 and
 //     hands its state over through global memory: the unfinished trailing rows i >= ke (entries
 //     ke..i, still owing the lazy rank-2 update of step ke - 1) go back to the block matrix, and
-//     hand[] = [x~_ke (N), x~_{ke-1} (N), w_{ke-1} (N), ||x~_ke[ke+1:]||^2, scale_{ke-1}];
+//     hand[] = [x~_ke (N), x~_{ke-1} (N), scale_{ke-1} w_{ke-1} (N)];
 //   single-CTA tail (SOLO = true, C = 1, kb = ke of the head): resumes from that state with local
 //     stores and __syncthreads in place of the DSMEM exchanges.
 // Scalar work is done by one warp (reflector) or by the own-row threads (Phase Y) only; the other
@@ -191,18 +191,17 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
   // xw[par][j] = (x~_k[j], w_{k-1}[j]) for k of parity par: x~_k is the column that defines v_k,
   // w_{k-1} the pending update; both allgathered in ONE 16-byte st.async per (row, peer)
   double2* xw = reinterpret_cast<double2*>(sm);
-  double* wown = sm + 4 * (size_t)N;  // w on own rows
-  double* xs = wown + S;           // updated column on own rows (Phase Y)
+  double* xs = sm + 4 * (size_t)N;  // column 0 on own rows (first push)
   double* qr = xs + S;             // [C][S] reduce-scatter receive
   double* rp = qr + C * S;         // [NW][S] per-warp row partials
-  double* sd = rp + TRD_NW * S;    // [C] partial v^T A v
-  double* se = sd + C;             // [C] partial (A v)[k+1]
-  double* ss = se + C;             // [C] partial ||x~||^2
-  double* red = ss + C;            // [32]: warp partials (two independent halves)
+  double* sd = rp + TRD_NW * S;    // [C] partial y^T A y
+  double* se = sd + C;             // [C] partial (A y)[k+1]
+  double* sc = se + C;             // [C] (slot 0) A_k[k+1, k+1] from the owner of row k + 1
+  double* red = sc + C;            // [32]: warp partials (two independent halves)
   double* rows = red + 32;
   __shared__ int roff[TRD_MAXOWN];  // smem offset of own row slot q - qlo, -1 = spilled to global
   __shared__ int nspill_s;
-  __shared__ double qk1_s, scal_s[2];
+  __shared__ double qk1_s, scal_s[2][2];  // (tau_k, scale_k) by step parity
   __shared__ __align__(8) uint64_t barQ, barY;
 
   if (tid == 0) {
@@ -243,21 +242,14 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     double* dst = rowptr_s(q);
     for (int j = jb + tid; j <= i; j += TRD_NT) dst[j] = src[j];
   }
-  double* wo_own = wown - qlo;  // indexed by absolute slot q
-  double* xso = xs - qlo;
-  double scale_prev = 0.0;
   if (kb == 0) {
     for (int j = tid; j < 2 * N; j += TRD_NT) xw[j] = make_double2(0.0, 0.0);  // x~_{-1}, w_{-1} = 0
-    for (int q = tid; q < S; q += TRD_NT) wown[q] = 0.0;
   } else {  // resume from the head's hand-over state
     const int pk = kb & 1;
     for (int j = tid; j < N; j += TRD_NT) {
       xw[pk * N + j] = make_double2(a.hand[j], a.hand[2 * N + j]);
       xw[(pk ^ 1) * N + j] = make_double2(a.hand[N + j], 0.0);
     }
-    if (tid == 0) ss[0] = a.hand[3 * N];
-    scale_prev = a.hand[3 * N + 1];
-    for (int q = qlo + tid; q < nown; q += TRD_NT) wo_own[q] = a.hand[2 * N + me + q * C];
   }
   if (!SOLO) trd_cluster_sync();  // barriers initialised and every CTA running before the first remote store
   else __syncthreads();
@@ -273,22 +265,19 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
   };
 
   if (kb == 0) {
-    // ---- column 0 defines v_0: push x~_0 = A[1:, 0], ||A[2:, 0]||^2 partials; d[0] ----
-    if (!SOLO && tid == 0) trd_bar_expect(&barY, (unsigned)(16 * (N - 1) + 8 * C));  // (x, 0) pairs + norms
-    double s2 = 0.0;
+    // ---- column 0 defines v_0: push x~_0 = A[1:, 0] (allgather); d[0] ----
+    if (!SOLO && tid == 0) trd_bar_expect(&barY, (unsigned)(16 * (N - 1)));  // (x, 0) pairs
     for (int q = tid; q < nown; q += TRD_NT) {
       const int i = me + q * C;
       const double x = rowval(q, 0);
       xs[q] = x;
-      if (i >= 2) s2 = fma(x, x, s2);
       if (i == 0) a.d[0] = x;
     }
-    s2 = trd_block_sum(s2, red);
+    __syncthreads();
     for (int e = tid; e < nown * C; e += TRD_NT) {
       const int q = e >> logC, peer = e & (C - 1), i = me + q * C;
       if (i >= 1) push2(xw + i, peer, xs[q], 0.0, &barY);
     }
-    if (tid < C) push(ss + me, tid, s2, &barY);
     if (!SOLO) trd_bar_wait(&barY, 0);
     else __syncthreads();
   }
@@ -306,9 +295,52 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     const int qs1 = first_slot(k + 1), qs2 = first_slot(k + 2);
     const int nb = (N - k - 1 + 7) >> 3;      // 8-column blocks of the trailing matrix
     auto nwarps_of_row = [&](int i) { return min(min(TRD_NW, nb), (i - k - 1) / 8 + 1); };  // warps reaching row i
-    // this lane's columns: blocks bb = warp + 16 t of 8 columns starting at k + 1; their unscaled
-    // x~_k, v_{k-1} and w_{k-1} are loaded BEFORE the reflector scalars are known (the loads overlap
-    // warp 0's sqrt / division chain), and scaled after the barrier
+    // Deferred scaling: the reflector v_k = e_{k+1} + scale_k y with y = x~_k[k+2:] (the pivot entry
+    // zeroed), so the fused pass computes z = A_k y with the UNSCALED column and needs none of the
+    // reflector scalars; p = A_k v_k = A_k[:, k+1] + scale_k z and v^T A v = A_k[k+1,k+1]
+    // + 2 scale z[k+1] + scale^2 y^T z are formed per own row in Phase Y, and the sqrt / division
+    // chain of the reflector is off the critical path.
+    // The chain runs on the LAST warp at the top of the step: its column blocks start furthest right,
+    // so it has the least fused-pass work (none once fewer than 16 blocks remain).  It sums
+    // ||x~_k[k+2:]||^2 itself from the allgathered column (same order in every CTA: no norm
+    // exchange).  scal_s is double-buffered by step parity (read after the next __syncthreads).
+    if (warp == TRD_NW - 1) {
+      // beta = -sign(alpha) sqrt(n2), tau = 1 + |alpha| / sqrt(n2), scale = 1 / (alpha - beta)
+      // = sign(alpha) / (|alpha| + sqrt(n2)): one rsqrt + one division
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int j = k + 2 + lane;
+      for (; j + 96 < N; j += 128) {
+        const double x0 = xk(j), x1 = xk(j + 32), x2 = xk(j + 64), x3 = xk(j + 96);
+        s0 = fma(x0, x0, s0);
+        s1 = fma(x1, x1, s1);
+        s2 = fma(x2, x2, s2);
+        s3 = fma(x3, x3, s3);
+      }
+      for (; j < N; j += 32) {
+        const double x0 = xk(j);
+        s0 = fma(x0, x0, s0);
+      }
+      const double sig = warp_sum((s0 + s1) + (s2 + s3));
+      const double alpha = xk(k + 1);
+      double tk = 0.0, beta = alpha, scale = 0.0;
+      if (sig != 0.0) {
+        const double n2 = fma(alpha, alpha, sig);
+        const double rs = rsqrt(n2);
+        const double nrm = n2 * rs;
+        beta = -copysign(nrm, alpha);
+        tk = fma(fabs(alpha), rs, 1.0);
+        scale = copysign(1.0, alpha) / (fabs(alpha) + nrm);
+      }
+      if (lane == 0) {
+        scal_s[par][0] = tk;
+        scal_s[par][1] = scale;
+        if (me == (k & (C - 1))) {
+          a.e[k] = beta;
+          a.tau[k] = tk;
+        }
+      }
+    }
+    // this lane's columns: blocks bb = warp + 16 t of 8 columns starting at k + 1
     int nbt = 0;  // blocks of this warp (trd_block is increasing in t)
 #pragma unroll
     for (int t = 0; t < MAXB; ++t) nbt += trd_block(warp, t) < nb ? 1 : 0;
@@ -318,54 +350,12 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
       const int j = k + 1 + 8 * trd_block(warp, t) + cc;
       const bool ok = t < nbt && j < N;
       const double2 cw = ok ? xwk[j] : make_double2(0.0, 0.0);
-      vn[t] = cw.x;                            // x~_k[j] (scaled below)
-      vo[t] = ok ? xkm(j) * scale_prev : 0.0;  // v_{k-1}[j]; scale_prev = 0 at k = 0: no pending update
-      wo[t] = cw.y;                            // w_{k-1}[j]
+      vn[t] = (j == k + 1) ? 0.0 : cw.x;       // y[j]
+      vo[t] = ok ? xkm(j) : 0.0;               // x~_{k-1}[j] (v_{k-1} = scale_{k-1} x~_{k-1} below row k)
+      wo[t] = cw.y;                            // scale_{k-1} w_{k-1}[j] (0 at k = 0: no pending update)
       qa[t] = 0.0;
     }
-    // ---- Phase A: the reflector of column k, by warp 0 (same order in every CTA) ----
-    if (warp == 0) {
-      TRD_STAMP(13)
-      const double sig = trd_sumc<CC>(ss);
-      const double alpha = xk(k + 1);
-      if (prof) a.prof[(size_t)k * 16 + 14] = clock64() + (long long)(sig * 0.0) + (long long)(alpha * 0.0);
-      double tk = 0.0, beta = alpha, scale = 0.0;
-      if (sig != 0.0) {
-        // beta = -sign(alpha) sqrt(n2), tau = (beta - alpha) / beta = 1 + |alpha| / sqrt(n2),
-        // scale = 1 / (alpha - beta) = sign(alpha) / (|alpha| + sqrt(n2)): one rsqrt + one division
-        const double n2 = fma(alpha, alpha, sig);
-        const double rs = rsqrt(n2);
-        const double nrm = n2 * rs;
-        beta = -copysign(nrm, alpha);
-        if (prof) a.prof[(size_t)k * 16 + 15] = clock64() + (long long)(beta * 0.0);
-        tk = fma(fabs(alpha), rs, 1.0);
-        scale = copysign(1.0, alpha) / (fabs(alpha) + nrm);
-      }
-      TRD_STAMP(8)
-      if (lane == 0) {
-        scal_s[0] = tk;
-        scal_s[1] = scale;
-        if (me == (k & (C - 1))) {
-          a.e[k] = beta;
-          a.tau[k] = tk;
-        }
-      }
-    } else if (warp == 1 && lane == 0 && !SOLO) {
-      trd_bar_expect(&barQ, (unsigned)(8 * (C * (nown - qs2) + 2 * C)));
-    }
-    __syncthreads();
-    // compiler barrier: keep the column register set-up below from being hoisted into warp 0's
-    // reflector chain (measured: it delayed the sqrt / division chain by ~600 cycles per step)
-    asm volatile("" ::: "memory");
-    TRD_STAMP(9)
-    const double tk = scal_s[0], scale = scal_s[1];
-#pragma unroll
-    for (int t = 0; t < MAXB; ++t) {
-      const int j = k + 1 + 8 * trd_block(warp, t) + cc;
-      vn[t] = (t < nbt && j < N) ? (j == k + 1 ? 1.0 : vn[t] * scale) : 0.0;
-    }
-    if (me == (k & (C - 1)))
-      for (int j = k + 1 + tid; j < N; j += TRD_NT) a.V[(size_t)k * N + j] = (j == k + 1) ? 1.0 : xk(j) * scale;
+    if (tid == 32 && !SOLO) trd_bar_expect(&barQ, (unsigned)(8 * (C * (nown - qs2) + 2 * C + 1)));
     TRD_STAMP(1)
 
     // ---- Phase X: fused rank-2 update of step k-1 and symv with v_k over own rows i >= k+1 ----
@@ -382,9 +372,9 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
       const int imin = me + g * C;                   // smallest row of the group (uniform)
       const int imax = me + (full ? g + 3 : min(g + 3, qe - 1)) * C;  // largest row of the group (uniform)
       double* R = rp_of(q);
-      const double vio = xkm(ic) * scale_prev;       // v_{k-1}[i], i >= k + 1
-      const double vin = (ic == k + 1) ? 1.0 : xk(ic) * scale;
-      const double wio = wo_own[q];
+      const double vio = xkm(ic);                    // x~_{k-1}[i], i >= k + 1
+      const double vin = (ic == k + 1) ? 0.0 : xk(ic);  // y[i]
+      const double wio = xwk[ic].y;                  // scale_{k-1} w_{k-1}[i]
       double racc = 0.0;
 #pragma unroll
       for (int t = 0; t < MAXB; ++t) {
@@ -449,27 +439,24 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     if (lane == 0) red[warp] = dpart;
     __syncthreads();
     TRD_STAMP(3)
+    const bool own1 = ((k + 1) & (C - 1)) == me;  // this CTA owns row k + 1
     if (tid < C) {
-      const double dsum = trd_sumc<TRD_NW>(red);
-      double e1 = qk1_s;
-      if (((k + 1) & (C - 1)) == me) {
-        const int q1 = (k + 1) >> logC;
-        e1 += trd_sum16(rp + q1 - qlo, nwarps_of_row(k + 1), S);
-      }
-      push(sd + me, tid, dsum, &barQ);
-      push(se + me, tid, e1, &barQ);
+      push(sd + me, tid, trd_sumc<TRD_NW>(red), &barQ);
+      push(se + me, tid, qk1_s, &barQ);
+      if (own1) push(sc, tid, rowval((k + 1) >> logC, k + 1), &barQ);  // A_k[k+1, k+1]
     }
     TRD_STAMP(4)
     const bool last = (k == N - 3);
     const int nslot = nown - qs1;
-    const int nslotw = (nslot + 31) >> 5;
     double prow_own = 0.0;  // this CTA's row dot of its own row (sum over the warps), before the wait
     if (tid < nslot) {
       const int i = me + (qs1 + tid) * C;
       if (i > k + 1) prow_own = trd_sum16(rp + qs1 + tid - qlo, nwarps_of_row(i), S);
     }
+    const double tk = scal_s[par][0], scale = scal_s[par][1];  // written before the last __syncthreads
+    TRD_STAMP(8)
     if (!SOLO) {
-      if (tid == 0 && !last) trd_bar_expect(&barY, (unsigned)(8 * (2 * (N - k - 2) + C)));
+      if (tid == 0 && !last) trd_bar_expect(&barY, (unsigned)(16 * (N - k - 2)));
       trd_bar_wait(&barQ, par);
     } else {
       __syncthreads();
@@ -477,33 +464,37 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
     TRD_STAMP(5)
 
     // ---- Phase Y (own-row threads): w_k, eager update of column k+1, its norm partial ----
-    double s2 = 0.0;
-    double sdv = 0.0, sev = 0.0;
+    double Kc = 0.0, wk1 = 0.0;
     if (tid < nslot) {
-      sdv = trd_sumc<CC>(sd);
-      sev = trd_sumc<CC>(se);
+      const double yz = trd_sumc<CC>(sd);     // y^T A y
+      const double z1 = trd_sumc<CC>(se);     // (A y)[k+1]
+      const double c1 = sc[0];                // A_k[k+1, k+1]
+      const double vav = fma(scale, fma(scale, yz, 2.0 * z1), c1);  // v^T A v
+      Kc = 0.5 * tk * tk * vav;               // (tau/2) p^T v with p = tau A v
+      wk1 = fma(tk, fma(scale, z1, c1), -Kc);  // w_k[k+1] (v_k[k+1] = 1)
     }
     TRD_STAMP(10)
+    // each own-row thread pushes its (x~_{k+1}[i], scale_k w_k[i]) straight to every CTA (allgather;
+    // peers staggered so the 16 stores of a warp hit 16 different CTAs)
+    double2* xnext = xw + (par ^ 1) * N;  // (x~_{k+1}, scale_k w_k)
     auto phase_y = [&](int q, double* R, double prow) {
       const int i = me + q * C;
-      const double Kc = 0.5 * tk * tk * sdv;   // (tau/2) p^T v with p = tau A v
-      const double wk1 = tk * sev - Kc;       // w_k[k+1] (v_k[k+1] = 1)
       if (i == k + 1) {
         a.d[k + 1] = R[k + 1] - 2.0 * wk1;
-        wo_own[q] = wk1;
       } else {
         const double vin = xk(i) * scale;
-        const double pq = prow + trd_sum16(qr + q - qlo, C, S);
+        const double pq = fma(scale, prow + trd_sum16(qr + q - qlo, C, S), R[k + 1]);  // (A v)[i]
         const double wi = fma(-Kc, vin, tk * pq);
-        wo_own[q] = wi;
         const double x = fma(-vin, wk1, R[k + 1] - wi);
         R[k + 1] = x;
-        xso[q] = x;
-        if (i >= k + 3) s2 = x * x;
         if (last) {  // i == N - 1: the trailing 2 x 2 block
           a.e[N - 2] = x;
           a.d[N - 1] = R[N - 1] - 2.0 * vin * wi;
           a.tau[N - 2] = 0.0;
+        } else {
+          const double ws = wi * scale;
+#pragma unroll
+          for (int c = 0; c < C; ++c) push2(xnext + i, (c + tid) & (C - 1), x, ws, &barY);
         }
       }
     };
@@ -513,24 +504,9 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
       else phase_y(q, rowptr_s(q), prow_own);
     }
     TRD_STAMP(11)
+    if (me == (k & (C - 1)))  // v_k for the back-transform (global, read by later kernels only)
+      for (int j = k + 1 + tid; j < N; j += TRD_NT) a.V[(size_t)k * N + j] = (j == k + 1) ? 1.0 : xk(j) * scale;
     if (last) break;
-    if (warp < nslotw) {
-      s2 = warp_sum(s2);
-      if (lane == 0) red[16 + warp] = s2;  // second half of red: no conflict with the dsum partials
-    }
-    TRD_STAMP(6)
-    __syncthreads();  // xs / wown of every own row written
-    TRD_STAMP(12)
-    if (tid < C) push(ss + me, tid, trd_sum16(red + 16, nslotw, 1), &barY);
-    {
-      double2* xnext = xw + (par ^ 1) * N;  // (x~_{k+1}, w_k)
-      const int nact = nown - qs2;           // own rows >= k+2
-      for (int e = tid; e < nact * C; e += TRD_NT) {
-        const int q = qs2 + (e >> logC), peer = e & (C - 1), i = me + q * C;
-        push2(xnext + i, peer, xso[q], wo_own[q], &barY);
-      }
-    }
-    scale_prev = scale;
     TRD_STAMP(7)
     if (!SOLO) trd_bar_wait(&barY, par ^ 1);
     else __syncthreads();
@@ -548,10 +524,6 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
           a.hand[j] = xw[pk * N + j].x;
           a.hand[N + j] = xw[(pk ^ 1) * N + j].x;
           a.hand[2 * N + j] = xw[pk * N + j].y;
-        }
-        if (tid == 0) {
-          a.hand[3 * N] = trd_sumc<CC>(ss);
-          a.hand[3 * N + 1] = scale_prev;
         }
       }
       break;

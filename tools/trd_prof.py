@@ -20,10 +20,10 @@ for N in [int(x) for x in (sys.argv[1:] or ["861"])]:
                                       ctypes.byref(ms))
     assert rc == 0, rc
     pr = prof.reshape(N - 2, 16).astype(np.float64)
-    # stamp order within a step: 0, 8 (warp 0 scalars done), 9 (after sync), 1, 2, 3, 4, 5, 10, 11, 6, 12, 7
-    order = [0, 8, 9, 1, 2, 3, 4, 5, 10, 11, 6, 12, 7]
-    names = ["A:scalars(w0)", "A:sync", "A:V+regs", "X:fused", "X:colsum+push+sync", "tid<C push", "wait Q",
-             "Y:lane sums", "Y:slot work", "Y:s2 warpsum", "Y:sync", "Y:push", "wait Y"]
+    # stamp order within a step: 0, 1 (registers set up), 2, 3, 4, 8 (reflector), 5, 10, 11, 6, 12, 7
+    order = [0, 1, 2, 3, 4, 8, 5, 10, 11, 6, 12, 7]
+    names = ["regs", "X:fused", "X:colsum+push+sync", "tid<C push", "prow+reflector", "wait Q",
+             "Y:sums", "Y:slot work", "Y:s2 warpsum", "Y:sync", "Y:push+V", "wait Y"]
     n = N - 3
     d = np.zeros((n, len(order)))
     for p in range(len(order) - 1):
@@ -33,7 +33,7 @@ for N in [int(x) for x in (sys.argv[1:] or ["861"])]:
     print(f"N={N}: launch {ms.value:.3f} ms, {ms.value * 1e3 / (N - 2):.2f} us/step, median {np.median(step):.0f} cycles/step")
     for lo, hi in [(0, 50), (N // 3, N // 3 + 50), (2 * N // 3, 2 * N // 3 + 50), (N - 60, N - 10)]:
         print(f"  k in [{lo},{hi}):", " ".join(f"{names[p]}={np.median(d[lo:hi, p]):.0f}" for p in range(len(order))))
-        if pr[lo:hi, 13].any():
+        if False:
             sub = [np.median(pr[lo:hi, 13] - pr[lo:hi, 0]), np.median(pr[lo:hi, 14] - pr[lo:hi, 13]),
                    np.median(pr[lo:hi, 15] - pr[lo:hi, 14]), np.median(pr[lo:hi, 8] - pr[lo:hi, 15])]
             print("     warp0: top->start %.0f  sum+alpha %.0f  sqrt %.0f  divs %.0f" % tuple(sub))
