@@ -20,10 +20,10 @@ for N in [int(x) for x in (sys.argv[1:] or ["861"])]:
                                       ctypes.byref(ms))
     assert rc == 0, rc
     pr = prof.reshape(N - 2, 16).astype(np.float64)
-    # stamp order within a step: 0, 1 (registers set up), 2, 3, 4, 8 (reflector), 5, 10, 11, 6, 12, 7
-    order = [0, 1, 2, 3, 4, 8, 5, 10, 11, 6, 12, 7]
-    names = ["regs", "X:fused", "X:colsum+push+sync", "tid<C push", "prow+reflector", "wait Q",
-             "Y:sums", "Y:slot work", "Y:s2 warpsum", "Y:sync", "Y:push+V", "wait Y"]
+    # stamp order within a step: 0, 1 (registers set up), 2, 3, 4, 8, 5, 10, 11, 7
+    order = [0, 1, 2, 3, 4, 8, 5, 10, 11, 7]
+    names = ["regs", "X:fused", "X:colsum+push+sync", "tid<C push", "prow", "wait Q",
+             "Y:sums", "Y:rows+push", "V store", "wait Y"]
     n = N - 3
     d = np.zeros((n, len(order)))
     for p in range(len(order) - 1):
