@@ -144,7 +144,8 @@ inline long long tridiag_rows_need(int N, int C, int c, int kb) {
 inline long long tridiag_row_budget(int N, int C) {
   const long long cap = TRD_MAX_DYN_SMEM / 8 - trd_fixed_doubles(N, C, (N + C - 1) / C);
   long long need = 0;
-  for (int c = 0; c < C; ++c) need = std::max(need, tridiag_rows_need(N, C, c, 0));
+  for (int c = 0; c < C; ++c)  // + 15 doubles of bank-alignment padding per row (k_tridiag)
+    need = std::max(need, tridiag_rows_need(N, C, c, 0) + 15LL * ((N - c + C - 1) / C));
   return std::min(cap, need);
 }
 // Number of trailing rows n the single-CTA tail takes over (the whole lower triangle of the last n
@@ -249,7 +250,7 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
       const int nt = tridiag_tail_rows(N);
       lb.ksw = (nt >= 16 && N - nt > 8) ? N - nt : N - 2;
       const int S = N - lb.ksw;
-      lb.tail_smem = tridiag_smem_bytes(N, 1, S, tridiag_rows_need(N, 1, 0, lb.ksw));
+      lb.tail_smem = tridiag_smem_bytes(N, 1, S, tridiag_rows_need(N, 1, 0, lb.ksw) + 15LL * S);
     }
     int q = 0;
     lb.d = (double*)p[q++];
@@ -373,7 +374,7 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     lb.ta_tail.C = 1;
     lb.ta_tail.kb = lb.ksw;
     lb.ta_tail.ke = N - 2;
-    lb.ta_tail.smem_rows_doubles = tridiag_rows_need(N, 1, 0, lb.ksw);
+    lb.ta_tail.smem_rows_doubles = tridiag_rows_need(N, 1, 0, lb.ksw) + 15LL * (N - lb.ksw);
     le.blocks.push_back(lb);
   });
   le.side = side_p;

@@ -205,20 +205,24 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
   __shared__ __align__(8) uint64_t barQ, barY;
 
   if (tid == 0) {
-    // smallest rows spill first; rows are stored from column jb to the diagonal
+    // smallest rows spill first; rows are stored from column jb to the diagonal.  Consecutive rows
+    // start 8 doubles apart modulo 16 (<= 15 doubles of padding each), so the two rows a half-warp
+    // touches in one 8-column block (lanes lr = 0, 1 or 2, 3) fall in disjoint bank halves.
     long long need = 0;
-    for (int q = qlo; q < nown; ++q) need += me + q * C + 1 - jb;
+    for (int q = qlo; q < nown; ++q) need += me + q * C + 1 - jb + 15;
     int ns = qlo;
     while (need > a.smem_rows_doubles && ns < nown) {
-      need -= me + ns * C + 1 - jb;
+      need -= me + ns * C + 1 - jb + 15;
       ++ns;
     }
-    long long off = 0;
+    long long off = 0, prev = -1;
     for (int q = qlo; q < nown; ++q) {
       if (q < ns) {
         roff[q - qlo] = -1;
       } else {
+        if (prev >= 0) off += (((prev + 8 - off) % 16) + 16) % 16;
         roff[q - qlo] = (int)off;
+        prev = off;
         off += me + q * C + 1 - jb;
       }
     }
