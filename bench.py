@@ -9,7 +9,10 @@ Timing: W warm-up steps, then K timed steps; before every timed step an L2 flush
 buffer, > 126 MB L2) runs on the same stream outside the timed window; each step is bracketed by
 CUDA events on the library's stream; barrier + synchronize around the region; max over ranks.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config pop40]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config pop40] [--batch B]
+
+`--batch B` runs B independent seeded instances per GPU concurrently, each on its
+own stream and CUDA graph, and reports the aggregate iterations/s (not the headline line).
 
 `--impl reference` times the CPU oracle (oracle/, plain FP64, generic KKT LU + LAPACK eigh) on
 the same workload.  For N > 1 every rank solves its own independent
@@ -332,6 +335,88 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
 
 
+def run_batch(args):
+    """B independent seeded instances of the config per GPU (seeds seed + B rank ..
+    seed + B rank + B - 1), each on its own stream with its own CUDA graph (sosadmm_iterate_async).
+    A step = one ADMM iteration of EVERY instance; steps run in lock-step (L2 flush, then all B
+    instances' iterations, then the next flush), value = B K world / max-over-ranks time."""
+    import torch
+
+    world, rank, local = dist_init()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    from paper_1708_04174_b200 import SosAdmm, iterate_batch
+    from sosgen import make_config
+
+    B = args.batch
+    probs = [make_config(args.config, seed=args.seed + B * rank + j) for j in range(B)]
+    sol = [SosAdmm.from_problem(p, tol=1e-300, max_iters=1 << 40, device=local) for p in probs]
+    main = torch.cuda.Stream(device=local)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    iterate_batch(sol, args.warmup)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    done = [torch.cuda.Event() for _ in sol]
+    barrier()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            with torch.cuda.stream(main):
+                flush.fill_(float(i))
+                ev0[i].record(main)
+            for j, s in enumerate(sol):
+                s.stream.wait_event(ev0[i])
+                s.iterate_async(1)
+                done[j].record(s.stream)
+            for e in done:
+                main.wait_event(e)
+            ev1[i].record(main)
+        barrier()
+    ms = sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))
+    infos = [s.info() for s in sol]
+    vals = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
+    ms = float(vals[0])
+    if rank != 0:
+        return
+    N = max(probs[0].psd_dims)
+    trd_flops = B * world * 4.0 / 3.0 * N ** 3 if N > 64 else None
+    total = B * world * args.steps
+    line = {
+        "metric": f"ADMM iters/s ({CONFIG_DESC.get(args.config, args.config)}; batch of {B} independent instances "
+                  f"per GPU, aggregate)",
+        "value": total / (ms * 1e-3), "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (seeded, BASELINE.json config {CONFIG_INDEX.get(args.config, '?')}, B seeds per GPU)",
+        "config": {"workload": f"{B} x {args.config} (N={N}, m={probs[0].m}) seeds {args.seed}..",
+                   "l2": "flushed before every timed step (512 MB write, > 126 MB L2)",
+                   "parallelism": f"{B} instances per GPU on {B} streams (CUDA graphs), lock-step"
+                                  + (f", {world} GPUs" if world > 1 else "")},
+        "per_instance_iters_per_s": args.steps / (ms * 1e-3),
+        "iters_done": [int(x["iter"]) for x in infos],
+        "roofline": None if trd_flops is None else {
+            "kernel": f"k_tridiag x {B} concurrent clusters (4/3 N^3 FP64 flops each, CUDA-core DFMA)",
+            "bound": "alu", "achieved": trd_flops * args.steps / (ms * 1e-3) / 1e12, "peak": DFMA_PEAK_TFLOPS,
+            "unit": "TFLOP/s", "frac": trd_flops * args.steps / (ms * 1e-3) / 1e12 / DFMA_PEAK_TFLOPS,
+            "traffic": None, "note": "whole-step time in the denominator (upper bound on the kernel time)"},
+        "cpu_baseline": None, "e2e": None,
+        "gpu_launches": int((sol[0].launches_per_iter + 1) * B * args.steps),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def time_to_tol(prob, device, args):
     """Wall time from setup to the first iterate with max residual <= 1e-4 and |gamma/gamma0 - 1| <= 1e-4
     (checked every 25 iterations; the solver's own stop rule is residual-only)."""
@@ -434,11 +519,14 @@ def main():
     ap.add_argument("--ttt-max", type=int, default=20000)
     ap.add_argument("--no-ttt", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--batch", type=int, default=1, help="B > 1: B independent instances per GPU (SURVEY f1)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.batch > 1:
+        run_batch(args)
     else:
         run_ours(args)
 

@@ -132,6 +132,14 @@ sosadmm_err sosadmm_setup_sharded(const sosadmm_problem* prob, const sosadmm_set
  * completed before return; *out (may be NULL) receives the state after the last iteration. */
 sosadmm_err sosadmm_iterate(sosadmm_ctx* ctx, int64_t k, sosadmm_info* out);
 
+/* Enqueue k ADMM iterations (k CUDA-graph replays) on the context's stream and return without
+ * waiting (independent instances, each set up with its own stream, run concurrently
+ * on one GPU — e.g. one 16-CTA tridiagonalisation cluster per instance).  The device-side
+ * termination rule still applies to every iteration.  sosadmm_get_info (or sosadmm_iterate)
+ * completes the work and reports; launch errors are returned here, asynchronous faults there.
+ * On a sharded context it is a collective like sosadmm_iterate. */
+sosadmm_err sosadmm_iterate_async(sosadmm_ctx* ctx, int64_t k);
+
 /* Same iterations launched without the CUDA graph, with CUDA events (on the library's stream)
  * around each phase; adds the phase durations (ms) to ms_phase[0..SOSADMM_NPHASE-1] = {affine
  * gather..row update, scatter, small-block Jacobi projections, large-block tridiagonalisation,

@@ -2,4 +2,4 @@
 
 The product path is the CUDA library `libsosadmm.so` (C ABI: include/sosadmm.h) and the thin
 ctypes binding `SosAdmm`.  It never imports `oracle/`."""
-from .sosadmm import EXPORTS, LIB_PATH, STATUS, SosAdmm, load_library  # noqa: F401
+from .sosadmm import EXPORTS, LIB_PATH, STATUS, SosAdmm, iterate_batch, load_library  # noqa: F401

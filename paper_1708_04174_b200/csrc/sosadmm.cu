@@ -834,6 +834,16 @@ sosadmm_err sosadmm_iterate(sosadmm_ctx* c, int64_t k, sosadmm_info* out) {
   return read_info(c, out);
 }
 
+sosadmm_err sosadmm_iterate_async(sosadmm_ctx* c, int64_t k) {
+  if (!c) return SOSADMM_E_ARG;
+  if (c->err) return c->err;
+  if (k < 0) return SOSADMM_E_ARG;
+  CK_CTX(c, cudaSetDevice(c->device));
+  if (build_graph(c)) return c->err;
+  for (int64_t i = 0; i < k; ++i) CK_CTX(c, cudaGraphLaunch(c->graph, c->stream));
+  return check_async(c);
+}
+
 sosadmm_err sosadmm_iterate_profiled(sosadmm_ctx* c, int64_t k, sosadmm_info* out, double* ms_phase) {
   if (!c) return SOSADMM_E_ARG;
   if (c->err) return c->err;

@@ -19,7 +19,7 @@ STATUS = {0: "RUNNING", 1: "OPTIMAL", 2: "PRIMAL_INFEASIBLE", 3: "DUAL_INFEASIBL
           5: "INCONCLUSIVE"}
 
 EXPORTS = ["sosadmm_workspace_size", "sosadmm_setup", "sosadmm_setup_sharded", "sosadmm_nccl_unique_id",
-           "sosadmm_iterate", "sosadmm_iterate_profiled",
+           "sosadmm_iterate", "sosadmm_iterate_async", "sosadmm_iterate_profiled",
            "sosadmm_get_info", "sosadmm_get_iterate", "sosadmm_set_iterate", "sosadmm_get_structure",
            "sosadmm_project_affine", "sosadmm_project_psd", "sosadmm_launches_per_iter", "sosadmm_destroy",
            "sosadmm_strerror", "sosadmm_last_error_message"]
@@ -72,6 +72,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.sosadmm_nccl_unique_id.argtypes = [ctypes.c_char_p]
     lib.sosadmm_iterate.argtypes = [V, I64, ctypes.POINTER(_Info)]
     lib.sosadmm_iterate_profiled.argtypes = [V, I64, ctypes.POINTER(_Info), P]
+    lib.sosadmm_iterate_async.argtypes = [V, I64]
     lib.sosadmm_get_info.argtypes = [V, ctypes.POINTER(_Info)]
     lib.sosadmm_get_iterate.argtypes = [V, P, P, P, P, P, P, ctypes.POINTER(I64)]
     lib.sosadmm_set_iterate.argtypes = [V, P, P, P, P, D, D, I64]
@@ -182,6 +183,10 @@ class SosAdmm:
         self._check(self.lib.sosadmm_iterate(self._ctx, int(k), ctypes.byref(info)), "iterate")
         return info.as_dict()
 
+    def iterate_async(self, k: int) -> None:
+        """Enqueue k iterations on this instance's stream and return at once (see iterate_batch)."""
+        self._check(self.lib.sosadmm_iterate_async(self._ctx, int(k)), "iterate_async")
+
     def iterate_profiled(self, k: int):
         info = _Info()
         ms = np.zeros(NPHASE)
@@ -250,3 +255,12 @@ class SosAdmm:
             self.close()
         except Exception:
             pass
+
+
+def iterate_batch(solvers, k: int) -> list:
+    """k iterations of independent instances on one GPU.  Each SosAdmm owns a stream,
+    so the k graph replays of every instance are enqueued first and then run concurrently (the
+    per-instance iterates are exactly those of solo runs); returns every instance's info."""
+    for s in solvers:
+        s.iterate_async(k)
+    return [s.info() for s in solvers]

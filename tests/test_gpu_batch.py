@@ -1,0 +1,59 @@
+"""batched independent instances on one GPU (sosadmm_iterate_async + iterate_batch).
+
+Each instance owns a stream and its own CUDA graph; iterate_batch enqueues every instance's graph
+replays before waiting, so the instances run concurrently.  The arithmetic of an instance does not
+depend on what runs beside it (fixed-order reductions, no shared state), so every batched iterate
+must be BIT-identical to the same instance run alone, and each instance must stop at its own
+residual-stop iteration.  Per-instance parity with the oracle is covered by test_gpu_parity.py.
+"""
+import numpy as np
+import pytest
+
+from sosgen import make_config
+
+pytestmark = pytest.mark.gpu
+
+
+def _iterates(s):
+    g = s.get_iterate()
+    return np.concatenate([g["xi"], g["y"], g["z"], g["s"], [g["tau"], g["kappa"], g["iter"]]])
+
+
+def _solo_and_batch(probs, k, **kw):
+    from paper_1708_04174_b200 import SosAdmm, iterate_batch
+
+    solo = []
+    for p in probs:
+        s = SosAdmm.from_problem(p, **kw)
+        info = s.iterate(k)
+        solo.append((info, _iterates(s)))
+        s.close()
+    batch = [SosAdmm.from_problem(p, **kw) for p in probs]
+    infos = iterate_batch(batch, k)
+    out = [(infos[i], _iterates(b)) for i, b in enumerate(batch)]
+    for b in batch:
+        b.close()
+    return solo, out
+
+
+@pytest.mark.parametrize("names", [[("pop6", 0), ("pop6", 1), ("pop6", 2)],
+                                   [("pop20", 0), ("lyap10", 0), ("pop6", 3), ("pop20", 1)]])
+def test_batch_bit_identical_to_solo(names):
+    probs = [make_config(n, seed=s) for n, s in names]
+    solo, batch = _solo_and_batch(probs, 20, max_iters=10_000)
+    for (si, sv), (bi, bv) in zip(solo, batch):
+        assert bi["iter"] == si["iter"] == 20
+        assert np.array_equal(sv, bv)
+        assert bi["res_pri"] == si["res_pri"] and bi["res_dual"] == si["res_dual"]
+
+
+def test_batch_independent_termination():
+    """Instances converge at different iterations; each stops at its own residual-stop k."""
+    probs = [make_config("pop6", seed=s) for s in range(4)]
+    solo, batch = _solo_and_batch(probs, 5000, max_iters=5000)
+    its = [si["iter"] for si, _ in solo]
+    assert len(set(its)) > 1  # the seeds really do stop at different iterations
+    for (si, sv), (bi, bv) in zip(solo, batch):
+        assert si["status_name"] == bi["status_name"] == "OPTIMAL"
+        assert bi["iter"] == si["iter"]
+        assert np.array_equal(sv, bv)
