@@ -289,250 +289,266 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
   const bool prof = a.prof != nullptr && me == 0 && tid == 0;
 #define TRD_STAMP(ph) \
   if (prof) a.prof[(size_t)k * 16 + (ph)] = clock64();
-  for (int k = kb; k < ke; ++k) {
-    const int par = k & 1;
-    TRD_STAMP(0)
-    const double2* xwk = xw + par * N;         // (x~_k, w_{k-1})
-    const double2* xwm = xw + (par ^ 1) * N;   // (x~_{k-1}, .)
-    auto xk = [&](int j) { return xwk[j].x; };
-    auto xkm = [&](int j) { return xwm[j].x; };
-    const int qs1 = first_slot(k + 1), qs2 = first_slot(k + 2);
-    const int nb = (N - k - 1 + 7) >> 3;      // 8-column blocks of the trailing matrix
-    auto nwarps_of_row = [&](int i) { return min(min(TRD_NW, nb), (i - k - 1) / 8 + 1); };  // warps reaching row i
-    // Deferred scaling: the reflector v_k = e_{k+1} + scale_k y with y = x~_k[k+2:] (the pivot entry
-    // zeroed), so the fused pass computes z = A_k y with the UNSCALED column and needs none of the
-    // reflector scalars; p = A_k v_k = A_k[:, k+1] + scale_k z and v^T A v = A_k[k+1,k+1]
-    // + 2 scale z[k+1] + scale^2 y^T z are formed per own row in Phase Y, and the sqrt / division
-    // chain of the reflector is off the critical path.
-    // The chain runs on the LAST warp at the top of the step: its column blocks start furthest right,
-    // so it has the least fused-pass work (none once fewer than 16 blocks remain).  It sums
-    // ||x~_k[k+2:]||^2 itself from the allgathered column (same order in every CTA: no norm
-    // exchange).  scal_s is double-buffered by step parity (read after the next __syncthreads).
-    if (warp == TRD_NW - 1) {
-      // beta = -sign(alpha) sqrt(n2), tau = 1 + |alpha| / sqrt(n2), scale = 1 / (alpha - beta)
-      // = sign(alpha) / (|alpha| + sqrt(n2)): one rsqrt + one division
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int j = k + 2 + lane;
-      for (; j + 96 < N; j += 128) {
-        const double x0 = xk(j), x1 = xk(j + 32), x2 = xk(j + 64), x3 = xk(j + 96);
-        s0 = fma(x0, x0, s0);
-        s1 = fma(x1, x1, s1);
-        s2 = fma(x2, x2, s2);
-        s3 = fma(x3, x3, s3);
-      }
-      for (; j < N; j += 32) {
-        const double x0 = xk(j);
-        s0 = fma(x0, x0, s0);
-      }
-      const double sig = warp_sum((s0 + s1) + (s2 + s3));
-      const double alpha = xk(k + 1);
-      double tk = 0.0, beta = alpha, scale = 0.0;
-      if (sig != 0.0) {
-        const double n2 = fma(alpha, alpha, sig);
-        const double rs = rsqrt(n2);
-        const double nrm = n2 * rs;
-        beta = -copysign(nrm, alpha);
-        tk = fma(fabs(alpha), rs, 1.0);
-        scale = copysign(1.0, alpha) / (fabs(alpha) + nrm);
-      }
-      if (lane == 0) {
-        scal_s[par][0] = tk;
-        scal_s[par][1] = scale;
-        if (me == (k & (C - 1))) {
-          a.e[k] = beta;
-          a.tau[k] = tk;
+  // Steps run through the smallest column-block variant that covers the trailing matrix: MB blocks
+  // per warp while nb > 16 * (next smaller MB), so late steps carry fewer register arrays and
+  // shorter unrolled loops (the variants share all state; k advances inside).
+  int k = kb;
+  auto run = [&](auto MBc, int nb_min) -> bool {
+    constexpr int MB = decltype(MBc)::value;
+    for (; k < ke; ++k) {
+      if (((N - k - 1 + 7) >> 3) <= nb_min) return false;
+      const int par = k & 1;
+      TRD_STAMP(0)
+      const double2* xwk = xw + par * N;         // (x~_k, w_{k-1})
+      const double2* xwm = xw + (par ^ 1) * N;   // (x~_{k-1}, .)
+      auto xk = [&](int j) { return xwk[j].x; };
+      auto xkm = [&](int j) { return xwm[j].x; };
+      const int qs1 = first_slot(k + 1), qs2 = first_slot(k + 2);
+      const int nb = (N - k - 1 + 7) >> 3;      // 8-column blocks of the trailing matrix
+      auto nwarps_of_row = [&](int i) { return min(min(TRD_NW, nb), (i - k - 1) / 8 + 1); };  // warps reaching row i
+      // Deferred scaling: the reflector v_k = e_{k+1} + scale_k y with y = x~_k[k+2:] (the pivot entry
+      // zeroed), so the fused pass computes z = A_k y with the UNSCALED column and needs none of the
+      // reflector scalars; p = A_k v_k = A_k[:, k+1] + scale_k z and v^T A v = A_k[k+1,k+1]
+      // + 2 scale z[k+1] + scale^2 y^T z are formed per own row in Phase Y, and the sqrt / division
+      // chain of the reflector is off the critical path.
+      // The chain runs on the LAST warp at the top of the step: its column blocks start furthest right,
+      // so it has the least fused-pass work (none once fewer than 16 blocks remain).  It sums
+      // ||x~_k[k+2:]||^2 itself from the allgathered column (same order in every CTA: no norm
+      // exchange).  scal_s is double-buffered by step parity (read after the next __syncthreads).
+      if (warp == TRD_NW - 1) {
+        // beta = -sign(alpha) sqrt(n2), tau = 1 + |alpha| / sqrt(n2), scale = 1 / (alpha - beta)
+        // = sign(alpha) / (|alpha| + sqrt(n2)): one rsqrt + one division
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int j = k + 2 + lane;
+        for (; j + 96 < N; j += 128) {
+          const double x0 = xk(j), x1 = xk(j + 32), x2 = xk(j + 64), x3 = xk(j + 96);
+          s0 = fma(x0, x0, s0);
+          s1 = fma(x1, x1, s1);
+          s2 = fma(x2, x2, s2);
+          s3 = fma(x3, x3, s3);
+        }
+        for (; j < N; j += 32) {
+          const double x0 = xk(j);
+          s0 = fma(x0, x0, s0);
+        }
+        const double sig = warp_sum((s0 + s1) + (s2 + s3));
+        const double alpha = xk(k + 1);
+        double tk = 0.0, beta = alpha, scale = 0.0;
+        if (sig != 0.0) {
+          const double n2 = fma(alpha, alpha, sig);
+          const double rs = rsqrt(n2);
+          const double nrm = n2 * rs;
+          beta = -copysign(nrm, alpha);
+          tk = fma(fabs(alpha), rs, 1.0);
+          scale = copysign(1.0, alpha) / (fabs(alpha) + nrm);
+        }
+        if (lane == 0) {
+          scal_s[par][0] = tk;
+          scal_s[par][1] = scale;
+          if (me == (k & (C - 1))) {
+            a.e[k] = beta;
+            a.tau[k] = tk;
+          }
         }
       }
-    }
-    // this lane's columns: blocks bb = warp + 16 t of 8 columns starting at k + 1
-    int nbt = 0;  // blocks of this warp (trd_block is increasing in t)
-#pragma unroll
-    for (int t = 0; t < MAXB; ++t) nbt += trd_block(warp, t) < nb ? 1 : 0;
-    double vn[MAXB], vo[MAXB], wo[MAXB], qa[MAXB];
-#pragma unroll
-    for (int t = 0; t < MAXB; ++t) {
-      const int j = k + 1 + 8 * trd_block(warp, t) + cc;
-      const bool ok = t < nbt && j < N;
-      const double2 cw = ok ? xwk[j] : make_double2(0.0, 0.0);
-      vn[t] = (j == k + 1) ? 0.0 : cw.x;       // y[j]
-      vo[t] = ok ? xkm(j) : 0.0;               // x~_{k-1}[j] (v_{k-1} = scale_{k-1} x~_{k-1} below row k)
-      wo[t] = cw.y;                            // scale_{k-1} w_{k-1}[j] (0 at k = 0: no pending update)
-      qa[t] = 0.0;
-    }
-    if (tid == 32 && !SOLO) trd_bar_expect(&barQ, (unsigned)(8 * (C * (nown - qs2) + 2 * C + 1)));
-    TRD_STAMP(1)
+      // this lane's columns: blocks bb = warp + 16 t of 8 columns starting at k + 1
+      int nbt = 0;  // blocks of this warp (trd_block is increasing in t)
+    #pragma unroll
+      for (int t = 0; t < MB; ++t) nbt += trd_block(warp, t) < nb ? 1 : 0;
+      double vn[MB], vo[MB], wo[MB], qa[MB];
+    #pragma unroll
+      for (int t = 0; t < MB; ++t) {
+        const int j = k + 1 + 8 * trd_block(warp, t) + cc;
+        const bool ok = t < nbt && j < N;
+        const double2 cw = ok ? xwk[j] : make_double2(0.0, 0.0);
+        vn[t] = (j == k + 1) ? 0.0 : cw.x;       // y[j]
+        vo[t] = ok ? xkm(j) : 0.0;               // x~_{k-1}[j] (v_{k-1} = scale_{k-1} x~_{k-1} below row k)
+        wo[t] = cw.y;                            // scale_{k-1} w_{k-1}[j] (0 at k = 0: no pending update)
+        qa[t] = 0.0;
+      }
+      if (tid == 32 && !SOLO) trd_bar_expect(&barQ, (unsigned)(8 * (C * (nown - qs2) + 2 * C + 1)));
+      TRD_STAMP(1)
 
-    // ---- Phase X: fused rank-2 update of step k-1 and symv with v_k over own rows i >= k+1 ----
-    double dpart = 0.0;  // this thread's share of v^T A v (row part: racc v_i; column part: q_j v_j)
-    const int qw = first_slot(k + 1 + 8 * warp);  // a warp only visits rows reaching its first block
-    // one group of 4 rows (lane row lr); FULL = all four rows exist (every group but possibly the
-    // last), which removes every per-lane validity test from the unmasked path
-    auto row_group = [&](int g, int qe, auto rp_of, auto FULL) {
-      constexpr bool full = decltype(FULL)::value;
-      const int q = full ? g + lr : min(g + lr, qe - 1);
-      const bool valid = full || g + lr < qe;
-      const int ic = me + q * C;                     // row (clamped on the padding lanes)
-      const int i = valid ? ic : -1;
-      const int imin = me + g * C;                   // smallest row of the group (uniform)
-      const int imax = me + (full ? g + 3 : min(g + 3, qe - 1)) * C;  // largest row of the group (uniform)
-      double* R = rp_of(q);
-      const double vio = xkm(ic);                    // x~_{k-1}[i], i >= k + 1
-      const double vin = (ic == k + 1) ? 0.0 : xk(ic);  // y[i]
-      const double wio = xwk[ic].y;                  // scale_{k-1} w_{k-1}[i]
-      double racc = 0.0;
-#pragma unroll
-      for (int t = 0; t < MAXB; ++t) {
-        const int jf = k + 1 + 8 * trd_block(warp, t);
-        if (t >= nbt || jf > imax) break;  // this and all later blocks lie right of the group's diagonal
-        const int j = jf + cc;
-        if (jf + 7 < imin) {  // strictly below every row's diagonal: no column masking
-          if (full || valid) {
+      // ---- Phase X: fused rank-2 update of step k-1 and symv with v_k over own rows i >= k+1 ----
+      double dpart = 0.0;  // this thread's share of v^T A v (row part: racc v_i; column part: q_j v_j)
+      const int qw = first_slot(k + 1 + 8 * warp);  // a warp only visits rows reaching its first block
+      // one group of 4 rows (lane row lr); FULL = all four rows exist (every group but possibly the
+      // last), which removes every per-lane validity test from the unmasked path
+      auto row_group = [&](int g, int qe, auto rp_of, auto FULL) {
+        constexpr bool full = decltype(FULL)::value;
+        const int q = full ? g + lr : min(g + lr, qe - 1);
+        const bool valid = full || g + lr < qe;
+        const int ic = me + q * C;                     // row (clamped on the padding lanes)
+        const int i = valid ? ic : -1;
+        const int imin = me + g * C;                   // smallest row of the group (uniform)
+        const int imax = me + (full ? g + 3 : min(g + 3, qe - 1)) * C;  // largest row of the group (uniform)
+        double* R = rp_of(q);
+        const double vio = xkm(ic);                    // x~_{k-1}[i], i >= k + 1
+        const double vin = (ic == k + 1) ? 0.0 : xk(ic);  // y[i]
+        const double wio = xwk[ic].y;                  // scale_{k-1} w_{k-1}[i]
+        double racc = 0.0;
+    #pragma unroll
+        for (int t = 0; t < MB; ++t) {
+          const int jf = k + 1 + 8 * trd_block(warp, t);
+          if (t >= nbt || jf > imax) break;  // this and all later blocks lie right of the group's diagonal
+          const int j = jf + cc;
+          if (jf + 7 < imin) {  // strictly below every row's diagonal: no column masking
+            if (full || valid) {
+              double x = R[j];
+              x = fma(-vio, wo[t], fma(-wio, vo[t], x));
+              R[j] = x;
+              racc = fma(x, vn[t], racc);
+              qa[t] = fma(x, vin, qa[t]);
+            }
+          } else if (j <= i) {  // i = -1 on the padding lanes of the last group
             double x = R[j];
             x = fma(-vio, wo[t], fma(-wio, vo[t], x));
             R[j] = x;
             racc = fma(x, vn[t], racc);
-            qa[t] = fma(x, vin, qa[t]);
+            qa[t] = fma(x, (j < i) ? vin : 0.0, qa[t]);
           }
-        } else if (j <= i) {  // i = -1 on the padding lanes of the last group
-          double x = R[j];
-          x = fma(-vio, wo[t], fma(-wio, vo[t], x));
-          R[j] = x;
-          racc = fma(x, vn[t], racc);
-          qa[t] = fma(x, (j < i) ? vin : 0.0, qa[t]);
         }
-      }
-      racc += __shfl_xor_sync(0xffffffffu, racc, 1);
-      racc += __shfl_xor_sync(0xffffffffu, racc, 2);
-      racc += __shfl_xor_sync(0xffffffffu, racc, 4);
-      if (valid && cc == 0) {
-        rp[warp * S + q - qlo] = racc;
-        dpart = fma(racc, vin, dpart);
-      }
-    };
-    auto row_groups = [&](int qb, int qe, auto rp_of) {
-      if (nbt == 0) return;
-      int g = max(qb, qw);
-#pragma unroll 2
-      for (; g + 4 <= qe; g += 4) row_group(g, qe, rp_of, std::true_type());
-      if (g < qe) row_group(g, qe, rp_of, std::false_type());
-    };
-    if (qs1 < nspill) row_groups(qs1, nspill, rowptr_g);
-    row_groups(max(qs1, nspill), nown, rowptr_s);
-    TRD_STAMP(2)
-    // column sums over the 4 row lanes; lanes with lr == 0 hold q[j] for their 8-column blocks
-#pragma unroll
-    for (int t = 0; t < MAXB; ++t) {
-      if (t >= nbt) break;
-      double v = qa[t];
-      v += __shfl_xor_sync(0xffffffffu, v, 8);
-      v += __shfl_xor_sync(0xffffffffu, v, 16);
-      qa[t] = v;
-      if (lr == 0) dpart = fma(v, vn[t], dpart);
-    }
-    if (warp == 0 && lane == 0) qk1_s = qa[0];  // column k+1 (block 0, cc 0)
-    // reduce-scatter of the transposed partials: column j's partial goes to the owner of row j
-    if (lr == 0) {
-#pragma unroll
-      for (int t = 0; t < MAXB; ++t) {
+        racc += __shfl_xor_sync(0xffffffffu, racc, 1);
+        racc += __shfl_xor_sync(0xffffffffu, racc, 2);
+        racc += __shfl_xor_sync(0xffffffffu, racc, 4);
+        if (valid && cc == 0) {
+          rp[warp * S + q - qlo] = racc;
+          dpart = fma(racc, vin, dpart);
+        }
+      };
+      auto row_groups = [&](int qb, int qe, auto rp_of) {
+        if (nbt == 0) return;
+        int g = max(qb, qw);
+    #pragma unroll 2
+        for (; g + 4 <= qe; g += 4) row_group(g, qe, rp_of, std::true_type());
+        if (g < qe) row_group(g, qe, rp_of, std::false_type());
+      };
+      if (qs1 < nspill) row_groups(qs1, nspill, rowptr_g);
+      row_groups(max(qs1, nspill), nown, rowptr_s);
+      TRD_STAMP(2)
+      // column sums over the 4 row lanes; lanes with lr == 0 hold q[j] for their 8-column blocks
+    #pragma unroll
+      for (int t = 0; t < MB; ++t) {
         if (t >= nbt) break;
-        const int j = k + 1 + 8 * trd_block(warp, t) + cc;
-        if (j >= k + 2 && j < N) push(qr + me * S + (j >> logC) - qlo, j & (C - 1), qa[t], &barQ);
+        double v = qa[t];
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        qa[t] = v;
+        if (lr == 0) dpart = fma(v, vn[t], dpart);
       }
-    }
-    dpart = warp_sum(dpart);
-    if (lane == 0) red[warp] = dpart;
-    __syncthreads();
-    TRD_STAMP(3)
-    const bool own1 = ((k + 1) & (C - 1)) == me;  // this CTA owns row k + 1
-    if (tid < C) {
-      push(sd + me, tid, trd_sumc<TRD_NW>(red), &barQ);
-      push(se + me, tid, qk1_s, &barQ);
-      if (own1) push(sc, tid, rowval((k + 1) >> logC, k + 1), &barQ);  // A_k[k+1, k+1]
-    }
-    TRD_STAMP(4)
-    const bool last = (k == N - 3);
-    const int nslot = nown - qs1;
-    double prow_own = 0.0;  // this CTA's row dot of its own row (sum over the warps), before the wait
-    if (tid < nslot) {
-      const int i = me + (qs1 + tid) * C;
-      if (i > k + 1) prow_own = trd_sum16(rp + qs1 + tid - qlo, nwarps_of_row(i), S);
-    }
-    const double tk = scal_s[par][0], scale = scal_s[par][1];  // written before the last __syncthreads
-    TRD_STAMP(8)
-    if (!SOLO) {
-      if (tid == 0 && !last) trd_bar_expect(&barY, (unsigned)(16 * (N - k - 2)));
-      trd_bar_wait(&barQ, par);
-    } else {
+      if (warp == 0 && lane == 0) qk1_s = qa[0];  // column k+1 (block 0, cc 0)
+      // reduce-scatter of the transposed partials: column j's partial goes to the owner of row j
+      if (lr == 0) {
+    #pragma unroll
+        for (int t = 0; t < MB; ++t) {
+          if (t >= nbt) break;
+          const int j = k + 1 + 8 * trd_block(warp, t) + cc;
+          if (j >= k + 2 && j < N) push(qr + me * S + (j >> logC) - qlo, j & (C - 1), qa[t], &barQ);
+        }
+      }
+      dpart = warp_sum(dpart);
+      if (lane == 0) red[warp] = dpart;
       __syncthreads();
-    }
-    TRD_STAMP(5)
-
-    // ---- Phase Y (own-row threads): w_k, eager update of column k+1, its norm partial ----
-    double Kc = 0.0, wk1 = 0.0;
-    if (tid < nslot) {
-      const double yz = trd_sumc<CC>(sd);     // y^T A y
-      const double z1 = trd_sumc<CC>(se);     // (A y)[k+1]
-      const double c1 = sc[0];                // A_k[k+1, k+1]
-      const double vav = fma(scale, fma(scale, yz, 2.0 * z1), c1);  // v^T A v
-      Kc = 0.5 * tk * tk * vav;               // (tau/2) p^T v with p = tau A v
-      wk1 = fma(tk, fma(scale, z1, c1), -Kc);  // w_k[k+1] (v_k[k+1] = 1)
-    }
-    TRD_STAMP(10)
-    // each own-row thread pushes its (x~_{k+1}[i], scale_k w_k[i]) straight to every CTA (allgather;
-    // peers staggered so the 16 stores of a warp hit 16 different CTAs)
-    double2* xnext = xw + (par ^ 1) * N;  // (x~_{k+1}, scale_k w_k)
-    auto phase_y = [&](int q, double* R, double prow) {
-      const int i = me + q * C;
-      if (i == k + 1) {
-        a.d[k + 1] = R[k + 1] - 2.0 * wk1;
+      TRD_STAMP(3)
+      const bool own1 = ((k + 1) & (C - 1)) == me;  // this CTA owns row k + 1
+      if (tid < C) {
+        push(sd + me, tid, trd_sumc<TRD_NW>(red), &barQ);
+        push(se + me, tid, qk1_s, &barQ);
+        if (own1) push(sc, tid, rowval((k + 1) >> logC, k + 1), &barQ);  // A_k[k+1, k+1]
+      }
+      TRD_STAMP(4)
+      const bool last = (k == N - 3);
+      const int nslot = nown - qs1;
+      double prow_own = 0.0;  // this CTA's row dot of its own row (sum over the warps), before the wait
+      if (tid < nslot) {
+        const int i = me + (qs1 + tid) * C;
+        if (i > k + 1) prow_own = trd_sum16(rp + qs1 + tid - qlo, nwarps_of_row(i), S);
+      }
+      const double tk = scal_s[par][0], scale = scal_s[par][1];  // written before the last __syncthreads
+      TRD_STAMP(8)
+      if (!SOLO) {
+        if (tid == 0 && !last) trd_bar_expect(&barY, (unsigned)(16 * (N - k - 2)));
+        trd_bar_wait(&barQ, par);
       } else {
-        const double vin = xk(i) * scale;
-        const double pq = fma(scale, prow + trd_sum16(qr + q - qlo, C, S), R[k + 1]);  // (A v)[i]
-        const double wi = fma(-Kc, vin, tk * pq);
-        const double x = fma(-vin, wk1, R[k + 1] - wi);
-        R[k + 1] = x;
-        if (last) {  // i == N - 1: the trailing 2 x 2 block
-          a.e[N - 2] = x;
-          a.d[N - 1] = R[N - 1] - 2.0 * vin * wi;
-          a.tau[N - 2] = 0.0;
-        } else {
-          const double ws = wi * scale;
-#pragma unroll
-          for (int c = 0; c < C; ++c) push2(xnext + i, (c + tid) & (C - 1), x, ws, &barY);
-        }
+        __syncthreads();
       }
-    };
-    if (tid < nslot) {
-      const int q = qs1 + tid;
-      if (q < nspill) phase_y(q, rowptr_g(q), prow_own);
-      else phase_y(q, rowptr_s(q), prow_own);
-    }
-    TRD_STAMP(11)
-    if (me == (k & (C - 1)))  // v_k for the back-transform (global, read by later kernels only)
-      for (int j = k + 1 + tid; j < N; j += TRD_NT) a.V[(size_t)k * N + j] = (j == k + 1) ? 1.0 : xk(j) * scale;
-    if (last) break;
-    TRD_STAMP(7)
-    if (!SOLO) trd_bar_wait(&barY, par ^ 1);
-    else __syncthreads();
-    if (k + 1 == ke && ke < N - 2) {
-      // ---- hand over to the single-CTA tail: rows i >= ke back to global, lazy state to hand[] ----
-      for (int q = max(first_slot(ke), nspill); q < nown; ++q) {
+      TRD_STAMP(5)
+
+      // ---- Phase Y (own-row threads): w_k, eager update of column k+1, its norm partial ----
+      double Kc = 0.0, wk1 = 0.0;
+      if (tid < nslot) {
+        const double yz = trd_sumc<CC>(sd);     // y^T A y
+        const double z1 = trd_sumc<CC>(se);     // (A y)[k+1]
+        const double c1 = sc[0];                // A_k[k+1, k+1]
+        const double vav = fma(scale, fma(scale, yz, 2.0 * z1), c1);  // v^T A v
+        Kc = 0.5 * tk * tk * vav;               // (tau/2) p^T v with p = tau A v
+        wk1 = fma(tk, fma(scale, z1, c1), -Kc);  // w_k[k+1] (v_k[k+1] = 1)
+      }
+      TRD_STAMP(10)
+      // each own-row thread pushes its (x~_{k+1}[i], scale_k w_k[i]) straight to every CTA (allgather;
+      // peers staggered so the 16 stores of a warp hit 16 different CTAs)
+      double2* xnext = xw + (par ^ 1) * N;  // (x~_{k+1}, scale_k w_k)
+      auto phase_y = [&](int q, double* R, double prow) {
         const int i = me + q * C;
-        const double* src = rowptr_s(q);
-        double* dst = a.M + (size_t)i * N;
-        for (int j = ke + tid; j <= i; j += TRD_NT) dst[j] = src[j];
-      }
-      if (me == 0) {
-        const int pk = ke & 1;
-        for (int j = tid; j < N; j += TRD_NT) {
-          a.hand[j] = xw[pk * N + j].x;
-          a.hand[N + j] = xw[(pk ^ 1) * N + j].x;
-          a.hand[2 * N + j] = xw[pk * N + j].y;
+        if (i == k + 1) {
+          a.d[k + 1] = R[k + 1] - 2.0 * wk1;
+        } else {
+          const double vin = xk(i) * scale;
+          const double pq = fma(scale, prow + trd_sum16(qr + q - qlo, C, S), R[k + 1]);  // (A v)[i]
+          const double wi = fma(-Kc, vin, tk * pq);
+          const double x = fma(-vin, wk1, R[k + 1] - wi);
+          R[k + 1] = x;
+          if (last) {  // i == N - 1: the trailing 2 x 2 block
+            a.e[N - 2] = x;
+            a.d[N - 1] = R[N - 1] - 2.0 * vin * wi;
+            a.tau[N - 2] = 0.0;
+          } else {
+            const double ws = wi * scale;
+    #pragma unroll
+            for (int c = 0; c < C; ++c) push2(xnext + i, (c + tid) & (C - 1), x, ws, &barY);
+          }
         }
+      };
+      if (tid < nslot) {
+        const int q = qs1 + tid;
+        if (q < nspill) phase_y(q, rowptr_g(q), prow_own);
+        else phase_y(q, rowptr_s(q), prow_own);
       }
-      break;
+      TRD_STAMP(11)
+      if (me == (k & (C - 1)))  // v_k for the back-transform (global, read by later kernels only)
+        for (int j = k + 1 + tid; j < N; j += TRD_NT) a.V[(size_t)k * N + j] = (j == k + 1) ? 1.0 : xk(j) * scale;
+      if (last) return true;
+      TRD_STAMP(7)
+      if (!SOLO) trd_bar_wait(&barY, par ^ 1);
+      else __syncthreads();
+      if (k + 1 == ke && ke < N - 2) {
+        // ---- hand over to the single-CTA tail: rows i >= ke back to global, lazy state to hand[] ----
+        for (int q = max(first_slot(ke), nspill); q < nown; ++q) {
+          const int i = me + q * C;
+          const double* src = rowptr_s(q);
+          double* dst = a.M + (size_t)i * N;
+          for (int j = ke + tid; j <= i; j += TRD_NT) dst[j] = src[j];
+        }
+        if (me == 0) {
+          const int pk = ke & 1;
+          for (int j = tid; j < N; j += TRD_NT) {
+            a.hand[j] = xw[pk * N + j].x;
+            a.hand[N + j] = xw[(pk ^ 1) * N + j].x;
+            a.hand[2 * N + j] = xw[pk * N + j].y;
+          }
+        }
+        return true;
+      }
     }
-  }
+    return true;
+  };
+  using std::integral_constant;
+  bool done = false;
+  if constexpr (MAXB >= 10) done = run(integral_constant<int, 10>(), TRD_NW * 7);
+  if constexpr (MAXB >= 7) if (!done) done = run(integral_constant<int, 7>(), TRD_NW * 4);
+  if constexpr (MAXB >= 4) if (!done) done = run(integral_constant<int, 4>(), TRD_NW * 2);
+  if (!done) done = run(integral_constant<int, 2>(), TRD_NW);
+  if (!done) run(integral_constant<int, 1>(), 0);
 #undef TRD_STAMP
   if (!SOLO) trd_cluster_sync();  // no CTA leaves while a peer may still address its shared memory
 }
