@@ -100,6 +100,28 @@ __global__ void k_dc_leaf(DcArgs a, int first_leaf, int nleaves, int buf) {
   }
 }
 
+// ordered stream compaction over [0, n) by one CTA of DC_NT threads: out[rank] = map(i) for the i
+// with pred(i), in increasing i; returns the count (every thread).  wcnt: DC_NT/32 ints of SMEM.
+template <class P, class M>
+__device__ int dc_compact(int n, P pred, M map, int* out, int* wcnt) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  int base = 0;
+  __syncthreads();
+  for (int i0 = 0; i0 < n; i0 += DC_NT) {
+    const int i = i0 + tid;
+    const bool p = i < n && pred(i);
+    const unsigned m = __ballot_sync(0xffffffffu, p);
+    if (lane == 0) wcnt[warp] = __popc(m);
+    __syncthreads();
+    int o = base;
+    for (int w = 0; w < warp; ++w) o += wcnt[w];
+    if (p) out[o + __popc(m & ((1u << lane) - 1u))] = map(i);
+    for (int w = 0; w < DC_NT / 32; ++w) base += wcnt[w];
+    __syncthreads();
+  }
+  return base;
+}
+
 // ---- merge step 1: z, sort, deflation (one CTA per node) ---------------------------------
 constexpr int DC_MAXN = 1280;
 __global__ void __launch_bounds__(DC_NT) k_dc_prep(DcArgs a, int node0, int ob) {
@@ -119,36 +141,40 @@ __global__ void __launch_bounds__(DC_NT) k_dc_prep(DcArgs a, int node0, int ob) 
   const double er = a.e[s + n1 - 1];
   const double rho = fabs(er);
   const double sg = (er < 0.0) ? -1.0 : 1.0;
-  // sorted merge of the two ascending child spectra (ties: left child first)
+  // sorted merge of the two ascending child spectra (ties: left child first); the children's
+  // eigenvalues are staged in shared memory (zsh as scratch) so the binary searches hit SMEM
+  for (int i = tid; i < n; i += DC_NT) zsh[i] = lo[s + i];
+  __syncthreads();
   for (int i = tid; i < n; i += DC_NT) {
-    const double di = lo[s + i];
+    const double di = zsh[i];
     int rank;
     if (i < n1) {  // count right elements < di
       int l = 0, h = n - n1;
       while (l < h) {
         const int mid = (l + h) >> 1;
-        if (lo[s + n1 + mid] < di) l = mid + 1; else h = mid;
+        if (zsh[n1 + mid] < di) l = mid + 1; else h = mid;
       }
       rank = i + l;
     } else {  // count left elements <= di
       int l = 0, h = n1;
       while (l < h) {
         const int mid = (l + h) >> 1;
-        if (lo[s + mid] <= di) l = mid + 1; else h = mid;
+        if (zsh[mid] <= di) l = mid + 1; else h = mid;
       }
       rank = (i - n1) + l;
     }
     perm[rank] = i;
   }
   __syncthreads();
+  for (int r = tid; r < n; r += DC_NT) dsh[r] = zsh[perm[r]];
+  __syncthreads();
   double z2 = 0.0, dmax = 0.0;
   for (int r = tid; r < n; r += DC_NT) {
     const int i = perm[r];
     const double zi = (i < n1) ? Qo[(size_t)(s + i) * N + (s + n1 - 1)] : sg * Qo[(size_t)(s + i) * N + (s + n1)];
-    dsh[r] = lo[s + i];
     zsh[r] = zi;
     z2 = fma(zi, zi, z2);
-    dmax = fmax(dmax, fabs(lo[s + i]));
+    dmax = fmax(dmax, fabs(dsh[r]));
   }
   // block reductions (sum, max)
   z2 = warp_sum(z2);
@@ -220,23 +246,38 @@ __global__ void __launch_bounds__(DC_NT) k_dc_prep(DcArgs a, int node0, int ob) 
     }
   }
   __syncthreads();
+  // Type 2 (close pairs).  The sequential rule: step c pairs r = cand[c] with pj = cand[c-1] (its
+  // values modified iff step c-1 rotated).  Step 1 (parallel): the pair test of every consecutive
+  // pair on the ORIGINAL values, compacted into a list of flagged steps (ndl as scratch).  Step 2
+  // (one thread): only rotation chains are walked — a chain starts at a flagged step whose
+  // predecessor did not rotate and continues while the modified pj keeps rotating, so the work is
+  // the number of flagged steps + rotations, not n.  Step 3 (parallel): ordered compaction of the
+  // non-deflated candidates and the type-2 deflations (= the pj of every rotation, in step order).
+  const int nc = ncand_s, ndf1 = ndf1_s;
+  auto ptest = [&](double zr, double dr, double zp, double dp) {
+    return fabs((dr - dp) * zr * zp) <= tol * fma(zr, zr, zp * zp);
+  };
+  __shared__ int rotf[DC_MAXN];
+  __shared__ int wcnt3[DC_NT / 32];
+  for (int c = tid; c < nc; c += DC_NT) rotf[c] = 0;
+  const int nf = dc_compact(
+      nc,
+      [&](int c) {
+        return c >= 1 && ptest(zsh[cand[c]], dsh[cand[c]], zsh[cand[c - 1]], dsh[cand[c - 1]]);
+      },
+      [&](int c) { return c; }, ndl, wcnt3);
   if (tid == 0) {
-    const int nc = ncand_s;
-    int k = 0, df = ndf1_s, nr = 0, pj = -1;
-    double zp = 0.0, dp = 0.0;
-    for (int c = 0; c < nc; ++c) {
-      const int r = cand[c];
-      const double zr = zsh[r], dr = dsh[r];
-      if (pj < 0) {
-        pj = r;
-        zp = zr;
-        dp = dr;
-        continue;
-      }
-      const double t = dr - dp;
-      const double nn = fma(zr, zr, zp * zp);
-      if (fabs(t * zr * zp) <= tol * nn) {
-        const double tt = sqrt(nn);
+    int nr = 0, cend = 0;  // steps < cend are settled
+    for (int u = 0; u < nf; ++u) {
+      int c = ndl[u];
+      if (c < cend) continue;
+      int pj = cand[c - 1];
+      double zp = zsh[pj], dp = dsh[pj];
+      for (; c < nc; ++c) {
+        const int r = cand[c];
+        const double zr = zsh[r], dr = dsh[r];
+        if (!ptest(zr, dr, zp, dp)) break;
+        const double tt = sqrt(fma(zr, zr, zp * zp));
         const double cv = zr / tt, sv = -zp / tt;
         zsh[r] = tt;
         zsh[pj] = 0.0;
@@ -250,22 +291,24 @@ __global__ void __launch_bounds__(DC_NT) k_dc_prep(DcArgs a, int node0, int ob) 
         const double dnew = dp * sv * sv + dr * cv * cv;
         dsh[r] = dnew;
         dsh[pj] = t1;
-        dfl[df++] = pj;
+        rotf[c] = 1;
         pj = r;
         zp = tt;
         dp = dnew;
-      } else {
-        ndl[k++] = pj;
-        pj = r;
-        zp = zr;
-        dp = dr;
       }
+      cend = c + 1;
     }
-    if (pj >= 0) ndl[k++] = pj;
-    nk = k;
-    ndf = df;
     nrot = nr;
     rho_s = rhop;
+  }
+  __syncthreads();
+  const int nkeep = dc_compact(
+      nc, [&](int c) { return !(c + 1 < nc && rotf[c + 1]); }, [&](int c) { return cand[c]; }, ndl, wcnt3);
+  const int ndf2 = dc_compact(
+      nc, [&](int c) { return c + 1 < nc && rotf[c + 1]; }, [&](int c) { return cand[c]; }, dfl + ndf1, wcnt3);
+  if (tid == 0) {
+    nk = nkeep;
+    ndf = ndf1 + ndf2;
   }
   __syncthreads();
   const int k = nk, df = ndf, nr = nrot;
