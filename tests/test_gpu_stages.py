@@ -29,6 +29,7 @@ def dp(a):
 
 
 @pytest.mark.parametrize("M,N,K,tb", [(64, 64, 16, 0), (100, 37, 53, 0), (861, 861, 40, 1), (7, 130, 300, 1),
+                                     (300, 257, 129, 0), (861, 700, 700, 0), (1280, 1100, 33, 1), (192, 192, 1, 0),
                                       (300, 5, 1, 0), (33, 33, 0, 0)])
 def test_dmma_gemm(M, N, K, tb):
     rng = np.random.default_rng(M + N + K)
