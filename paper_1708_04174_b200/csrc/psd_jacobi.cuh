@@ -31,32 +31,38 @@ __device__ __forceinline__ void rr_pair(int r, int k, int Np, int& p, int& q) {
   }
 }
 
+// MAXN: compile-time bound of the launch's largest block (32 or 64), sizing the per-thread element
+// slots.  Per round: the Np/2 rotation parameters (one thread each), ONE __syncthreads, the
+// elementwise update A' = J^T A J, V' = V J from the ping-pong copy (no read/write hazard, the
+// annihilated couplings written as exact zeros in the same pass), ONE __syncthreads.
+template <int MAXN>
 __global__ void __launch_bounds__(JAC_NT) k_psd_jacobi(JacobiArgs a) {
   if (a.check_state && (a.st->done || !a.is->proceed)) return;
   const int b = a.small_blk[blockIdx.x];
   const int N = a.blk_N[b];
   const int Np = (N + 1) & ~1;  // even; a padded zero row/column never rotates
+  const int NN = Np * Np;
   double* G = a.mats + a.blk_mat[b];
   extern __shared__ double smem[];
-  double* A = smem;               // Np x Np, column-major
-  double* V = A + Np * Np;        // Np x Np
-  double* alpha = V + Np * Np;    // Np
-  double* beta = alpha + Np;      // Np
-  double* tval = beta + Np;       // Np/2
-  int* partner = (int*)(tval + Np / 2);
+  // A (ping-pong: smem + c NN) and V (smem + (2 + c) NN), Np x Np column-major each
+  auto Ab = [&](int c) { return smem + (size_t)c * NN; };
+  auto Vb = [&](int c) { return smem + (size_t)(2 + c) * NN; };
+  double* alpha = smem + 4 * NN;                  // Np
+  double* beta = alpha + Np;                      // Np
+  int* partner = (int*)(beta + Np);
   __shared__ int nrot;
   __shared__ double normF;
   const int tid = threadIdx.x;
 
-  for (int e = tid; e < Np * Np; e += JAC_NT) {
+  for (int e = tid; e < NN; e += JAC_NT) {
     const int i = e % Np, j = e / Np;
-    A[e] = (i < N && j < N) ? G[(size_t)j * N + i] : 0.0;
-    V[e] = (i == j) ? 1.0 : 0.0;
+    Ab(0)[e] = (i < N && j < N) ? G[(size_t)j * N + i] : 0.0;
+    Vb(0)[e] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
   if (tid < 32) {
     double s = 0.0;
-    for (int e = tid; e < Np * Np; e += 32) s = fma(A[e], A[e], s);
+    for (int e = tid; e < NN; e += 32) s = fma(Ab(0)[e], Ab(0)[e], s);
     s = warp_sum(s);
     if (tid == 0) normF = sqrt(s);
   }
@@ -67,8 +73,7 @@ __global__ void __launch_bounds__(JAC_NT) k_psd_jacobi(JacobiArgs a) {
   // couplings of ~EPS ||A|| every round — without the floor the relative test below (high relative
   // accuracy next to (near-)zero eigenvalues) never reports a quiet sweep and all 60 sweeps run.
   const double tiny = fmax((double)N * EPS * normF, 1e-300);
-  constexpr int PER = JAC_MAXN * JAC_MAXN / JAC_NT;
-  double nv[PER];
+  constexpr int PER = MAXN * MAXN / JAC_NT;
   int ei[PER], ej[PER];  // (row, column) of this thread's element slots, fixed for the whole solve
 #pragma unroll
   for (int cnt = 0; cnt < PER; ++cnt) {
@@ -76,67 +81,47 @@ __global__ void __launch_bounds__(JAC_NT) k_psd_jacobi(JacobiArgs a) {
     ei[cnt] = e % Np;
     ej[cnt] = e / Np;
   }
-
+  int cur = 0;
   for (int sweep = 0; sweep < 60; ++sweep) {
     if (tid == 0) nrot = 0;
-    __syncthreads();
     for (int r = 0; r < Np - 1; ++r) {
-      // 1. rotation parameters of the Np/2 disjoint pairs (GvL sym.schur2)
+      const double* A = Ab(cur);
+      const double* V = Vb(cur);
+      // 1. rotation parameters of the Np/2 disjoint pairs (GvL sym.schur2, rewritten with
+      //    d = a_qq - a_pp: t = sign(d) 2 a_pq / (|d| + sqrt(d^2 + 4 a_pq^2)), c = rsqrt(1 + t^2))
       if (tid < Np / 2) {
         int p, q;
         rr_pair(r, tid, Np, p, q);
         const double apq = A[p + q * Np], app = A[p + p * Np], aqq = A[q + q * Np];
-        double c = 1.0, s = 0.0, t = 0.0;
-        if (fabs(apq) > EPS * sqrt(fabs(app) * fabs(aqq)) && fabs(apq) > tiny) {
-          const double th = (aqq - app) / (2.0 * apq);
-          t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(fma(th, th, 1.0)));
-          c = 1.0 / sqrt(fma(t, t, 1.0));
+        double c = 1.0, s = 0.0;
+        if (apq * apq > EPS * EPS * fabs(app * aqq) && fabs(apq) > tiny) {
+          const double d = aqq - app, tw = 2.0 * apq;
+          const double t = copysign(1.0, d) * tw / (fabs(d) + sqrt(fma(d, d, tw * tw)));
+          c = rsqrt(fma(t, t, 1.0));
           s = t * c;
-          atomicAdd(&nrot, 1);
+          nrot = 1;
         }
         alpha[p] = c; beta[p] = -s; partner[p] = q;
         alpha[q] = c; beta[q] = s;  partner[q] = p;
-        tval[tid] = t;
       }
       __syncthreads();
-      // 2. A <- J^T A J elementwise from the 2x2 coupling (all reads before any write)
-      // (compile-time trip counts keep nv / vv in registers)
-      double vv[JAC_MAXN * JAC_MAXN / JAC_NT];
+      // 2. A' = J^T A J, V' = V J elementwise from the 2 x 2 coupling of (row i, ip) x (col j, jp)
+      double* An = Ab(cur ^ 1);
+      double* Vn = Vb(cur ^ 1);
 #pragma unroll
-      for (int cnt = 0; cnt < JAC_MAXN * JAC_MAXN / JAC_NT; ++cnt) {
+      for (int cnt = 0; cnt < PER; ++cnt) {
         const int e = tid + cnt * JAC_NT;
-        if (e < Np * Np) {
+        if (e < NN) {
           const int i = ei[cnt], j = ej[cnt];
           const int ip = partner[i], jp = partner[j];
           const double ai = alpha[i], bi = beta[i], aj = alpha[j], bj = beta[j];
-          nv[cnt] = ai * (aj * A[i + j * Np] + bj * A[i + jp * Np]) +
-                    bi * (aj * A[ip + j * Np] + bj * A[ip + jp * Np]);
-          // V <- V J (column j mixes with its partner)
-          vv[cnt] = aj * V[i + j * Np] + bj * V[i + jp * Np];
+          const double na = ai * (aj * A[i + j * Np] + bj * A[i + jp * Np]) +
+                            bi * (aj * A[ip + j * Np] + bj * A[ip + jp * Np]);
+          An[e] = (j == ip && bi != 0.0) ? 0.0 : na;  // the coupling of a rotated pair: exact zero
+          Vn[e] = aj * V[i + j * Np] + bj * V[i + jp * Np];
         }
       }
-      __syncthreads();
-#pragma unroll
-      for (int cnt = 0; cnt < JAC_MAXN * JAC_MAXN / JAC_NT; ++cnt) {
-        const int e = tid + cnt * JAC_NT;
-        if (e < Np * Np) {
-          A[e] = nv[cnt];
-          V[e] = vv[cnt];
-        }
-      }
-      __syncthreads();
-      // exact annihilation and the standard diagonal update
-      if (tid < Np / 2) {
-        const double t = tval[tid];
-        if (t != 0.0) {
-          int p, q;
-          rr_pair(r, tid, Np, p, q);
-          // recompute from the pre-rotation values is not possible any more; use the rotated
-          // diagonal (already c^2 a_pp - 2cs a_pq + s^2 a_qq) and zero the coupling exactly
-          A[p + q * Np] = 0.0;
-          A[q + p * Np] = 0.0;
-        }
-      }
+      cur ^= 1;
       __syncthreads();
     }
     if (nrot == 0) {
@@ -145,8 +130,10 @@ __global__ void __launch_bounds__(JAC_NT) k_psd_jacobi(JacobiArgs a) {
 #endif
       break;
     }
-    __syncthreads();
+    __syncthreads();  // every thread has read nrot before thread 0 clears it
   }
+  const double* A = Ab(cur);
+  const double* V = Vb(cur);
   // Pi(A) = V diag(max(lambda, 0)) V^T, lambda_k = A[k, k]
   for (int k = tid; k < Np; k += JAC_NT) alpha[k] = fmax(A[k + k * Np], 0.0);
   __syncthreads();
@@ -162,5 +149,10 @@ __global__ void __launch_bounds__(JAC_NT) k_psd_jacobi(JacobiArgs a) {
 
 inline size_t jacobi_smem_bytes(int N) {
   const int Np = (N + 1) & ~1;
-  return sizeof(double) * (2 * (size_t)Np * Np + 2 * Np + Np / 2) + sizeof(int) * Np;
+  return sizeof(double) * (4 * (size_t)Np * Np + 2 * Np) + sizeof(int) * Np;
+}
+
+typedef void (*JacobiKernel)(JacobiArgs);
+inline JacobiKernel jacobi_kernel(int max_small_N) {
+  return max_small_N <= 32 ? k_psd_jacobi<32> : k_psd_jacobi<64>;
 }
