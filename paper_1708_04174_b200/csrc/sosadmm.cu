@@ -94,6 +94,8 @@ struct Analysis {
   std::vector<int> small_blk, large_blk;
   long long mat_total = 0;
   int max_small_N = 0;
+  std::vector<long long> blk_vp;  // small blocks: offset of the warm-start eigenvector matrix (-1: none)
+  long long vp_total = 0;
   std::vector<int> colown;  // 1: this rank accounts for the column in the sharded partial sums
 };
 
@@ -234,6 +236,7 @@ sosadmm_err analyse(const sosadmm_problem* p, Analysis& an, std::string& msg, co
   // PSD blocks (only the blocks this rank owns are scattered, projected and packed)
   long long col = an.t;
   an.mat_total = 0;
+  an.vp_total = 0;
   an.colown.assign(an.n, 0);
   for (int j = 0; j < an.t; ++j) an.colown[j] = sp.rank == 0 ? 1 : 0;
   for (int b = 0; b < an.nblk; ++b) {
@@ -258,10 +261,13 @@ sosadmm_err analyse(const sosadmm_problem* p, Analysis& an, std::string& msg, co
       if (N <= JAC_MAXN) {
         an.small_blk.push_back(b);
         an.max_small_N = std::max(an.max_small_N, N);
+        an.blk_vp.push_back(an.vp_total);
+        an.vp_total += (long long)N * N;
       } else {
         an.large_blk.push_back(b);
       }
     }
+    if ((long long)an.blk_vp.size() < (long long)an.blk_N.size()) an.blk_vp.push_back(-1);
     col += L;
   }
   return SOSADMM_OK;
@@ -368,6 +374,8 @@ struct DevPtrs {
   long long *blk_col, *blk_mat, *cta_q0;
   int *blk_N, *cta_blk, *small_blk;
   int* colown;
+  double* jvp;         // warm-start eigenvectors of the small blocks
+  long long* blk_vp;
   double *shbuf, *shpart;
 };
 
@@ -420,6 +428,8 @@ void carve(const Analysis& an, Arena& ar, DevPtrs& d, int gather_blocks) {
   d.cta_q0 = ar.take<long long>(an.cta_q0.size());
   d.small_blk = ar.take<int>(an.small_blk.size());
   d.colown = ar.take<int>(n);
+  d.jvp = ar.take<double>((size_t)std::max<long long>(an.vp_total, 1));
+  d.blk_vp = ar.take<long long>(an.nblk);
   d.shbuf = ar.take<double>(2 * m + 3);
   d.shpart = ar.take<double>(3 * (size_t)std::max(gather_blocks, low_blocks(an)));
 }
@@ -711,6 +721,16 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
   CK_CTX(c, h2d(d.cta_q0, an.cta_q0, s));
   CK_CTX(c, h2d(d.small_blk, an.small_blk, s));
   CK_CTX(c, h2d(d.colown, an.colown, s));
+  CK_CTX(c, h2d(d.blk_vp, an.blk_vp, s));
+  if (an.vp_total > 0) {  // warm-start eigenvectors start as identities (the first solve is cold)
+    std::vector<double> eye((size_t)an.vp_total, 0.0);
+    for (int b : an.small_blk) {
+      const int N = an.blk_N[b];
+      for (int i = 0; i < N; ++i) eye[(size_t)an.blk_vp[b] + (size_t)i * N + i] = 1.0;
+    }
+    CK_CTX(c, cudaMemcpyAsync(d.jvp, eye.data(), sizeof(double) * eye.size(), cudaMemcpyHostToDevice, s));
+    CK_CTX(c, cudaStreamSynchronize(s));  // `eye` leaves scope
+  }
   CK_CTX(c, cudaMemsetAsync(d.shbuf, 0, sizeof(double) * (2 * (size_t)an.m + 3), s));
   CK_CTX(c, cudaMemsetAsync(d.xi, 0, sizeof(double) * an.n, s));
   CK_CTX(c, cudaMemsetAsync(d.z, 0, sizeof(double) * an.n, s));
@@ -752,6 +772,7 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
   JacobiArgs& ja = c->ja;
   ja.mats = d.mats; ja.blk_mat = d.blk_mat; ja.blk_N = d.blk_N; ja.small_blk = d.small_blk;
   ja.st = d.st; ja.is = d.is; ja.check_state = 1;
+  ja.vp = d.jvp; ja.blk_vp = d.blk_vp; ja.warm = 1;
   if (!an.small_blk.empty()) {
     // the attribute is per kernel and process-wide: set the template's bound, never a per-context
     // size (a later context with smaller blocks would otherwise shrink it under an earlier one)
