@@ -17,7 +17,7 @@ from sosgen.matrix_sos import brute_force_counts, matrix_planted_kkt, matrix_sos
 
 pytestmark = pytest.mark.gpu
 
-SMALL = ["pop6", "sq", "neg", "one", "pop3k2", "ball4", "msos2"]
+SMALL = ["pop6", "sq", "neg", "one", "pop3k2", "ball4", "msos2", "pop8"]
 LARGE = ["pop20", "lyap10", "box24", "pop40", "msos3"]
 
 
@@ -32,6 +32,8 @@ def make(name):
         return planted_pop("pop3k2", 3, 2, seed=5)
     if name == "ball4":
         return ball_pop(4)
+    if name == "pop8":  # N = 45: the CTA-per-block Jacobi (33 <= N <= 64); N <= 32 use one warp per block
+        return planted_pop("pop8", 8, 4, seed=2)
     if name == "msos2":  # matrix-valued SOS (Proposition 2): Y in S^{2 * 10} (Jacobi path)
         return matrix_sos_pop("msos2", 3, 2, 2, 2, seed=3)
     if name == "msos3":  # Y in S^{3 * 28} (cluster tridiagonalisation path)
