@@ -196,7 +196,7 @@ def roofline_table(prob, tl, phase, large, hbm, hbm_src, config="pop40"):
 
 
 def TRD_CLUSTER(N):
-    return 16 if N > 512 else (8 if N > 160 else 4)
+    return 16 if N > 160 else 4
 
 
 def run_ours(args):

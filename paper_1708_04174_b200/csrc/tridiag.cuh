@@ -559,7 +559,7 @@ inline size_t tridiag_smem_bytes(int N, int C, int S, long long row_doubles) {
 
 typedef void (*TridiagKernel)(TridiagArgs);
 // (MAXB, C) pairs reachable from tridiag_maxb / tridiag_cluster_size, plus the single-CTA tails.
-#define TRD_KERNELS(X) X(2, 4) X(2, 8) X(4, 8) X(4, 16) X(7, 16) X(10, 16) X(2, 1) X(4, 1) X(7, 1) X(10, 1)
+#define TRD_KERNELS(X) X(2, 4) X(4, 4) X(2, 8) X(4, 8) X(7, 8) X(2, 16) X(4, 16) X(7, 16) X(10, 16) X(2, 1) X(4, 1) X(7, 1) X(10, 1)
 inline TridiagKernel tridiag_kernel_mc(int maxb, int C) {
 #define TRD_CASE(MB, CCX) \
   if (maxb == MB && C == CCX) return k_tridiag<MB, CCX>;
