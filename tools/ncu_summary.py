@@ -36,7 +36,7 @@ STALL = "smsp__pcsamp_warps_issue_stalled_"
 traffic = {}
 for r in rows[2:]:
     d, u = dict(zip(head, r)), dict(zip(head, units))
-    name = d["Kernel Name"].split("(")[0]
+    name = d["Kernel Name"].split("(")[0].replace("void ", "")
     ms = val(d, u, "gpu__time_duration.sum")
     rd = val(d, u, "dram__bytes_read.sum") or 0.0
     wr = val(d, u, "dram__bytes_write.sum") or 0.0
