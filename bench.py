@@ -266,6 +266,7 @@ def run_ours(args):
     # ---- end-to-end through the C ABI with host buffers: H2D state, iterate, D2H state --------
     it = gpu.get_iterate()
     pin = {k: torch.from_numpy(np.ascontiguousarray(it[k])).pin_memory() for k in ("xi", "y", "z", "s")}
+    pout = {k: torch.empty_like(pin[k]).pin_memory().numpy() for k in ("xi", "y", "z", "s")}  # pinned results
     h2d = 8 * (2 * prob.n + 2 * prob.m) + 16
     d2h = 8 * (2 * prob.n + 2 * prob.m) + 24
     barrier()
@@ -276,7 +277,7 @@ def run_ours(args):
         gpu.set_iterate(pin["xi"].numpy(), pin["y"].numpy(), pin["z"].numpy(), pin["s"].numpy(), it["tau"],
                         it["kappa"], it["iter"])
         gpu.iterate(1)
-        g = gpu.get_iterate()
+        g = gpu.get_iterate(out=pout)
     eb.record(st)
     barrier()
     e2e_ms = ea.elapsed_time(eb)

@@ -199,9 +199,17 @@ class SosAdmm:
         self._check(self.lib.sosadmm_get_info(self._ctx, ctypes.byref(info)), "get_info")
         return info.as_dict()
 
-    def get_iterate(self):
-        xi, z = np.empty(self.n), np.empty(self.n)
-        y, s = np.empty(self.m), np.empty(self.m)
+    def get_iterate(self, out: dict | None = None):
+        """The iterate (u, v) = (xi, y, tau, z, s, kappa) on the host.  out: preallocated float64 arrays
+        {"xi", "y", "z", "s"} (e.g. views of pinned host tensors, so the copies run at full DMA rate)."""
+        if out is not None:
+            xi, y, z, s = (out[k] for k in ("xi", "y", "z", "s"))
+            for arr, size in ((xi, self.n), (z, self.n), (y, self.m), (s, self.m)):
+                if arr.dtype != np.float64 or arr.size != size or not arr.flags.c_contiguous:
+                    raise ValueError("get_iterate(out=...): contiguous float64 arrays of the iterate's sizes")
+        else:
+            xi, z = np.empty(self.n), np.empty(self.n)
+            y, s = np.empty(self.m), np.empty(self.m)
         tau, kappa, it = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
         self._check(self.lib.sosadmm_get_iterate(self._ctx, _dptr(xi), _dptr(y), _dptr(z), _dptr(s),
                                                  ctypes.byref(tau), ctypes.byref(kappa), ctypes.byref(it)),

@@ -57,3 +57,20 @@ def test_batch_independent_termination():
         assert si["status_name"] == bi["status_name"] == "OPTIMAL"
         assert bi["iter"] == si["iter"]
         assert np.array_equal(sv, bv)
+
+
+def test_get_iterate_into_preallocated_buffers():
+    """get_iterate(out=...) (the e2e path copies into pinned host buffers) returns the same iterate."""
+    from paper_1708_04174_b200 import SosAdmm
+
+    s = SosAdmm.from_problem(make_config("pop6"))
+    s.iterate(7)
+    ref = s.get_iterate()
+    out = {k: np.full_like(ref[k], np.nan) for k in ("xi", "y", "z", "s")}
+    got = s.get_iterate(out=out)
+    for k in ("xi", "y", "z", "s"):
+        assert got[k] is out[k] and np.array_equal(out[k], ref[k])
+    assert (got["tau"], got["kappa"], got["iter"]) == (ref["tau"], ref["kappa"], ref["iter"])
+    with pytest.raises(ValueError):
+        s.get_iterate(out={k: np.zeros(3) for k in ("xi", "y", "z", "s")})
+    s.close()
