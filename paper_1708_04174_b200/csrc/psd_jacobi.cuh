@@ -43,8 +43,8 @@ __device__ __forceinline__ void rr_pair(int r, int k, int Np, int& p, int& q) {
 // new input; Jacobi runs on B = P^T A P (measured on pop6: 8.6 -> 4.9 sweeps, tools/
 // warm_jacobi_probe.py) and the eigenvectors are P V_B.  Every 64th iteration starts cold (P = I)
 // so that the rounding of the accumulated product never builds up.
-template <int MAXN>
-__global__ void __launch_bounds__(JAC_NT) k_psd_jacobi(JacobiArgs a) {
+template <int MAXN, int NT>
+__global__ void __launch_bounds__(NT) k_psd_jacobi(JacobiArgs a) {
   if (a.check_state && (a.st->done || !a.is->proceed)) return;
   const int b = a.small_blk[blockIdx.x];
   const int N = a.blk_N[b];
@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(JAC_NT) k_psd_jacobi(JacobiArgs a) {
   __shared__ double normF;
   const int tid = threadIdx.x;
 
-  for (int e = tid; e < NN; e += JAC_NT) {
+  for (int e = tid; e < NN; e += NT) {
     const int i = e % Np, j = e / Np;
     Ab(0)[e] = (i < N && j < N) ? G[(size_t)j * N + i] : 0.0;
     Vb(0)[e] = (i == j) ? 1.0 : 0.0;
@@ -82,11 +82,11 @@ __global__ void __launch_bounds__(JAC_NT) k_psd_jacobi(JacobiArgs a) {
   // couplings of ~EPS ||A|| every round — without the floor the relative test below (high relative
   // accuracy next to (near-)zero eigenvalues) never reports a quiet sweep and all 60 sweeps run.
   const double tiny = fmax((double)N * EPS * normF, 1e-300);
-  constexpr int PER = MAXN * MAXN / JAC_NT;
+  constexpr int PER = MAXN * MAXN / NT;
   int ei[PER], ej[PER];  // (row, column) of this thread's element slots, fixed for the whole solve
 #pragma unroll
   for (int cnt = 0; cnt < PER; ++cnt) {
-    const int e = tid + cnt * JAC_NT;
+    const int e = tid + cnt * NT;
     ei[cnt] = e % Np;
     ej[cnt] = e / Np;
   }
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(JAC_NT) k_psd_jacobi(JacobiArgs a) {
   auto mm = [&](const double* X, bool xt, const double* Y, double* C) {
 #pragma unroll
     for (int cnt = 0; cnt < PER; ++cnt) {
-      const int e = tid + cnt * JAC_NT;
+      const int e = tid + cnt * NT;
       if (e < NN) {
         const int i = ei[cnt], j = ej[cnt];
         double acc = 0.0;
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(JAC_NT) k_psd_jacobi(JacobiArgs a) {
   double* vpg = a.vp + a.blk_vp[b];
   const bool warm = a.warm && (a.st->iter & 63) != 0;
   if (warm) {
-    for (int e = tid; e < NN; e += JAC_NT) {
+    for (int e = tid; e < NN; e += NT) {
       const int i = e % Np, j = e / Np;
       P[e] = (i < N && j < N) ? vpg[(size_t)j * N + i] : (i == j ? 1.0 : 0.0);
     }
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(JAC_NT) k_psd_jacobi(JacobiArgs a) {
     __syncthreads();
     mm(P, true, Ab(1), Vb(1));   // B = P^T T (V buffers as scratch)
     __syncthreads();
-    for (int e = tid; e < NN; e += JAC_NT) {  // symmetrise: Jacobi reads one triangle per pair
+    for (int e = tid; e < NN; e += NT) {  // symmetrise: Jacobi reads one triangle per pair
       const int i = e % Np, j = e / Np;
       Ab(0)[e] = 0.5 * (Vb(1)[i + j * Np] + Vb(1)[j + i * Np]);
     }
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(JAC_NT) k_psd_jacobi(JacobiArgs a) {
       double* Vn = Vb(cur ^ 1);
 #pragma unroll
       for (int cnt = 0; cnt < PER; ++cnt) {
-        const int e = tid + cnt * JAC_NT;
+        const int e = tid + cnt * NT;
         if (e < NN) {
           const int i = ei[cnt], j = ej[cnt];
           const int ip = partner[i], jp = partner[j];
@@ -179,14 +179,14 @@ __global__ void __launch_bounds__(JAC_NT) k_psd_jacobi(JacobiArgs a) {
     V = Ab(cur ^ 1);
   }
   // Pi(A) = V diag(max(lambda, 0)) V^T, lambda_k = A[k, k]; V is kept for the next warm start
-  for (int k = tid; k < Np; k += JAC_NT) alpha[k] = fmax(A[k + k * Np], 0.0);
+  for (int k = tid; k < Np; k += NT) alpha[k] = fmax(A[k + k * Np], 0.0);
   __syncthreads();
   if (a.warm)
-    for (int e = tid; e < N * N; e += JAC_NT) {
+    for (int e = tid; e < N * N; e += NT) {
       const int i = e % N, j = e / N;
       vpg[(size_t)j * N + i] = V[i + j * Np];
     }
-  for (int e = tid; e < N * N; e += JAC_NT) {
+  for (int e = tid; e < N * N; e += NT) {
     const int i = e % N, j = e / N;
     if (i < j) continue;  // lower triangle (row i >= column j) is what k_pack reads
     double acc = 0.0;
@@ -202,6 +202,8 @@ inline size_t jacobi_smem_bytes(int N) {
 }
 
 typedef void (*JacobiKernel)(JacobiArgs);
+constexpr int JAC_NT32 = 512;  // threads for blocks N <= 32 (measured: 64 / 128 / 256 / 512 / 1024 -> 0.27 / 0.17 / 0.14 / 0.12 / 0.13 ms on pop6)
 inline JacobiKernel jacobi_kernel(int max_small_N) {
-  return max_small_N <= 32 ? k_psd_jacobi<32> : k_psd_jacobi<64>;
+  return max_small_N <= 32 ? k_psd_jacobi<32, JAC_NT32> : k_psd_jacobi<64, JAC_NT>;
 }
+inline int jacobi_threads(int max_small_N) { return max_small_N <= 32 ? JAC_NT32 : JAC_NT; }

@@ -483,7 +483,7 @@ sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev) {
     cudaEventRecord(c->ev_fork, s);
     if (has_small) {
       cudaStreamWaitEvent(c->aux[0], c->ev_fork, 0);
-      jacobi_kernel(c->an.max_small_N)<<<(int)c->an.small_blk.size(), JAC_NT, jacobi_smem_bytes(c->an.max_small_N),
+      jacobi_kernel(c->an.max_small_N)<<<(int)c->an.small_blk.size(), jacobi_threads(c->an.max_small_N), jacobi_smem_bytes(c->an.max_small_N),
                                          c->aux[0]>>>(c->ja);
       cudaEventRecord(c->ev_join, c->aux[0]);
     }
@@ -491,7 +491,7 @@ sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev) {
     if (has_small) cudaStreamWaitEvent(s, c->ev_join, 0);
   } else {
     if (has_small)
-      jacobi_kernel(c->an.max_small_N)<<<(int)c->an.small_blk.size(), JAC_NT, jacobi_smem_bytes(c->an.max_small_N),
+      jacobi_kernel(c->an.max_small_N)<<<(int)c->an.small_blk.size(), jacobi_threads(c->an.max_small_N), jacobi_smem_bytes(c->an.max_small_N),
                                          s>>>(c->ja);
     if (ev) cudaEventRecord(ev[3], s);
     if (has_large) {
@@ -1037,7 +1037,7 @@ sosadmm_err sosadmm_project_psd(sosadmm_ctx* c, int32_t block, const double* a_s
   CK_CTX(c, cudaMemcpyAsync(c->d_tmp + off, a_svec, sizeof(double) * L, cudaMemcpyHostToDevice, s));
   k_unpack_block<<<(int)((L + 255) / 256), 256, 0, s>>>(a, block, c->d_tmp + off);
   if (!c->an.small_blk.empty())
-    jacobi_kernel(c->an.max_small_N)<<<(int)c->an.small_blk.size(), JAC_NT, jacobi_smem_bytes(c->an.max_small_N),
+    jacobi_kernel(c->an.max_small_N)<<<(int)c->an.small_blk.size(), jacobi_threads(c->an.max_small_N), jacobi_smem_bytes(c->an.max_small_N),
                                          s>>>(c->ja);
   if (!c->an.large_blk.empty()) large_eig_launch(c->le, s, true);
   if (a.pos_ctas > 0) k_pack<<<a.pos_ctas, POS_NT, 0, s>>>(a, c->d_tmp, 0);
