@@ -48,6 +48,12 @@ struct DcArgs {
   const DevState* st;
   const IterScal* is;
   int check_state;
+  // top-level selection (partial spectrum): the projection needs only the spectral
+  // side with fewer eigenpairs (k_select's rule), so the root merge forms only those eigenvectors.
+  // topsel = [selected root count, first selected root, side (0 = lambda > 0, 1 = lambda < 0,
+  // -1 = all)]; topsel_on = 0 keeps every eigenvector (the stage tests).
+  int* topsel;
+  int topsel_on;
 };
 
 __device__ __forceinline__ bool dc_skip(const DcArgs& a) {
@@ -476,7 +482,7 @@ __global__ void __launch_bounds__(DC_NT) k_dc_zhat(DcArgs a, int level) {
 }
 
 // ---- merge step 4: eigenvector matrix U (k x k) and output ranks, one warp per root j -------
-__global__ void __launch_bounds__(DC_NT) k_dc_vec(DcArgs a, int level, int nb) {
+__global__ void __launch_bounds__(DC_NT) k_dc_vec(DcArgs a, int level, int nb, int top) {
   if (dc_skip(a)) return;
   const int N = a.N;
   const int p = (blockIdx.x * DC_NT + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -488,15 +494,17 @@ __global__ void __launch_bounds__(DC_NT) k_dc_vec(DcArgs a, int level, int nb) {
   const double* d = a.ndd + s;
   const double dj = d[a.org[p]], tj = a.tau_r[p];
   double* U = a.U + nd.u_off + (size_t)j * nd.n;  // column stride n (static upper bound of k)
-  double nrm = 0.0;
-  for (int i = lane; i < k; i += 32) {
-    const double u = a.zhat[s + i] / ((d[i] - dj) - tj);
-    U[i] = u;
-    nrm = fma(u, u, nrm);
+  if (!top || (j >= a.topsel[1] && j < a.topsel[1] + a.topsel[0])) {  // root: selected columns only
+    double nrm = 0.0;
+    for (int i = lane; i < k; i += 32) {
+      const double u = a.zhat[s + i] / ((d[i] - dj) - tj);
+      U[i] = u;
+      nrm = fma(u, u, nrm);
+    }
+    nrm = warp_sum(nrm);
+    const double inv = 1.0 / sqrt(nrm);
+    for (int i = lane; i < k; i += 32) U[i] *= inv;
   }
-  nrm = warp_sum(nrm);
-  const double inv = 1.0 / sqrt(nrm);
-  for (int i = lane; i < k; i += 32) U[i] *= inv;
   // rank among (roots ascending) U (deflated values; deflated first on ties)
   const double lj = a.lam_r[p];
   int cnt = 0;
@@ -546,10 +554,50 @@ __global__ void __launch_bounds__(DCR_NT) k_dc_rot(DcArgs a, int level, int ob) 
   Qo[(size_t)ccol * N + row] = cval;
 }
 
+// ---- root merge, between the secular roots and the eigenvectors: which side is projected ----
+// k_select's rule on the final spectrum (roots and deflated values): r = min(#lambda > 0,
+// #lambda < 0), positives on ties; the selected roots are a contiguous range since roots ascend.
+__global__ void __launch_bounds__(DC_NT) k_dc_topsel(DcArgs a, int root) {
+  if (dc_skip(a)) return;
+  const int s = a.nodes[root].s, k = a.node_k[root], df = a.node_nd[root];
+  __shared__ int cnt[4];
+  if (threadIdx.x < 4) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  int rp = 0, rn = 0, dp = 0, dn = 0;
+  for (int j = threadIdx.x; j < k; j += DC_NT) {
+    rp += a.lam_r[s + j] > 0.0;
+    rn += a.lam_r[s + j] < 0.0;
+  }
+  for (int q = threadIdx.x; q < df; q += DC_NT) {
+    dp += a.dfv[s + q] > 0.0;
+    dn += a.dfv[s + q] < 0.0;
+  }
+  atomicAdd(&cnt[0], rp);
+  atomicAdd(&cnt[1], rn);
+  atomicAdd(&cnt[2], dp);
+  atomicAdd(&cnt[3], dn);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (!a.topsel_on) {
+      a.topsel[0] = k;
+      a.topsel[1] = 0;
+      a.topsel[2] = -1;
+    } else if (cnt[0] + cnt[2] <= cnt[1] + cnt[3]) {  // positives: the last #roots>0 roots
+      a.topsel[0] = cnt[0];
+      a.topsel[1] = k - cnt[0];
+      a.topsel[2] = 0;
+    } else {  // negatives: the first #roots<0 roots
+      a.topsel[0] = cnt[1];
+      a.topsel[1] = 0;
+      a.topsel[2] = 1;
+    }
+  }
+}
+
 // ---- merge step 6: deflated eigenpairs (copied columns).  grid (node, column chunk): one warp per
 // deflated column computes its rank among the merged spectrum, then copies the column. ----
 constexpr int DCF_COLS = DC_NT / 32;  // deflated columns per CTA (one per warp)
-__global__ void __launch_bounds__(DC_NT) k_dc_final(DcArgs a, int node0, int ob, int nb) {
+__global__ void __launch_bounds__(DC_NT) k_dc_final(DcArgs a, int node0, int ob, int nb, int top) {
   if (dc_skip(a)) return;
   const int node = node0 + blockIdx.x;
   const DcNode nd = a.nodes[node];
@@ -571,6 +619,10 @@ __global__ void __launch_bounds__(DC_NT) k_dc_final(DcArgs a, int node0, int ob,
   for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
   const int col = s + cnt;
   if (lane == 0) a.lam[nb][col] = x;
+  if (top) {  // root: copy only the selected side's deflated eigenvectors
+    const int side = a.topsel[2];
+    if ((side == 0 && !(x > 0.0)) || (side == 1 && !(x < 0.0))) return;
+  }
   const double* src = Qo + (size_t)a.dfcol[s + q] * N;
   double* dst = Qn + (size_t)col * N;
   for (int r = s + lane; r < s + n; r += 32) dst[r] = src[r];

@@ -19,6 +19,7 @@ struct GemmDesc {
   const int* ccol;
   const int* Kdev;     // if non-null, K = *Kdev
   const int* Ndev;     // if non-null, N = *Ndev
+  const int* Noff;     // if non-null, column j of op(B) / C is j + *Noff (a device-chosen column range)
   int transB;
   double alpha, beta;
   int skip;            // 1 = this batch entry does nothing
@@ -46,6 +47,7 @@ __global__ void __launch_bounds__(GM_NT) k_gemm_f64(const GemmDesc* __restrict__
   const int M = g.M;
   const int N = g.Ndev ? *g.Ndev : g.N;
   const int K = g.Kdev ? *g.Kdev : g.K;
+  const int joff = g.Noff ? *g.Noff : 0;
   const int i0 = blockIdx.x * GM_BM, j0 = blockIdx.y * GM_BN;
   if (i0 >= M || j0 >= N) return;
   __shared__ __align__(16) double As[2][GM_BK][GM_BM + GM_PAD];
@@ -76,7 +78,7 @@ __global__ void __launch_bounds__(GM_NT) k_gemm_f64(const GemmDesc* __restrict__
         const int k = idx % GM_BK, j = idx / GM_BK;
         const int gk = k0 + k, gj = j0 + j;
         const bool ok = gk < K && gj < N;
-        cp_async8z(&Bs[buf][k][j], g.B + (ok ? (size_t)gj * g.ldb + gk : 0), ok);
+        cp_async8z(&Bs[buf][k][j], g.B + (ok ? (size_t)(gj + joff) * g.ldb + gk : 0), ok);
       }
     } else {  // op(B)[k, j] = B[k * ldb + j]: contiguous in j
 #pragma unroll
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__(GM_NT) k_gemm_f64(const GemmDesc* __restrict__
         const int j = idx % GM_BN, k = idx / GM_BN;
         const int gk = k0 + k, gj = j0 + j;
         const bool ok = gk < K && gj < N;
-        cp_async8z(&Bs[buf][k][j], g.B + (ok ? (size_t)gk * g.ldb + gj : 0), ok);
+        cp_async8z(&Bs[buf][k][j], g.B + (ok ? (size_t)gk * g.ldb + gj + joff : 0), ok);
       }
     }
     cp_async_commit();
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(GM_NT) k_gemm_f64(const GemmDesc* __restrict__
         const int gi = i0 + wm * 32 + a * 8 + (lane >> 2);
         const int gj = j0 + wn * 16 + b * 8 + 2 * (lane & 3) + h;
         if (gi < M && gj < N) {
-          const int col = g.ccol ? g.ccol[gj] : gj;
+          const int col = g.ccol ? g.ccol[gj + joff] : gj + joff;
           double* cp = g.C + (size_t)col * g.ldc + gi;
           const double v = g.alpha * acc[a][b][h];
           *cp = (g.beta == 0.0) ? v : fma(g.beta, *cp, v);

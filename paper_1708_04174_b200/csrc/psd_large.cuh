@@ -206,7 +206,7 @@ inline size_t large_carve(const std::vector<int>& blk_N, const std::vector<int>&
     p[q++] = take(16 * N);                // rot_cs
     p[q++] = take(4 * nodes.size());      // rot_cnt
     p[q++] = take(sizeof(GemmDesc) * (nodes.size() + 1));
-    p[q++] = take(4 * 4);                 // sel
+    p[q++] = take(4 * 8);                 // sel [r, c0, side] + the D&C root selection (topsel)
     p[q++] = take(8 * ((size_t)3 * N + 2));  // tridiagonalisation hand-over state
     p[q++] = take(8 * (size_t)2 * N * TRB_NB);  // blocked tridiagonalisation panels Vg, Wg
     p[q++] = take(8 * (size_t)BTW_NB * BTW_NB * ((N - 2 + BTW_NB - 1) / BTW_NB));  // Twy
@@ -295,6 +295,8 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     dc.check_state = 1;
     lb.gdesc = (GemmDesc*)p[q++];
     lb.sel = (int*)p[q++];
+    dc.topsel = lb.sel + 4;
+    dc.topsel_on = 1;
     double* hand = (double*)p[q++];
     double* vwg = (double*)p[q++];
     lb.Twy = (double*)p[q++];
@@ -327,6 +329,10 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
         g.K = nd.n;
         g.Kdev = dc.node_k + id;
         g.Ndev = dc.node_k + id;
+        if (h == D) {  // root: only the selected eigenvector columns (k_dc_topsel)
+          g.Ndev = dc.topsel;
+          g.Noff = dc.topsel + 1;
+        }
         g.alpha = 1.0;
         g.beta = 0.0;
         gd[id] = g;
@@ -455,11 +461,12 @@ inline void large_block_dc(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool ch
     k_dc_prep<<<nn, DC_NT, 0, s>>>(lb.dc, n0, ob);
     k_dc_rot<<<(N + DCR_NT - 1) / DCR_NT, DCR_NT, 0, s>>>(lb.dc, h, ob);
     k_dc_secular<<<wblocks, DC_NT, 0, s>>>(lb.dc, h);
+    if (h == lb.D) k_dc_topsel<<<1, DC_NT, 0, s>>>(lb.dc, n0);  // root: which eigenvectors to form
     k_dc_zhat<<<wblocks, DC_NT, 0, s>>>(lb.dc, h);
-    k_dc_vec<<<wblocks, DC_NT, 0, s>>>(lb.dc, h, nb);
+    k_dc_vec<<<wblocks, DC_NT, 0, s>>>(lb.dc, h, nb, h == lb.D ? 1 : 0);
     dim3 gg((nmax + GM_BM - 1) / GM_BM, (nmax + GM_BN - 1) / GM_BN, nn);
     k_gemm_f64<<<gg, GM_NT, 0, s>>>(lb.gdesc + n0, le.st, le.is, check);
-    k_dc_final<<<dim3(nn, (nmax + DCF_COLS - 1) / DCF_COLS), DC_NT, 0, s>>>(lb.dc, n0, ob, nb);
+    k_dc_final<<<dim3(nn, (nmax + DCF_COLS - 1) / DCF_COLS), DC_NT, 0, s>>>(lb.dc, n0, ob, nb, h == lb.D ? 1 : 0);
   }
 }
 
@@ -535,7 +542,7 @@ inline void large_eig_launch_concurrent(LargeEig& le, cudaStream_t s, bool check
 
 inline int large_eig_launches(const LargeEig& le) {
   int k = 0;
-  for (const auto& lb : le.blocks) k += (!lb.blk && lb.ksw < lb.N - 2 ? 2 : 1) + 2 + 1 + 7 * lb.D + 5;
+  for (const auto& lb : le.blocks) k += (!lb.blk && lb.ksw < lb.N - 2 ? 2 : 1) + 2 + 1 + 7 * lb.D + 1 + 5;
   return k;
 }
 

@@ -1174,6 +1174,7 @@ extern "C" int sosadmm_debug_stedc(int N, const double* d, const double* e, doub
   LargeBlock& lb = dl.le.blocks[0];
   cudaMemcpyAsync(lb.d, d, 8ull * N, cudaMemcpyHostToDevice, dl.s);
   cudaMemcpyAsync(lb.e, e, 8ull * (N - 1), cudaMemcpyHostToDevice, dl.s);
+  lb.dc.topsel_on = 0;  // the stage test checks every eigenvector
   large_block_dc(dl.le, lb, dl.s, false);
   cudaError_t err = cudaStreamSynchronize(dl.s);
   if (err != cudaSuccess) return -4;
