@@ -76,3 +76,52 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dp, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+(oracle|sosgen)\b", txt, re.M), f
+
+
+def _problem(prob, m=None, n_free=None, dims=None, colptr=None, rowidx=None):
+    from paper_1708_04174_b200.sosadmm import _Problem, _dptr
+
+    A = prob.A.tocsc()
+    keep = {}
+    keep["cp"] = np.ascontiguousarray(A.indptr if colptr is None else colptr, dtype=np.int64)
+    keep["ri"] = np.ascontiguousarray(A.indices if rowidx is None else rowidx, dtype=np.int32)
+    keep["va"] = np.ascontiguousarray(A.data, dtype=np.float64)
+    keep["dims"] = np.array(prob.psd_dims if dims is None else dims, dtype=np.int32)
+    p = _Problem(prob.m if m is None else m, prob.n_free if n_free is None else n_free, len(keep["dims"]),
+                 keep["dims"].ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                 keep["cp"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                 keep["ri"].ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), _dptr(keep["va"]), _dptr(prob.b),
+                 _dptr(prob.c))
+    return p, keep
+
+
+def test_setup_rejects_malformed_problems_before_any_device_work():
+    """include/sosadmm.h error contract: analysis runs on the host first, so malformed or unsupported
+    input fails with E_ARG / E_STRUCT and a message, with no GPU needed (this runs on CPU)."""
+    from paper_1708_04174_b200.sosadmm import _Settings
+    from sosgen import make_config
+
+    lib = load_library()
+    prob = make_config("pop6")
+    st = _Settings(1e-4, 100, 1, 0, None, None, 0)
+    A = prob.A.tocsc()
+    bad_rows = A.indices.copy()
+    bad_rows[5] = prob.m  # row index out of range
+    cases = [
+        (dict(dims=[1281]), -2),          # block > SOSADMM_MAX_BLOCK
+        (dict(m=0), -1),                  # empty row space
+        (dict(n_free=-1), -1),            # negative size
+        (dict(rowidx=bad_rows), -1),      # CSC row index out of range
+    ]
+    for kw, want in cases:
+        p, keep = _problem(prob, **kw)
+        ctx = ctypes.c_void_p()
+        err = lib.sosadmm_setup(ctypes.byref(p), ctypes.byref(st), ctypes.byref(ctx))
+        assert err == want, (kw.keys(), err)
+        assert lib.sosadmm_workspace_size(ctypes.byref(p)) == 0
+        assert len(lib.sosadmm_last_error_message(ctx)) > 0
+        lib.sosadmm_destroy(ctx)
+    ctx = ctypes.c_void_p()
+    assert lib.sosadmm_setup(None, ctypes.byref(st), ctypes.byref(ctx)) == -1
+    lib.sosadmm_destroy(ctx)
+    assert lib.sosadmm_setup(ctypes.byref(_problem(prob)[0]), ctypes.byref(st), None) == -1
