@@ -235,6 +235,9 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
   }
   __syncthreads();
   const int nspill = nspill_s;
+  // Phase Y maps YP threads to every own row slot: S * YP <= TRD_NT holds for every supported size
+  // (N <= SOSADMM_MAX_BLOCK = 1280: S <= 80 with C = 16, YP = 4); fail loudly otherwise
+  if (S * (CC >= 16 ? 4 : (CC >= 4 ? 2 : 1)) > TRD_NT) __trap();
   auto rowptr_g = [&](int q) -> double* { return a.M + (size_t)(me + q * C) * N; };
   auto rowptr_s = [&](int q) -> double* { return rows + roff[q - qlo] - jb; };
   auto rowval = [&](int q, int j) -> double {  // entry (i, j) of own row slot q
@@ -459,10 +462,13 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
       TRD_STAMP(4)
       const bool last = (k == N - 3);
       const int nslot = nown - qs1;
+      // Phase Y runs YP threads per own row (each pushes to C / YP of the peers)
+      constexpr int YP = CC >= 16 ? 4 : (CC >= 4 ? 2 : 1);  // measured: 1 / 2 / 4 -> 4.59 / 4.58 / 4.55 ms
+      const int yq = tid / YP, yh = tid % YP;
       double prow_own = 0.0;  // this CTA's row dot of its own row (sum over the warps), before the wait
-      if (tid < nslot) {
-        const int i = me + (qs1 + tid) * C;
-        if (i > k + 1) prow_own = trd_sum16(rp + qs1 + tid - qlo, nwarps_of_row(i), S);
+      if (yq < nslot) {
+        const int i = me + (qs1 + yq) * C;
+        if (i > k + 1) prow_own = trd_sum16(rp + qs1 + yq - qlo, nwarps_of_row(i), S);
       }
       const double tk = scal_s[par][0], scale = scal_s[par][1];  // written before the last __syncthreads
       TRD_STAMP(8)
@@ -476,7 +482,7 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
 
       // ---- Phase Y (own-row threads): w_k, eager update of column k+1, its norm partial ----
       double Kc = 0.0, wk1 = 0.0;
-      if (tid < nslot) {
+      if (yq < nslot) {
         const double yz = trd_sumc<CC>(sd);     // y^T A y
         const double z1 = trd_sumc<CC>(se);     // (A y)[k+1]
         const double c1 = sc[0];                // A_k[k+1, k+1]
@@ -491,26 +497,28 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
       auto phase_y = [&](int q, double* R, double prow) {
         const int i = me + q * C;
         if (i == k + 1) {
-          a.d[k + 1] = R[k + 1] - 2.0 * wk1;
+          if (yh == 0) a.d[k + 1] = R[k + 1] - 2.0 * wk1;
         } else {
           const double vin = xk(i) * scale;
           const double pq = fma(scale, prow + trd_sum16(qr + q - qlo, C, S), R[k + 1]);  // (A v)[i]
           const double wi = fma(-Kc, vin, tk * pq);
           const double x = fma(-vin, wk1, R[k + 1] - wi);
-          R[k + 1] = x;
           if (last) {  // i == N - 1: the trailing 2 x 2 block
-            a.e[N - 2] = x;
-            a.d[N - 1] = R[N - 1] - 2.0 * vin * wi;
-            a.tau[N - 2] = 0.0;
+            if (yh == 0) {
+              R[k + 1] = x;
+              a.e[N - 2] = x;
+              a.d[N - 1] = R[N - 1] - 2.0 * vin * wi;
+              a.tau[N - 2] = 0.0;
+            }
           } else {
             const double ws = wi * scale;
     #pragma unroll
-            for (int c = 0; c < C; ++c) push2(xnext + i, (c + tid) & (C - 1), x, ws, &barY);
+            for (int c = 0; c < C / YP; ++c) push2(xnext + i, (c * YP + yh + yq) & (C - 1), x, ws, &barY);
           }
         }
       };
-      if (tid < nslot) {
-        const int q = qs1 + tid;
+      if (yq < nslot) {
+        const int q = qs1 + yq;
         if (q < nspill) phase_y(q, rowptr_g(q), prow_own);
         else phase_y(q, rowptr_s(q), prow_own);
       }
