@@ -127,18 +127,22 @@ __global__ void __launch_bounds__(NT) k_psd_jacobi(JacobiArgs a) {
     for (int r = 0; r < Np - 1; ++r) {
       const double* A = Ab(cur);
       const double* V = Vb(cur);
-      // 1. rotation parameters of the Np/2 disjoint pairs (GvL sym.schur2, rewritten with
-      //    d = a_qq - a_pp: t = sign(d) 2 a_pq / (|d| + sqrt(d^2 + 4 a_pq^2)), c = rsqrt(1 + t^2))
+      // 1. rotation parameters of the Np/2 disjoint pairs (GvL sym.schur2: the rotation that
+      //    annihilates a_pq, with d = a_qq - a_pp)
       if (tid < Np / 2) {
         int p, q;
         rr_pair(r, tid, Np, p, q);
         const double apq = A[p + q * Np], app = A[p + p * Np], aqq = A[q + q * Np];
         double c = 1.0, s = 0.0;
         if (apq * apq > EPS * EPS * fabs(app * aqq) && fabs(apq) > tiny) {
+          // half-angle form, two rsqrt and no division: with h = sqrt(d^2 + (2 a_pq)^2),
+          // c^2 = (1 + |d| / h) / 2 in [1/2, 1] (no cancellation), s = sign(d) a_pq / (h c)
           const double d = aqq - app, tw = 2.0 * apq;
-          const double t = copysign(1.0, d) * tw / (fabs(d) + sqrt(fma(d, d, tw * tw)));
-          c = rsqrt(fma(t, t, 1.0));
-          s = t * c;
+          const double rh = rsqrt(fma(d, d, tw * tw));
+          const double cc = 0.5 * fma(fabs(d), rh, 1.0);
+          const double rc = rsqrt(cc);
+          c = cc * rc;
+          s = copysign(1.0, d) * (0.5 * tw) * rh * rc;
           nrot = 1;
         }
         alpha[p] = c; beta[p] = -s; partner[p] = q;
