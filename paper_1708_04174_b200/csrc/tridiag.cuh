@@ -154,7 +154,7 @@ __device__ __forceinline__ double trd_block_sum(double v, double* red) {
 // Shared-memory layout (doubles): xw[2][N] (double2: x~_k[j], scale_{k-1} w_{k-1}[j], by step
 // parity) | per own slot (S slots): xs[S] qr[C][S] rp[NW][S] | scalars sd[C] se[C] sc[C] red[32] | rows.
 __host__ __device__ inline long long trd_fixed_doubles(int N, int C, int S) {
-  return 4LL * N + (long long)S + (long long)C * S + (long long)TRD_NW * S + 3LL * C + 32;
+  return 4LL * N + 2LL * C + (long long)S + (long long)C * S + (long long)TRD_NW * S + 32;
 }
 __host__ __device__ inline int trd_log2(int C) { return C >= 16 ? 4 : (C >= 8 ? 3 : (C >= 4 ? 2 : (C >= 2 ? 1 : 0))); }
 
@@ -191,13 +191,12 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
   // xw[par][j] = (x~_k[j], w_{k-1}[j]) for k of parity par: x~_k is the column that defines v_k,
   // w_{k-1} the pending update; both allgathered in ONE 16-byte st.async per (row, peer)
   double2* xw = reinterpret_cast<double2*>(sm);
-  double* xs = sm + 4 * (size_t)N;  // column 0 on own rows (first push)
+  // [C] per-CTA partials of (v^T A v, (A v)[k+1]), already scaled (one 16-byte push per peer)
+  double2* sde = reinterpret_cast<double2*>(sm + 4 * (size_t)N);
+  double* xs = sm + 4 * (size_t)N + 2 * C;  // column 0 on own rows (first push)
   double* qr = xs + S;             // [C][S] reduce-scatter receive
   double* rp = qr + C * S;         // [NW][S] per-warp row partials
-  double* sd = rp + TRD_NW * S;    // [C] partial y^T A y
-  double* se = sd + C;             // [C] partial (A y)[k+1]
-  double* sc = se + C;             // [C] (slot 0) A_k[k+1, k+1] from the owner of row k + 1
-  double* red = sc + C;            // [32]: warp partials (two independent halves)
+  double* red = rp + TRD_NW * S;   // [32]: warp partials (two independent halves)
   double* rows = red + 32;
   __shared__ int roff[TRD_MAXOWN];  // smem offset of own row slot q - qlo, -1 = spilled to global
   __shared__ int nspill_s;
@@ -369,7 +368,7 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
         wo[t] = cw.y;                            // scale_{k-1} w_{k-1}[j] (0 at k = 0: no pending update)
         qa[t] = 0.0;
       }
-      if (tid == 32 && !SOLO) trd_bar_expect(&barQ, (unsigned)(8 * (C * (nown - qs2) + 2 * C + 1)));
+      if (tid == 32 && !SOLO) trd_bar_expect(&barQ, (unsigned)(8 * (C * (nown - qs2) + 2 * C)));
       TRD_STAMP(1)
 
       // ---- Phase X: fused rank-2 update of step k-1 and symv with v_k over own rows i >= k+1 ----
@@ -455,9 +454,13 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
       TRD_STAMP(3)
       const bool own1 = ((k + 1) & (C - 1)) == me;  // this CTA owns row k + 1
       if (tid < C) {
-        push(sd + me, tid, trd_sumc<TRD_NW>(red), &barQ);
-        push(se + me, tid, qk1_s, &barQ);
-        if (own1) push(sc, tid, rowval((k + 1) >> logC, k + 1), &barQ);  // A_k[k+1, k+1]
+        // scale_k is known here (scal_s, before the last __syncthreads), so each CTA pushes its share
+        // of v^T A v = c1 + 2 scale z1 + scale^2 y^T z and of p[k+1] = c1 + scale z1 directly, the
+        // owner of row k + 1 adding c1 = A_k[k+1, k+1]: one st.async per peer
+        const double scl = scal_s[par][1];
+        const double yzp = trd_sumc<TRD_NW>(red), z1p = qk1_s;
+        const double c1p = own1 ? rowval((k + 1) >> logC, k + 1) : 0.0;
+        push2(sde + me, tid, fma(scl, fma(scl, yzp, 2.0 * z1p), c1p), fma(scl, z1p, c1p), &barQ);
       }
       TRD_STAMP(4)
       const bool last = (k == N - 3);
@@ -483,12 +486,22 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
       // ---- Phase Y (own-row threads): w_k, eager update of column k+1, its norm partial ----
       double Kc = 0.0, wk1 = 0.0;
       if (yq < nslot) {
-        const double yz = trd_sumc<CC>(sd);     // y^T A y
-        const double z1 = trd_sumc<CC>(se);     // (A y)[k+1]
-        const double c1 = sc[0];                // A_k[k+1, k+1]
-        const double vav = fma(scale, fma(scale, yz, 2.0 * z1), c1);  // v^T A v
-        Kc = 0.5 * tk * tk * vav;               // (tau/2) p^T v with p = tau A v
-        wk1 = fma(tk, fma(scale, z1, c1), -Kc);  // w_k[k+1] (v_k[k+1] = 1)
+        double vv[CC], pp[CC];  // fixed-order sums of the C partials
+#pragma unroll
+        for (int c = 0; c < CC; ++c) {
+          const double2 t = sde[c];
+          vv[c] = t.x;
+          pp[c] = t.y;
+        }
+#pragma unroll
+        for (int h = CC / 2; h >= 1; h >>= 1)
+#pragma unroll
+          for (int c = 0; c < h; ++c) {
+            vv[c] += vv[c + h];
+            pp[c] += pp[c + h];
+          }
+        Kc = 0.5 * tk * tk * vv[0];             // (tau/2) p^T v with p = tau A v; vv[0] = v^T A v
+        wk1 = fma(tk, pp[0], -Kc);               // w_k[k+1] (v_k[k+1] = 1); pp[0] = (A v)[k+1]
       }
       TRD_STAMP(10)
       // each own-row thread pushes its (x~_{k+1}[i], scale_k w_k[i]) straight to every CTA (allgather;
