@@ -448,7 +448,12 @@ inline void large_block_tridiag(LargeEig& le, LargeBlock& lb, cudaStream_t s, bo
     tridiag_kernel_mc(tridiag_maxb(lb.N), 1)<<<1, TRD_NT, lb.tail_smem, s>>>(lb.ta_tail);
 }
 
-inline void large_block_dc(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool check) {
+// side, ev (4 events): optional second stream — the deflation rotations and the deflated copies of
+// each merge then run beside the secular / eigenvector / GEMM chain (5 dependent launches per level
+// instead of 7): rot needs prep, final needs rot, secular (and the root selection); the GEMM needs
+// rot; the next level needs final.
+inline void large_block_dc(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool check, cudaStream_t side = nullptr,
+                           const cudaEvent_t* ev = nullptr) {
   const int N = lb.N;
   lb.dc.check_state = check;
   cudaMemsetAsync(lb.dc.Q[0], 0, sizeof(double) * N * N, s);
@@ -458,15 +463,29 @@ inline void large_block_dc(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool ch
   for (int h = 1; h <= lb.D; ++h) {
     const int ob = (h - 1) & 1, nb = h & 1;
     const int n0 = lb.level_node0[h], nn = lb.level_nn[h], nmax = lb.level_nmax[h];
+    const bool two = side != nullptr;
+    cudaStream_t s2 = two ? side : s;
     k_dc_prep<<<nn, DC_NT, 0, s>>>(lb.dc, n0, ob);
-    k_dc_rot<<<(N + DCR_NT - 1) / DCR_NT, DCR_NT, 0, s>>>(lb.dc, h, ob);
+    if (two) {
+      cudaEventRecord(ev[0], s);
+      cudaStreamWaitEvent(s2, ev[0], 0);
+    }
+    k_dc_rot<<<(N + DCR_NT - 1) / DCR_NT, DCR_NT, 0, s2>>>(lb.dc, h, ob);
+    if (two) cudaEventRecord(ev[1], s2);
     k_dc_secular<<<wblocks, DC_NT, 0, s>>>(lb.dc, h);
     if (h == lb.D) k_dc_topsel<<<1, DC_NT, 0, s>>>(lb.dc, n0);  // root: which eigenvectors to form
+    if (two) {
+      cudaEventRecord(ev[2], s);
+      cudaStreamWaitEvent(s2, ev[2], 0);
+    }
+    k_dc_final<<<dim3(nn, (nmax + DCF_COLS - 1) / DCF_COLS), DC_NT, 0, s2>>>(lb.dc, n0, ob, nb, h == lb.D ? 1 : 0);
+    if (two) cudaEventRecord(ev[3], s2);
     k_dc_zhat<<<wblocks, DC_NT, 0, s>>>(lb.dc, h);
     k_dc_vec<<<wblocks, DC_NT, 0, s>>>(lb.dc, h, nb, h == lb.D ? 1 : 0);
+    if (two) cudaStreamWaitEvent(s, ev[1], 0);  // the GEMM reads the rotated columns
     dim3 gg((nmax + GM_BM - 1) / GM_BM, (nmax + GM_BN - 1) / GM_BN, nn);
     k_gemm_f64<<<gg, GM_NT, 0, s>>>(lb.gdesc + n0, le.st, le.is, check);
-    k_dc_final<<<dim3(nn, (nmax + DCF_COLS - 1) / DCF_COLS), DC_NT, 0, s>>>(lb.dc, n0, ob, nb, h == lb.D ? 1 : 0);
+    if (two) cudaStreamWaitEvent(s, ev[3], 0);  // next level reads the deflated copies
   }
 }
 
@@ -518,26 +537,27 @@ inline void large_eig_launch(LargeEig& le, cudaStream_t s, bool check, cudaEvent
 
 // Concurrent variant (graph path): every large block runs its chain on its own stream (block 0 on
 // s), and inside a chain the WY factors run on a side stream beside the divide-and-conquer solve.
-// fork: event already recorded on s; aux: >= 2 * nblocks streams; evs: >= 3 * nblocks events.
+// fork: event already recorded on s; aux: >= 3 * nblocks streams; evs: >= 7 * nblocks events.
 inline void large_eig_launch_concurrent(LargeEig& le, cudaStream_t s, bool check, cudaEvent_t fork,
                                         const cudaStream_t* aux, const cudaEvent_t* evs) {
   const int nb = (int)le.blocks.size();
   for (int b = 0; b < nb; ++b) {
     LargeBlock& lb = le.blocks[b];
-    cudaStream_t sb = b == 0 ? s : aux[2 * b];
-    cudaStream_t sw = aux[2 * b + 1];
+    cudaStream_t sb = b == 0 ? s : aux[3 * b];
+    cudaStream_t sw = aux[3 * b + 1];
+    cudaStream_t sd = aux[3 * b + 2];
     if (b > 0) cudaStreamWaitEvent(sb, fork, 0);
     large_block_tridiag(le, lb, sb, check);
-    cudaEventRecord(evs[3 * b], sb);         // tridiagonal + reflectors ready
-    cudaStreamWaitEvent(sw, evs[3 * b], 0);
+    cudaEventRecord(evs[7 * b], sb);         // tridiagonal + reflectors ready
+    cudaStreamWaitEvent(sw, evs[7 * b], 0);
     large_block_wy(le, lb, sw, check);
-    cudaEventRecord(evs[3 * b + 1], sw);
-    large_block_dc(le, lb, sb, check);
-    cudaStreamWaitEvent(sb, evs[3 * b + 1], 0);
+    cudaEventRecord(evs[7 * b + 1], sw);
+    large_block_dc(le, lb, sb, check, sd, evs + 7 * b + 3);
+    cudaStreamWaitEvent(sb, evs[7 * b + 1], 0);
     large_block_recon(le, lb, sb, check, false);
-    if (b > 0) cudaEventRecord(evs[3 * b + 2], sb);
+    if (b > 0) cudaEventRecord(evs[7 * b + 2], sb);
   }
-  for (int b = 1; b < nb; ++b) cudaStreamWaitEvent(s, evs[3 * b + 2], 0);
+  for (int b = 1; b < nb; ++b) cudaStreamWaitEvent(s, evs[7 * b + 2], 0);
 }
 
 inline int large_eig_launches(const LargeEig& le) {

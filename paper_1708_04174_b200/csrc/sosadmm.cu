@@ -341,9 +341,9 @@ struct sosadmm_ctx {
   ShardArgs sh{};
   int nb_low = 1;
   // parallel branches of the PSD projection inside the CUDA graph
-  static constexpr int kMaxAux = 1 + 2 * 8;
+  static constexpr int kMaxAux = 1 + 3 * 8;
   cudaStream_t aux[kMaxAux] = {};
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_blk[3 * 8] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_blk[7 * 8] = {};
   bool aux_ok = false;
 };
 
@@ -794,11 +794,11 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
   for (int j = an.t; j < an.n; ++j)
     if (an.code[j] >= -1) c->row_of[j] = an.code[j];
   if (!an.large_blk.empty() && an.large_blk.size() <= 8) {
-    const int naux = 1 + 2 * (int)an.large_blk.size();
+    const int naux = 1 + 3 * (int)an.large_blk.size();
     for (int q = 0; q < naux; ++q) CK_CTX(c, cudaStreamCreateWithFlags(&c->aux[q], cudaStreamNonBlocking));
     CK_CTX(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK_CTX(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
-    for (int q = 0; q < 3 * (int)an.large_blk.size(); ++q)
+    for (int q = 0; q < 7 * (int)an.large_blk.size(); ++q)
       CK_CTX(c, cudaEventCreateWithFlags(&c->ev_blk[q], cudaEventDisableTiming));
     c->aux_ok = true;
   }
