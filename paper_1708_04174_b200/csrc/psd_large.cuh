@@ -448,7 +448,7 @@ inline void large_block_tridiag(LargeEig& le, LargeBlock& lb, cudaStream_t s, bo
     tridiag_kernel_mc(tridiag_maxb(lb.N), 1)<<<1, TRD_NT, lb.tail_smem, s>>>(lb.ta_tail);
 }
 
-// side, ev (4 events): optional second stream — the deflation rotations and the deflated copies of
+// side, ev (5 events): optional second stream — the deflation rotations and the deflated copies of
 // each merge then run beside the secular / eigenvector / GEMM chain (5 dependent launches per level
 // instead of 7): rot needs prep, final needs rot, secular (and the root selection); the GEMM needs
 // rot; the next level needs final.
@@ -456,8 +456,12 @@ inline void large_block_dc(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool ch
                            const cudaEvent_t* ev = nullptr) {
   const int N = lb.N;
   lb.dc.check_state = check;
-  cudaMemsetAsync(lb.dc.Q[0], 0, sizeof(double) * N * N, s);
-  cudaMemsetAsync(lb.dc.Q[1], 0, sizeof(double) * N * N, s);
+  if (side) {  // the eigenvector buffers were zeroed on `side` beside the tridiagonalisation (ev[4])
+    cudaStreamWaitEvent(s, ev[4], 0);
+  } else {
+    cudaMemsetAsync(lb.dc.Q[0], 0, sizeof(double) * N * N, s);
+    cudaMemsetAsync(lb.dc.Q[1], 0, sizeof(double) * N * N, s);
+  }
   k_dc_leaf<<<(lb.nleaves + 127) / 128, 128, 0, s>>>(lb.dc, lb.leaf0, lb.nleaves, 0);
   const int wblocks = (N * 32 + DC_NT - 1) / DC_NT;
   for (int h = 1; h <= lb.D; ++h) {
@@ -537,7 +541,7 @@ inline void large_eig_launch(LargeEig& le, cudaStream_t s, bool check, cudaEvent
 
 // Concurrent variant (graph path): every large block runs its chain on its own stream (block 0 on
 // s), and inside a chain the WY factors run on a side stream beside the divide-and-conquer solve.
-// fork: event already recorded on s; aux: >= 3 * nblocks streams; evs: >= 7 * nblocks events.
+// fork: event already recorded on s; aux: >= 3 * nblocks streams; evs: >= 8 * nblocks events.
 inline void large_eig_launch_concurrent(LargeEig& le, cudaStream_t s, bool check, cudaEvent_t fork,
                                         const cudaStream_t* aux, const cudaEvent_t* evs) {
   const int nb = (int)le.blocks.size();
@@ -547,17 +551,22 @@ inline void large_eig_launch_concurrent(LargeEig& le, cudaStream_t s, bool check
     cudaStream_t sw = aux[3 * b + 1];
     cudaStream_t sd = aux[3 * b + 2];
     if (b > 0) cudaStreamWaitEvent(sb, fork, 0);
+    // the D&C eigenvector buffers are zeroed beside the tridiagonalisation
+    cudaStreamWaitEvent(sd, fork, 0);
+    cudaMemsetAsync(lb.dc.Q[0], 0, sizeof(double) * lb.N * lb.N, sd);
+    cudaMemsetAsync(lb.dc.Q[1], 0, sizeof(double) * lb.N * lb.N, sd);
+    cudaEventRecord(evs[8 * b + 7], sd);
     large_block_tridiag(le, lb, sb, check);
-    cudaEventRecord(evs[7 * b], sb);         // tridiagonal + reflectors ready
-    cudaStreamWaitEvent(sw, evs[7 * b], 0);
+    cudaEventRecord(evs[8 * b], sb);         // tridiagonal + reflectors ready
+    cudaStreamWaitEvent(sw, evs[8 * b], 0);
     large_block_wy(le, lb, sw, check);
-    cudaEventRecord(evs[7 * b + 1], sw);
-    large_block_dc(le, lb, sb, check, sd, evs + 7 * b + 3);
-    cudaStreamWaitEvent(sb, evs[7 * b + 1], 0);
+    cudaEventRecord(evs[8 * b + 1], sw);
+    large_block_dc(le, lb, sb, check, sd, evs + 8 * b + 3);
+    cudaStreamWaitEvent(sb, evs[8 * b + 1], 0);
     large_block_recon(le, lb, sb, check, false);
-    if (b > 0) cudaEventRecord(evs[7 * b + 2], sb);
+    if (b > 0) cudaEventRecord(evs[8 * b + 2], sb);
   }
-  for (int b = 1; b < nb; ++b) cudaStreamWaitEvent(s, evs[7 * b + 2], 0);
+  for (int b = 1; b < nb; ++b) cudaStreamWaitEvent(s, evs[8 * b + 2], 0);
 }
 
 inline int large_eig_launches(const LargeEig& le) {

@@ -343,7 +343,7 @@ struct sosadmm_ctx {
   // parallel branches of the PSD projection inside the CUDA graph
   static constexpr int kMaxAux = 1 + 3 * 8;
   cudaStream_t aux[kMaxAux] = {};
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_blk[7 * 8] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_blk[8 * 8] = {};
   bool aux_ok = false;
 };
 
@@ -798,7 +798,7 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
     for (int q = 0; q < naux; ++q) CK_CTX(c, cudaStreamCreateWithFlags(&c->aux[q], cudaStreamNonBlocking));
     CK_CTX(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK_CTX(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
-    for (int q = 0; q < 7 * (int)an.large_blk.size(); ++q)
+    for (int q = 0; q < 8 * (int)an.large_blk.size(); ++q)
       CK_CTX(c, cudaEventCreateWithFlags(&c->ev_blk[q], cudaEventDisableTiming));
     c->aux_ok = true;
   }
