@@ -439,14 +439,23 @@ __global__ void __launch_bounds__(TRD_NT, 1) k_tridiag(TridiagArgs a) {
         if (lr == 0) dpart = fma(v, vn[t], dpart);
       }
       if (warp == 0 && lane == 0) qk1_s = qa[0];  // column k+1 (block 0, cc 0)
-      // reduce-scatter of the transposed partials: column j's partial goes to the owner of row j
-      if (lr == 0) {
+      // reduce-scatter of the transposed partials: column j's partial goes to the owner of row j.
+      // After the column sums every row lane holds all of its blocks' sums, so the 4 row lanes
+      // split the blocks (lane row lr sends block 4 g + lr): one 32-lane push per 4 blocks
     #pragma unroll
-        for (int t = 0; t < MB; ++t) {
-          if (t >= nbt) break;
-          const int j = k + 1 + 8 * trd_block(warp, t) + cc;
-          if (j >= k + 2 && j < N) push(qr + me * S + (j >> logC) - qlo, j & (C - 1), qa[t], &barQ);
-        }
+      for (int g = 0; g < (MB + 3) / 4; ++g) {
+        if (4 * g >= nbt) break;
+        double v = 0.0;
+        int t = 4 * g;
+    #pragma unroll
+        for (int u = 1; u < 4; ++u)
+          if (4 * g + u < MB && lr == u) t = 4 * g + u;
+    #pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (4 * g + u < MB && lr == u) v = qa[4 * g + u];
+        const int j = k + 1 + 8 * trd_block(warp, t) + cc;
+        if (4 * g + lr < MB && t < nbt && j >= k + 2 && j < N)  // row lanes past the last block stay idle
+          push(qr + me * S + (j >> logC) - qlo, j & (C - 1), v, &barQ);
       }
       dpart = warp_sum(dpart);
       if (lane == 0) red[warp] = dpart;
