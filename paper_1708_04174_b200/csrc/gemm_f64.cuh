@@ -26,7 +26,7 @@ struct GemmDesc {
   int lower;           // 1 = only tiles that meet the lower triangle (row >= column) are needed
 };
 
-constexpr int GM_BM = 32, GM_BN = 64, GM_BK = 16, GM_NT = 128;
+constexpr int GM_BM = 32, GM_BN = 64, GM_BK = 16, GM_NT = 128, GM_ST = 3;
 constexpr int GM_PAD = 8;
 
 __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
@@ -52,8 +52,8 @@ __global__ void __launch_bounds__(GM_NT) k_gemm_f64(const GemmDesc* __restrict__
   const int i0 = blockIdx.x * GM_BM, j0 = blockIdx.y * GM_BN;
   if (i0 >= M || j0 >= N) return;
   if (g.lower && j0 > i0 + GM_BM - 1) return;  // tile strictly above the diagonal
-  __shared__ __align__(16) double As[2][GM_BK][GM_BM + GM_PAD];
-  __shared__ __align__(16) double Bs[2][GM_BK][GM_BN + GM_PAD];
+  __shared__ __align__(16) double As[GM_ST][GM_BK][GM_BM + GM_PAD];
+  __shared__ __align__(16) double Bs[GM_ST][GM_BK][GM_BN + GM_PAD];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = 0, wn = warp;  // warp tile origin (wm*32, wn*16)
   double acc[4][2][2];
@@ -95,16 +95,16 @@ __global__ void __launch_bounds__(GM_NT) k_gemm_f64(const GemmDesc* __restrict__
     cp_async_commit();
   };
 
+  // GM_ST-stage ring: slices sl + 1 .. sl + GM_ST - 1 are in flight while slice sl is multiplied
   const int nslices = (K + GM_BK - 1) / GM_BK;
-  if (nslices > 0) issue(0, 0);
+  for (int p = 0; p < GM_ST - 1 && p < nslices; ++p) issue(p * GM_BK, p);
   for (int sl = 0; sl < nslices; ++sl) {
-    const int buf = sl & 1;
-    if (sl + 1 < nslices) {
-      issue((sl + 1) * GM_BK, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    const int buf = sl % GM_ST;
+    if (sl + GM_ST - 1 < nslices) issue((sl + GM_ST - 1) * GM_BK, (sl + GM_ST - 1) % GM_ST);
+    const int ahead = min(GM_ST - 1, nslices - 1 - sl);  // groups allowed to stay in flight
+    if (ahead >= 2) cp_async_wait<2>();
+    else if (ahead == 1) cp_async_wait<1>();
+    else cp_async_wait<0>();
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < GM_BK; kk += 4) {
@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(GM_NT) k_gemm_f64(const GemmDesc* __restrict__
 #pragma unroll
         for (int b = 0; b < 2; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
     }
-    __syncthreads();  // buffer `buf` is refilled by the issue of slice sl + 2
+    __syncthreads();  // buffer `buf` is refilled by the next iteration's issue (slice sl + GM_ST)
   }
   // epilogue: c0/c1 at (row = lane >> 2, col = 2 (lane & 3) + {0, 1}) of each 8 x 8 tile
 #pragma unroll
