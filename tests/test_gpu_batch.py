@@ -74,3 +74,25 @@ def test_get_iterate_into_preallocated_buffers():
     with pytest.raises(ValueError):
         s.get_iterate(out={k: np.zeros(3) for k in ("xi", "y", "z", "s")})
     s.close()
+
+
+def test_iterate_stops_enqueueing_after_termination():
+    """iterate(k) with k far beyond the stop returns promptly (chunked enqueue with device-state polling)
+    and leaves exactly the iterate of a run that asked for just a few more iterations than needed."""
+    import time
+
+    from paper_1708_04174_b200 import SosAdmm
+
+    prob = make_config("pop6")
+    s = SosAdmm.from_problem(prob, max_iters=10**7)
+    s.iterate(1)
+    t0 = time.perf_counter()
+    info = s.iterate(10**7 - 1)
+    dt = time.perf_counter() - t0
+    assert info["status_name"] == "OPTIMAL" and dt < 5.0, dt
+    r = SosAdmm.from_problem(prob, max_iters=10**7)
+    ri = r.iterate(info["iter"] + 3)
+    assert ri["iter"] == info["iter"]
+    assert np.array_equal(_iterates(s), _iterates(r))
+    s.close()
+    r.close()
