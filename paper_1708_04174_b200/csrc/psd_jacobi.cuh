@@ -35,9 +35,10 @@ __device__ __forceinline__ void rr_pair(int r, int k, int Np, int& p, int& q) {
 }
 
 // MAXN: compile-time bound of the launch's largest block (32 or 64), sizing the per-thread element
-// slots.  Per round: the Np/2 rotation parameters (one thread each), ONE __syncthreads, the
-// elementwise update A' = J^T A J, V' = V J from the ping-pong copy (no read/write hazard, the
-// annihilated couplings written as exact zeros in the same pass), ONE __syncthreads.
+// slots.  Per round: the elementwise update A' = J^T A J, V' = V J from the ping-pong copy (no
+// read/write hazard, the annihilated couplings written as exact zeros in the same pass), the next
+// round's Np/2 rotation parameters (one thread each, from its own copies of the three entries it
+// needs), ONE __syncthreads.
 // Warm start (iterates unchanged up to rounding): consecutive ADMM iterations
 // project slowly changing matrices, so the previous solve's eigenvectors P nearly diagonalise the
 // new input; Jacobi runs on B = P^T A P (measured on pop6: 8.6 -> 4.9 sweeps, tools/
@@ -56,10 +57,9 @@ __global__ void __launch_bounds__(NT) k_psd_jacobi(JacobiArgs a) {
   auto Ab = [&](int c) { return smem + (size_t)c * NN; };
   auto Vb = [&](int c) { return smem + (size_t)(2 + c) * NN; };
   double* P = smem + 4 * NN;                      // previous eigenvectors / final V
-  double* alpha = smem + 5 * NN;                  // Np
-  double* beta = alpha + Np;                      // Np
-  int* partner = (int*)(beta + Np);
-  __shared__ int nrot;
+  double* alpha = smem + 5 * NN;                  // 2 Np (round-parity slots)
+  double* beta = alpha + 2 * Np;                  // 2 Np
+  __shared__ int nrot[4];
   __shared__ double normF;
   const int tid = threadIdx.x;
 
@@ -121,60 +121,88 @@ __global__ void __launch_bounds__(NT) k_psd_jacobi(JacobiArgs a) {
     }
     __syncthreads();
   }
-  int cur = 0;
+  // Rotation parameters, ping-pong by round parity: round g reads slot g & 1 while its parameter
+  // threads (tid < Np/2) write round g + 1's into slot (g + 1) & 1.  They compute the three entries
+  // a'_pp, a'_qq, a'_pq of the next round's pair from THIS round's update (the same expression, hence
+  // the same bits, as the elementwise pass writes), so a round needs ONE __syncthreads.
+  // nrot[s & 3] flags a rotation in sweep s (round 0 of sweep s + 1 is decided in sweep s's last round).
+  auto params = [&](double apq, double app, double aqq, int p, int q, double* al, double* be, int slot) {
+    double c = 1.0, sn = 0.0;
+    if (apq * apq > EPS * EPS * fabs(app * aqq) && fabs(apq) > tiny) {
+      // half-angle form (GvL sym.schur2), two rsqrt and no division: with h = sqrt(d^2 + (2 a_pq)^2),
+      // c^2 = (1 + |d| / h) / 2 in [1/2, 1] (no cancellation), s = sign(d) a_pq / (h c)
+      const double d = aqq - app, tw = 2.0 * apq;
+      const double rh = rsqrt(fma(d, d, tw * tw));
+      const double cc = 0.5 * fma(fabs(d), rh, 1.0);
+      const double rc = rsqrt(cc);
+      c = cc * rc;
+      sn = copysign(1.0, d) * (0.5 * tw) * rh * rc;
+      nrot[slot] = 1;
+    }
+    al[p] = c; be[p] = -sn;
+    al[q] = c; be[q] = sn;
+  };
+  const int M = Np - 1;
+  // partner of i in round r of the tournament: p + q = 2 r (mod M), the fixed player M meets r
+  auto partner = [&](int i, int r2) {  // r2 = 2 r mod M
+    if (i == M) return r2 & 1 ? (r2 + M) >> 1 : r2 >> 1;  // r = r2 / 2 (mod M, M odd)
+    int t = r2 - i;
+    t += t < 0 ? M : 0;
+    return t == i ? M : t;
+  };
+  if (tid < 4) nrot[tid] = 0;
+  __syncthreads();
+  if (tid < Np / 2) {  // round 0 from the (warm-started) input
+    int p, q;
+    rr_pair(0, tid, Np, p, q);
+    params(Ab(0)[p + q * Np], Ab(0)[p + p * Np], Ab(0)[q + q * Np], p, q, alpha, beta, 0);
+  }
+  __syncthreads();
+  int cur = 0, g = 0;
   for (int sweep = 0; sweep < 60; ++sweep) {
-    if (tid == 0) nrot = 0;
-    for (int r = 0; r < Np - 1; ++r) {
+    for (int r = 0; r < M; ++r, ++g) {
       const double* A = Ab(cur);
       const double* V = Vb(cur);
-      // 1. rotation parameters of the Np/2 disjoint pairs (GvL sym.schur2: the rotation that
-      //    annihilates a_pq, with d = a_qq - a_pp)
-      if (tid < Np / 2) {
-        int p, q;
-        rr_pair(r, tid, Np, p, q);
-        const double apq = A[p + q * Np], app = A[p + p * Np], aqq = A[q + q * Np];
-        double c = 1.0, s = 0.0;
-        if (apq * apq > EPS * EPS * fabs(app * aqq) && fabs(apq) > tiny) {
-          // half-angle form, two rsqrt and no division: with h = sqrt(d^2 + (2 a_pq)^2),
-          // c^2 = (1 + |d| / h) / 2 in [1/2, 1] (no cancellation), s = sign(d) a_pq / (h c)
-          const double d = aqq - app, tw = 2.0 * apq;
-          const double rh = rsqrt(fma(d, d, tw * tw));
-          const double cc = 0.5 * fma(fabs(d), rh, 1.0);
-          const double rc = rsqrt(cc);
-          c = cc * rc;
-          s = copysign(1.0, d) * (0.5 * tw) * rh * rc;
-          nrot = 1;
-        }
-        alpha[p] = c; beta[p] = -s; partner[p] = q;
-        alpha[q] = c; beta[q] = s;  partner[q] = p;
-      }
-      __syncthreads();
-      // 2. A' = J^T A J, V' = V J elementwise from the 2 x 2 coupling of (row i, ip) x (col j, jp)
+      const double* al = alpha + (g & 1) * Np;
+      const double* be = beta + (g & 1) * Np;
+      const int r2 = (2 * r) % M;
       double* An = Ab(cur ^ 1);
       double* Vn = Vb(cur ^ 1);
+      // A' = J^T A J, V' = V J elementwise from the 2 x 2 coupling of (row i, ip) x (col j, jp)
+      auto elem = [&](int i, int j) {
+        const int ip = partner(i, r2), jp = partner(j, r2);
+        const double ai = al[i], bi = be[i], aj = al[j], bj = be[j];
+        const double na = ai * (aj * A[i + j * Np] + bj * A[i + jp * Np]) +
+                          bi * (aj * A[ip + j * Np] + bj * A[ip + jp * Np]);
+        return (j == ip && bi != 0.0) ? 0.0 : na;  // the coupling of a rotated pair: exact zero
+      };
 #pragma unroll
       for (int cnt = 0; cnt < PER; ++cnt) {
         const int e = tid + cnt * NT;
         if (e < NN) {
           const int i = ei[cnt], j = ej[cnt];
-          const int ip = partner[i], jp = partner[j];
-          const double ai = alpha[i], bi = beta[i], aj = alpha[j], bj = beta[j];
-          const double na = ai * (aj * A[i + j * Np] + bj * A[i + jp * Np]) +
-                            bi * (aj * A[ip + j * Np] + bj * A[ip + jp * Np]);
-          An[e] = (j == ip && bi != 0.0) ? 0.0 : na;  // the coupling of a rotated pair: exact zero
-          Vn[e] = aj * V[i + j * Np] + bj * V[i + jp * Np];
+          const int jp = partner(j, r2);
+          An[e] = elem(i, j);
+          Vn[e] = al[j] * V[i + j * Np] + be[j] * V[i + jp * Np];
         }
+      }
+      if (tid < Np / 2) {  // the next round's parameters from this round's a'_pq, a'_pp, a'_qq
+        const int rn = r + 1 == M ? 0 : r + 1;
+        int p, q;
+        rr_pair(rn, tid, Np, p, q);
+        params(elem(p, q), elem(p, p), elem(q, q), p, q, alpha + ((g + 1) & 1) * Np, beta + ((g + 1) & 1) * Np,
+               (sweep + (rn == 0)) & 3);
       }
       cur ^= 1;
       __syncthreads();
     }
-    if (nrot == 0) {
+    if (nrot[sweep & 3] == 0) {
 #ifdef SOSADMM_JACOBI_DEBUG
       if (tid == 0) printf("jacobi block %d N %d sweeps %d\n", b, N, sweep + 1);
 #endif
       break;
     }
-    __syncthreads();  // every thread has read nrot before thread 0 clears it
+    if (tid == 0) nrot[(sweep + 2) & 3] = 0;  // read at the end of sweep - 2; next written in sweep + 1
   }
   const double* A = Ab(cur);
   const double* V = Vb(cur);
@@ -202,7 +230,7 @@ __global__ void __launch_bounds__(NT) k_psd_jacobi(JacobiArgs a) {
 
 inline size_t jacobi_smem_bytes(int N) {
   const int Np = (N + 1) & ~1;
-  return sizeof(double) * (5 * (size_t)Np * Np + 2 * Np) + sizeof(int) * Np;
+  return sizeof(double) * (5 * (size_t)Np * Np + 4 * Np);
 }
 
 typedef void (*JacobiKernel)(JacobiArgs);
