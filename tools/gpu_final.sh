@@ -14,3 +14,4 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_tridiag|k_gather|k_scatter|k_pack" -c 5 -o gpurun_out/final_full python bench.py --steps 1 --warmup 3 --no-ttt --no-cpu > gpurun_out/final_ncu_full.log 2>&1; echo full=$?
 timeout 600 ncu --set full --clock-control none -k "regex:k_gemm_f64|k_dc_secular|k_dc_prep" --launch-skip 40 -c 8 -o gpurun_out/final_dc python bench.py --steps 1 --warmup 3 --no-ttt --no-cpu > gpurun_out/final_ncu_dc.log 2>&1; echo dc=$?
 timeout 600 ncu --set full --clock-control none -k "regex:k_kinv" -c 1 -o gpurun_out/final_kinv python bench.py --config box24 --steps 1 --warmup 3 --no-ttt --no-cpu > gpurun_out/final_ncu_kinv.log 2>&1; echo kinv=$?
+timeout 900 python tools/table1_gpu.py --out gpurun_out/final_table1_gpu.jsonl > gpurun_out/final_table1.log 2>&1; echo table1=$?
