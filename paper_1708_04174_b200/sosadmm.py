@@ -265,10 +265,21 @@ class SosAdmm:
             pass
 
 
-def iterate_batch(solvers, k: int) -> list:
+def iterate_batch(solvers, k: int, chunk: int = 256) -> list:
     """k iterations of independent instances on one GPU.  Each SosAdmm owns a stream,
-    so the k graph replays of every instance are enqueued first and then run concurrently (the
-    per-instance iterates are exactly those of solo runs); returns every instance's info."""
-    for s in solvers:
-        s.iterate_async(k)
+    so every instance's graph replays are enqueued before any is waited on and the instances run
+    concurrently (the per-instance iterates are exactly those of solo runs).  Replays are enqueued in
+    rounds of `chunk` per instance; after each round the instances that reached a terminal status
+    (their replays would be device-side no-ops) drop out, so solving a batch to convergence with a
+    large k costs at most one round past each instance's stop.  Returns every instance's info."""
+    if k < 0 or chunk < 1:
+        raise ValueError("k must be >= 0 and chunk >= 1")
+    left = [int(k)] * len(solvers)
+    active = list(range(len(solvers)))
+    while active:
+        for i in active:
+            n = min(chunk, left[i])
+            solvers[i].iterate_async(n)
+            left[i] -= n
+        active = [i for i in active if left[i] > 0 and solvers[i].info()["status"] == 0]
     return [s.info() for s in solvers]

@@ -19,7 +19,7 @@ def _iterates(s):
     return np.concatenate([g["xi"], g["y"], g["z"], g["s"], [g["tau"], g["kappa"], g["iter"]]])
 
 
-def _solo_and_batch(probs, k, **kw):
+def _solo_and_batch(probs, k, chunk=256, **kw):
     from paper_1708_04174_b200 import SosAdmm, iterate_batch
 
     solo = []
@@ -29,7 +29,7 @@ def _solo_and_batch(probs, k, **kw):
         solo.append((info, _iterates(s)))
         s.close()
     batch = [SosAdmm.from_problem(p, **kw) for p in probs]
-    infos = iterate_batch(batch, k)
+    infos = iterate_batch(batch, k, chunk=chunk)
     out = [(infos[i], _iterates(b)) for i, b in enumerate(batch)]
     for b in batch:
         b.close()
@@ -47,10 +47,12 @@ def test_batch_bit_identical_to_solo(names):
         assert bi["res_pri"] == si["res_pri"] and bi["res_dual"] == si["res_dual"]
 
 
-def test_batch_independent_termination():
-    """Instances converge at different iterations; each stops at its own residual-stop k."""
+@pytest.mark.parametrize("chunk", [256, 7])
+def test_batch_independent_termination(chunk):
+    """Instances converge at different iterations; each stops at its own residual-stop k (whatever the
+    enqueue round size, finished instances drop out between rounds)."""
     probs = [make_config("pop6", seed=s) for s in range(4)]
-    solo, batch = _solo_and_batch(probs, 5000, max_iters=5000)
+    solo, batch = _solo_and_batch(probs, 5000, chunk=chunk, max_iters=5000)
     its = [si["iter"] for si, _ in solo]
     assert len(set(its)) > 1  # the seeds really do stop at different iterations
     for (si, sv), (bi, bv) in zip(solo, batch):
