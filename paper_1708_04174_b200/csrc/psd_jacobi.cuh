@@ -37,7 +37,7 @@ __device__ __forceinline__ void rr_pair(int r, int k, int Np, int& p, int& q) {
 // MAXN: compile-time bound of the launch's largest block (32 or 64), sizing the per-thread element
 // slots.  Per round: the elementwise update A' = J^T A J, V' = V J from the ping-pong copy (no
 // read/write hazard, the annihilated couplings written as exact zeros in the same pass), the next
-// round's Np/2 rotation parameters (one thread each, from its own copies of the three entries it
+// round's Np/2 rotation parameters (one of the last Np/2 threads each, from its own copies of the three entries it
 // needs), ONE __syncthreads.
 // Warm start (iterates unchanged up to rounding): consecutive ADMM iterations
 // project slowly changing matrices, so the previous solve's eigenvectors P nearly diagonalise the
@@ -150,11 +150,15 @@ __global__ void __launch_bounds__(NT) k_psd_jacobi(JacobiArgs a) {
     t += t < 0 ? M : 0;
     return t == i ? M : t;
   };
+  // parameter threads: the LAST Np/2 threads of the CTA, whose second element slot is empty when
+  // Np^2 <= NT (MAXN) + NT - Np/2 (e.g. pop6's Np = 28 at NT = 512), so the round's longest thread
+  // carries one element update fewer
+  const int pt = tid - (NT - Np / 2);
   if (tid < 4) nrot[tid] = 0;
   __syncthreads();
-  if (tid < Np / 2) {  // round 0 from the (warm-started) input
+  if (pt >= 0) {  // round 0 from the (warm-started) input
     int p, q;
-    rr_pair(0, tid, Np, p, q);
+    rr_pair(0, pt, Np, p, q);
     params(Ab(0)[p + q * Np], Ab(0)[p + p * Np], Ab(0)[q + q * Np], p, q, alpha, beta, 0);
   }
   __syncthreads();
@@ -186,10 +190,10 @@ __global__ void __launch_bounds__(NT) k_psd_jacobi(JacobiArgs a) {
           Vn[e] = al[j] * V[i + j * Np] + be[j] * V[i + jp * Np];
         }
       }
-      if (tid < Np / 2) {  // the next round's parameters from this round's a'_pq, a'_pp, a'_qq
+      if (pt >= 0) {  // the next round's parameters from this round's a'_pq, a'_pp, a'_qq
         const int rn = r + 1 == M ? 0 : r + 1;
         int p, q;
-        rr_pair(rn, tid, Np, p, q);
+        rr_pair(rn, pt, Np, p, q);
         params(elem(p, q), elem(p, p), elem(q, q), p, q, alpha + ((g + 1) & 1) * Np, beta + ((g + 1) & 1) * Np,
                (sweep + (rn == 0)) & 3);
       }
@@ -202,7 +206,9 @@ __global__ void __launch_bounds__(NT) k_psd_jacobi(JacobiArgs a) {
 #endif
       break;
     }
-    if (tid == 0) nrot[(sweep + 2) & 3] = 0;  // read at the end of sweep - 2; next written in sweep + 1
+    // slot of sweep + 3 (= sweep - 1): read by every thread at the end of sweep - 1 (a barrier ago),
+    // next written in the last round of sweep + 2 (a barrier ahead), whichever thread computes parameters
+    if (tid == 0) nrot[(sweep + 3) & 3] = 0;
   }
   const double* A = Ab(cur);
   const double* V = Vb(cur);
