@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(NT) k_psd_jacobi(JacobiArgs a) {
   double* alpha = smem + 5 * NN;                  // 2 Np (round-parity slots)
   double* beta = alpha + 2 * Np;                  // 2 Np
   __shared__ int nrot[4];
+  __shared__ double offp[2 * (NT / 32)];  // per-warp off(A')^2 of a sweep's last round, by sweep parity
   __shared__ double normF;
   const int tid = threadIdx.x;
 
@@ -180,15 +181,22 @@ __global__ void __launch_bounds__(NT) k_psd_jacobi(JacobiArgs a) {
                           bi * (aj * A[ip + j * Np] + bj * A[ip + jp * Np]);
         return (j == ip && bi != 0.0) ? 0.0 : na;  // the coupling of a rotated pair: exact zero
       };
+      double off2 = 0.0;  // this thread's share of off(A')^2, summed in a sweep's last round
 #pragma unroll
       for (int cnt = 0; cnt < PER; ++cnt) {
         const int e = tid + cnt * NT;
         if (e < NN) {
           const int i = ei[cnt], j = ej[cnt];
           const int jp = partner(j, r2);
-          An[e] = elem(i, j);
+          const double v = elem(i, j);
+          An[e] = v;
           Vn[e] = al[j] * V[i + j * Np] + be[j] * V[i + jp * Np];
+          off2 = i != j ? fma(v, v, off2) : off2;
         }
+      }
+      if (r == M - 1) {
+        off2 = warp_sum(off2);
+        if ((tid & 31) == 0) offp[(sweep & 1) * (NT / 32) + (tid >> 5)] = off2;
       }
       if (pt >= 0) {  // the next round's parameters from this round's a'_pq, a'_pp, a'_qq
         const int rn = r + 1 == M ? 0 : r + 1;
@@ -200,7 +208,12 @@ __global__ void __launch_bounds__(NT) k_psd_jacobi(JacobiArgs a) {
       cur ^= 1;
       __syncthreads();
     }
-    if (nrot[sweep & 3] == 0) {
+    // Stop after a quiet sweep, or as soon as off(A)_F <= N tiny (the bound a quiet sweep leaves: every
+    // coupling <= tiny): |Pi(A) - V diag(lambda_+) V^T|_F <= off(A)_F since Pi is 1-Lipschitz
+    double off2 = 0.0;
+#pragma unroll 4
+    for (int w = 0; w < NT / 32; ++w) off2 += offp[(sweep & 1) * (NT / 32) + w];
+    if (nrot[sweep & 3] == 0 || off2 <= (double)N * N * tiny * tiny) {
 #ifdef SOSADMM_JACOBI_DEBUG
       if (tid == 0) printf("jacobi block %d N %d sweeps %d\n", b, N, sweep + 1);
 #endif
