@@ -166,7 +166,12 @@ def roofline_table(prob, tl, phase, large, hbm, hbm_src, config="pop40"):
                     "traffic": traffic_of("k_tridiag", traffic) if len(large) == 1 else None,
                     "algorithmic_per_launch": fl,
                     "peak_source": "measured FP64 DFMA peak of this pool's B200 (profiles/r01_probe_fp64.log); "
-                                   "MEASURED_PEAKS.json has no FP64 entry", "ms_per_iter": tms})
+                                   "MEASURED_PEAKS.json has no FP64 entry", "ms_per_iter": tms,
+                    # context: the pass is N - 2 dependent steps on one cluster, so it can use at most
+                    # C of the 148 SMs; the same achieved rate against those SMs' share of the peak
+                    "sms_used": sum(TRD_CLUSTER(N) for N in large),
+                    "frac_of_used_sms": fl / (tms * 1e-3) / 1e12
+                    / (DFMA_PEAK_TFLOPS * min(148, sum(TRD_CLUSTER(N) for N in large)) / 148)})
         fd = sum(4.0 / 3.0 * N ** 3 for N in large)
         out.append({"kernel": "divide-and-conquer tridiagonal eigensolver (k_dc_*, merge GEMMs on DMMA; 4/3 N^3 "
                               "dense-count flops, deflation lowers the real count)",
