@@ -333,7 +333,8 @@ def run_ours(args):
         "time_to_1e-4": ttt,
         "phase_ms_per_iter": phase,
         "roofline": {k: dominant[k] for k in ("kernel", "bound", "achieved", "peak", "unit", "frac", "traffic",
-                                              "algorithmic_per_launch", "peak_source", "ms_per_iter")},
+                                              "algorithmic_per_launch", "peak_source", "ms_per_iter", "sms_used",
+                                              "frac_of_used_sms") if k in dominant},
         "roofline_kernels": rooflines,
         "cpu_baseline": cpu,
         "e2e": {"value": total_steps / (e2e_ms * 1e-3), "unit": "iters/s", "h2d_bytes_per_step": h2d,
