@@ -113,7 +113,8 @@ def eig_flops(N: int) -> float:
 
 def affine_bytes(prob, tl: int) -> float:
     """Algorithmic HBM bytes of the affine projection per iteration:
-    36 L + 68 m + 24 nnz(A_low) + 8 t'^2 (dense K^{-1} apply), L = PSD svec entries."""
+    36 L + 68 m + 24 nnz(A_low) + 4 t'(t'+1) (the K^{-1} apply reads one triangle of the symmetric
+    inverse: SURVEY's 8 t'^2 halved by symmetry), L = PSD svec entries."""
     L = prob.n - prob.n_free
     A = prob.A.tocsc()
     nnz_low = 0
@@ -121,7 +122,7 @@ def affine_bytes(prob, tl: int) -> float:
     nnz_low += A[:, :prob.n_free].nnz
     col_nnz = np.diff(A.indptr)[prob.n_free:]
     nnz_low += int(col_nnz[col_nnz > 1].sum())
-    return 36.0 * L + 68.0 * prob.m + 24.0 * nnz_low + 8.0 * tl * tl
+    return 36.0 * L + 68.0 * prob.m + 24.0 * nnz_low + 4.0 * tl * (tl + 1)
 
 
 def kernel_traffic():
@@ -152,7 +153,7 @@ def roofline_table(prob, tl, phase, large, hbm, hbm_src, config="pop40"):
     aff_ms = phase["affine"] + phase["scatter"] + phase["pack"]
     abytes = affine_bytes(prob, tl)
     out.append({"kernel": "affine projection: k_gather, k_lowT, k_kinv, k_tphase, k_rowupdate, k_scatter, k_pack "
-                          "(36 L + 68 m + 24 nnz(A_low) + 8 t'^2 algorithmic bytes)",
+                          "(36 L + 68 m + 24 nnz(A_low) + 4 t'(t'+1) algorithmic bytes)",
                 "bound": "hbm", "achieved": abytes / (aff_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                 "frac": abytes / (aff_ms * 1e-3) / 1e9 / hbm, "traffic": None, "algorithmic_per_launch": abytes,
                 "peak_source": hbm_src, "ms_per_iter": aff_ms})

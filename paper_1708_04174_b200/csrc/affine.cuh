@@ -69,6 +69,7 @@ struct AffineArgs {
   double* aty;
   double* part;
   int gather_blocks;
+  double* kpart;  // symmetric K^{-1} apply (tl >= KINV_SYM_MIN): nt x nt x KT per-tile partials
   double* asvec;  // PSD part of u_hat_xi - z (size npsd)
   // PSD blocks
   int nblk;
@@ -183,6 +184,93 @@ __global__ void __launch_bounds__(256) k_kinv(AffineArgs a) {
   for (int j = lane; j < a.tl; j += 32) acc = fma(row[j], a.yt[j], acc);
   acc = warp_sum(acc);
   if (lane == 0) a.zt[wid] = acc;
+}
+
+// Symmetric K^{-1} apply for large t' (config 3: t' = 7,801, K^{-1} = 487 MB, HBM-bound): read only
+// the tiles on and below the diagonal (half the bytes).  Tile (I, J), I >= J, of KT x KT contributes
+// K_IJ y_J to block I and, when I > J, K_IJ^T y_I = K_JI y_I to block J; the first is stored at
+// kpart[I][J], the second at kpart[J][I], so z_I = sum_J kpart[I][J] in fixed J order (k_kinv_sum):
+// deterministic, no atomics.
+constexpr int KT = 64;
+constexpr int KINV_SYM_MIN = 2048;  // below it K^{-1} (<= 32 MB) is L2-resident: one warp per row
+__global__ void __launch_bounds__(256) k_kinv_tiles(AffineArgs a) {
+  if (a.st->done) return;
+  __shared__ double rsum[2][KT];   // row partials of the two column halves
+  __shared__ double csum[4][KT];   // column partials of the four row quarters
+  const int nt = (a.tl + KT - 1) / KT;
+  const int bidx = blockIdx.x;
+  int I = (int)((sqrt(8.0 * bidx + 1.0) - 1.0) * 0.5);
+  while ((I + 1) * (I + 2) / 2 <= bidx) ++I;
+  while (I * (I + 1) / 2 > bidx) --I;
+  const int J = bidx - I * (I + 1) / 2;
+  const int tid = threadIdx.x, c = tid & (KT - 1), r0 = tid >> 6, lane = tid & 31;
+  const int jc = J * KT + c;
+  const bool cok = jc < a.tl;
+  const double yj = cok ? a.yt[jc] : 0.0;
+  double cacc = 0.0;
+  double kv[KT / 4];
+#pragma unroll
+  for (int u = 0; u < KT / 4; ++u) {  // all loads first: 16 independent 8-byte loads in flight
+    const int i = I * KT + r0 + 4 * u;
+    kv[u] = (cok && i < a.tl) ? __ldcs(a.Kinv + (size_t)i * a.tl + jc) : 0.0;
+  }
+  double v[KT / 4];
+#pragma unroll
+  for (int u = 0; u < KT / 4; ++u) {
+    const int i = I * KT + r0 + 4 * u;
+    const double yi = i < a.tl ? a.yt[i] : 0.0;
+    cacc = fma(kv[u], yi, cacc);
+    v[u] = kv[u] * yj;
+  }
+  // the 16 row sums over this warp's 32 columns by a halving butterfly (16 shuffles, not 16 x 5):
+  // at offset o the lanes with bit o set keep the upper half of their values and receive the
+  // partner's upper half, so lane L ends with row u(L) = bits (16, 8, 4, 2) of L
+#pragma unroll
+  for (int n = KT / 4, o = 16; n > 1; n >>= 1, o >>= 1) {
+    const bool hi = lane & o;
+#pragma unroll
+    for (int u = 0; u < n / 2; ++u) {
+      const double send = hi ? v[u] : v[u + n / 2];
+      const double keep = hi ? v[u + n / 2] : v[u];
+      v[u] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  if ((lane & 1) == 0) {
+    const int u = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+    rsum[(tid >> 5) & 1][r0 + 4 * u] = v[0];
+  }
+  csum[r0][c] = cacc;
+  __syncthreads();
+  double* out = a.kpart + ((size_t)I * nt + J) * KT;
+  if (tid < KT) out[tid] = rsum[0][tid] + rsum[1][tid];
+  else if (tid < 2 * KT && I != J) {
+    const int cc = tid - KT;
+    a.kpart[((size_t)J * nt + I) * KT + cc] = (csum[0][cc] + csum[1][cc]) + (csum[2][cc] + csum[3][cc]);
+  }
+}
+
+// one CTA per output block I: thread (r, q) sums the partials J = q, q + 4, ... of row r (loads
+// issued 8 at a time), the four chains combined in a fixed order
+__global__ void __launch_bounds__(256) k_kinv_sum(AffineArgs a) {
+  if (a.st->done) return;
+  __shared__ double ps[4][KT];
+  const int nt = (a.tl + KT - 1) / KT, I = blockIdx.x, r = threadIdx.x & (KT - 1), q = threadIdx.x >> 6;
+  const double* p = a.kpart + (size_t)I * nt * KT + r;
+  double acc = 0.0;
+  int J = q;
+  for (; J + 28 < nt; J += 32) {
+    double t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t[u] = p[(size_t)(J + 4 * u) * KT];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += t[u];
+  }
+  for (; J < nt; J += 4) acc += p[(size_t)J * KT];
+  ps[q][r] = acc;
+  __syncthreads();
+  const int i = I * KT + threadIdx.x;
+  if (threadIdx.x < KT && i < a.tl) a.zt[i] = (ps[0][threadIdx.x] + ps[1][threadIdx.x]) + (ps[2][threadIdx.x] + ps[3][threadIdx.x]);
 }
 
 // k_tphase: single CTA.  mode 0 = full iteration, 1 = check-only (residuals of u^k, no update),

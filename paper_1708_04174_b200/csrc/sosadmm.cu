@@ -371,7 +371,7 @@ void layout(const Analysis& an, Arena& ar, F&& bind) {
 struct DevPtrs {
   int *seg_ptr, *seg_col, *low_col, *lr_ptr, *lr_idx, *lc_ptr, *lc_row, *empty_cols, *code;
   double *seg_val, *lr_val, *lc_val, *c_low, *h1_low, *beta_low, *Kinv, *b, *Pinv, *h2, *aval;
-  double *xi, *z, *y, *s, *x, *uhat2, *yt, *zt, *ulow, *aty, *part, *asvec, *mats, *tmp;
+  double *xi, *z, *y, *s, *x, *uhat2, *yt, *zt, *ulow, *aty, *part, *asvec, *mats, *tmp, *kpart = nullptr;
   DevState* st;
   IterScal* is;
   long long *blk_col, *blk_mat, *cta_q0;
@@ -418,6 +418,10 @@ void carve(const Analysis& an, Arena& ar, DevPtrs& d, int gather_blocks) {
   d.zt = ar.take<double>(tl);
   d.ulow = ar.take<double>(tl);
   d.aty = ar.take<double>(tl);
+  if (tl >= KINV_SYM_MIN) {
+    const size_t nt = (size_t)(tl + KT - 1) / KT;
+    d.kpart = ar.take<double>(nt * nt * KT);
+  }
   d.part = ar.take<double>((size_t)NPART * gather_blocks);
   d.asvec = ar.take<double>(an.npsd);
   d.mats = ar.take<double>((size_t)an.mat_total);
@@ -452,6 +456,18 @@ cudaError_t h2d(T* dst, const std::vector<T>& src, cudaStream_t s) {
   return cudaMemcpyAsync(dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, s);
 }
 
+// z_t = K^{-1} y_t: one warp per row while K^{-1} is L2-sized, else the lower-triangle tile apply
+// (half the HBM bytes; affine.cuh k_kinv_tiles / k_kinv_sum)
+void launch_kinv(const AffineArgs& a, cudaStream_t s) {
+  if (a.tl >= KINV_SYM_MIN) {
+    const int nt = (a.tl + KT - 1) / KT;
+    k_kinv_tiles<<<nt * (nt + 1) / 2, 256, 0, s>>>(a);
+    k_kinv_sum<<<nt, 256, 0, s>>>(a);
+  } else {
+    k_kinv<<<std::max(1, (a.tl * 32 + 255) / 256), 256, 0, s>>>(a);
+  }
+}
+
 sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev) {
   AffineArgs& a = c->aa;
   cudaStream_t s = c->stream;
@@ -473,7 +489,7 @@ sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev) {
     k_gather<<<c->gather_blocks, GATHER_NT, 0, s>>>(a);
   }
   k_lowT<<<tlw, 256, 0, s>>>(a);
-  k_kinv<<<tlw, 256, 0, s>>>(a);
+  launch_kinv(a, s);
   k_tphase<<<1, TP_NT, 0, s>>>(a, mode_full ? 0 : 1);
   if (!mode_full) return SOSADMM_OK;
   k_rowupdate<<<(a.m + 255) / 256, 256, 0, s>>>(a, 1);
@@ -511,6 +527,7 @@ sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev) {
 
 int64_t count_launches(const sosadmm_ctx* c) {
   int64_t k = c->sp.sharded ? 9 : 6;  // gather (sharded: 4 kernels + allreduce), lowT, kinv, tphase, rowupdate, pack
+  if (c->an.tl >= KINV_SYM_MIN) k += 1;  // symmetric K^{-1} apply: tiles + fixed-order sum
   if (c->aa.pos_ctas > 0) k += 1;
   if (!c->an.small_blk.empty()) k += 1;
   if (!c->an.large_blk.empty()) k += large_eig_launches(c->le);
@@ -760,7 +777,7 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
   a.denom = denom; a.bh2 = bh; a.nb = std::sqrt(nb); a.nc = std::sqrt(nc);
   a.code = d.code; a.aval = d.aval;
   a.xi = d.xi; a.z = d.z; a.y = d.y; a.s = d.s; a.st = d.st; a.is = d.is;
-  a.x = d.x; a.uhat2 = d.uhat2; a.yt = d.yt; a.zt = d.zt; a.ulow = d.ulow; a.aty = d.aty;
+  a.x = d.x; a.uhat2 = d.uhat2; a.yt = d.yt; a.zt = d.zt; a.ulow = d.ulow; a.aty = d.aty; a.kpart = d.kpart;
   a.part = d.part; a.gather_blocks = c->gather_blocks; a.asvec = d.asvec;
   a.nblk = an.nblk; a.blk_col = d.blk_col; a.blk_N = d.blk_N; a.blk_mat = d.blk_mat; a.mats = d.mats;
   a.cta_blk = d.cta_blk; a.cta_q0 = d.cta_q0; a.pos_ctas = (int)an.cta_blk.size();
@@ -1028,7 +1045,7 @@ sosadmm_err sosadmm_project_affine(sosadmm_ctx* c, const double* w1, const doubl
   const int tlw = std::max(1, (a.tl * 32 + 255) / 256);
   k_gather<<<c->gather_blocks, GATHER_NT, 0, s>>>(a);
   k_lowT<<<tlw, 256, 0, s>>>(a);
-  k_kinv<<<tlw, 256, 0, s>>>(a);
+  launch_kinv(a, s);
   k_tphase<<<1, TP_NT, 0, s>>>(a, 2);
   k_rowupdate<<<(m + 255) / 256, 256, 0, s>>>(a, 0);
   if (a.pos_ctas > 0) k_scatter<<<a.pos_ctas, POS_NT, 0, s>>>(a, 1);

@@ -25,7 +25,8 @@ def test_reference_arm_json_line():
 
 
 def test_affine_algorithmic_bytes_formula():
-    """DESIGN.md §5 / SURVEY §8(d): affine algorithmic bytes = 36 L + 68 m + 24 nnz(A_low) + 8 t'^2; for
+    """DESIGN.md §5 / SURVEY §8(d): affine algorithmic bytes = 36 L + 68 m + 24 nnz(A_low) + 4 t'(t'+1) (one
+    triangle of the symmetric K^{-1}); for
     config 0 (A_low = the single gamma column e_const, t' = 1) that is 36 L + 68 m + 24 + 8."""
     sys.path.insert(0, ROOT)
     import bench
