@@ -42,7 +42,8 @@ struct AffineArgs {
   const double* c_low;
   const double* h1_low;
   const double* beta_low;
-  const double* Kinv;  // tl x tl, symmetric
+  const double* Kinv;  // tl x tl, symmetric, row i at Kinv + i * ldk (ldk = tl rounded up to even:
+  int ldk;             //   16-byte aligned column pairs for the tile apply)
   const int* empty_cols;
   int n_empty;
   // row data
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(256) k_kinv(AffineArgs a) {
   if (a.st->done) return;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wid >= a.tl) return;
-  const double* row = a.Kinv + (size_t)wid * a.tl;
+  const double* row = a.Kinv + (size_t)wid * a.ldk;
   double acc = 0.0;
   for (int j = lane; j < a.tl; j += 32) acc = fma(row[j], a.yt[j], acc);
   acc = warp_sum(acc);
@@ -195,38 +196,42 @@ constexpr int KT = 64;
 constexpr int KINV_SYM_MIN = 2048;  // below it K^{-1} (<= 32 MB) is L2-resident: one warp per row
 __global__ void __launch_bounds__(256) k_kinv_tiles(AffineArgs a) {
   if (a.st->done) return;
-  __shared__ double rsum[2][KT];   // row partials of the two column halves
-  __shared__ double csum[4][KT];   // column partials of the four row quarters
+  __shared__ double rsum[KT];      // row partials (each warp owns whole rows)
+  __shared__ double csum[8][KT];   // column partials of the eight warps
   const int nt = (a.tl + KT - 1) / KT;
   const int bidx = blockIdx.x;
   int I = (int)((sqrt(8.0 * bidx + 1.0) - 1.0) * 0.5);
   while ((I + 1) * (I + 2) / 2 <= bidx) ++I;
   while (I * (I + 1) / 2 > bidx) --I;
   const int J = bidx - I * (I + 1) / 2;
-  const int tid = threadIdx.x, c = tid & (KT - 1), r0 = tid >> 6, lane = tid & 31;
-  const int jc = J * KT + c;
-  const bool cok = jc < a.tl;
-  const double yj = cok ? a.yt[jc] : 0.0;
-  double cacc = 0.0;
-  double kv[KT / 4];
+  // lane l owns the column pair (2l, 2l + 1) of the tile (one 16-byte load per row), warp w the rows
+  // w, w + 8, ..., w + 56
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int jc = J * KT + 2 * lane;
+  const bool c0 = jc < a.tl, c1 = jc + 1 < a.tl;
+  const double yj0 = c0 ? a.yt[jc] : 0.0, yj1 = c1 ? a.yt[jc + 1] : 0.0;
+  double2 kv[KT / 8];
 #pragma unroll
-  for (int u = 0; u < KT / 4; ++u) {  // all loads first: 16 independent 8-byte loads in flight
-    const int i = I * KT + r0 + 4 * u;
-    kv[u] = (cok && i < a.tl) ? __ldcs(a.Kinv + (size_t)i * a.tl + jc) : 0.0;
+  for (int u = 0; u < KT / 8; ++u) {  // all loads first: 8 independent 16-byte loads in flight
+    const int i = I * KT + w + 8 * u;
+    kv[u] = (c0 && i < a.tl) ? __ldcs(reinterpret_cast<const double2*>(a.Kinv + (size_t)i * a.ldk + jc))
+                             : make_double2(0.0, 0.0);
+    if (!c1) kv[u].y = 0.0;  // the padding column of an odd t'
   }
-  double v[KT / 4];
+  double ca0 = 0.0, ca1 = 0.0, v[KT / 8];
 #pragma unroll
-  for (int u = 0; u < KT / 4; ++u) {
-    const int i = I * KT + r0 + 4 * u;
+  for (int u = 0; u < KT / 8; ++u) {
+    const int i = I * KT + w + 8 * u;
     const double yi = i < a.tl ? a.yt[i] : 0.0;
-    cacc = fma(kv[u], yi, cacc);
-    v[u] = kv[u] * yj;
+    ca0 = fma(kv[u].x, yi, ca0);
+    ca1 = fma(kv[u].y, yi, ca1);
+    v[u] = fma(kv[u].x, yj0, kv[u].y * yj1);
   }
-  // the 16 row sums over this warp's 32 columns by a halving butterfly (16 shuffles, not 16 x 5):
-  // at offset o the lanes with bit o set keep the upper half of their values and receive the
-  // partner's upper half, so lane L ends with row u(L) = bits (16, 8, 4, 2) of L
+  // the 8 row sums over the warp's 32 lanes by a halving butterfly: at offset o the lanes with bit o
+  // set keep the upper half of their values and receive the partner's upper half, so lane L ends
+  // with row u(L) = bits (16, 8, 4) of L, then the last two xor steps complete the sums
 #pragma unroll
-  for (int n = KT / 4, o = 16; n > 1; n >>= 1, o >>= 1) {
+  for (int n = KT / 8, o = 16; n > 1; n >>= 1, o >>= 1) {
     const bool hi = lane & o;
 #pragma unroll
     for (int u = 0; u < n / 2; ++u) {
@@ -235,18 +240,21 @@ __global__ void __launch_bounds__(256) k_kinv_tiles(AffineArgs a) {
       v[u] = keep + __shfl_xor_sync(0xffffffffu, send, o);
     }
   }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
   v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-  if ((lane & 1) == 0) {
-    const int u = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-    rsum[(tid >> 5) & 1][r0 + 4 * u] = v[0];
+  if ((lane & 3) == 0) {
+    const int u = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+    rsum[w + 8 * u] = v[0];
   }
-  csum[r0][c] = cacc;
+  csum[w][2 * lane] = ca0;
+  csum[w][2 * lane + 1] = ca1;
   __syncthreads();
-  double* out = a.kpart + ((size_t)I * nt + J) * KT;
-  if (tid < KT) out[tid] = rsum[0][tid] + rsum[1][tid];
-  else if (tid < 2 * KT && I != J) {
+  if (tid < KT) {
+    a.kpart[((size_t)I * nt + J) * KT + tid] = rsum[tid];
+  } else if (tid < 2 * KT && I != J) {
     const int cc = tid - KT;
-    a.kpart[((size_t)J * nt + I) * KT + cc] = (csum[0][cc] + csum[1][cc]) + (csum[2][cc] + csum[3][cc]);
+    a.kpart[((size_t)J * nt + I) * KT + cc] = ((csum[0][cc] + csum[1][cc]) + (csum[2][cc] + csum[3][cc])) +
+                                              ((csum[4][cc] + csum[5][cc]) + (csum[6][cc] + csum[7][cc]));
   }
 }
 

@@ -401,7 +401,7 @@ void carve(const Analysis& an, Arena& ar, DevPtrs& d, int gather_blocks) {
   d.c_low = ar.take<double>(tl);
   d.h1_low = ar.take<double>(tl);
   d.beta_low = ar.take<double>(tl);
-  d.Kinv = ar.take<double>(tl * tl);
+  d.Kinv = ar.take<double>(tl * (tl + (tl & 1)));  // leading dimension tl rounded up to even
   d.empty_cols = ar.take<int>(an.empty_cols.size());
   d.b = ar.take<double>(m);
   d.Pinv = ar.take<double>(m);
@@ -727,7 +727,11 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
   CK_CTX(c, h2d(d.c_low, c_low, s));
   CK_CTX(c, h2d(d.h1_low, h1_low, s));
   CK_CTX(c, h2d(d.beta_low, beta_low, s));
-  CK_CTX(c, h2d(d.Kinv, K, s));
+  {  // K^{-1} rows at an even pitch (16-byte aligned column pairs); the padding column is never read
+    const size_t ldk = (size_t)tl + (tl & 1);
+    CK_CTX(c, cudaMemcpy2DAsync(d.Kinv, ldk * sizeof(double), K.data(), (size_t)tl * sizeof(double),
+                                (size_t)tl * sizeof(double), (size_t)tl, cudaMemcpyHostToDevice, s));
+  }
   CK_CTX(c, h2d(d.empty_cols, an.empty_cols, s));
   CK_CTX(c, h2d(d.b, an.b, s));
   CK_CTX(c, h2d(d.Pinv, an.Pinv, s));
@@ -772,6 +776,7 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
   a.low_col = d.low_col; a.lr_ptr = d.lr_ptr; a.lr_idx = d.lr_idx; a.lr_val = d.lr_val;
   a.lc_ptr = d.lc_ptr; a.lc_row = d.lc_row; a.lc_val = d.lc_val;
   a.c_low = d.c_low; a.h1_low = d.h1_low; a.beta_low = d.beta_low; a.Kinv = d.Kinv;
+  a.ldk = an.tl + (an.tl & 1);
   a.empty_cols = d.empty_cols; a.n_empty = (int)an.empty_cols.size();
   a.b = d.b; a.Pinv = d.Pinv; a.h2 = d.h2;
   a.denom = denom; a.bh2 = bh; a.nb = std::sqrt(nb); a.nc = std::sqrt(nc);
