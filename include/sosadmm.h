@@ -128,8 +128,11 @@ sosadmm_err sosadmm_setup_sharded(const sosadmm_problem* prob, const sosadmm_set
                                   int32_t rank, int32_t world, const int32_t* block_owner, sosadmm_ctx** out);
 
 /* Run up to k ADMM iterations (`eq:ADMMSteps`) on the device, stopping early when the C9 rule
- * fires or max_iters is reached; every iteration's residuals are checked.  Asynchronous work is
- * completed before return; *out (may be NULL) receives the state after the last iteration. */
+ * fires or max_iters is reached; every iteration's residuals are checked.  The iterations are
+ * CUDA-graph replays enqueued in chunks; once a finished chunk shows the device's latched stop, no
+ * further replays are enqueued (replays after the stop would be no-ops), so a large k costs little
+ * past the stop.  Asynchronous work is completed before return; *out (may be NULL) receives the
+ * state after the last iteration. */
 sosadmm_err sosadmm_iterate(sosadmm_ctx* ctx, int64_t k, sosadmm_info* out);
 
 /* Enqueue k ADMM iterations (k CUDA-graph replays) on the context's stream and return without
