@@ -35,6 +35,7 @@ struct AffineArgs {
   const int* low_col;
   const int* lr_ptr;
   const int* lr_idx;
+  const int* lr_col;   // low_col[lr_idx[e]] (the gather's direct column index)
   const double* lr_val;
   const int* lc_ptr;
   const int* lc_row;
@@ -117,9 +118,9 @@ __global__ void __launch_bounds__(GATHER_NT) k_gather(AffineArgs a) {
     }
     double gl = 0.0, axl = 0.0;
     const int l0 = a.lr_ptr[r], l1 = a.lr_ptr[r + 1];
+#pragma unroll 4
     for (int e = l0; e < l1; ++e) {
-      const int jl = a.lr_idx[e];
-      const int j = a.low_col[jl];
+      const int j = a.lr_col[e];
       const double v = a.lr_val[e];
       const double xj = a.xi[j];
       const double r1 = xj + a.z[j];  // w1 on the low columns (q = M^{-1} w_12, reading C15)

@@ -83,7 +83,7 @@ struct Analysis {
   std::vector<double> aval;
   std::vector<int> seg_ptr, seg_col;
   std::vector<double> seg_val;
-  std::vector<int> low_col, lr_ptr, lr_idx, lc_ptr, lc_row;
+  std::vector<int> low_col, lr_ptr, lr_idx, lr_col, lc_ptr, lc_row;
   std::vector<double> lr_val, lc_val;
   std::vector<int> empty_cols;
   std::vector<double> D, Pinv, b, c;
@@ -233,6 +233,8 @@ sosadmm_err analyse(const sosadmm_problem* p, Analysis& an, std::string& msg, co
         fill[r]++;
       }
   }
+  an.lr_col.resize(an.lr_idx.size());  // direct column of each row entry (one indirection less in the gather)
+  for (size_t e = 0; e < an.lr_idx.size(); ++e) an.lr_col[e] = an.low_col[an.lr_idx[e]];
   // PSD blocks (only the blocks this rank owns are scattered, projected and packed)
   long long col = an.t;
   an.mat_total = 0;
@@ -369,7 +371,7 @@ void layout(const Analysis& an, Arena& ar, F&& bind) {
 }
 
 struct DevPtrs {
-  int *seg_ptr, *seg_col, *low_col, *lr_ptr, *lr_idx, *lc_ptr, *lc_row, *empty_cols, *code;
+  int *seg_ptr, *seg_col, *low_col, *lr_ptr, *lr_idx, *lr_col, *lc_ptr, *lc_row, *empty_cols, *code;
   double *seg_val, *lr_val, *lc_val, *c_low, *h1_low, *beta_low, *Kinv, *b, *Pinv, *h2, *aval;
   double *xi, *z, *y, *s, *x, *uhat2, *yt, *zt, *ulow, *aty, *part, *asvec, *mats, *tmp, *kpart = nullptr;
   DevState* st;
@@ -394,6 +396,7 @@ void carve(const Analysis& an, Arena& ar, DevPtrs& d, int gather_blocks) {
   d.low_col = ar.take<int>(tl);
   d.lr_ptr = ar.take<int>(m + 1);
   d.lr_idx = ar.take<int>(an.lr_idx.size());
+  d.lr_col = ar.take<int>(an.lr_col.size());
   d.lr_val = ar.take<double>(an.lr_val.size());
   d.lc_ptr = ar.take<int>(tl + 1);
   d.lc_row = ar.take<int>(an.lc_row.size());
@@ -720,6 +723,7 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
   CK_CTX(c, h2d(d.low_col, an.low_col, s));
   CK_CTX(c, h2d(d.lr_ptr, an.lr_ptr, s));
   CK_CTX(c, h2d(d.lr_idx, an.lr_idx, s));
+  CK_CTX(c, h2d(d.lr_col, an.lr_col, s));
   CK_CTX(c, h2d(d.lr_val, an.lr_val, s));
   CK_CTX(c, h2d(d.lc_ptr, an.lc_ptr, s));
   CK_CTX(c, h2d(d.lc_row, an.lc_row, s));
@@ -773,7 +777,7 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
   AffineArgs& a = c->aa;
   a.m = an.m; a.n = an.n; a.t_free = an.t; a.tl = an.tl; a.npsd = an.npsd;
   a.seg_ptr = d.seg_ptr; a.seg_col = d.seg_col; a.seg_val = d.seg_val;
-  a.low_col = d.low_col; a.lr_ptr = d.lr_ptr; a.lr_idx = d.lr_idx; a.lr_val = d.lr_val;
+  a.low_col = d.low_col; a.lr_ptr = d.lr_ptr; a.lr_idx = d.lr_idx; a.lr_col = d.lr_col; a.lr_val = d.lr_val;
   a.lc_ptr = d.lc_ptr; a.lc_row = d.lc_row; a.lc_val = d.lc_val;
   a.c_low = d.c_low; a.h1_low = d.h1_low; a.beta_low = d.beta_low; a.Kinv = d.Kinv;
   a.ldk = an.tl + (an.tl & 1);
