@@ -36,6 +36,7 @@ struct AffineArgs {
   const int* lr_ptr;
   const int* lr_idx;
   const int* lr_col;   // low_col[lr_idx[e]] (the gather's direct column index)
+  int row_lanes;       // k_rowupdate lanes per row: 8 when some row has >= 16 low-rank entries, else 1
   const double* lr_val;
   const int* lc_ptr;
   const int* lc_row;
@@ -446,6 +447,30 @@ __global__ void __launch_bounds__(256) k_rowupdate(AffineArgs a, int write_state
   if (r >= a.m) return;
   double v = 0.0;
   for (int e = a.lr_ptr[r]; e < a.lr_ptr[r + 1]; ++e) v = fma(a.lr_val[e], a.zt[a.lr_idx[e]], v);
+  const double sig2 = a.x[r] - a.Pinv[r] * v;
+  const double u2 = sig2 - a.is->coef * a.h2[r];
+  a.uhat2[r] = u2;
+  if (write_state) {
+    const double so = a.s[r];
+    const double yn = u2 - so;
+    a.y[r] = yn;
+    a.s[r] = (so - u2) + yn;
+  }
+}
+
+// k_rowupdate with 8 lanes per row (rows with many low-rank entries, e.g. config 2's ~66): the
+// lanes take entries l, l + 8, ... and combine by a fixed xor-shuffle tree
+__global__ void __launch_bounds__(256) k_rowupdate8(AffineArgs a, int write_state) {
+  if (a.st->done || !a.is->proceed) return;
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = g >> 3, l = g & 7;
+  double v = 0.0;
+  if (r < a.m)
+    for (int e = a.lr_ptr[r] + l; e < a.lr_ptr[r + 1]; e += 8) v = fma(a.lr_val[e], a.zt[a.lr_idx[e]], v);
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  if (r >= a.m || l != 0) return;
   const double sig2 = a.x[r] - a.Pinv[r] * v;
   const double u2 = sig2 - a.is->coef * a.h2[r];
   a.uhat2[r] = u2;

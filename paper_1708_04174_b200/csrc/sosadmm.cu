@@ -471,6 +471,13 @@ void launch_kinv(const AffineArgs& a, cudaStream_t s) {
   }
 }
 
+void launch_rowupdate(const AffineArgs& a, cudaStream_t s, int write_state) {
+  if (a.row_lanes == 8)
+    k_rowupdate8<<<(int)(((long long)a.m * 8 + 255) / 256), 256, 0, s>>>(a, write_state);
+  else
+    k_rowupdate<<<(a.m + 255) / 256, 256, 0, s>>>(a, write_state);
+}
+
 sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev) {
   AffineArgs& a = c->aa;
   cudaStream_t s = c->stream;
@@ -495,7 +502,7 @@ sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev) {
   launch_kinv(a, s);
   k_tphase<<<1, TP_NT, 0, s>>>(a, mode_full ? 0 : 1);
   if (!mode_full) return SOSADMM_OK;
-  k_rowupdate<<<(a.m + 255) / 256, 256, 0, s>>>(a, 1);
+  launch_rowupdate(a, s, 1);
   if (ev) cudaEventRecord(ev[1], s);
   if (a.pos_ctas > 0) k_scatter<<<a.pos_ctas, POS_NT, 0, s>>>(a, 0);
   if (ev) cudaEventRecord(ev[2], s);
@@ -778,6 +785,11 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
   a.m = an.m; a.n = an.n; a.t_free = an.t; a.tl = an.tl; a.npsd = an.npsd;
   a.seg_ptr = d.seg_ptr; a.seg_col = d.seg_col; a.seg_val = d.seg_val;
   a.low_col = d.low_col; a.lr_ptr = d.lr_ptr; a.lr_idx = d.lr_idx; a.lr_col = d.lr_col; a.lr_val = d.lr_val;
+  {
+    int mx = 0;
+    for (int r = 0; r < an.m; ++r) mx = std::max(mx, an.lr_ptr[r + 1] - an.lr_ptr[r]);
+    a.row_lanes = mx >= 16 ? 8 : 1;
+  }
   a.lc_ptr = d.lc_ptr; a.lc_row = d.lc_row; a.lc_val = d.lc_val;
   a.c_low = d.c_low; a.h1_low = d.h1_low; a.beta_low = d.beta_low; a.Kinv = d.Kinv;
   a.ldk = an.tl + (an.tl & 1);
@@ -1056,7 +1068,7 @@ sosadmm_err sosadmm_project_affine(sosadmm_ctx* c, const double* w1, const doubl
   k_lowT<<<tlw, 256, 0, s>>>(a);
   launch_kinv(a, s);
   k_tphase<<<1, TP_NT, 0, s>>>(a, 2);
-  k_rowupdate<<<(m + 255) / 256, 256, 0, s>>>(a, 0);
+  launch_rowupdate(a, s, 0);
   if (a.pos_ctas > 0) k_scatter<<<a.pos_ctas, POS_NT, 0, s>>>(a, 1);
   if (check_async(c)) return c->err;
   std::vector<double> asv(std::max(a.npsd, 1)), ulow(std::max(a.tl, 1));
