@@ -39,7 +39,8 @@ CONFIG_DESC = {"pop6": "n=6 quartic POP, config 0", "pop20": "n=20 quartic POP, 
                "pop40": "n=40 quartic POP, config 4"}
 
 # roofline denominators: measured on this pool's B200s
-DMMA_PEAK_TFLOPS = 74.3   # profiles/r01_probe_fp64.log: mma.sync m8n8k4 f64 (SASS DMMA), measured
+DMMA_PEAK_TFLOPS = 37.1   # profiles/r01_probe_fp64.log: mma.sync m8n8k4 f64 (SASS DMMA), measured 74.3 with
+#                           the probe counting 2x512 flop per m8n8k4; one is 8*8*4 = 256 FMA = 512 flop
 DFMA_PEAK_TFLOPS = 34.2   # same probe, scalar DFMA
 
 

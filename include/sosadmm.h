@@ -22,9 +22,9 @@
  *  - A is CSC (m x n, n = t + sum N_b(N_b+1)/2), 0-based, int64 column pointers, int32 rows;
  *  - FP64 everywhere; indices int32/int64 as declared.
  * Ownership: inputs are borrowed for the duration of the call and copied.  The context owns its
- *  device state, which lives in the caller-provided device workspace (e.g. a torch tensor) or,
- *  if settings.workspace is NULL, in memory the library allocates itself.  Outputs are written
- *  to caller buffers.  A context is not thread-safe; distinct contexts are independent.
+ *  device state, which lives in the caller-provided device workspace (e.g. a torch tensor); the
+ *  library allocates no device memory of its own (settings.workspace is required: E_ARG if NULL).
+ *  Outputs are written to caller buffers.  A context is not thread-safe; distinct contexts are independent.
  * Errors: every call returns sosadmm_err (0 = OK).  The first error is latched in the context and
  *  returned by every later call; sosadmm_last_error_message() gives a human-readable detail.
  * Initialisation (reading C7): u0 = (0, 0, 1), v0 = (0, 0, 0).  No scaling, no
@@ -83,7 +83,7 @@ typedef struct {
   int32_t check_every;   /* residual check stride (1 = every iteration; the only supported value) */
   int32_t device;        /* CUDA device ordinal */
   void* stream;          /* cudaStream_t to launch on (NULL = the library's own stream) */
-  void* workspace;       /* device memory of >= sosadmm_workspace_size() bytes, or NULL */
+  void* workspace;       /* device memory of >= sosadmm_workspace_size() bytes (required) */
   size_t workspace_bytes;
 } sosadmm_settings;
 
@@ -154,11 +154,15 @@ sosadmm_err sosadmm_iterate_profiled(sosadmm_ctx* ctx, int64_t k, sosadmm_info* 
 /* Current info without iterating (residuals of u^k are computed on demand). */
 sosadmm_err sosadmm_get_info(sosadmm_ctx* ctx, sosadmm_info* out);
 
-/* Copy the unscaled iterates u = (xi, y, tau), v = (z, s, kappa) to host buffers (n, m, n, m). */
+/* Copy the unscaled HSDE iterates u = (xi, y, tau), v = (z, s, kappa) of `eq:ADMMSteps` (
+ * u, v in the embedding of P:362-389) to host buffers of n, m, n, m doubles; tau, kappa, iter to
+ * scalars.  The scaled solution is xi/tau, y/tau.  Any output pointer may be NULL. */
 sosadmm_err sosadmm_get_iterate(sosadmm_ctx* ctx, double* xi, double* y, double* z, double* s,
                                 double* tau, double* kappa, int64_t* iter);
 
-/* Overwrite the iterates (resume / fixed-point tests).  s may be NULL (= 0).  Resets status. */
+/* Overwrite the iterates u = (xi, y, tau), v = (z, s, kappa) of the HSDE with host data
+ * (n, m, n, m doubles; resume, warm start and the fixed-point tests of the planted KKT point).
+ * s may be NULL (= 0, its value for every k >= 1).  Resets the termination status and residuals. */
 sosadmm_err sosadmm_set_iterate(sosadmm_ctx* ctx, const double* xi, const double* y, const double* z,
                                 const double* s, double tau, double kappa, int64_t iter);
 
@@ -179,6 +183,9 @@ sosadmm_err sosadmm_project_psd(sosadmm_ctx* ctx, int32_t block, const double* a
 /* Number of kernel launches one iteration issues (for the bench's gpu_launches claim). */
 int64_t sosadmm_launches_per_iter(const sosadmm_ctx* ctx);
 
+/* Release the context (its device state lives in the caller's workspace, which the caller frees;
+ * the context's streams, events, CUDA graph and NCCL communicator are destroyed here).  NULL is a
+ * no-op.  Ownership rule of SURVEY §8(b) (S:227 cache immutable until destroyed). */
 void sosadmm_destroy(sosadmm_ctx* ctx);
 const char* sosadmm_strerror(sosadmm_err e);
 const char* sosadmm_last_error_message(const sosadmm_ctx* ctx);

@@ -102,7 +102,8 @@ struct Analysis {
 // Column classification and the orthogonal / low-rank split (Proposition 1, P:302-311;
 // Proposition 3): a PSD column with at most one nonzero and c_j = 0 is orthogonal.
 sosadmm_err analyse(const sosadmm_problem* p, Analysis& an, std::string& msg, const ShardSpec& sp = ShardSpec()) {
-  if (!p || p->m <= 0 || p->n_free < 0 || p->n_psd < 0 || !p->A_colptr || !p->b || !p->c) {
+  if (!p || p->m <= 0 || p->n_free < 0 || p->n_psd < 0 || !p->A_colptr || !p->b || !p->c ||
+      (p->n_psd > 0 && !p->psd_dim)) {
     msg = "null pointer or negative size in sosadmm_problem";
     return SOSADMM_E_ARG;
   }
@@ -138,6 +139,10 @@ sosadmm_err analyse(const sosadmm_problem* p, Analysis& an, std::string& msg, co
     msg = "bad CSC column pointers";
     return SOSADMM_E_ARG;
   }
+  if (nnz > 0 && (!p->A_rowidx || !p->A_val)) {
+    msg = "null A_rowidx / A_val with nnz > 0";
+    return SOSADMM_E_ARG;
+  }
   for (long long j = 0; j < n; ++j)
     if (p->A_colptr[j + 1] < p->A_colptr[j]) {
       msg = "CSC column pointers must be nondecreasing";
@@ -153,6 +158,14 @@ sosadmm_err analyse(const sosadmm_problem* p, Analysis& an, std::string& msg, co
   an.code.assign(an.n, -2);
   an.aval.assign(an.n, 0.0);
   std::vector<int> cnt(an.m, 0);
+  if (sp.sharded)
+    for (int j = an.t; j < an.n; ++j)
+      if (p->c[j] != 0.0) {
+        // every rank evaluates c^T xi over all low columns in k_tphase, but only owned PSD columns are
+        // updated: a PSD column with c_j != 0 would make the ranks' tau/kappa diverge
+        msg = "sharded mode needs c_j = 0 on every PSD column (column " + std::to_string(j) + ")";
+        return SOSADMM_E_STRUCT;
+      }
   for (int j = an.t; j < an.n; ++j) {
     const long long e0 = p->A_colptr[j], e1 = p->A_colptr[j + 1];
     if (e1 - e0 <= 1 && p->c[j] == 0.0) {
@@ -450,6 +463,7 @@ size_t total_bytes(const Analysis& an) {
   const int gb = std::max(1, (an.m + GATHER_NT - 1) / GATHER_NT);
   carve(an, ar, d, gb);
   ar.used += large_eig_bytes(an.blk_N, an.large_blk) + kAlign;
+  if (an.tl > 256) ar.used += spdinv_scratch_bytes(an.tl) + kAlign;  // setup-time scratch of the K inverse
   return ar.used + kAlign;
 }
 
@@ -626,25 +640,25 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
     c->own_stream = true;
   }
   const size_t need = total_bytes(an);
-  if (settings && settings->workspace) {
-    if (settings->workspace_bytes < need) {
-      c->err = SOSADMM_E_OOM;
-      c->msg = "workspace too small: need " + std::to_string(need) + " bytes";
-      return c->err;
-    }
-    c->ws = (char*)settings->workspace;
-    c->ws_bytes = settings->workspace_bytes;
-  } else {
-    CK_CTX(c, cudaMalloc(&c->own_mem, need));
-    c->ws = (char*)c->own_mem;
-    c->ws_bytes = need;
+  if (!settings || !settings->workspace) {  // the caller owns all device memory (SURVEY §8(b) ownership)
+    c->err = SOSADMM_E_ARG;
+    c->msg = "settings.workspace is required (sosadmm_workspace_size bytes of device memory)";
+    return c->err;
   }
+  if (settings->workspace_bytes < need) {
+    c->err = SOSADMM_E_OOM;
+    c->msg = "workspace too small: need " + std::to_string(need) + " bytes";
+    return c->err;
+  }
+  c->ws = (char*)settings->workspace;
+  c->ws_bytes = settings->workspace_bytes;
   c->gather_blocks = std::max(1, (an.m + GATHER_NT - 1) / GATHER_NT);
   Arena ar;
   ar.base = (char*)(((uintptr_t)c->ws + kAlign - 1) / kAlign * kAlign);
   DevPtrs d;
   carve(an, ar, d, c->gather_blocks);
   char* large_base = ar.take<char>(large_eig_bytes(an.blk_N, an.large_blk));
+  char* spd_scratch = an.tl > 256 ? ar.take<char>(spdinv_scratch_bytes(an.tl)) : nullptr;
 
   // ---- cache (row a0): K = I + A_low^T P^{-1} A_low, K^{-1}, h = M^{-1} zeta, denom --------
   const int tl = an.tl, m = an.m;
@@ -661,7 +675,7 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
     spd_ok = spd_inverse(K, tl);
   } else {  // large t' (weighted SOS, config 3): blocked Cholesky + inverse on the DMMA GEMM
     CK_CTX(c, cudaMemcpyAsync(d.Kinv, K.data(), sizeof(double) * K.size(), cudaMemcpyHostToDevice, c->stream));
-    const int rc = gpu_spd_inverse(d.Kinv, tl, c->stream);
+    const int rc = gpu_spd_inverse(d.Kinv, tl, c->stream, spd_scratch);
     if (rc == 2) {
       c->err = SOSADMM_E_CUDA;
       c->msg = "GPU inverse of I + A_low^T P^{-1} A_low failed";
@@ -879,9 +893,16 @@ sosadmm_err sosadmm_setup_sharded(const sosadmm_problem* prob, const sosadmm_set
 static sosadmm_err build_graph(sosadmm_ctx* c) {
   if (c->graph) return SOSADMM_OK;
   CK_CTX(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-  launch_iteration(c, 1, nullptr);
-  cudaGraph_t g;
-  CK_CTX(c, cudaStreamEndCapture(c->stream, &g));
+  const sosadmm_err le = launch_iteration(c, 1, nullptr);
+  cudaGraph_t g = nullptr;
+  const cudaError_t ee = cudaStreamEndCapture(c->stream, &g);
+  if (le != SOSADMM_OK || ee != cudaSuccess) {  // a failed capture (e.g. ncclAllReduce) is never instantiated
+    if (g) cudaGraphDestroy(g);
+    if (le != SOSADMM_OK) return c->err = le;
+    c->err = SOSADMM_E_CUDA;
+    c->msg = std::string("cudaStreamEndCapture: ") + cudaGetErrorString(ee);
+    return c->err;
+  }
   CK_CTX(c, cudaGraphInstantiate(&c->graph, g, 0));
   c->graph_raw = g;
   return SOSADMM_OK;
@@ -1060,6 +1081,12 @@ sosadmm_err sosadmm_project_affine(sosadmm_ctx* c, const double* w1, const doubl
   double stau, skap;
   int64_t sit;
   if (sosadmm_get_iterate(c, sxi.data(), sy.data(), sz.data(), ss.data(), &stau, &skap, &sit)) return c->err;
+  // the whole device state (termination latch, status, residuals) is restored afterwards, not rebuilt
+  DevState sst;
+  IterScal sis;
+  CK_CTX(c, cudaMemcpyAsync(&sst, a.st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+  CK_CTX(c, cudaMemcpyAsync(&sis, a.is, sizeof(IterScal), cudaMemcpyDeviceToHost, c->stream));
+  CK_CTX(c, cudaStreamSynchronize(c->stream));
   std::vector<double> zero_n(n, 0.0), zero_m(m, 0.0);
   if (sosadmm_set_iterate(c, w1, w2, zero_n.data(), zero_m.data(), w3, 0.0, 0)) return c->err;
   cudaStream_t s = c->stream;
@@ -1082,7 +1109,14 @@ sosadmm_err sosadmm_project_affine(sosadmm_ctx* c, const double* w1, const doubl
   for (int j = c->an.t; j < n; ++j) u1[j] = asv[j - c->an.t];
   for (int jl = 0; jl < a.tl; ++jl) u1[c->an.low_col[jl]] = ulow[jl];
   *u3 = is.u3;
-  return sosadmm_set_iterate(c, sxi.data(), sy.data(), sz.data(), ss.data(), stau, skap, sit);
+  CK_CTX(c, cudaMemcpyAsync(a.xi, sxi.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  CK_CTX(c, cudaMemcpyAsync(a.z, sz.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  CK_CTX(c, cudaMemcpyAsync(a.y, sy.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s));
+  CK_CTX(c, cudaMemcpyAsync(a.s, ss.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s));
+  CK_CTX(c, cudaMemcpyAsync(a.st, &sst, sizeof(DevState), cudaMemcpyHostToDevice, s));
+  CK_CTX(c, cudaMemcpyAsync(a.is, &sis, sizeof(IterScal), cudaMemcpyHostToDevice, s));
+  CK_CTX(c, cudaStreamSynchronize(s));
+  return SOSADMM_OK;
 }
 
 // Unit entry point: Pi_{S+} of one block given in svec coordinates.
@@ -1265,11 +1299,17 @@ extern "C" int sosadmm_debug_spdinv(int t, double* K) {
   double* dK;
   cudaStream_t s;
   if (cudaStreamCreate(&s)) return -4;
+  char* scr;
   if (cudaMalloc(&dK, 8ull * t * t)) return -7;
+  if (cudaMalloc(&scr, spdinv_scratch_bytes(t))) {
+    cudaFree(dK);
+    return -7;
+  }
   cudaMemcpy(dK, K, 8ull * t * t, cudaMemcpyHostToDevice);
-  const int rc = gpu_spd_inverse(dK, t, s);
+  const int rc = gpu_spd_inverse(dK, t, s, scr);
   cudaMemcpy(K, dK, 8ull * t * t, cudaMemcpyDeviceToHost);
   cudaFree(dK);
+  cudaFree(scr);
   cudaStreamDestroy(s);
   return rc == 0 ? 0 : (rc == 1 ? -3 : -4);
 }

@@ -88,15 +88,30 @@ __global__ void k_set_identity_block(double* R, int ldr, int rows, int col0, int
   R[(size_t)(col0 + j) * ldr + i] = (i == j) ? 1.0 : 0.0;
 }
 
+// Scratch of gpu_spd_inverse (carved from the caller's workspace: the library allocates nothing).
+inline size_t spdinv_scratch_bytes(int t) {
+  const size_t nb = SPD_NB, nblk = (t + nb - 1) / nb, tt = (size_t)t * t;
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  return al(8 * t * nb) + al(8 * nblk * nb * nb) + al(8 * tt) + al(8 * nb * t) + al(sizeof(int)) +
+         al(sizeof(GemmDesc) * (4 * nblk + 2)) + al(8 * tt) + 256;
+}
+
 // In-place K <- K^{-1} (t x t, column-major, full symmetric on input).  Returns 0, or 1 when K is
-// not numerically positive definite.  Temporary device memory is allocated and freed here.
-inline int gpu_spd_inverse(double* K, int t, cudaStream_t s) {
+// not numerically positive definite, 2 on a CUDA error.  Temporaries live in `scratch`
+// (>= spdinv_scratch_bytes(t) bytes of device memory).
+inline int gpu_spd_inverse(double* K, int t, cudaStream_t s, char* scratch) {
   const int nb = SPD_NB;
   const int nblk = (t + nb - 1) / nb;
   double *T = nullptr, *Linv = nullptr, *X = nullptr, *R = nullptr;
   int* fail = nullptr;
   GemmDesc* dg = nullptr;
   std::vector<GemmDesc> gd;
+  size_t used = ((uintptr_t)scratch + 255) / 256 * 256 - (uintptr_t)scratch;
+  auto take = [&](size_t bytes) -> void* {
+    void* p = scratch + used;
+    used += (bytes + 255) / 256 * 256;
+    return p;
+  };
   auto gemm = [&](const double* A, int lda, const double* B, int ldb, int transB, double* C, int ldc, int M, int N,
                   int Kd, double alpha, double beta) {
     GemmDesc g{};
@@ -108,10 +123,11 @@ inline int gpu_spd_inverse(double* K, int t, cudaStream_t s) {
   struct Step { int kind, j0, nbj, gi; };
   std::vector<Step> plan;
   const size_t tt = (size_t)t * t;
-  if (cudaMalloc(&T, sizeof(double) * (size_t)t * nb) || cudaMalloc(&Linv, sizeof(double) * (size_t)nblk * nb * nb) ||
-      cudaMalloc(&X, sizeof(double) * tt) || cudaMalloc(&R, sizeof(double) * (size_t)nb * t) ||
-      cudaMalloc(&fail, sizeof(int)))
-    return 2;
+  T = (double*)take(sizeof(double) * (size_t)t * nb);
+  Linv = (double*)take(sizeof(double) * (size_t)nblk * nb * nb);
+  X = (double*)take(sizeof(double) * tt);
+  R = (double*)take(sizeof(double) * (size_t)nb * t);
+  fail = (int*)take(sizeof(int));
   // 1. Cholesky
   for (int b = 0; b < nblk; ++b) {
     const int j0 = b * nb, nbj = std::min(nb, t - j0), j1 = j0 + nbj, rest = t - j1;
@@ -135,10 +151,10 @@ inline int gpu_spd_inverse(double* K, int t, cudaStream_t s) {
   // 3. K^{-1} = X^T X: transpose X into T-sized? use K as X^T storage
   plan.push_back({6, 0, 0, (int)gd.size()});
   gemm(K, t, X, t, 0, nullptr, t, t, t, t, 1.0, 0.0);  // C filled below (X^T X into R? no: into X2)
-  if (cudaMalloc(&dg, sizeof(GemmDesc) * gd.size())) return 2;
-  // the last GEMM writes into a fresh buffer: reuse X's space is impossible (input), allocate Y
-  double* Y = nullptr;
-  if (cudaMalloc(&Y, sizeof(double) * tt)) return 2;
+  if (gd.size() > 4 * (size_t)nblk + 2) return 2;
+  dg = (GemmDesc*)take(sizeof(GemmDesc) * (4 * (size_t)nblk + 2));
+  // the last GEMM writes into a fresh buffer (X is its input)
+  double* Y = (double*)take(sizeof(double) * tt);
   gd.back().C = Y;
   cudaMemcpyAsync(dg, gd.data(), sizeof(GemmDesc) * gd.size(), cudaMemcpyHostToDevice, s);
   cudaMemsetAsync(fail, 0, sizeof(int), s);
@@ -183,6 +199,5 @@ inline int gpu_spd_inverse(double* K, int t, cudaStream_t s) {
   int hfail = 0;
   cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, s);
   cudaStreamSynchronize(s);
-  cudaFree(T); cudaFree(Linv); cudaFree(X); cudaFree(R); cudaFree(fail); cudaFree(dg); cudaFree(Y);
   return hfail ? 1 : (cudaGetLastError() == cudaSuccess ? 0 : 2);
 }

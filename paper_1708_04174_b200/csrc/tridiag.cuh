@@ -86,12 +86,20 @@ __device__ __forceinline__ void trd_bar_expect(uint64_t* bar, unsigned bytes) {
 __device__ __forceinline__ void trd_bar_wait(uint64_t* bar, unsigned parity) {
   const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
   unsigned ok = 0, spins = 0;
+  unsigned long long t0 = 0;
   while (!ok) {
     asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
                  : "=r"(ok)
                  : "r"(b), "r"(parity)
                  : "memory");
-    if (++spins == (1u << 26)) __trap();  // a lost exchange is a bug: fail loudly instead of hanging the GPU
+    // a lost exchange is a bug: fail loudly instead of hanging the GPU — but only after 20 s of wall
+    // clock (%globaltimer), so time-slicing / MPS contention can never trip it on a correct exchange
+    if (!ok && (++spins & 0xFFFFu) == 0) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 20000000000ull) __trap();
+    }
   }
 }
 __device__ __forceinline__ unsigned trd_cluster_rank() {

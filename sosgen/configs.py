@@ -150,6 +150,33 @@ def ball_pop(nvars: int) -> Problem:
     return assemble(f"ballpop{n}", n, [con], np.array([-1.0]), dict(kind="ball_pop", nvars=n))
 
 
+def unbounded_pop(name: str, nvars: int) -> Problem:
+    """A dual-infeasible (primal-unbounded) program for the DUAL_INFEASIBLE status (SPEC S:270, S:348;
+    PAPER.md P:361 "certificate of ... dual infeasibility"): max u s.t. 1 + u (1 + |x|^2)^2 SOS over the
+    Gram basis of degree <= 2.  (1 + |x|^2)^2 is SOS, so every u >= 0 is feasible and the objective -u is
+    unbounded below.  Recession direction: u = 1, X = G with v2(x)^T G v2(x) = (1 + |x|^2)^2
+    (A xi = 0, xi in K, c^T xi = -1 < 0).  No random draws."""
+    # (1 + |x|^2)^2 = 1 + 2 sum_i x_i^2 + sum_i x_i^4 + 2 sum_{i<j} x_i^2 x_j^2
+    ex, co = [np.zeros(nvars, dtype=np.int64)], [1.0]
+    for i in range(nvars):
+        e = np.zeros(nvars, dtype=np.int64)
+        e[i] = 2
+        ex.append(e)
+        co.append(2.0)
+        e4 = np.zeros(nvars, dtype=np.int64)
+        e4[i] = 4
+        ex.append(e4)
+        co.append(1.0)
+        for j in range(i + 1, nvars):
+            eij = np.zeros(nvars, dtype=np.int64)
+            eij[i] = eij[j] = 2
+            ex.append(eij)
+            co.append(2.0)
+    g1 = Poly(-np.array(co), np.array(ex))
+    con = SosConstraint(g0=Poly.const(nvars, 1.0), g=[g1], blocks=[GramBlock(basis(nvars, 0, 2))])
+    return assemble(name, nvars, [con], np.array([-1.0]), dict(kind="unbounded_pop", nvars=nvars))
+
+
 def univariate_feasibility(name: str, coeffs: list[float]) -> Problem:
     """Is g0(x) = sum_k coeffs[k] x^k SOS?  (SPEC.md S:169-170 examples.)  t = 0."""
     deg = len(coeffs) - 1

@@ -11,14 +11,14 @@ import numpy as np
 import pytest
 
 from oracle import HsdeOracle, Status, brute_force_structure, proj_psd_svec, svec
-from sosgen import ball_pop, make_config, planted_kkt, univariate_feasibility
+from sosgen import ball_pop, make_config, planted_kkt, unbounded_pop, univariate_feasibility
 from sosgen.configs import planted_pop
 from sosgen.matrix_sos import brute_force_counts, matrix_planted_kkt, matrix_sos_pop
 
 pytestmark = pytest.mark.gpu
 
-SMALL = ["pop6", "sq", "neg", "one", "pop3k2", "ball4", "msos2", "pop8"]
-LARGE = ["pop20", "lyap10", "box24", "pop40", "msos3"]
+SMALL = ["pop6", "sq", "neg", "one", "pop3k2", "ball4", "msos2", "pop8", "unb6"]
+LARGE = ["pop20", "lyap10", "box24", "pop40", "msos3", "unb10"]
 
 
 def make(name):
@@ -38,6 +38,8 @@ def make(name):
         return matrix_sos_pop("msos2", 3, 2, 2, 2, seed=3)
     if name == "msos3":  # Y in S^{3 * 28} (cluster tridiagonalisation path)
         return matrix_sos_pop("msos3", 6, 3, 2, 3, seed=4)
+    if name.startswith("unb"):  # dual infeasible (unbounded) program: N = 28 (Jacobi) / 66 (large-block path)
+        return unbounded_pop(name, int(name[3:]))
     return make_config(name)
 
 
@@ -132,6 +134,7 @@ def test_first_20_iterates(name, solvers):
     gpu.set_iterate(np.zeros(prob.n), np.zeros(prob.m), np.zeros(prob.n), None, 1.0, 0.0, 0)
     st = orc.initial_state()
     worst_u = worst_v = 0.0
+    worst_part = (0.0, "")
     for k in range(1, 21):
         st = orc.step(st)
         gpu.iterate(1)
@@ -143,10 +146,27 @@ def test_first_20_iterates(name, solvers):
         scale = np.linalg.norm(np.concatenate([st.u(), st.v()]))
         worst_u = max(worst_u, _rel(ug, st.u(), scale))
         worst_v = max(worst_v, _rel(vg, st.v(), scale))
+        # per component (tau ~ 2e-6 at k = 1 on pop20 is invisible in the joint norm): tau, kappa,
+        # the free part, y and every PSD block of xi and z, each relative to its own size, with an absolute
+        # floor of 1e-12 of the joint norm for parts that are (near) zero on both sides
+        parts = [("tau", [g["tau"]], [st.tau]), ("kappa", [g["kappa"]], [st.kappa]), ("y", g["y"], st.y),
+                 ("xi_free", g["xi"][:prob.n_free], st.xi[:prob.n_free])]
+        off = prob.n_free
+        for bi, N in enumerate(prob.psd_dims):
+            L = N * (N + 1) // 2
+            parts.append((f"xi_{bi}", g["xi"][off:off + L], st.xi[off:off + L]))
+            parts.append((f"z_{bi}", g["z"][off:off + L], st.z[off:off + L]))
+            off += L
+        for pname, a, b in parts:
+            a, b = np.asarray(a), np.asarray(b)
+            err = np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-3 * scale)
+            if err > worst_part[0]:
+                worst_part = (err, f"{pname}@k={k}")
+            assert np.linalg.norm(a - b) <= 1e-8 * np.linalg.norm(b) + 1e-12 * scale, (pname, k, a[:3], b[:3])
     assert worst_u <= 1e-9 and worst_v <= 1e-9, (worst_u, worst_v)
 
 
-@pytest.mark.parametrize("name", ["pop6", "sq", "neg", "pop3k2", "ball4", "msos2"])
+@pytest.mark.parametrize("name", ["pop6", "sq", "neg", "pop3k2", "ball4", "msos2", "unb6", "unb10"])
 def test_convergence_parity(name, solvers):
     prob, gpu, orc = solvers(name, tol=1e-4, max_iters=5000)
     st, status, hist = orc.solve(tol=1e-4, max_iters=5000)
@@ -170,3 +190,44 @@ def test_planted_fixed_point(name, solvers):
     assert np.linalg.norm(g["z"] - z) <= 1e-12 * scale
     assert np.linalg.norm(g["y"] - y) <= 1e-12 * scale
     assert abs(g["tau"] - 1.0) <= 1e-12 and abs(g["kappa"]) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["unb6", "unb10"])
+def test_dual_infeasible_certificate(name, solvers):
+    """DUAL_INFEASIBLE: the GPU's final xi is a certificate — xi in K,
+    c^T xi < 0, |A xi| <= tol (-c^T xi) — and tau = 0 < kappa, as on the oracle."""
+    prob, gpu, _ = solvers(name, tol=1e-4, max_iters=5000)
+    gpu.set_iterate(np.zeros(prob.n), np.zeros(prob.m), np.zeros(prob.n), None, 1.0, 0.0, 0)
+    info = gpu.iterate(5000)
+    assert info["status_name"] == "DUAL_INFEASIBLE", info
+    g = gpu.get_iterate()
+    cx = prob.c @ g["xi"]
+    assert cx < 0 and np.linalg.norm(prob.A @ g["xi"]) <= 1e-4 * (-cx)
+    assert g["tau"] == 0.0 and g["kappa"] > 0.0
+    N = prob.psd_dims[0]
+    X = np.zeros((N, N))
+    q = 0
+    for j in range(N):
+        for i in range(j + 1):
+            X[i, j] = X[j, i] = g["xi"][1 + q] / (1.0 if i == j else np.sqrt(2.0))
+            q += 1
+    assert np.linalg.eigvalsh(X).min() >= -1e-10 * np.abs(X).max()
+
+
+def test_nonfinite_iterate_reported():
+    """a non-finite iterate stops the solve with E_NONFINITE naming the iteration; the
+    error is latched (every later call returns it)."""
+    from paper_1708_04174_b200 import SosAdmm
+
+    prob = make_config("pop6")
+    gpu = SosAdmm.from_problem(prob, tol=1e-4, max_iters=100)
+    try:
+        xi = np.zeros(prob.n)
+        xi[5] = np.nan
+        gpu.set_iterate(xi, np.zeros(prob.m), np.zeros(prob.n), None, 1.0, 0.0, 0)
+        with pytest.raises(RuntimeError, match="non-finite"):
+            gpu.iterate(10)
+        with pytest.raises(RuntimeError, match="non-finite"):
+            gpu.iterate(1)
+    finally:
+        gpu.close()

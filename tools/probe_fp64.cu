@@ -92,7 +92,7 @@ int main() {
     CK(cudaEventSynchronize(e1));
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
-    double flops = 2.0 * 512.0 * 32.0 * (double)iters * blocks * wpb;  // 32 mma per iter per warp
+    double flops = 512.0 * 32.0 * (double)iters * blocks * wpb;  // 32 mma per iter per warp, 512 flop each
     printf("DMMA m8n8k4: warps/block=%d blocks=%d  %.3f ms  %.2f TFLOP/s\n", wpb, blocks, ms, flops / ms / 1e9);
   }
   for (int tpb : {256, 512}) {
