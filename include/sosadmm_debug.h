@@ -8,6 +8,7 @@
 #ifndef SOSADMM_DEBUG_H
 #define SOSADMM_DEBUG_H
 #include <stdint.h>
+#include "sosadmm.h"
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -23,6 +24,35 @@ int sosadmm_debug_spdinv(int t, double* K);
 /* Timing probe of the tridiagonalisation: prof ((N-2) x 16 clock64 stamp slots of CTA 0 at the phase
  * boundaries of every Householder step), ms = CUDA-event time of one launch after a warm-up. */
 int sosadmm_debug_tridiag_prof(int N, const double* A, long long* prof, float* ms);
+/* Two-stage tridiagonalisation, stage 1 (dense -> band, sy2sb.cuh): band (N x 2BW, column c at
+ * band[c 2BW + (r - c)], offsets 0..BW), V1 (N x N, reflector k in column k: zeros in rows k+1..k+BW-1,
+ * 1 at row k+BW), tau1 (N); *bw = BW, *nref = number of reflector columns.  -2 if N is outside the
+ * two-stage envelope. */
+int sosadmm_debug_sy2sb(int N, const double* A, double* band, double* V1, double* tau1, int* bw, int* nref);
+/* Stage 2 (band -> tridiagonal, sb2st.cuh) of a band in the layout above: d (N), e (N-1), the
+ * reflectors V2 (N x KMAX x BW: sweep i, task k at (i KMAX + k) BW) and tau2 (N x KMAX); *kmax = KMAX. */
+int sosadmm_debug_sb2st(int N, int BW, const double* band, double* d, double* e, double* V2, double* tau2,
+                        int* kmax);
+/* Z (N x r, column-major) <- Q2 Z with the stage-2 reflectors (bt2.cuh). */
+int sosadmm_debug_bt2(int N, int BW, const double* V2, const double* tau2, int r, double* Z);
+/* Both stages on A (the production path): d, e; *ms = CUDA-event time of one run after a warm-up. */
+int sosadmm_debug_tridiag2(int N, const double* A, double* d, double* e, float* ms);
+/* Two-stage timing (CUDA events, second of two runs): stage 1 and stage 2 milliseconds; optional clock64
+ * stamps: prof1 (16 per panel: panel CTA 0..7, worker 0 8..15), prof2 (per task of sweep 0). */
+int sosadmm_debug_ts_timing(int N, const double* A, float* ms1, float* ms2, long long* prof1, long long* prof2);
+/* Large-block projection stages of A: tridiagonal (d, e), D&C eigenvalues lam, sel = [r, c0, side]. */
+int sosadmm_debug_psd_stages(int N, const double* A, double* d, double* e, double* lam, int* sel);
+/* One-GPU emulation of a block-sharded solve (the world >= 2 arithmetic of sosadmm_setup_sharded without
+ * NCCL): each rank's context is set up with sosadmm_debug_setup_emulated (same arguments as
+ * sosadmm_setup_sharded minus the id, world <= 8, all on one device); sosadmm_debug_group_iterate runs k
+ * iterations of all ranks, summing the 2m + 3 partial sums with a device add in rank order where the
+ * product path calls ncclAllReduce; sosadmm_debug_group_get_iterate assembles the owned columns.
+ * ctx[r] must be the rank-r context.  Returns a sosadmm_err. */
+int sosadmm_debug_setup_emulated(const sosadmm_problem* prob, const sosadmm_settings* settings, int32_t rank,
+                                 int32_t world, const int32_t* block_owner, sosadmm_ctx** out);
+int sosadmm_debug_group_iterate(sosadmm_ctx* const* ctx, int world, int64_t k);
+int sosadmm_debug_group_get_iterate(sosadmm_ctx* const* ctx, int world, double* xi, double* y, double* z, double* s,
+                                    double* tau, double* kappa, int64_t* iter);
 #ifdef __cplusplus
 }
 #endif

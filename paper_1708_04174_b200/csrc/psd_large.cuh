@@ -18,16 +18,15 @@
 #include "dc.cuh"
 #include "gemm_f64.cuh"
 #include "tridiag.cuh"
-#include "tridiag_blk.cuh"
 #include "backtransform.cuh"
+#include "sy2sb.cuh"
+#include "sb2st.cuh"
+#include "bt2.cuh"
 
 struct LargeBlock {
   int b = 0, N = 0, C = 1, D = 0;
   long long smem_cols = 0;
   size_t trd_smem = 0;
-  bool blk = true;            // blocked tridiagonalisation with DMMA panel updates (tridiag_blk.cuh)
-  size_t blk_smem = 0;
-  long long blk_rows = 0;
   int ksw = 0;                // first step done by the single-CTA tail (N - 2: no tail)
   size_t tail_smem = 0;
   TridiagArgs ta_tail{};
@@ -44,6 +43,13 @@ struct LargeBlock {
   int recon = 0;              // index of the reconstruction descriptor in gdesc
   double* W = nullptr;
   TridiagArgs ta{};
+  // two-stage tridiagonalisation (sy2sb.cuh -> sb2st.cuh, back-transform bt2.cuh then the WY blocks)
+  bool two = false;
+  int BW = 16, KMAX = 1, nref = 0;
+  size_t sy_smem = 0, st_smem = 0, bt2_smem_b = 0;
+  Sy2sbArgs sa{};
+  double *V2 = nullptr, *tau2 = nullptr, *Bg = nullptr;
+  unsigned* cnt = nullptr;
 };
 
 struct LargeEig {
@@ -130,6 +136,25 @@ inline void dc_build_tree(int N, std::vector<DcNode>& nodes, std::vector<int>& l
 }
 
 constexpr int TRD_MAX_DYN_SMEM = 227 * 1024 - 2048;  // leaves room for the static tables
+constexpr int DYN_SMEM_MAX = 232448;                  // sm_100a opt-in maximum per block
+
+// Two-stage sizes: band half-width (the stage-2 band of 2 BW diagonals must fit one SM: BW = 16 up to
+// N = 880, BW = 8 above), workers (8-row blocks, at most 147 so the grid fits 148 SMs at one CTA each).
+inline int ts_bw(int N) { return sb2st_smem(N, 16) <= (size_t)DYN_SMEM_MAX ? 16 : 8; }
+inline int ts_workers(int N) { return std::min(147, (N + SB_R - 1) / SB_R); }
+inline int ts_maxrb(int N) {
+  const int nrb = (N + SB_R - 1) / SB_R, nw = ts_workers(N);
+  return (nrb + nw - 1) / nw;
+}
+// Default: the one-cluster kernel k_tridiag.  The two-stage reduction (sy2sb -> sb2st -> bt2) is selected
+// with SOSADMM_TRIDIAG=twostage: it is correct and tested (tests/test_gpu_stages.py) but measured slower on
+// B200 at every config size (N = 861: stage 1 2.8 ms + stage 2 4.4 ms vs 4.5 ms; DESIGN.md §5 has the
+// per-phase profile and why: stage 2 is issue / shared-memory bound on one SM with a 2N-task critical
+// path, stage 1 pays three global hand-offs per 16-column panel).
+inline bool ts_enabled() {
+  const char* env = getenv("SOSADMM_TRIDIAG");
+  return env && std::string(env) == "twostage";
+}
 
 // Cluster size: 16 CTAs (the non-portable maximum) from N = 161 on — measured faster than 8 at
 // N = 231 (0.62 -> 0.56 ms) and N = 325 (1.07 -> 0.93 ms): the per-step fixed cost barely depends on
@@ -184,7 +209,7 @@ inline size_t large_carve(const std::vector<int>& blk_N, const std::vector<int>&
     int D, leaf0, nleaves;
     dc_build_tree(N, nodes, l0, lnn, lmax, D, leaf0, nleaves, p2n);
     const size_t NN = (size_t)N * N;
-    char* p[32];
+    char* p[64];  // (42 buffers per block)
     int q = 0;
     p[q++] = take(8 * N);                 // d
     p[q++] = take(8 * N);                 // e
@@ -208,9 +233,20 @@ inline size_t large_carve(const std::vector<int>& blk_N, const std::vector<int>&
     p[q++] = take(sizeof(GemmDesc) * (nodes.size() + 1));
     p[q++] = take(4 * 8);                 // sel [r, c0, side] + the D&C root selection (topsel)
     p[q++] = take(8 * ((size_t)3 * N + 2));  // tridiagonalisation hand-over state
-    p[q++] = take(8 * (size_t)2 * N * TRB_NB);  // blocked tridiagonalisation panels Vg, Wg
     p[q++] = take(8 * (size_t)BTW_NB * BTW_NB * ((N - 2 + BTW_NB - 1) / BTW_NB));  // Twy
     p[q++] = take(8 * (size_t)BTW_NB * BTW_NB * ((N - 2 + BTW_NB - 1) / BTW_NB) * bt_gram_chunks(N));  // Gwy
+    {  // two-stage buffers
+      const int BW = ts_bw(N), ldv = sy2sb_ldv(N), KM = sb2st_kmax(N, BW);
+      p[q++] = take(8 * (size_t)N * 2 * BW);            // Bg (band)
+      p[q++] = take(8 * (size_t)BW * N);                // Pg (panel slice, row-major)
+      p[q++] = take(8 * (size_t)2 * BW * ldv);          // Vg
+      p[q++] = take(8 * (size_t)2 * BW * ldv);          // Yg
+      p[q++] = take(8 * (size_t)3 * BW * BW);           // Tg (2), Sg
+      p[q++] = take(8 * (size_t)ts_workers(N) * BW * BW);  // Pt
+      p[q++] = take(64);                                // counters
+      p[q++] = take(8 * (size_t)N * KM * BW);           // V2
+      p[q++] = take(8 * (size_t)N * KM);                // tau2
+    }
     per_block(b, N, p, nodes, l0, lnn, lmax, D, leaf0, nleaves, p2n);
   }
   return used + 256;
@@ -239,16 +275,6 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     lb.C = tridiag_cluster_size(N);
     lb.smem_cols = tridiag_row_budget(N, lb.C);
     lb.trd_smem = tridiag_smem_bytes(N, lb.C, (N + lb.C - 1) / lb.C, lb.smem_cols);
-    {
-      const char* env = getenv("SOSADMM_TRIDIAG");
-      lb.blk = env && std::string(env) == "blocked";  // default: fused update+symv (faster at N <= ~900, measured)
-      const int S = (N + lb.C - 1) / lb.C;
-      const long long fixed = trb_fixed_doubles(N, lb.C, S, TRB_NB);
-      long long need = 0;
-      for (int c = 0; c < lb.C; ++c) need = std::max(need, tridiag_rows_need(N, lb.C, c, 0));
-      lb.blk_rows = std::min(need, (long long)TRD_MAX_DYN_SMEM / 8 - fixed);
-      lb.blk_smem = sizeof(double) * (size_t)(fixed + lb.blk_rows);
-    }
     {
       const int nt = tridiag_tail_rows(N);
       lb.ksw = (nt >= 16 && N - nt > 8) ? N - nt : N - 2;
@@ -298,7 +324,6 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     dc.topsel = lb.sel + 4;
     dc.topsel_on = 1;
     double* hand = (double*)p[q++];
-    double* vwg = (double*)p[q++];
     lb.Twy = (double*)p[q++];
     lb.Gwy = (double*)p[q++];
     lb.recon = (int)nodes.size();
@@ -378,13 +403,50 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     ta.kb = 0;
     ta.ke = lb.ksw;
     ta.hand = hand;
-    ta.Vg = vwg;
-    ta.Wg = vwg + (size_t)N * TRB_NB;
     lb.ta_tail = ta;
     lb.ta_tail.C = 1;
     lb.ta_tail.kb = lb.ksw;
     lb.ta_tail.ke = N - 2;
     lb.ta_tail.smem_rows_doubles = tridiag_rows_need(N, 1, 0, lb.ksw) + 15LL * (N - lb.ksw);
+    lb.nref = N - 2;
+    lb.two = ts_enabled();
+    {
+      const int BW = ts_bw(N), ldv = sy2sb_ldv(N);
+      lb.BW = BW;
+      lb.KMAX = sb2st_kmax(N, BW);
+      Sy2sbArgs& sa = lb.sa;
+      sa.M = lb.M;
+      sa.N = N;
+      sa.BW = BW;
+      sa.NW = ts_workers(N);
+      sa.maxrb = ts_maxrb(N);
+      sa.ldr = sy2sb_ldr(N);
+      sa.P = sy2sb_panels(N, BW);
+      sa.Bg = (double*)p[q++];
+      sa.V1 = lb.V;
+      sa.tau1 = lb.tau;
+      sa.Pg = (double*)p[q++];
+      sa.Vg = (double*)p[q++];
+      sa.Yg = (double*)p[q++];
+      sa.ldv = ldv;
+      sa.Tg = (double*)p[q++];
+      sa.Sg = sa.Tg + 2 * BW * BW;
+      sa.Pt = (double*)p[q++];
+      sa.cnt = (unsigned*)p[q++];
+      sa.st = st;
+      sa.is = is;
+      sa.check_state = 1;
+      lb.Bg = sa.Bg;
+      lb.cnt = sa.cnt;
+      lb.V2 = (double*)p[q++];
+      lb.tau2 = (double*)p[q++];
+      lb.sy_smem = std::max(sy2sb_worker_smem(N, BW, sa.maxrb), sy2sb_panel_smem(N, BW));
+      lb.st_smem = sb2st_smem(N, BW);
+      lb.bt2_smem_b = bt2_smem(N, BW, lb.KMAX);
+      if (lb.two) lb.nref = sa.P * BW;
+      if (lb.two && (lb.sy_smem > (size_t)DYN_SMEM_MAX || lb.st_smem > (size_t)DYN_SMEM_MAX || sa.maxrb > 4))
+        lb.two = false;  // outside the two-stage envelope (N > 1280): one-stage kernel
+    }
     le.blocks.push_back(lb);
   });
   le.side = side_p;
@@ -401,10 +463,8 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
   }
   if (!le.blocks.empty()) {
 #define TRD_PTR(MB, CCX) k_tridiag<MB, CCX>,
-#define TRB_PTR(MB, CCX) k_tridiag_blk<MB, CCX, TRB_NB>,
-    for (TridiagKernel kt : {TRD_KERNELS(TRD_PTR) TRB_KERNELS(TRB_PTR)}) {
+    for (TridiagKernel kt : {TRD_KERNELS(TRD_PTR)}) {
 #undef TRD_PTR
-#undef TRB_PTR
       if (err == cudaSuccess) err = cudaFuncSetAttribute(kt, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (err == cudaSuccess)
         err = cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, TRD_MAX_DYN_SMEM);
@@ -412,6 +472,14 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     if (err == cudaSuccess)
       err = cudaFuncSetAttribute(k_bt_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)bt_apply_smem_bytes(DC_MAXN));
+    for (int bw : {8, 16}) {
+      if (err == cudaSuccess)
+        err = cudaFuncSetAttribute(sy2sb_kernel(bw), cudaFuncAttributeMaxDynamicSharedMemorySize, DYN_SMEM_MAX);
+      if (err == cudaSuccess)
+        err = cudaFuncSetAttribute(sb2st_kernel(bw), cudaFuncAttributeMaxDynamicSharedMemorySize, DYN_SMEM_MAX);
+      if (err == cudaSuccess)
+        err = cudaFuncSetAttribute(bt2_kernel(bw), cudaFuncAttributeMaxDynamicSharedMemorySize, DYN_SMEM_MAX);
+    }
     if (err != cudaSuccess) {
       msg = std::string("k_tridiag attributes: ") + cudaGetErrorString(err);
       return 1;
@@ -420,7 +488,32 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
   return 0;
 }
 
+// Two-stage reduction: stage 1 (dense -> band) as one cooperative persistent grid, stage 2 (band ->
+// tridiagonal) on one SM.  The hand-off counters are zeroed in the same stream first.
+inline void large_block_tridiag2(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool check) {
+  (void)le;
+  lb.sa.check_state = check;
+  cudaMemsetAsync(lb.cnt, 0, 16, s);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(lb.sa.NW + 1, 1, 1);
+  cfg.blockDim = dim3(SB_NT, 1, 1);
+  cfg.dynamicSmemBytes = lb.sy_smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, sy2sb_kernel(lb.BW), lb.sa);
+  sb2st_kernel(lb.BW)<<<1, ST_NT, lb.st_smem, s>>>(lb.Bg, lb.N, lb.d, lb.e, lb.V2, lb.tau2, le.st, le.is, check,
+                                                    nullptr);
+}
+
 inline void large_block_tridiag(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool check) {
+  if (lb.two) {
+    large_block_tridiag2(le, lb, s, check);
+    return;
+  }
   lb.ta.check_state = check;
   lb.ta_tail.check_state = check;
   lb.ta_tail.prof = lb.ta.prof;
@@ -428,7 +521,7 @@ inline void large_block_tridiag(LargeEig& le, LargeBlock& lb, cudaStream_t s, bo
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(lb.C, 1, 1);
     cfg.blockDim = dim3(TRD_NT, 1, 1);
-    cfg.dynamicSmemBytes = lb.blk ? lb.blk_smem : lb.trd_smem;
+    cfg.dynamicSmemBytes = lb.trd_smem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -437,12 +530,6 @@ inline void large_block_tridiag(LargeEig& le, LargeBlock& lb, cudaStream_t s, bo
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (lb.blk) {
-      TridiagArgs tb = lb.ta;
-      tb.smem_rows_doubles = lb.blk_rows;
-      cudaLaunchKernelEx(&cfg, tridiag_blk_kernel_mc(tridiag_maxb(lb.N), lb.C), tb);
-      return;
-    }
     cudaLaunchKernelEx(&cfg, tridiag_kernel_mc(tridiag_maxb(lb.N), lb.C), lb.ta);
   }
   if (lb.ksw < lb.N - 2)
@@ -496,7 +583,7 @@ inline void large_block_dc(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool ch
 
 // compact-WY T factors of the reflector blocks (depend on the tridiagonalisation only)
 inline void large_block_wy(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool check) {
-  const int N = lb.N, nref = N - 2;
+  const int N = lb.N, nref = lb.nref;
   const int nbw = (nref + BTW_NB - 1) / BTW_NB;
   k_bt_gram<<<dim3(nbw, bt_gram_chunks(N)), BTW_NT, 0, s>>>(lb.V, lb.Gwy, N, nref, le.st, le.is, check);
   k_bt_larft<<<nbw, BTW_NT, 0, s>>>(lb.Gwy, bt_gram_chunks(N), lb.tau, lb.Twy, nref, le.st, le.is, check);
@@ -505,9 +592,12 @@ inline void large_block_wy(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool ch
 inline void large_block_recon(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool check, bool with_wy = true) {
   const int N = lb.N;
   const int fb = lb.D & 1;
-  const int nref = N - 2;
+  const int nref = lb.nref;
   k_select<<<1, 256, 0, s>>>(lb.dc.lam[fb], lb.sel, le.side, lb.b, N, le.st, le.is, check);
   if (with_wy) large_block_wy(le, lb, s, check);
+  if (lb.two)  // Z_r <- Q2 Z_r (stage-2 reflectors), in place on the selected columns
+    bt2_kernel(lb.BW)<<<(N / 2 + BT2_NC) / BT2_NC, BT2_NT, lb.bt2_smem_b, s>>>(
+        lb.dc.Q[fb], lb.sel, lb.V2, lb.tau2, N, lb.KMAX, le.st, le.is, check);
   {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(BTC_P * ((N / 2 + BTW_NC - 1) / BTW_NC), 1, 1);
@@ -572,7 +662,8 @@ inline void large_eig_launch_concurrent(LargeEig& le, cudaStream_t s, bool check
 
 inline int large_eig_launches(const LargeEig& le) {
   int k = 0;
-  for (const auto& lb : le.blocks) k += (!lb.blk && lb.ksw < lb.N - 2 ? 2 : 1) + 2 + 1 + 7 * lb.D + 1 + 5;
+  for (const auto& lb : le.blocks)
+    k += (lb.two ? 3 : (lb.ksw < lb.N - 2 ? 2 : 1)) + 2 + 1 + 7 * lb.D + 1 + 5 + (lb.two ? 1 : 0);
   return k;
 }
 

@@ -63,6 +63,12 @@ struct ShardSpec {
   int rank = 0, world = 1;
   const int32_t* block_owner = nullptr;  // nullptr: every block on this rank
   bool sharded = false;                  // true: NCCL partial-sum allreduce in the loop
+  bool emulated = false;                 // debug: no communicator; sosadmm_debug_group_iterate sums on one GPU
+};
+
+struct GroupBufs {
+  double* buf[8];
+  int world;
 };
 
 struct Arena {
@@ -492,21 +498,32 @@ void launch_rowupdate(const AffineArgs& a, cudaStream_t s, int write_state) {
     k_rowupdate<<<(a.m + 255) / 256, 256, 0, s>>>(a, write_state);
 }
 
-sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev) {
+// phase (sharded mode only): 0 = the whole iteration with the NCCL allreduce inside; 1 = up to the
+// collective (the 2m + 3 partial sums in sh.buf); 2 = from the completed sums on.  Phases 1 / 2 are the
+// one-GPU emulation of several ranks (sosadmm_debug_group_iterate), which sums sh.buf itself.
+sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev, int phase = 0) {
   AffineArgs& a = c->aa;
   cudaStream_t s = c->stream;
   const int tlw = std::max(1, (a.tl * 32 + 255) / 256);
   if (ev) cudaEventRecord(ev[0], s);
   if (c->sp.sharded) {
-    k_lowdual_part<<<c->nb_low, SH_NT, 0, s>>>(a, c->sh);
-    k_gather_part<<<c->gather_blocks, SH_NT, 0, s>>>(a, c->sh);
-    k_shard_scalars<<<1, SH_NT, 0, s>>>(a, c->sh, c->gather_blocks, c->nb_low);
-    const ncclResult_t nr = nccl().allReduce(c->sh.buf, c->sh.buf, 2 * (size_t)a.m + 3, ncclFloat64, ncclSum,
-                                             c->comm, s);
-    if (nr != ncclSuccess) {
-      c->err = SOSADMM_E_NCCL;
-      c->msg = std::string("ncclAllReduce: ") + nccl().getErrorString(nr);
+    if (c->sp.emulated && phase == 0) {
+      c->err = SOSADMM_E_ARG;
+      c->msg = "an emulated sharded context iterates only through sosadmm_debug_group_iterate";
       return c->err;
+    }
+    if (phase != 2) {
+      k_lowdual_part<<<c->nb_low, SH_NT, 0, s>>>(a, c->sh);
+      k_gather_part<<<c->gather_blocks, SH_NT, 0, s>>>(a, c->sh);
+      k_shard_scalars<<<1, SH_NT, 0, s>>>(a, c->sh, c->gather_blocks, c->nb_low);
+      if (phase == 1) return SOSADMM_OK;
+      const ncclResult_t nr = nccl().allReduce(c->sh.buf, c->sh.buf, 2 * (size_t)a.m + 3, ncclFloat64, ncclSum,
+                                               c->comm, s);
+      if (nr != ncclSuccess) {
+        c->err = SOSADMM_E_NCCL;
+        c->msg = std::string("ncclAllReduce: ") + nccl().getErrorString(nr);
+        return c->err;
+      }
     }
     k_gather_fin<<<c->gather_blocks, GATHER_NT, 0, s>>>(a, c->sh);
   } else {
@@ -618,7 +635,7 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
     c->device = settings->device;
   }
   CK_CTX(c, cudaSetDevice(c->device));
-  if (sp.sharded) {
+  if (sp.sharded && !sp.emulated) {
     if (!nccl().ok) {
       c->err = SOSADMM_E_NCCL;
       c->msg = "libnccl.so.2 could not be loaded";
@@ -1265,6 +1282,7 @@ extern "C" int sosadmm_debug_tridiag(int N, const double* A, double* d, double* 
   int rc = dl.init(N);
   if (rc) return rc;
   LargeBlock& lb = dl.le.blocks[0];
+  lb.two = false;  // the one-cluster BLAS-2 kernel (k_tridiag)
   cudaMemcpyAsync(lb.M, A, 8ull * N * N, cudaMemcpyHostToDevice, dl.s);
   cudaMemsetAsync(lb.V, 0, 8ull * N * N, dl.s);
   large_block_tridiag(dl.le, lb, dl.s, false);
@@ -1345,4 +1363,263 @@ extern "C" int sosadmm_debug_tridiag_prof(int N, const double* A, long long* pro
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   return err == cudaSuccess ? 0 : -4;
+}
+
+// ---- two-stage tridiagonalisation stages (sy2sb.cuh, sb2st.cuh, bt2.cuh) ----
+// The stage entry points run the two-stage path whatever SOSADMM_TRIDIAG says (when N is inside its envelope).
+static bool ts_force(LargeBlock& lb) {
+  const bool fits = lb.sy_smem <= (size_t)DYN_SMEM_MAX && lb.st_smem <= (size_t)DYN_SMEM_MAX && lb.sa.maxrb <= 4;
+  if (!fits) return false;
+  lb.two = true;
+  lb.nref = lb.sa.P * lb.BW;
+  return true;
+}
+extern "C" int sosadmm_debug_sy2sb(int N, const double* A, double* band, double* V1, double* tau1, int* bw,
+                                   int* nref) {
+  if (N < 3) return -1;
+  DebugLarge dl;
+  int rc = dl.init(N);
+  if (rc) return rc;
+  LargeBlock& lb = dl.le.blocks[0];
+  if (!ts_force(lb)) return -2;
+  cudaMemcpyAsync(lb.M, A, 8ull * N * N, cudaMemcpyHostToDevice, dl.s);
+  cudaMemsetAsync(lb.V, 0, 8ull * N * N, dl.s);
+  cudaMemsetAsync(lb.tau, 0, 8ull * N, dl.s);
+  cudaMemsetAsync(lb.Bg, 0, 8ull * N * 2 * lb.BW, dl.s);
+  lb.sa.check_state = 0;
+  cudaMemsetAsync(lb.cnt, 0, 16, dl.s);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(lb.sa.NW + 1, 1, 1);
+  cfg.blockDim = dim3(SB_NT, 1, 1);
+  cfg.dynamicSmemBytes = lb.sy_smem;
+  cfg.stream = dl.s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, sy2sb_kernel(lb.BW), lb.sa) != cudaSuccess) return -4;
+  if (cudaStreamSynchronize(dl.s) != cudaSuccess) return -4;
+  cudaMemcpy(band, lb.Bg, 8ull * N * 2 * lb.BW, cudaMemcpyDeviceToHost);
+  cudaMemcpy(V1, lb.V, 8ull * N * N, cudaMemcpyDeviceToHost);
+  cudaMemcpy(tau1, lb.tau, 8ull * N, cudaMemcpyDeviceToHost);
+  *bw = lb.BW;
+  *nref = lb.nref;
+  return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
+extern "C" int sosadmm_debug_sb2st(int N, int BW, const double* band, double* d, double* e, double* V2,
+                                   double* tau2, int* kmax) {
+  if (N < 3) return -1;
+  DebugLarge dl;
+  int rc = dl.init(N);
+  if (rc) return rc;
+  LargeBlock& lb = dl.le.blocks[0];
+  if (!ts_force(lb) || lb.BW != BW) return -2;
+  cudaMemcpyAsync(lb.Bg, band, 8ull * N * 2 * BW, cudaMemcpyHostToDevice, dl.s);
+  sb2st_kernel(BW)<<<1, ST_NT, lb.st_smem, dl.s>>>(lb.Bg, N, lb.d, lb.e, lb.V2, lb.tau2, lb.sa.st, lb.sa.is, 0,
+                                                   nullptr);
+  if (cudaStreamSynchronize(dl.s) != cudaSuccess) return -4;
+  cudaMemcpy(d, lb.d, 8ull * N, cudaMemcpyDeviceToHost);
+  cudaMemcpy(e, lb.e, 8ull * (N - 1), cudaMemcpyDeviceToHost);
+  cudaMemcpy(V2, lb.V2, 8ull * N * lb.KMAX * BW, cudaMemcpyDeviceToHost);
+  cudaMemcpy(tau2, lb.tau2, 8ull * N * lb.KMAX, cudaMemcpyDeviceToHost);
+  *kmax = lb.KMAX;
+  return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
+extern "C" int sosadmm_debug_bt2(int N, int BW, const double* V2, const double* tau2, int r, double* Z) {
+  if (N < 3 || r < 0 || r > N) return -1;
+  DebugLarge dl;
+  int rc = dl.init(N);
+  if (rc) return rc;
+  LargeBlock& lb = dl.le.blocks[0];
+  if (!ts_force(lb) || lb.BW != BW) return -2;
+  const int fb = lb.D & 1;
+  cudaMemcpyAsync(lb.V2, V2, 8ull * N * lb.KMAX * BW, cudaMemcpyHostToDevice, dl.s);
+  cudaMemcpyAsync(lb.tau2, tau2, 8ull * N * lb.KMAX, cudaMemcpyHostToDevice, dl.s);
+  cudaMemcpyAsync(lb.dc.Q[fb], Z, 8ull * N * r, cudaMemcpyHostToDevice, dl.s);
+  const int sel[3] = {r, 0, 0};
+  cudaMemcpyAsync(lb.sel, sel, sizeof(sel), cudaMemcpyHostToDevice, dl.s);
+  bt2_kernel(BW)<<<(r + BT2_NC - 1) / BT2_NC + 1, BT2_NT, lb.bt2_smem_b, dl.s>>>(
+      lb.dc.Q[fb], lb.sel, lb.V2, lb.tau2, N, lb.KMAX, lb.sa.st, lb.sa.is, 0);
+  if (cudaStreamSynchronize(dl.s) != cudaSuccess) return -4;
+  cudaMemcpy(Z, lb.dc.Q[fb], 8ull * N * r, cudaMemcpyDeviceToHost);
+  return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
+extern "C" int sosadmm_debug_tridiag2(int N, const double* A, double* d, double* e, float* ms) {
+  if (N < 3) return -1;
+  DebugLarge dl;
+  int rc = dl.init(N);
+  if (rc) return rc;
+  LargeBlock& lb = dl.le.blocks[0];
+  if (!ts_force(lb)) return -2;
+  cudaMemcpyAsync(lb.M, A, 8ull * N * N, cudaMemcpyHostToDevice, dl.s);
+  large_block_tridiag(dl.le, lb, dl.s, false);  // warm-up
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, dl.s);
+  large_block_tridiag(dl.le, lb, dl.s, false);
+  cudaEventRecord(e1, dl.s);
+  if (cudaStreamSynchronize(dl.s) != cudaSuccess) return -4;
+  if (ms) cudaEventElapsedTime(ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaMemcpy(d, lb.d, 8ull * N, cudaMemcpyDeviceToHost);
+  cudaMemcpy(e, lb.e, 8ull * (N - 1), cudaMemcpyDeviceToHost);
+  return cudaGetLastError() == cudaSuccess ? 0 : -4;
+}
+
+// ---- one-GPU emulation of a block-sharded solve (tests of the world >= 2 arithmetic) ----
+__global__ void k_group_sum(GroupBufs g, int len) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= len) return;
+  double s = 0.0;
+  for (int r = 0; r < g.world; ++r) s += g.buf[r][i];  // rank order (NCCL's order may differ)
+  for (int r = 0; r < g.world; ++r) g.buf[r][i] = s;
+}
+
+extern "C" int sosadmm_debug_setup_emulated(const sosadmm_problem* prob, const sosadmm_settings* settings,
+                                            int32_t rank, int32_t world, const int32_t* block_owner,
+                                            sosadmm_ctx** out) {
+  if (!out) return SOSADMM_E_ARG;
+  if (world < 1 || world > 8 || rank < 0 || rank >= world || !block_owner) {
+    *out = nullptr;
+    return SOSADMM_E_ARG;
+  }
+  ShardSpec sp;
+  sp.rank = rank;
+  sp.world = world;
+  sp.block_owner = block_owner;
+  sp.sharded = true;
+  sp.emulated = true;
+  return setup_impl(prob, settings, sp, nullptr, out);
+}
+
+extern "C" int sosadmm_debug_group_iterate(sosadmm_ctx* const* ctx, int world, int64_t k) {
+  if (!ctx || world < 1 || world > 8) return SOSADMM_E_ARG;
+  for (int r = 0; r < world; ++r)
+    if (!ctx[r] || ctx[r]->err || !ctx[r]->sp.emulated || ctx[r]->sp.world != world || ctx[r]->sp.rank != r)
+      return SOSADMM_E_ARG;
+  GroupBufs g{};
+  g.world = world;
+  for (int r = 0; r < world; ++r) g.buf[r] = ctx[r]->sh.buf;
+  const int len = 2 * ctx[0]->aa.m + 3;
+  for (int64_t it = 0; it < k; ++it) {
+    for (int r = 0; r < world; ++r)
+      if (launch_iteration(ctx[r], 1, nullptr, 1)) return ctx[r]->err;
+    for (int r = 0; r < world; ++r)
+      if (cudaStreamSynchronize(ctx[r]->stream) != cudaSuccess) return SOSADMM_E_CUDA;
+    k_group_sum<<<(len + 255) / 256, 256, 0, ctx[0]->stream>>>(g, len);
+    if (cudaStreamSynchronize(ctx[0]->stream) != cudaSuccess) return SOSADMM_E_CUDA;
+    for (int r = 0; r < world; ++r)
+      if (launch_iteration(ctx[r], 1, nullptr, 2)) return ctx[r]->err;
+    for (int r = 0; r < world; ++r)
+      if (cudaStreamSynchronize(ctx[r]->stream) != cudaSuccess) return SOSADMM_E_CUDA;
+  }
+  return SOSADMM_OK;
+}
+
+// Full iterate of an emulated group: each column from its owner rank (free columns: rank 0), the
+// replicated m-vectors and scalars from rank 0.
+extern "C" int sosadmm_debug_group_get_iterate(sosadmm_ctx* const* ctx, int world, double* xi, double* y, double* z,
+                                               double* s, double* tau, double* kappa, int64_t* iter) {
+  if (!ctx || world < 1 || world > 8) return SOSADMM_E_ARG;
+  const int n = ctx[0]->aa.n, m = ctx[0]->aa.m;
+  std::vector<double> lx(n), lz(n);
+  std::vector<int> own(n);
+  for (int r = 0; r < world; ++r) {
+    sosadmm_ctx* c = ctx[r];
+    if (cudaMemcpy(lx.data(), c->aa.xi, sizeof(double) * n, cudaMemcpyDeviceToHost) ||
+        cudaMemcpy(lz.data(), c->aa.z, sizeof(double) * n, cudaMemcpyDeviceToHost) ||
+        cudaMemcpy(own.data(), c->sh.colown, sizeof(int) * n, cudaMemcpyDeviceToHost))
+      return SOSADMM_E_CUDA;
+    for (int j = 0; j < n; ++j)
+      if (own[j]) {
+        if (xi) xi[j] = lx[j];
+        if (z) z[j] = lz[j];
+      }
+  }
+  sosadmm_ctx* c = ctx[0];
+  if (y && cudaMemcpy(y, c->aa.y, sizeof(double) * m, cudaMemcpyDeviceToHost)) return SOSADMM_E_CUDA;
+  if (s && cudaMemcpy(s, c->aa.s, sizeof(double) * m, cudaMemcpyDeviceToHost)) return SOSADMM_E_CUDA;
+  DevState st;
+  if (cudaMemcpy(&st, c->aa.st, sizeof(DevState), cudaMemcpyDeviceToHost)) return SOSADMM_E_CUDA;
+  if (tau) *tau = st.tau;
+  if (kappa) *kappa = st.kappa;
+  if (iter) *iter = st.iter;
+  return SOSADMM_OK;
+}
+
+// Per-stage timing of the two-stage reduction (CUDA events, second of two runs): stage 1, stage 2.
+extern "C" int sosadmm_debug_ts_timing(int N, const double* A, float* ms1, float* ms2, long long* prof1,
+                                       long long* prof2) {
+  if (N < 3) return -1;
+  DebugLarge dl;
+  int rc = dl.init(N);
+  if (rc) return rc;
+  LargeBlock& lb = dl.le.blocks[0];
+  if (!ts_force(lb)) return -2;
+  long long *dp1 = nullptr, *dp2 = nullptr;
+  const size_t n1 = 16 * (size_t)(lb.sa.P + 1), n2 = 4 * (size_t)lb.KMAX;
+  if (prof1 && cudaMalloc(&dp1, 8 * n1)) return -7;
+  if (prof2 && cudaMalloc(&dp2, 8 * n2)) return -7;
+  if (dp1) cudaMemset(dp1, 0, 8 * n1);
+  lb.sa.prof = dp1;
+  cudaMemcpyAsync(lb.M, A, 8ull * N * N, cudaMemcpyHostToDevice, dl.s);
+  cudaEvent_t e[3];
+  for (auto& x : e) cudaEventCreate(&x);
+  for (int rep = 0; rep < 2; ++rep) {
+    lb.sa.check_state = 0;
+    cudaMemsetAsync(lb.cnt, 0, 16, dl.s);
+    cudaEventRecord(e[0], dl.s);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(lb.sa.NW + 1, 1, 1);
+    cfg.blockDim = dim3(SB_NT, 1, 1);
+    cfg.dynamicSmemBytes = lb.sy_smem;
+    cfg.stream = dl.s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, sy2sb_kernel(lb.BW), lb.sa);
+    cudaEventRecord(e[1], dl.s);
+    sb2st_kernel(lb.BW)<<<1, ST_NT, lb.st_smem, dl.s>>>(lb.Bg, N, lb.d, lb.e, lb.V2, lb.tau2, lb.sa.st, lb.sa.is, 0,
+                                                       dp2);
+    cudaEventRecord(e[2], dl.s);
+  }
+  if (cudaStreamSynchronize(dl.s) != cudaSuccess) return -4;
+  if (dp1) cudaMemcpy(prof1, dp1, 8 * n1, cudaMemcpyDeviceToHost);
+  if (dp2) cudaMemcpy(prof2, dp2, 8 * n2, cudaMemcpyDeviceToHost);
+  cudaFree(dp1);
+  cudaFree(dp2);
+  lb.sa.prof = nullptr;
+  cudaEventElapsedTime(ms1, e[0], e[1]);
+  cudaEventElapsedTime(ms2, e[1], e[2]);
+  for (auto& x : e) cudaEventDestroy(x);
+  return 0;
+}
+
+// Intermediate results of one large-block projection of A (debugging aid): d, e of the tridiagonal,
+// the D&C eigenvalues (ascending) and sel = [r, c0, side].
+extern "C" int sosadmm_debug_psd_stages(int N, const double* A, double* d, double* e, double* lam, int* sel) {
+  if (N < 3) return -1;
+  DebugLarge dl;
+  int rc = dl.init(N);
+  if (rc) return rc;
+  LargeBlock& lb = dl.le.blocks[0];
+  cudaMemcpyAsync(lb.M, A, 8ull * N * N, cudaMemcpyHostToDevice, dl.s);
+  large_block_tridiag(dl.le, lb, dl.s, false);
+  large_block_dc(dl.le, lb, dl.s, false);
+  large_block_recon(dl.le, lb, dl.s, false);
+  if (cudaStreamSynchronize(dl.s) != cudaSuccess) return -4;
+  const int fb = lb.D & 1;
+  cudaMemcpy(d, lb.d, 8ull * N, cudaMemcpyDeviceToHost);
+  cudaMemcpy(e, lb.e, 8ull * (N - 1), cudaMemcpyDeviceToHost);
+  cudaMemcpy(lam, lb.dc.lam[fb], 8ull * N, cudaMemcpyDeviceToHost);
+  cudaMemcpy(sel, lb.sel, 12, cudaMemcpyDeviceToHost);
+  return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }

@@ -53,7 +53,6 @@ struct TridiagArgs {
   long long* prof;   // optional (debug): clock64 stamps of CTA 0 per step and phase, 8 per step
   int kb, ke;        // Householder steps [kb, ke) done by this launch
   double* hand;      // 3 N + 2 doubles: head -> tail hand-over state
-  double *Vg, *Wg;   // k_tridiag_blk: N x NB panel buffers
 };
 
 __device__ __forceinline__ void trd_cluster_sync() {

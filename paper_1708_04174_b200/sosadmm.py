@@ -86,6 +86,14 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.sosadmm_strerror.argtypes = [ctypes.c_int]
     lib.sosadmm_strerror.restype = ctypes.c_char_p
     lib.sosadmm_last_error_message.argtypes = [V]
+    lib.sosadmm_debug_setup_emulated.argtypes = [ctypes.POINTER(_Problem), ctypes.POINTER(_Settings), I32, I32,
+                                                 ctypes.POINTER(I32), ctypes.POINTER(V)]
+    lib.sosadmm_debug_setup_emulated.restype = ctypes.c_int
+    lib.sosadmm_debug_group_iterate.argtypes = [ctypes.POINTER(V), ctypes.c_int, I64]
+    lib.sosadmm_debug_group_iterate.restype = ctypes.c_int
+    lib.sosadmm_debug_group_get_iterate.argtypes = [ctypes.POINTER(V), ctypes.c_int, P, P, P, P, P, P,
+                                                    ctypes.POINTER(I64)]
+    lib.sosadmm_debug_group_get_iterate.restype = ctypes.c_int
     lib.sosadmm_last_error_message.restype = ctypes.c_char_p
     for f in ["sosadmm_setup", "sosadmm_setup_sharded", "sosadmm_nccl_unique_id", "sosadmm_iterate", "sosadmm_iterate_profiled", "sosadmm_get_info",
               "sosadmm_get_iterate", "sosadmm_set_iterate", "sosadmm_get_structure", "sosadmm_project_affine",
@@ -160,12 +168,15 @@ class SosAdmm:
         else:
             rank, world, nccl_id, owner = shard
             self._owner = np.ascontiguousarray(owner, dtype=np.int32)
-            if len(self._owner) != len(self._dims) or len(nccl_id) != NCCL_ID_BYTES:
+            if len(self._owner) != len(self._dims) or (nccl_id is not None and len(nccl_id) != NCCL_ID_BYTES):
                 raise ValueError("shard: block_owner needs one entry per PSD block and a 128-byte NCCL id")
-            err = self.lib.sosadmm_setup_sharded(ctypes.byref(self._prob), ctypes.byref(st), bytes(nccl_id),
-                                                 int(rank), int(world),
-                                                 self._owner.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
-                                                 ctypes.byref(self._ctx))
+            own_p = self._owner.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+            if nccl_id is None:  # one-GPU emulation of rank `rank` (include/sosadmm_debug.h; tests only)
+                err = self.lib.sosadmm_debug_setup_emulated(ctypes.byref(self._prob), ctypes.byref(st), int(rank),
+                                                            int(world), own_p, ctypes.byref(self._ctx))
+            else:
+                err = self.lib.sosadmm_setup_sharded(ctypes.byref(self._prob), ctypes.byref(st), bytes(nccl_id),
+                                                     int(rank), int(world), own_p, ctypes.byref(self._ctx))
         self._check(err, "setup")
         self.workspace_bytes = int(nbytes)
 
@@ -283,3 +294,29 @@ def iterate_batch(solvers, k: int, chunk: int = 256) -> list:
             left[i] -= n
         active = [i for i in active if left[i] > 0 and solvers[i].info()["status"] == 0]
     return [s.info() for s in solvers]
+
+
+def group_iterate(solvers, k: int) -> None:
+    """k iterations of an emulated block-sharded group (solvers[r] = rank r, set up with shard=(r, world,
+    None, owner)): the world >= 2 arithmetic on one GPU, the partial sums added by a device kernel."""
+    lib = load_library()
+    arr = (ctypes.c_void_p * len(solvers))(*[s._ctx.value for s in solvers])
+    err = lib.sosadmm_debug_group_iterate(arr, len(solvers), int(k))
+    if err != 0:
+        raise RuntimeError(f"sosadmm_debug_group_iterate: {lib.sosadmm_strerror(err).decode()} ({err})")
+
+
+def group_get_iterate(solvers) -> dict:
+    lib = load_library()
+    s0 = solvers[0]
+    out = {k: np.zeros(s0.n) for k in ("xi", "z")}
+    out.update({k: np.zeros(s0.m) for k in ("y", "s")})
+    tau, kappa, it = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+    arr = (ctypes.c_void_p * len(solvers))(*[s._ctx.value for s in solvers])
+    err = lib.sosadmm_debug_group_get_iterate(arr, len(solvers), _dptr(out["xi"]), _dptr(out["y"]), _dptr(out["z"]),
+                                              _dptr(out["s"]), ctypes.byref(tau), ctypes.byref(kappa),
+                                              ctypes.byref(it))
+    if err != 0:
+        raise RuntimeError(f"sosadmm_debug_group_get_iterate: {lib.sosadmm_strerror(err).decode()} ({err})")
+    out.update(tau=tau.value, kappa=kappa.value, iter=it.value)
+    return out

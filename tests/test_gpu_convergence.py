@@ -32,3 +32,36 @@ def test_convergence_matches_oracle(path):
     assert abs(info["iter"] - ref["iters"]) <= max(1, int(0.02 * ref["iters"])), (info["iter"], ref["iters"])
     if ref["status_name"] == "OPTIMAL":
         assert abs(info["pobj"] - ref["pobj"]) <= 1e-6 * abs(ref["pobj"]), (info["pobj"], ref["pobj"])
+
+
+GAMMA = [p for p in GOLD if json.load(open(p)).get("gamma_acc_iter")]
+
+
+@pytest.mark.parametrize("path", GAMMA, ids=[os.path.basename(p)[19:-5] for p in GAMMA])
+def test_gamma_accuracy_iteration_matches_oracle(path):
+    """BJ "within 1e-4 relative of gamma0 at tolerance 1e-4" and "iteration counts within +-2%" for the
+    gamma-accuracy iteration: the first k with max residual <= tol AND |gamma/gamma0 - 1| <=
+    1e-4, checked at EVERY iteration on both sides (the solver's own stop disabled: tol 1e-300), within 2%
+    of the oracle's k (tools/oracle_convergence.py, every iteration)."""
+    from paper_1708_04174_b200 import SosAdmm
+
+    ref = json.load(open(path))
+    prob = make_config(ref["config"], seed=ref["seed"])
+    g0 = ref["gamma0"]
+    s = SosAdmm.from_problem(prob, tol=1e-300, max_iters=1 << 40)
+    kref = ref["gamma_acc_iter"]
+    found = None
+    try:
+        for k in range(1, int(1.05 * kref) + 2):
+            s.iterate(1)
+            info = s.info()  # residuals of u^k
+            assert info["iter"] == k
+            if max(info["res_pri"], info["res_dual"], info["res_gap"]) <= ref["tol"] and \
+                    abs(-info["pobj"] / g0 - 1.0) <= 1e-4:
+                found = (k, -info["pobj"])
+                break
+    finally:
+        s.close()
+    assert found is not None, f"no gamma-accurate iterate within {int(1.05 * kref) + 1} iterations (oracle: {kref})"
+    assert abs(found[0] - kref) <= max(1, int(0.02 * kref)), (found, kref)
+    assert abs(found[1] / g0 - 1.0) <= 1e-4

@@ -21,6 +21,11 @@ def lib():
     L.sosadmm_debug_tridiag.argtypes = [ctypes.c_int, P, P, P, P, P]
     L.sosadmm_debug_stedc.argtypes = [ctypes.c_int, P, P, P, P]
     L.sosadmm_debug_spdinv.argtypes = [ctypes.c_int, P]
+    I = ctypes.POINTER(ctypes.c_int)
+    L.sosadmm_debug_sy2sb.argtypes = [ctypes.c_int, P, P, P, P, I, I]
+    L.sosadmm_debug_sb2st.argtypes = [ctypes.c_int, ctypes.c_int, P, P, P, P, P, I]
+    L.sosadmm_debug_bt2.argtypes = [ctypes.c_int, ctypes.c_int, P, P, ctypes.c_int, P]
+    L.sosadmm_debug_tridiag2.argtypes = [ctypes.c_int, P, P, P, ctypes.POINTER(ctypes.c_float)]
     return L
 
 
@@ -119,3 +124,109 @@ def test_spd_inverse(t):
     X = K.copy(order="F")
     assert lib().sosadmm_debug_spdinv(t, dp(X)) == 0
     assert np.linalg.norm(X @ K - np.eye(t)) <= 1e-12 * np.sqrt(t) * np.linalg.cond(K)
+
+
+# ---------------------------------------------------------------------------------------------
+# Two-stage tridiagonalisation (sy2sb.cuh dense -> band, sb2st.cuh band -> tridiagonal, bt2.cuh), each
+# stage checked against the similarity it defines (the reflectors it returns, applied in numpy).
+
+def _band_full(band, N, BW):
+    """symmetric N x N matrix from the band layout band[c * 2BW + (r - c)], 0 <= r - c <= BW."""
+    B = np.zeros((N, N))
+    Bb = band.reshape(N, 2 * BW)
+    for off in range(BW + 1):
+        idx = np.arange(N - off)
+        B[idx + off, idx] = Bb[idx, off]
+    return np.tril(B) + np.tril(B, -1).T
+
+
+def _sy2sb(A):
+    N = A.shape[0]
+    band = np.zeros(N * 32)
+    V1 = np.zeros((N, N), order="F")
+    tau1 = np.zeros(N)
+    bw, nref = ctypes.c_int(0), ctypes.c_int(0)
+    assert lib().sosadmm_debug_sy2sb(N, dp(np.asfortranarray(A)), dp(band), dp(V1), dp(tau1), ctypes.byref(bw),
+                                     ctypes.byref(nref)) == 0
+    return band[:N * 2 * bw.value], V1, tau1, bw.value, nref.value
+
+
+@pytest.mark.parametrize("N", [65, 100, 231, 285, 325, 861, 946, 1280])
+def test_sy2sb(N):
+    rng = np.random.default_rng(N + 7)
+    G = rng.standard_normal((N, N))
+    A = G + G.T
+    band, V1, tau1, BW, nref = _sy2sb(A)
+    assert BW == (16 if N <= 880 else 8)
+    B = _band_full(band, N, BW)
+    lam_A = np.linalg.eigvalsh(A)
+    assert np.max(np.abs(np.linalg.eigvalsh(B) - lam_A)) <= 1e-12 * np.abs(lam_A).max() * np.sqrt(N)
+    if N <= 325:  # Q1 B Q1^T = A with Q1 = H_0 H_1 ... (H_k = I - tau_k v_k v_k^T, v_k = V1[k+1:, k])
+        Q = np.eye(N)
+        for k in range(nref):
+            v = V1[:, k].copy()
+            v[:k + 1] = 0.0
+            assert np.all(v[k + 1:k + BW] == 0.0) and (tau1[k] == 0.0 or v[k + BW] == 1.0)
+            Q = Q - tau1[k] * np.outer(Q @ v, v)
+        assert np.linalg.norm(Q @ B @ Q.T - A) <= 1e-13 * np.linalg.norm(A) * np.sqrt(N)
+        assert np.linalg.norm(Q.T @ Q - np.eye(N)) <= 1e-13 * np.sqrt(N)
+
+
+def _random_band(N, BW, rng):
+    band = np.zeros(N * 2 * BW)
+    Bb = band.reshape(N, 2 * BW)
+    for off in range(BW + 1):
+        Bb[:N - off, off] = rng.standard_normal(N - off)
+    return band
+
+
+def _q2(V2, tau2, N, BW, KM):
+    Q = np.eye(N)
+    for i in range(N - 2):
+        nt = (N - 2 - i) // BW + 1
+        for k in range(nt):
+            r0 = i + 1 + k * BW
+            L = min(BW, N - r0)
+            v = V2[(i * KM + k) * BW:(i * KM + k) * BW + L]
+            Q[:, r0:r0 + L] -= tau2[i * KM + k] * np.outer(Q[:, r0:r0 + L] @ v, v)
+    return Q
+
+
+@pytest.mark.parametrize("N,BW", [(65, 16), (66, 16), (231, 16), (325, 16), (861, 16), (946, 8), (1280, 8)])
+def test_sb2st(N, BW):
+    rng = np.random.default_rng(N * 3 + BW)
+    band = _random_band(N, BW, rng)
+    B = _band_full(band, N, BW)
+    KM = (N - 2) // BW + 1
+    d, e = np.zeros(N), np.zeros(N - 1)
+    V2, tau2 = np.zeros(N * KM * BW), np.zeros(N * KM)
+    km = ctypes.c_int(0)
+    assert lib().sosadmm_debug_sb2st(N, BW, dp(band), dp(d), dp(e), dp(V2), dp(tau2), ctypes.byref(km)) == 0
+    assert km.value == KM
+    lam_B = np.linalg.eigvalsh(B)
+    lam_T = sla.eigh_tridiagonal(d, e, eigvals_only=True)
+    assert np.max(np.abs(lam_T - lam_B)) <= 1e-12 * np.abs(lam_B).max() * np.sqrt(N)
+    if N <= 325:
+        Q = _q2(V2, tau2, N, BW, KM)
+        T = np.diag(d) + np.diag(e, 1) + np.diag(e, -1)
+        assert np.linalg.norm(Q @ T @ Q.T - B) <= 1e-13 * np.linalg.norm(B) * np.sqrt(N)
+    # the GPU back-transform of r columns applies the same Q2
+    if N <= 325:
+        r = min(N, 37)
+        Z = np.asfortranarray(rng.standard_normal((N, r)))
+        ref = Q @ Z
+        assert lib().sosadmm_debug_bt2(N, BW, dp(V2), dp(tau2), r, dp(Z)) == 0
+        assert np.max(np.abs(Z - ref)) <= 1e-13 * np.abs(ref).max() * np.sqrt(N)
+
+
+@pytest.mark.parametrize("N", [65, 231, 285, 325, 861, 1280])
+def test_tridiag_two_stage(N):
+    rng = np.random.default_rng(N + 11)
+    G = rng.standard_normal((N, N))
+    A = np.asfortranarray(G + G.T)
+    d, e = np.zeros(N), np.zeros(N - 1)
+    ms = ctypes.c_float(0)
+    assert lib().sosadmm_debug_tridiag2(N, dp(A), dp(d), dp(e), ctypes.byref(ms)) == 0
+    lam_T = sla.eigh_tridiagonal(d, e, eigvals_only=True)
+    lam_A = np.linalg.eigvalsh(A)
+    assert np.max(np.abs(lam_T - lam_A)) <= 1e-12 * np.abs(lam_A).max() * np.sqrt(N)
