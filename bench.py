@@ -39,7 +39,7 @@ CONFIG_DESC = {"pop6": "n=6 quartic POP, config 0", "pop20": "n=20 quartic POP, 
                "pop40": "n=40 quartic POP, config 4"}
 
 # roofline denominators: measured on this pool's B200s
-DMMA_PEAK_TFLOPS = 37.1   # profiles/r01_probe_fp64.log: mma.sync m8n8k4 f64 (SASS DMMA), measured 74.3 with
+DMMA_PEAK_TFLOPS = 37.1   # profiles/r02_probe_fp64.log: mma.sync m8n8k4 f64 (SASS DMMA); round 1 printed 74.3 with
 #                           the probe counting 2x512 flop per m8n8k4; one is 8*8*4 = 256 FMA = 512 flop
 DFMA_PEAK_TFLOPS = 34.2   # same probe, scalar DFMA
 
@@ -146,7 +146,7 @@ def traffic_of(prefix, table):
     return None
 
 
-def roofline_table(prob, tl, phase, large, hbm, hbm_src, config="pop40"):
+def roofline_table(prob, tl, phase, large, hbm, hbm_src, config="pop40", work=None):
     """Per-kernel-class rooflines.  achieved = algorithmic work per iteration /
     measured phase time per iteration (CUDA events on the library stream)."""
     out = []
@@ -167,29 +167,33 @@ def roofline_table(prob, tl, phase, large, hbm, hbm_src, config="pop40"):
                     "frac": fl / (tms * 1e-3) / 1e12 / DFMA_PEAK_TFLOPS,
                     "traffic": traffic_of("k_tridiag", traffic) if len(large) == 1 else None,
                     "algorithmic_per_launch": fl,
-                    "peak_source": "measured FP64 DFMA peak of this pool's B200 (profiles/r01_probe_fp64.log); "
+                    "peak_source": "measured FP64 DFMA peak of this pool's B200 (profiles/r02_probe_fp64.log); "
                                    "MEASURED_PEAKS.json has no FP64 entry", "ms_per_iter": tms,
                     # context: the pass is N - 2 dependent steps on one cluster, so it can use at most
                     # C of the 148 SMs; the same achieved rate against those SMs' share of the peak
                     "sms_used": sum(TRD_CLUSTER(N) for N in large),
                     "frac_of_used_sms": fl / (tms * 1e-3) / 1e12
                     / (DFMA_PEAK_TFLOPS * min(148, sum(TRD_CLUSTER(N) for N in large)) / 148)})
-        fd = sum(4.0 / 3.0 * N ** 3 for N in large)
-        out.append({"kernel": "divide-and-conquer tridiagonal eigensolver (k_dc_*, merge GEMMs on DMMA; 4/3 N^3 "
-                              "dense-count flops, deflation lowers the real count)",
+        # D&C merge GEMMs and back-transform + reconstruction: the work the method actually did in the last
+        # projection (sosadmm_psd_work: deflated merge sizes k, the selected spectral side's rank r)
+        fd = sum(w["dc_gemm"] for w in work) if work else sum(4.0 / 3.0 * N ** 3 for N in large)
+        rs = [int(w["r"]) for w in work] if work else None
+        out.append({"kernel": "divide-and-conquer tridiagonal eigensolver (k_dc_*, merge GEMMs on DMMA; "
+                              "sum 2 n k K over the merges from the device-side deflated sizes k)",
                     "bound": "tensor", "achieved": fd / (phase["dc"] * 1e-3) / 1e12, "peak": DMMA_PEAK_TFLOPS,
                     "unit": "TFLOP/s", "frac": fd / (phase["dc"] * 1e-3) / 1e12 / DMMA_PEAK_TFLOPS, "traffic": None,
                     "algorithmic_per_launch": fd,
-                    "peak_source": "measured FP64 DMMA (mma.sync m8n8k4) peak, profiles/r01_probe_fp64.log",
+                    "peak_source": "measured FP64 DMMA (mma.sync m8n8k4) peak, profiles/r02_probe_fp64.log",
                     "ms_per_iter": phase["dc"]})
-        fb = sum(2.0 * N ** 3 for N in large)  # back-transform 2 N^2 r + reconstruction 2 N^2 r at r = N / 2
+        fb = (sum(w["backtransform"] + w["recon"] for w in work) if work
+              else sum(2.0 * N ** 3 for N in large))
         out.append({"kernel": "back-transform + reconstruction (k_bt_gram, k_bt_larft, k_bt_apply, k_gemm_f64 on "
-                              "DMMA; 4 N^2 r flops, counted at the r = N/2 upper bound)",
+                              f"DMMA; 2 N^2 r + N (N + 32) r flops at the selected rank r = {rs})",
                     "bound": "tensor", "achieved": fb / (phase["backtransform_recon"] * 1e-3) / 1e12,
                     "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                     "frac": fb / (phase["backtransform_recon"] * 1e-3) / 1e12 / DMMA_PEAK_TFLOPS, "traffic": None,
                     "algorithmic_per_launch": fb,
-                    "peak_source": "measured FP64 DMMA (mma.sync m8n8k4) peak, profiles/r01_probe_fp64.log",
+                    "peak_source": "measured FP64 DMMA (mma.sync m8n8k4) peak, profiles/r02_probe_fp64.log",
                     "ms_per_iter": phase["backtransform_recon"]})
     if phase["jacobi"] > 0:
         small = [d for d in prob.psd_dims if d <= 64]
@@ -198,7 +202,7 @@ def roofline_table(prob, tl, phase, large, hbm, hbm_src, config="pop40"):
                     "bound": "alu", "achieved": fj / (phase["jacobi"] * 1e-3) / 1e12, "peak": DFMA_PEAK_TFLOPS,
                     "unit": "TFLOP/s", "frac": fj / (phase["jacobi"] * 1e-3) / 1e12 / DFMA_PEAK_TFLOPS,
                     "traffic": None, "algorithmic_per_launch": fj,
-                    "peak_source": "measured FP64 DFMA peak, profiles/r01_probe_fp64.log", "ms_per_iter": phase["jacobi"]})
+                    "peak_source": "measured FP64 DFMA peak, profiles/r02_probe_fp64.log", "ms_per_iter": phase["jacobi"]})
     return out
 
 
@@ -308,7 +312,8 @@ def run_ours(args):
     hbm, hbm_src = hbm_peak()
     _, _, tl = gpu.get_structure()
     large = [d for d in prob.psd_dims if d > 64]
-    rooflines = roofline_table(prob, tl, phase, large, hbm, hbm_src, args.config)
+    work = gpu.psd_work() if large else []  # flops of the last projection from the device-side sizes
+    rooflines = roofline_table(prob, tl, phase, large, hbm, hbm_src, args.config, work)
     dominant = max(rooflines, key=lambda r: r["ms_per_iter"])
     cpu = cpu_baseline(args) if not args.no_cpu else None
     total_steps = args.steps * (1 if sharded else world)  # sharded: all ranks advance ONE problem

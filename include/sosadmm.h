@@ -180,6 +180,13 @@ sosadmm_err sosadmm_project_affine(sosadmm_ctx* ctx, const double* w1, const dou
 /* PSD projection of one block in svec coordinates (`eq:HsdeStep2`). */
 sosadmm_err sosadmm_project_psd(sosadmm_ctx* ctx, int32_t block, const double* a_svec, double* out_svec);
 
+/* Algorithmic FP64 work of the last large-block PSD projections (measurement), 6 doubles per
+ * large block (N > 64) in setup order: [tridiagonalisation 4/3 N^3, divide-and-conquer merge GEMM flops
+ * sum 2 n k K from the device-side deflated sizes, back-transform 2 N^2 r, reconstruction N (N + 32) r, r,
+ * number of fully deflated merges] with r = the selected spectral side's rank.  In: *nblocks = capacity of
+ * `work` in blocks (work may be NULL to query); out: *nblocks = number of large blocks. */
+sosadmm_err sosadmm_psd_work(sosadmm_ctx* ctx, double* work, int32_t* nblocks);
+
 /* Number of kernel launches one iteration issues (for the bench's gpu_launches claim). */
 int64_t sosadmm_launches_per_iter(const sosadmm_ctx* ctx);
 

@@ -50,6 +50,7 @@ struct LargeBlock {
   Sy2sbArgs sa{};
   double *V2 = nullptr, *tau2 = nullptr, *Bg = nullptr;
   unsigned* cnt = nullptr;
+  std::vector<int> node_n;  // host copy: size of every D&C node (index = node id), for the work accounting
 };
 
 struct LargeEig {
@@ -327,6 +328,8 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     lb.Twy = (double*)p[q++];
     lb.Gwy = (double*)p[q++];
     lb.recon = (int)nodes.size();
+    lb.node_n.clear();
+    for (const DcNode& nd : nodes) lb.node_n.push_back(nd.n);
     lb.D = D;
     lb.level_node0 = l0;
     lb.level_nn = lnn;
@@ -665,6 +668,39 @@ inline int large_eig_launches(const LargeEig& le) {
   for (const auto& lb : le.blocks)
     k += (lb.two ? 3 : (lb.ksw < lb.N - 2 ? 2 : 1)) + 2 + 1 + 7 * lb.D + 1 + 5 + (lb.two ? 1 : 0);
   return k;
+}
+
+// Algorithmic FP64 flops of the last projection of one large block, from the device-side sizes it used
+// (the roofline counts the method's own work, not dense upper bounds):
+//   w[0] tridiagonalisation 4/3 N^3;  w[1] divide-and-conquer merge GEMMs sum 2 n k K over the merge nodes
+//   (k = non-deflated count; the root forms only the selected columns);  w[2] back-transform 2 N^2 r
+//   (+ 2 N^2 r through the stage-2 reflectors on the two-stage path);  w[3] reconstruction N (N + 32) r
+//   (lower-triangle tiles of W W^T);  w[4] = r, w[5] = number of deflated-to-zero merges (context).
+inline int large_block_work(const LargeBlock& lb, cudaStream_t s, double* w) {
+  const int N = lb.N;
+  std::vector<int> nk(lb.node_n.size());
+  int top[4] = {0, 0, 0, 0}, sel[3] = {0, 0, 0};
+  if (cudaMemcpyAsync(nk.data(), lb.dc.node_k, 4 * nk.size(), cudaMemcpyDeviceToHost, s) ||
+      cudaMemcpyAsync(top, lb.dc.topsel, 12, cudaMemcpyDeviceToHost, s) ||
+      cudaMemcpyAsync(sel, lb.sel, 12, cudaMemcpyDeviceToHost, s) || cudaStreamSynchronize(s))
+    return 1;
+  double dc = 0.0, zero = 0.0;
+  for (int h = 1; h <= lb.D; ++h)
+    for (int t = 0; t < lb.level_nn[h]; ++t) {
+      const int id = lb.level_node0[h] + t;
+      const double n = lb.node_n[id], k = nk[id];
+      const double cols = (h == lb.D && lb.dc.topsel_on) ? top[0] : k;
+      dc += 2.0 * n * cols * k;
+      zero += k == 0;
+    }
+  const double r = sel[0];
+  w[0] = 4.0 / 3.0 * (double)N * N * N;
+  w[1] = dc;
+  w[2] = 2.0 * (double)N * N * r * (lb.two ? 2.0 : 1.0);
+  w[3] = (double)N * (N + 32) * r;
+  w[4] = r;
+  w[5] = zero;
+  return 0;
 }
 
 inline void large_eig_free(LargeEig& le) { le.blocks.clear(); }

@@ -1176,6 +1176,22 @@ sosadmm_err sosadmm_project_psd(sosadmm_ctx* c, int32_t block, const double* a_s
 
 int64_t sosadmm_launches_per_iter(const sosadmm_ctx* c) { return c ? c->launches : 0; }
 
+sosadmm_err sosadmm_psd_work(sosadmm_ctx* c, double* work, int32_t* nblocks) {
+  if (!c || !nblocks) return SOSADMM_E_ARG;
+  if (c->err) return c->err;
+  CK_CTX(c, cudaSetDevice(c->device));
+  const int nb = (int)c->le.blocks.size();
+  if (work)
+    for (int b = 0; b < std::min(nb, *nblocks); ++b)
+      if (large_block_work(c->le.blocks[b], c->stream, work + 6 * b)) {
+        c->err = SOSADMM_E_CUDA;
+        c->msg = "sosadmm_psd_work: device read failed";
+        return c->err;
+      }
+  *nblocks = nb;
+  return SOSADMM_OK;
+}
+
 void sosadmm_destroy(sosadmm_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);

@@ -21,7 +21,8 @@ STATUS = {0: "RUNNING", 1: "OPTIMAL", 2: "PRIMAL_INFEASIBLE", 3: "DUAL_INFEASIBL
 EXPORTS = ["sosadmm_workspace_size", "sosadmm_setup", "sosadmm_setup_sharded", "sosadmm_nccl_unique_id",
            "sosadmm_iterate", "sosadmm_iterate_async", "sosadmm_iterate_profiled",
            "sosadmm_get_info", "sosadmm_get_iterate", "sosadmm_set_iterate", "sosadmm_get_structure",
-           "sosadmm_project_affine", "sosadmm_project_psd", "sosadmm_launches_per_iter", "sosadmm_destroy",
+           "sosadmm_project_affine", "sosadmm_project_psd", "sosadmm_launches_per_iter", "sosadmm_psd_work",
+           "sosadmm_destroy",
            "sosadmm_strerror", "sosadmm_last_error_message"]
 
 
@@ -79,6 +80,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.sosadmm_get_structure.argtypes = [V, ctypes.POINTER(I32), P, ctypes.POINTER(I64)]
     lib.sosadmm_project_affine.argtypes = [V, P, P, D, P, P, P]
     lib.sosadmm_project_psd.argtypes = [V, I32, P, P]
+    lib.sosadmm_psd_work.argtypes = [V, P, ctypes.POINTER(I32)]
+    lib.sosadmm_psd_work.restype = ctypes.c_int
     lib.sosadmm_launches_per_iter.argtypes = [V]
     lib.sosadmm_launches_per_iter.restype = I64
     lib.sosadmm_destroy.argtypes = [V]
@@ -204,6 +207,15 @@ class SosAdmm:
         self._check(self.lib.sosadmm_iterate_profiled(self._ctx, int(k), ctypes.byref(info), _dptr(ms)),
                     "iterate_profiled")
         return info.as_dict(), ms
+
+    def psd_work(self) -> list:
+        """Per large block: dict of the algorithmic FP64 flops of the last projection (sosadmm_psd_work)."""
+        n = ctypes.c_int32(0)
+        self._check(self.lib.sosadmm_psd_work(self._ctx, None, ctypes.byref(n)), "psd_work")
+        w = np.zeros(6 * max(n.value, 1))
+        self._check(self.lib.sosadmm_psd_work(self._ctx, _dptr(w), ctypes.byref(n)), "psd_work")
+        keys = ["tridiag", "dc_gemm", "backtransform", "recon", "r", "dc_zero_merges"]
+        return [dict(zip(keys, w[6 * b:6 * b + 6].tolist())) for b in range(n.value)]
 
     def info(self) -> dict:
         info = _Info()
