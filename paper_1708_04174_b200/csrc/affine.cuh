@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(256) k_rowupdate8(AffineArgs a, int write_stat
 }
 
 // k_scatter: projection input a = u_hat_xi - z for every PSD svec position, written to
-// asvec and unpacked (÷sqrt 2 off the diagonal) into both triangles of the block's matrix.
+// asvec and unpacked (÷sqrt 2 off the diagonal) into the upper triangle of the block's matrix.
 __global__ void __launch_bounds__(POS_NT) k_scatter(AffineArgs a, int zero_z) {
   if (a.st->done || !a.is->proceed) return;
   const int b = a.cta_blk[blockIdx.x];
@@ -505,13 +505,10 @@ __global__ void __launch_bounds__(POS_NT) k_scatter(AffineArgs a, int zero_z) {
     a.asvec[col - a.t_free] = v;
     int i, j;
     svec_ij(q, i, j);
-    if (i == j) {
-      M[(size_t)i * N + i] = v;
-    } else {
-      const double h = v * SOS_IRT2;
-      M[(size_t)j * N + i] = h;
-      M[(size_t)i * N + j] = h;
-    }
+    // upper triangle only (column j, row i <= j: consecutive q are consecutive addresses); every
+    // projection kernel reads the upper triangle (the Jacobi kernel symmetrically, the cluster
+    // tridiagonalisation as "row i of the lower triangle")
+    M[(size_t)j * N + i] = (i == j) ? v : v * SOS_IRT2;
   }
 }
 
@@ -532,8 +529,8 @@ __global__ void __launch_bounds__(POS_NT) k_pack(AffineArgs a, double* out_xi, i
     const long long col = col0 + q;
     int i, j;
     svec_ij(q, i, j);
-    // the projection kernels leave their result in the lower triangle (row j, column i, j >= i)
-    const double mij = M[(size_t)i * N + j];
+    // the projection kernels leave their result in the upper triangle (column j, row i <= j)
+    const double mij = M[(size_t)j * N + i];
     const double sv = (i == j) ? mij : mij * SOS_RT2;
     const double av = a.asvec[col - a.t_free];
     double xn, zn;

@@ -23,7 +23,7 @@ struct GemmDesc {
   int transB;
   double alpha, beta;
   int skip;            // 1 = this batch entry does nothing
-  int lower;           // 1 = only tiles that meet the lower triangle (row >= column) are needed
+  int upper;           // 1 = only tiles that meet the upper triangle (row <= column) are needed
 };
 
 constexpr int GM_BM = 32, GM_BN = 64, GM_BK = 16, GM_NT = 128, GM_ST = 3;
@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(GM_NT) k_gemm_f64(const GemmDesc* __restrict__
   const int joff = g.Noff ? *g.Noff : 0;
   const int i0 = blockIdx.x * GM_BM, j0 = blockIdx.y * GM_BN;
   if (i0 >= M || j0 >= N) return;
-  if (g.lower && j0 > i0 + GM_BM - 1) return;  // tile strictly above the diagonal
+  if (g.upper && i0 > j0 + GM_BN - 1) return;  // tile strictly below the diagonal
   __shared__ __align__(16) double As[GM_ST][GM_BK][GM_BM + GM_PAD];
   __shared__ __align__(16) double Bs[GM_ST][GM_BK][GM_BN + GM_PAD];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

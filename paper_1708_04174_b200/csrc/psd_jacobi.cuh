@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(NT) k_psd_jacobi(JacobiArgs a) {
 
   for (int e = tid; e < NN; e += NT) {
     const int i = e % Np, j = e / Np;
-    Ab(0)[e] = (i < N && j < N) ? G[(size_t)j * N + i] : 0.0;
+    Ab(0)[e] = (i < N && j < N) ? G[(size_t)max(i, j) * N + min(i, j)] : 0.0;  // upper triangle (k_scatter)
     Vb(0)[e] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
@@ -239,10 +239,9 @@ __global__ void __launch_bounds__(NT) k_psd_jacobi(JacobiArgs a) {
     }
   for (int e = tid; e < N * N; e += NT) {
     const int i = e % N, j = e / N;
-    if (i < j) continue;  // lower triangle (row i >= column j) is what k_pack reads
+    if (i < j) continue;  // one entry per pair: k_pack reads the upper triangle (column i, row j <= i)
     double acc = 0.0;
     for (int k = 0; k < Np; ++k) acc = fma(V[i + k * Np] * alpha[k], V[j + k * Np], acc);
-    G[(size_t)j * N + i] = acc;
     G[(size_t)i * N + j] = acc;
   }
 }

@@ -383,7 +383,7 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
       g.Kdev = lb.sel;
       g.alpha = 1.0;
       g.beta = 0.0;
-      g.lower = 1;  // k_pack reads the lower triangle of the projection only
+      g.upper = 1;  // k_pack reads the upper triangle of the projection only
       gd[nodes.size()] = g;
     }
     if (err == cudaSuccess) err = cudaMemcpyAsync(dnodes, nodes.data(), sizeof(DcNode) * nodes.size(), cudaMemcpyHostToDevice, s);

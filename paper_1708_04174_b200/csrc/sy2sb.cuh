@@ -32,7 +32,7 @@ constexpr int SB_KC = 128;   // streamed chunk width (columns)
 constexpr int SB_LDC = SB_KC + 4;
 
 struct Sy2sbArgs {
-  const double* M;   // N x N column-major block matrix, both triangles valid (input, not modified)
+  const double* M;   // N x N column-major block matrix, upper triangle valid (input, not modified)
   int N, BW;         // BW = 16 or 8 (template parameter copy)
   int NW;            // worker CTAs (grid = NW + 1)
   int maxrb;         // row blocks per worker
@@ -401,7 +401,9 @@ __global__ void __launch_bounds__(SB_NT, 1) k_sy2sb(Sy2sbArgs a) {
     for (int rr = 0; rr < SB_R; ++rr) {
       const int i = row_of(s, rr);
       double* dst = Aown + ((size_t)s * SB_R + rr) * ldr;
-      for (int c = tid; c < ldr; c += SB_NT) dst[c] = (i < N && c < N) ? __ldg(a.M + (size_t)i * N + c) : 0.0;
+      // row i of the symmetric block from its upper triangle (column max(i, c), row min(i, c))
+      for (int c = tid; c < ldr; c += SB_NT)
+        dst[c] = (i < N && c < N) ? __ldg(a.M + (c <= i ? (size_t)i * N + c : (size_t)c * N + i)) : 0.0;
     }
   __syncthreads();
   // slice of panel 0: all own rows, columns 0..BW-1

@@ -39,7 +39,7 @@ inline int tridiag_maxb(int N) {
 }
 
 struct TridiagArgs {
-  double* M;         // N x N column-major block matrix (both triangles valid on input)
+  double* M;         // N x N column-major block matrix (upper triangle valid on input)
   int N;
   int C;             // cluster size (CTAs)
   long long smem_rows_doubles;  // per-CTA shared-memory budget for row storage
