@@ -51,6 +51,11 @@ int sosadmm_debug_psd_stages(int N, const double* A, double* d, double* e, doubl
 int sosadmm_debug_setup_emulated(const sosadmm_problem* prob, const sosadmm_settings* settings, int32_t rank,
                                  int32_t world, const int32_t* block_owner, sosadmm_ctx** out);
 int sosadmm_debug_group_iterate(sosadmm_ctx* const* ctx, int world, int64_t k);
+/* Switch an emulated group (after setup, before iterating) to the peer-memory reduction of SURVEY §8(f)
+ * f4: the partial sums are reduced inside k_gather_fin_peer from every rank's buffer (rank order), after
+ * a per-round flag hand-off (k_peer_signal), instead of a separate allreduce.  Real ranks select it with
+ * SOSADMM_ALLREDUCE=peer (CUDA IPC handles of the workspaces exchanged by one ncclAllGather at setup). */
+int sosadmm_debug_group_link_peers(sosadmm_ctx* const* ctx, int world);
 int sosadmm_debug_group_get_iterate(sosadmm_ctx* const* ctx, int world, double* xi, double* y, double* z, double* s,
                                     double* tau, double* kappa, int64_t* iter);
 #ifdef __cplusplus

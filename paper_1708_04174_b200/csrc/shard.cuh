@@ -19,10 +19,23 @@ constexpr int SH_NT = 256;
 
 struct ShardArgs {
   const int* colown;   // n: 1 if this rank accounts for column j in the partial sums
-  double* buf;         // 2m + 3: all-reduced partial sums
+  double* buf;         // 2m + 3: all-reduced partial sums (NCCL mode); peer mode: 2 x (2m + 3) by epoch parity
   double* part;        // 3 * nblk_part: per-CTA partials of the three scalars
   int nparts;          // number of per-CTA partial slots per scalar
+  // ---- peer mode (f4: the reduction fused into the consumer over peer memory, no NCCL call) ----
+  unsigned long long* epoch;             // device round counter (replicated; nullptr = NCCL mode)
+  unsigned long long* flags;             // [world] arrival epochs written by the peers (P2P stores)
+  double* const* peer_buf;               // [world] every rank's 2 x (2m + 3) partial buffers (own included)
+  unsigned long long* const* peer_flags; // [world] every rank's flag array
+  double* red3;                          // the three reduced scalars (k_tphase's shard_scal)
+  int world, rank;
 };
+
+// Partial-sum buffer of this round: peer mode alternates two buffers by epoch parity (a rank can be at
+// most one round ahead of a peer still reading its previous round), NCCL mode has one.
+__device__ __forceinline__ double* shard_buf(const ShardArgs& s, int m) {
+  return s.epoch ? s.buf + (size_t)(*s.epoch & 1ull) * (2 * (size_t)m + 3) : s.buf;
+}
 
 // Per-row partial sums over the owned columns (the sharded counterpart of k_gather's first half).
 __global__ void __launch_bounds__(SH_NT) k_gather_part(AffineArgs a, ShardArgs s) {
@@ -52,8 +65,9 @@ __global__ void __launch_bounds__(SH_NT) k_gather_part(AffineArgs a, ShardArgs s
       gl = fma(v, xj + a.z[j], gl);
       axl = fma(v, xj, axl);
     }
-    s.buf[r] = (gx + gz) + gl;
-    s.buf[a.m + r] = gx + axl;
+    double* buf = shard_buf(s, a.m);
+    buf[r] = (gx + gz) + gl;
+    buf[a.m + r] = gx + axl;
   }
   const double v = block_sum<SH_NT>(dres, sh);
   if (threadIdx.x == 0) s.part[blockIdx.x] = v;
@@ -103,7 +117,7 @@ __global__ void __launch_bounds__(SH_NT) k_shard_scalars(AffineArgs a, ShardArgs
     double v = 0.0;
     for (int i = threadIdx.x; i < cnt[q]; i += SH_NT) v += s.part[q * s.nparts + i];
     v = block_sum<SH_NT>(v, sh);
-    if (threadIdx.x == 0) s.buf[2 * a.m + q] = v;
+    if (threadIdx.x == 0) shard_buf(s, a.m)[2 * a.m + q] = v;
   }
 }
 
@@ -140,6 +154,100 @@ __global__ void __launch_bounds__(GATHER_NT) k_gather_fin(AffineArgs a, ShardArg
   if (threadIdx.x == 0) {
     a.part[PART_BY * a.gather_blocks + blockIdx.x] = v;
     a.part[PART_DRES * a.gather_blocks + blockIdx.x] = (blockIdx.x == 0) ? s.buf[2 * a.m] : 0.0;
+  }
+}
+
+// ---- peer mode ----
+// Arrival: this rank's partials of round E are complete (stream order); publish E + 1 into every peer's
+// flag slot `rank` (system-scope release after a system fence: the peers read the partials over NVLink)
+// and advance the local epoch.  One thread.
+__global__ void k_peer_signal(AffineArgs a, ShardArgs s) {
+  if (a.st->done) return;
+  const unsigned long long e = *s.epoch + 1ull;
+  __threadfence_system();
+  for (int q = 0; q < s.world; ++q) {
+    unsigned long long* f = s.peer_flags[q] + s.rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
+  }
+  *s.epoch = e;
+}
+
+__device__ __forceinline__ unsigned long long peer_ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ double peer_ld(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// k_gather_fin with the allreduce fused in: wait until every rank published round E (local flags,
+// written by the peers), then read the round's partial sums of EVERY rank straight from their memory
+// (NVLink peer loads) and add them in rank order — deterministic, and the same order as the one-GPU
+// emulation's device sum.  CTA 0 also reduces the three scalars into red3 for k_tphase.
+__global__ void __launch_bounds__(GATHER_NT) k_gather_fin_peer(AffineArgs a, ShardArgs s) {
+  __shared__ double sh[2 * (GATHER_NT / 32)];
+  if (a.st->done) return;
+  const unsigned long long e = *s.epoch;  // = E + 1 after k_peer_signal
+  if (threadIdx.x == 0) {
+    unsigned long long t0 = 0;
+    unsigned spins = 0;
+    for (int q = 0; q < s.world; ++q)
+      while (peer_ld_acquire(s.flags + q) < e) {
+        __nanosleep(64);
+        if ((++spins & 0xFFFu) == 0) {  // a lost peer traps after 20 s instead of hanging the GPU
+          unsigned long long now;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+          if (t0 == 0) t0 = now;
+          else if (now - t0 > 20000000000ull) __trap();
+        }
+      }
+    __threadfence_system();
+  }
+  __syncthreads();
+  const size_t len = 2 * (size_t)a.m + 3, off = (size_t)((e - 1ull) & 1ull) * len;
+  auto sum = [&](size_t i) {
+    double v = 0.0;
+    for (int q = 0; q < s.world; ++q) v += peer_ld(s.peer_buf[q] + off + i);
+    return v;
+  };
+  const double tau = a.st->tau;
+  const int r = blockIdx.x * GATHER_NT + threadIdx.x;
+  double p_pres = 0, p_axi = 0, p_by = 0;
+  dd bxd{0.0, 0.0};
+  if (r < a.m) {
+    const double g = sum(r);
+    const double axi = sum(a.m + r);
+    const double yr = a.y[r];
+    const double xr = ((yr + a.s[r]) - g) * a.Pinv[r];
+    a.x[r] = xr;
+    const double pr = axi - a.b[r] * tau;
+    bxd = dd_prod(a.b[r], xr);
+    p_pres = pr * pr;
+    p_axi = axi * axi;
+    p_by = a.b[r] * yr;
+  }
+  double dres0 = 0.0;
+  if (blockIdx.x == 0 && threadIdx.x < 3) {
+    const double v = sum(2 * (size_t)a.m + threadIdx.x);
+    s.red3[threadIdx.x] = v;
+    if (threadIdx.x == 0) dres0 = v;
+  }
+  const dd bxs = dd_block_sum<GATHER_NT>(bxd, sh);
+  if (threadIdx.x == 0) {
+    a.part[PART_BX * a.gather_blocks + blockIdx.x] = bxs.hi;
+    a.part[PART_BXLO * a.gather_blocks + blockIdx.x] = bxs.lo;
+  }
+  double v = block_sum<GATHER_NT>(p_pres, sh);
+  if (threadIdx.x == 0) a.part[PART_PRES * a.gather_blocks + blockIdx.x] = v;
+  v = block_sum<GATHER_NT>(p_axi, sh);
+  if (threadIdx.x == 0) a.part[PART_AXI * a.gather_blocks + blockIdx.x] = v;
+  v = block_sum<GATHER_NT>(p_by, sh);
+  if (threadIdx.x == 0) {
+    a.part[PART_BY * a.gather_blocks + blockIdx.x] = v;
+    a.part[PART_DRES * a.gather_blocks + blockIdx.x] = (blockIdx.x == 0) ? dres0 : 0.0;
   }
 }
 

@@ -7,6 +7,7 @@
 // iterate(k) needs no host round trip inside the loop.
 #include "../../include/sosadmm.h"
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -40,6 +41,7 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
 };
 NcclApi& nccl() {
   static NcclApi api;
@@ -53,6 +55,7 @@ NcclApi& nccl() {
       api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
       api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
       api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
+      api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
       api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.commDestroy && api.getErrorString;
     }
   }
@@ -64,7 +67,10 @@ struct ShardSpec {
   const int32_t* block_owner = nullptr;  // nullptr: every block on this rank
   bool sharded = false;                  // true: NCCL partial-sum allreduce in the loop
   bool emulated = false;                 // debug: no communicator; sosadmm_debug_group_iterate sums on one GPU
+  bool peer = false;                     // f4: partial sums reduced over peer memory inside k_gather_fin_peer
 };
+
+constexpr int PEER_MAXW = 8;
 
 struct GroupBufs {
   double* buf[8];
@@ -332,6 +338,24 @@ bool spd_inverse(std::vector<double>& K, int t) {
   return true;
 }
 
+struct DevPtrs {
+  int *seg_ptr, *seg_col, *low_col, *lr_ptr, *lr_idx, *lr_col, *lc_ptr, *lc_row, *empty_cols, *code;
+  double *seg_val, *lr_val, *lc_val, *c_low, *h1_low, *beta_low, *Kinv, *b, *Pinv, *h2, *aval;
+  double *xi, *z, *y, *s, *x, *uhat2, *yt, *zt, *ulow, *aty, *part, *asvec, *mats, *tmp, *kpart = nullptr;
+  DevState* st;
+  IterScal* is;
+  long long *blk_col, *blk_mat, *cta_q0;
+  int *blk_N, *cta_blk, *small_blk;
+  int* colown;
+  double* jvp;         // warm-start eigenvectors of the small blocks
+  long long* blk_vp;
+  double *shbuf, *shpart;
+  unsigned long long *pflags, *pepoch;  // peer mode: [PEER_MAXW] arrival epochs, the round counter
+  double** ppeer_buf;                    // [PEER_MAXW] device pointers (peer mode)
+  unsigned long long** ppeer_flags;      // [PEER_MAXW]
+  double* pred3;                         // the three reduced scalars
+};
+
 }  // namespace
 
 struct sosadmm_ctx {
@@ -360,6 +384,8 @@ struct sosadmm_ctx {
   ShardSpec sp;
   ncclComm_t comm = nullptr;
   ShardArgs sh{};
+  DevPtrs dp{};
+  std::vector<void*> ipc_open;  // peer bases opened with cudaIpcOpenMemHandle (closed in destroy)
   int nb_low = 1;
   // parallel branches of the PSD projection inside the CUDA graph
   static constexpr int kMaxAux = 1 + 3 * 8;
@@ -389,19 +415,6 @@ void layout(const Analysis& an, Arena& ar, F&& bind) {
   bind(ar);
 }
 
-struct DevPtrs {
-  int *seg_ptr, *seg_col, *low_col, *lr_ptr, *lr_idx, *lr_col, *lc_ptr, *lc_row, *empty_cols, *code;
-  double *seg_val, *lr_val, *lc_val, *c_low, *h1_low, *beta_low, *Kinv, *b, *Pinv, *h2, *aval;
-  double *xi, *z, *y, *s, *x, *uhat2, *yt, *zt, *ulow, *aty, *part, *asvec, *mats, *tmp, *kpart = nullptr;
-  DevState* st;
-  IterScal* is;
-  long long *blk_col, *blk_mat, *cta_q0;
-  int *blk_N, *cta_blk, *small_blk;
-  int* colown;
-  double* jvp;         // warm-start eigenvectors of the small blocks
-  long long* blk_vp;
-  double *shbuf, *shpart;
-};
 
 int low_blocks(const Analysis& an) {
   return std::max(1, std::max((an.tl + SH_NT / 32 - 1) / (SH_NT / 32), ((int)an.empty_cols.size() + SH_NT - 1) / SH_NT));
@@ -459,7 +472,12 @@ void carve(const Analysis& an, Arena& ar, DevPtrs& d, int gather_blocks) {
   d.colown = ar.take<int>(n);
   d.jvp = ar.take<double>((size_t)std::max<long long>(an.vp_total, 1));
   d.blk_vp = ar.take<long long>(an.nblk);
-  d.shbuf = ar.take<double>(2 * m + 3);
+  d.shbuf = ar.take<double>(2 * (2 * m + 3));  // peer mode alternates two buffers by epoch parity
+  d.pflags = ar.take<unsigned long long>(PEER_MAXW);
+  d.pepoch = ar.take<unsigned long long>(1);
+  d.ppeer_buf = ar.take<double*>(PEER_MAXW);
+  d.ppeer_flags = ar.take<unsigned long long*>(PEER_MAXW);
+  d.pred3 = ar.take<double>(3);
   d.shpart = ar.take<double>(3 * (size_t)std::max(gather_blocks, low_blocks(an)));
 }
 
@@ -516,16 +534,23 @@ sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev, int
       k_lowdual_part<<<c->nb_low, SH_NT, 0, s>>>(a, c->sh);
       k_gather_part<<<c->gather_blocks, SH_NT, 0, s>>>(a, c->sh);
       k_shard_scalars<<<1, SH_NT, 0, s>>>(a, c->sh, c->gather_blocks, c->nb_low);
+      if (c->sp.peer) k_peer_signal<<<1, 1, 0, s>>>(a, c->sh);
       if (phase == 1) return SOSADMM_OK;
-      const ncclResult_t nr = nccl().allReduce(c->sh.buf, c->sh.buf, 2 * (size_t)a.m + 3, ncclFloat64, ncclSum,
-                                               c->comm, s);
-      if (nr != ncclSuccess) {
-        c->err = SOSADMM_E_NCCL;
-        c->msg = std::string("ncclAllReduce: ") + nccl().getErrorString(nr);
-        return c->err;
-      }
     }
-    k_gather_fin<<<c->gather_blocks, GATHER_NT, 0, s>>>(a, c->sh);
+    if (c->sp.peer) {  // the reduction over peer memory, fused into the consumer (no NCCL call)
+      k_gather_fin_peer<<<c->gather_blocks, GATHER_NT, 0, s>>>(a, c->sh);
+    } else {
+      if (phase != 2) {
+        const ncclResult_t nr = nccl().allReduce(c->sh.buf, c->sh.buf, 2 * (size_t)a.m + 3, ncclFloat64, ncclSum,
+                                                 c->comm, s);
+        if (nr != ncclSuccess) {
+          c->err = SOSADMM_E_NCCL;
+          c->msg = std::string("ncclAllReduce: ") + nccl().getErrorString(nr);
+          return c->err;
+        }
+      }
+      k_gather_fin<<<c->gather_blocks, GATHER_NT, 0, s>>>(a, c->sh);
+    }
   } else {
     k_gather<<<c->gather_blocks, GATHER_NT, 0, s>>>(a);
   }
@@ -606,6 +631,89 @@ sosadmm_err read_info(sosadmm_ctx* c, sosadmm_info* out) {
     out->dinf = st.dinf;
   }
   return c->err;
+}
+
+// Peer mode (f4): every rank's partial buffers and flag slots, device pointers in rank order
+// (own entries included), installed into the context; the round counter and the flags start at 0.
+sosadmm_err peer_wire(sosadmm_ctx* c, const std::vector<double*>& bufs, const std::vector<unsigned long long*>& flags) {
+  const int W = c->sp.world;
+  if (W > PEER_MAXW || (int)bufs.size() != W || (int)flags.size() != W) {
+    c->err = SOSADMM_E_ARG;
+    c->msg = "peer mode supports at most 8 ranks";
+    return c->err;
+  }
+  DevPtrs& d = c->dp;
+  cudaStream_t s = c->stream;
+  CK_CTX(c, cudaMemcpyAsync(d.ppeer_buf, bufs.data(), sizeof(double*) * W, cudaMemcpyHostToDevice, s));
+  CK_CTX(c, cudaMemcpyAsync(d.ppeer_flags, flags.data(), sizeof(unsigned long long*) * W, cudaMemcpyHostToDevice, s));
+  CK_CTX(c, cudaMemsetAsync(d.pflags, 0, sizeof(unsigned long long) * PEER_MAXW, s));
+  CK_CTX(c, cudaMemsetAsync(d.pepoch, 0, sizeof(unsigned long long), s));
+  CK_CTX(c, cudaStreamSynchronize(s));
+  c->sp.peer = true;
+  c->sh.epoch = d.pepoch;
+  c->sh.flags = d.pflags;
+  c->sh.peer_buf = d.ppeer_buf;
+  c->sh.peer_flags = d.ppeer_flags;
+  c->sh.red3 = d.pred3;
+  c->aa.shard_scal = d.pred3;
+  return SOSADMM_OK;
+}
+
+// Real multi-GPU peer mode: exchange CUDA IPC handles of every rank's workspace allocation (one
+// ncclAllGather at setup) and open the peers' buffers (NVLink peer mappings).
+struct PeerRec {
+  cudaIpcMemHandle_t h;
+  unsigned long long off_buf, off_flags;
+};
+sosadmm_err peer_setup_ipc(sosadmm_ctx* c) {
+  typedef CUresult (*GetRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult qr;
+  CK_CTX(c, cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &qr));
+  if (!fn || qr != cudaDriverEntryPointSuccess || !nccl().allGather) {
+    c->err = SOSADMM_E_CUDA;
+    c->msg = "peer mode: cuMemGetAddressRange / ncclAllGather unavailable";
+    return c->err;
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (((GetRange)fn)(&base, &size, (CUdeviceptr)c->dp.shbuf) != CUDA_SUCCESS) {
+    c->err = SOSADMM_E_CUDA;
+    c->msg = "peer mode: cuMemGetAddressRange failed";
+    return c->err;
+  }
+  PeerRec me{};
+  CK_CTX(c, cudaIpcGetMemHandle(&me.h, (void*)base));
+  me.off_buf = (unsigned long long)((CUdeviceptr)c->dp.shbuf - base);
+  me.off_flags = (unsigned long long)((CUdeviceptr)c->dp.pflags - base);
+  const int W = c->sp.world;
+  char* dsend = (char*)c->d_tmp;  // scratch (>= (W + 1) * sizeof(PeerRec) bytes: checked by the caller)
+  char* drecv = dsend + sizeof(PeerRec);
+  CK_CTX(c, cudaMemcpyAsync(dsend, &me, sizeof(me), cudaMemcpyHostToDevice, c->stream));
+  const ncclResult_t nr = nccl().allGather(dsend, drecv, sizeof(PeerRec), ncclUint8, c->comm, c->stream);
+  if (nr != ncclSuccess) {
+    c->err = SOSADMM_E_NCCL;
+    c->msg = std::string("ncclAllGather: ") + nccl().getErrorString(nr);
+    return c->err;
+  }
+  std::vector<PeerRec> all(W);
+  CK_CTX(c, cudaMemcpyAsync(all.data(), drecv, sizeof(PeerRec) * W, cudaMemcpyDeviceToHost, c->stream));
+  CK_CTX(c, cudaStreamSynchronize(c->stream));
+  std::vector<double*> bufs(W);
+  std::vector<unsigned long long*> flags(W);
+  for (int q = 0; q < W; ++q) {
+    if (q == c->sp.rank) {
+      bufs[q] = c->dp.shbuf;
+      flags[q] = c->dp.pflags;
+      continue;
+    }
+    void* pb = nullptr;
+    CK_CTX(c, cudaIpcOpenMemHandle(&pb, all[q].h, cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_open.push_back(pb);
+    bufs[q] = (double*)((char*)pb + all[q].off_buf);
+    flags[q] = (unsigned long long*)((char*)pb + all[q].off_flags);
+  }
+  return peer_wire(c, bufs, flags);
 }
 
 }  // namespace
@@ -841,6 +949,9 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
   c->sh.buf = d.shbuf;
   c->sh.part = d.shpart;
   c->sh.nparts = std::max(c->gather_blocks, c->nb_low);
+  c->sh.world = sp.world;
+  c->sh.rank = sp.rank;
+  c->dp = d;  // kept for the peer-mode wiring (sosadmm_debug_group_link_peers, IPC exchange)
   JacobiArgs& ja = c->ja;
   ja.mats = d.mats; ja.blk_mat = d.blk_mat; ja.blk_N = d.blk_N; ja.small_blk = d.small_blk;
   ja.st = d.st; ja.is = d.is; ja.check_state = 1;
@@ -876,6 +987,18 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
   }
   c->launches = count_launches(c);
   CK_CTX(c, cudaStreamSynchronize(s));
+  {  // f4 peer mode on real ranks (opt-in: SOSADMM_ALLREDUCE=peer; NCCL otherwise)
+    const char* env = getenv("SOSADMM_ALLREDUCE");
+    if (sp.sharded && !sp.emulated && env && std::string(env) == "peer") {
+      if ((size_t)an.n * sizeof(double) < (sp.world + 1) * sizeof(PeerRec)) {
+        c->err = SOSADMM_E_ARG;
+        c->msg = "peer mode: problem too small for the handle exchange scratch";
+        return c->err;
+      }
+      if (peer_setup_ipc(c)) return c->err;
+      c->launches = count_launches(c);
+    }
+  }
   return SOSADMM_OK;
 }
 
@@ -1209,6 +1332,7 @@ void sosadmm_destroy(sosadmm_ctx* c) {
   if (c->h_poll) cudaFreeHost(c->h_poll);
   for (auto& e : c->ev_blk)
     if (e) cudaEventDestroy(e);
+  for (void* pb : c->ipc_open) cudaIpcCloseMemHandle(pb);
   if (c->own_mem) cudaFree(c->own_mem);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -1514,11 +1638,41 @@ extern "C" int sosadmm_debug_setup_emulated(const sosadmm_problem* prob, const s
   return setup_impl(prob, settings, sp, nullptr, out);
 }
 
+// Switch an emulated group to the peer-memory reduction (f4): every rank's k_gather_fin_peer reads the
+// other ranks' partial buffers directly (same device here, NVLink peer mappings on real ranks).
+extern "C" int sosadmm_debug_group_link_peers(sosadmm_ctx* const* ctx, int world) {
+  if (!ctx || world < 1 || world > PEER_MAXW) return SOSADMM_E_ARG;
+  std::vector<double*> bufs(world);
+  std::vector<unsigned long long*> flags(world);
+  for (int r = 0; r < world; ++r) {
+    if (!ctx[r] || ctx[r]->err || !ctx[r]->sp.emulated || ctx[r]->sp.world != world || ctx[r]->sp.rank != r)
+      return SOSADMM_E_ARG;
+    bufs[r] = ctx[r]->dp.shbuf;
+    flags[r] = ctx[r]->dp.pflags;
+  }
+  for (int r = 0; r < world; ++r)
+    if (peer_wire(ctx[r], bufs, flags)) return ctx[r]->err;
+  return SOSADMM_OK;
+}
+
 extern "C" int sosadmm_debug_group_iterate(sosadmm_ctx* const* ctx, int world, int64_t k) {
   if (!ctx || world < 1 || world > 8) return SOSADMM_E_ARG;
   for (int r = 0; r < world; ++r)
     if (!ctx[r] || ctx[r]->err || !ctx[r]->sp.emulated || ctx[r]->sp.world != world || ctx[r]->sp.rank != r)
       return SOSADMM_E_ARG;
+  if (ctx[0]->sp.peer) {  // every rank publishes its round, then every rank reduces over the peers' buffers
+    for (int64_t it = 0; it < k; ++it) {
+      for (int r = 0; r < world; ++r)
+        if (launch_iteration(ctx[r], 1, nullptr, 1)) return ctx[r]->err;
+      for (int r = 0; r < world; ++r)
+        if (cudaStreamSynchronize(ctx[r]->stream) != cudaSuccess) return SOSADMM_E_CUDA;
+      for (int r = 0; r < world; ++r)
+        if (launch_iteration(ctx[r], 1, nullptr, 2)) return ctx[r]->err;
+      for (int r = 0; r < world; ++r)
+        if (cudaStreamSynchronize(ctx[r]->stream) != cudaSuccess) return SOSADMM_E_CUDA;
+    }
+    return SOSADMM_OK;
+  }
   GroupBufs g{};
   g.world = world;
   for (int r = 0; r < world; ++r) g.buf[r] = ctx[r]->sh.buf;

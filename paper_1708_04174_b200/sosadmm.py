@@ -97,6 +97,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.sosadmm_debug_group_get_iterate.argtypes = [ctypes.POINTER(V), ctypes.c_int, P, P, P, P, P, P,
                                                     ctypes.POINTER(I64)]
     lib.sosadmm_debug_group_get_iterate.restype = ctypes.c_int
+    lib.sosadmm_debug_group_link_peers.argtypes = [ctypes.POINTER(V), ctypes.c_int]
+    lib.sosadmm_debug_group_link_peers.restype = ctypes.c_int
     lib.sosadmm_last_error_message.restype = ctypes.c_char_p
     for f in ["sosadmm_setup", "sosadmm_setup_sharded", "sosadmm_nccl_unique_id", "sosadmm_iterate", "sosadmm_iterate_profiled", "sosadmm_get_info",
               "sosadmm_get_iterate", "sosadmm_set_iterate", "sosadmm_get_structure", "sosadmm_project_affine",
@@ -316,6 +318,15 @@ def group_iterate(solvers, k: int) -> None:
     err = lib.sosadmm_debug_group_iterate(arr, len(solvers), int(k))
     if err != 0:
         raise RuntimeError(f"sosadmm_debug_group_iterate: {lib.sosadmm_strerror(err).decode()} ({err})")
+
+
+def group_link_peers(solvers) -> None:
+    """Switch an emulated group to the peer-memory reduction fused into k_gather_fin_peer (f4)."""
+    lib = load_library()
+    arr = (ctypes.c_void_p * len(solvers))(*[s._ctx.value for s in solvers])
+    err = lib.sosadmm_debug_group_link_peers(arr, len(solvers))
+    if err != 0:
+        raise RuntimeError(f"sosadmm_debug_group_link_peers: {lib.sosadmm_strerror(err).decode()} ({err})")
 
 
 def group_get_iterate(solvers) -> dict:

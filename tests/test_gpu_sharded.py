@@ -64,22 +64,30 @@ def test_sharded_rejects_bad_owner(nccl_id):
         SosAdmm.from_problem(prob, shard=(0, 1, nccl_id, np.array([3], dtype=np.int32)))
 
 
+@pytest.mark.parametrize("peer", [False, True], ids=["devsum", "peer"])
 @pytest.mark.parametrize("name,world,owner", [("lyap10", 2, [1, 0]), ("lyap10", 2, [0, 1]), ("box24", 2, None),
                                               ("box24", 4, None), ("box24", 8, None)])
-def test_sharded_world_n_emulated(name, world, owner):
+def test_sharded_world_n_emulated(name, world, owner, peer):
     """The world >= 2 arithmetic (owned-column partial gathers k_gather_part / k_lowdual_part /
     k_shard_scalars, the 2m + 3 sum, replicated m-phase, owner-only projection) on one GPU:
     every rank's context on the same device, the partial sums added by a device kernel where the product
     path calls ncclAllReduce (NCCL refuses two ranks on one GPU).  20 iterates against the single-GPU path
-    (1e-12: only the summation order of the partial sums differs) and the oracle (1e-9, reading C13)."""
+    (1e-12: only the summation order of the partial sums differs) and the oracle (1e-9, reading C13).
+    peer: the f4 path — each rank's k_gather_fin_peer reads every rank's partial buffer after the
+    per-round flag hand-off (k_peer_signal) and adds them in rank order, fused into the gather's consumer;
+    it must be bit-identical to the device-sum emulation (same rank-order sum)."""
     from paper_1708_04174_b200 import SosAdmm
     from paper_1708_04174_b200.parallel import block_owner
-    from paper_1708_04174_b200.sosadmm import group_get_iterate, group_iterate
+    from paper_1708_04174_b200.sosadmm import group_get_iterate, group_iterate, group_link_peers
 
     prob = make_config(name)
     own = np.array(owner if owner is not None else block_owner(prob.psd_dims, world), dtype=np.int32)
     assert len(set(own.tolist())) == min(world, len(prob.psd_dims))  # every rank that can own a block does
     ranks = [SosAdmm.from_problem(prob, shard=(r, world, None, own)) for r in range(world)]
+    ref_ranks = None
+    if peer:
+        group_link_peers(ranks)
+        ref_ranks = [SosAdmm.from_problem(prob, shard=(r, world, None, own)) for r in range(world)]
     one = SosAdmm.from_problem(prob)
     orc = HsdeOracle.from_problem(prob)
     st = orc.initial_state()
@@ -91,12 +99,15 @@ def test_sharded_world_n_emulated(name, world, owner):
             one.iterate(1)
             g = group_get_iterate(ranks)
             assert g["iter"] == k
+            if ref_ranks is not None:  # peer reduction == device-sum emulation, bit for bit
+                group_iterate(ref_ranks, 1)
+                assert np.array_equal(_state(g), _state(group_get_iterate(ref_ranks))), k
             a, b = _state(g), _state(one.get_iterate())
             ref = np.concatenate([st.u(), st.v()])
             worst_one = max(worst_one, np.linalg.norm(a - b) / np.linalg.norm(b))
             worst_orc = max(worst_orc, np.linalg.norm(a - ref) / np.linalg.norm(ref))
     finally:
-        for r in ranks:
+        for r in ranks + (ref_ranks or []):
             r.close()
         one.close()
     assert worst_one <= 1e-12, worst_one
