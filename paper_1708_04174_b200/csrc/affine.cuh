@@ -31,6 +31,11 @@ struct AffineArgs {
   const int* seg_ptr;
   const int* seg_col;
   const double* seg_val;
+  // alpha-ordered copies of xi and z on the orthogonal columns (entry e of the CSR = column seg_col[e]),
+  // maintained by k_pack so the gather streams its segments contiguously; segpos[col] = e (-1: none)
+  double* xis;
+  double* zs;
+  const int* segpos;
   // A_low: columns low_col[j]; CSR (rows) and CSC (low columns)
   const int* low_col;
   const int* lr_ptr;
@@ -105,13 +110,13 @@ __global__ void __launch_bounds__(GATHER_NT) k_gather(AffineArgs a) {
   double p_pres = 0, p_axi = 0, p_dres = 0, p_by = 0;
   dd bxd{0.0, 0.0};
   if (r < a.m) {
-    const double yr = a.y[r];
+    // the row's scalars first (independent loads in flight together with the segment's)
+    const double yr = a.y[r], sr = a.s[r], br = a.b[r], pinv = a.Pinv[r];
     double gx = 0.0, gz = 0.0, dres = 0.0;
     const int e0 = a.seg_ptr[r], e1 = a.seg_ptr[r + 1];
-    for (int e = e0; e < e1; ++e) {
-      const int j = a.seg_col[e];
+    for (int e = e0; e < e1; ++e) {  // alpha-ordered copies: row r's segment is contiguous
       const double v = a.seg_val[e];
-      const double xj = a.xi[j], zj = a.z[j];
+      const double xj = a.xis[e], zj = a.zs[e];
       gx = fma(v, xj, gx);
       gz = fma(v, zj, gz);
       const double d = fma(v, yr, zj);
@@ -129,16 +134,16 @@ __global__ void __launch_bounds__(GATHER_NT) k_gather(AffineArgs a) {
       axl = fma(v, xj, axl);
     }
     const double g = (gx + gz) + gl;
-    const double r2 = yr + a.s[r];  // w2
-    const double xr = (r2 - g) * a.Pinv[r];
+    const double r2 = yr + sr;  // w2
+    const double xr = (r2 - g) * pinv;
     a.x[r] = xr;
     const double axi = gx + axl;
-    const double pr = axi - a.b[r] * tau;
-    bxd = dd_prod(a.b[r], xr);
+    const double pr = axi - br * tau;
+    bxd = dd_prod(br, xr);
     p_pres = pr * pr;
     p_axi = axi * axi;
     p_dres = dres;
-    p_by = a.b[r] * yr;
+    p_by = br * yr;
   }
   double v;
   const dd bxs = dd_block_sum<GATHER_NT>(bxd, sh);
@@ -492,23 +497,44 @@ __global__ void __launch_bounds__(POS_NT) k_scatter(AffineArgs a, int zero_z) {
   const long long L = (long long)N * (N + 1) / 2;
   const long long col0 = a.blk_col[b];
   double* M = a.mats + a.blk_mat[b];
-  for (int k = threadIdx.x; k < POS_PER_CTA; k += POS_NT) {
-    const long long q = q0 + k;
-    if (q >= L) break;
+  constexpr int PT = POS_PER_CTA / POS_NT;  // positions per thread, q = q0 + tid + t POS_NT
+  // all loads of the thread's positions first (independent: memory-level parallelism), then the writes
+  double v[PT];
+  int ii[PT], jj[PT];
+  {
+    int i, j;
+    svec_ij(q0 + threadIdx.x, i, j);
+#pragma unroll
+    for (int t = 0; t < PT; ++t) {  // advance (i, j) by POS_NT positions without another sqrt
+      ii[t] = i;
+      jj[t] = j;
+      i += POS_NT;
+      while (i > j && j < N) {
+        i -= j + 1;
+        ++j;
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < PT; ++t) {
+    const long long q = q0 + threadIdx.x + t * POS_NT;
+    v[t] = 0.0;
+    if (q >= L) continue;
     const long long col = col0 + q;
     const int code = a.code[col];
-    const double zc = zero_z ? 0.0 : a.z[col];
-    double v;
-    if (code >= 0) v = fma(a.aval[col], a.uhat2[code], a.xi[col]);
-    else if (code == -1) v = a.xi[col];
-    else v = a.ulow[-2 - code] - zc;
-    a.asvec[col - a.t_free] = v;
-    int i, j;
-    svec_ij(q, i, j);
+    if (code >= 0) v[t] = fma(a.aval[col], a.uhat2[code], a.xi[col]);
+    else if (code == -1) v[t] = a.xi[col];
+    else v[t] = a.ulow[-2 - code] - (zero_z ? 0.0 : a.z[col]);
+  }
+#pragma unroll
+  for (int t = 0; t < PT; ++t) {
+    const long long q = q0 + threadIdx.x + t * POS_NT;
+    if (q >= L) continue;
+    a.asvec[col0 + q - a.t_free] = v[t];
     // upper triangle only (column j, row i <= j: consecutive q are consecutive addresses); every
     // projection kernel reads the upper triangle (the Jacobi kernel symmetrically, the cluster
     // tridiagonalisation as "row i of the lower triangle")
-    M[(size_t)j * N + i] = (i == j) ? v : v * SOS_IRT2;
+    M[(size_t)jj[t] * N + ii[t]] = (ii[t] == jj[t]) ? v[t] : v[t] * SOS_IRT2;
   }
 }
 
@@ -523,29 +549,49 @@ __global__ void __launch_bounds__(POS_NT) k_pack(AffineArgs a, double* out_xi, i
   const long long col0 = a.blk_col[b];
   const double* M = a.mats + a.blk_mat[b];
   const int neg = a.side ? a.side[b] : 0;
-  for (int k = threadIdx.x; k < POS_PER_CTA; k += POS_NT) {
-    const long long q = q0 + k;
-    if (q >= L) break;
-    const long long col = col0 + q;
+  constexpr int PT = POS_PER_CTA / POS_NT;
+  double mv[PT], av[PT];
+  int sp[PT];
+  {
     int i, j;
-    svec_ij(q, i, j);
-    // the projection kernels leave their result in the upper triangle (column j, row i <= j)
-    const double mij = M[(size_t)j * N + i];
-    const double sv = (i == j) ? mij : mij * SOS_RT2;
-    const double av = a.asvec[col - a.t_free];
+    svec_ij(q0 + threadIdx.x, i, j);
+#pragma unroll
+    for (int t = 0; t < PT; ++t) {
+      const long long q = q0 + threadIdx.x + t * POS_NT;
+      const bool ok = q < L;
+      // the projection kernels leave their result in the upper triangle (column j, row i <= j)
+      mv[t] = ok ? M[(size_t)j * N + i] * (i == j ? 1.0 : SOS_RT2) : 0.0;
+      av[t] = ok ? a.asvec[col0 + q - a.t_free] : 0.0;
+      sp[t] = (ok && !out_xi) ? a.segpos[col0 + q] : -1;
+      i += POS_NT;
+      while (i > j && j < N) {
+        i -= j + 1;
+        ++j;
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < PT; ++t) {
+    const long long q = q0 + threadIdx.x + t * POS_NT;
+    if (q >= L) continue;
+    const long long col = col0 + q;
     double xn, zn;
     if (neg) {  // M = Pi(-a): z = M, xi = a + M (Moreau decomposition a = Pi(a) - Pi(-a))
-      zn = sv;
-      xn = av + sv;
+      zn = mv[t];
+      xn = av[t] + mv[t];
     } else {    // M = Pi(a): xi = M, z = xi - a
-      xn = sv;
-      zn = sv - av;
+      xn = mv[t];
+      zn = mv[t] - av[t];
     }
     if (out_xi) {
       out_xi[col - a.t_free] = xn;
     } else {
       a.xi[col] = xn;
       a.z[col] = zn;
+      if (sp[t] >= 0) {  // the gather's alpha-ordered copies
+        a.xis[sp[t]] = xn;
+        a.zs[sp[t]] = zn;
+      }
     }
   }
   if (commit && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -554,6 +600,15 @@ __global__ void __launch_bounds__(POS_NT) k_pack(AffineArgs a, double* out_xi, i
     st->kappa = a.is->kappa_new;
     st->iter += 1;
   }
+}
+
+// Refresh the alpha-ordered copies from xi, z (after set_iterate / a restore).
+__global__ void k_seg_copy(AffineArgs a) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= a.seg_ptr[a.m]) return;
+  const int j = a.seg_col[e];
+  a.xis[e] = a.xi[j];
+  a.zs[e] = a.z[j];
 }
 
 // For configurations without PSD positions the commit happens here.

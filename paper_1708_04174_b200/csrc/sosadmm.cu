@@ -93,7 +93,7 @@ struct Analysis {
   int m = 0, n = 0, t = 0, tl = 0, npsd = 0, nblk = 0;
   std::vector<int> code;
   std::vector<double> aval;
-  std::vector<int> seg_ptr, seg_col;
+  std::vector<int> seg_ptr, seg_col, segpos;
   std::vector<double> seg_val;
   std::vector<int> low_col, lr_ptr, lr_idx, lr_col, lc_ptr, lc_row;
   std::vector<double> lr_val, lc_val;
@@ -206,6 +206,7 @@ sosadmm_err analyse(const sosadmm_problem* p, Analysis& an, std::string& msg, co
   an.seg_ptr.assign(an.m + 1, 0);
   for (int r = 0; r < an.m; ++r) an.seg_ptr[r + 1] = an.seg_ptr[r] + cnt[r];
   an.seg_col.resize(an.seg_ptr[an.m]);
+  an.segpos.assign(an.n, -1);
   an.seg_val.resize(an.seg_ptr[an.m]);
   an.D.assign(an.m, 0.0);
   {
@@ -213,6 +214,7 @@ sosadmm_err analyse(const sosadmm_problem* p, Analysis& an, std::string& msg, co
     for (int j = an.t; j < an.n; ++j)
       if (an.code[j] >= 0) {
         const int r = an.code[j];
+        an.segpos[j] = fill[r];
         an.seg_col[fill[r]] = j;
         an.seg_val[fill[r]] = an.aval[j];
         fill[r]++;
@@ -339,7 +341,8 @@ bool spd_inverse(std::vector<double>& K, int t) {
 }
 
 struct DevPtrs {
-  int *seg_ptr, *seg_col, *low_col, *lr_ptr, *lr_idx, *lr_col, *lc_ptr, *lc_row, *empty_cols, *code;
+  int *seg_ptr, *seg_col, *segpos, *low_col, *lr_ptr, *lr_idx, *lr_col, *lc_ptr, *lc_row, *empty_cols, *code;
+  double *xis, *zs;
   double *seg_val, *lr_val, *lc_val, *c_low, *h1_low, *beta_low, *Kinv, *b, *Pinv, *h2, *aval;
   double *xi, *z, *y, *s, *x, *uhat2, *yt, *zt, *ulow, *aty, *part, *asvec, *mats, *tmp, *kpart = nullptr;
   DevState* st;
@@ -424,6 +427,9 @@ void carve(const Analysis& an, Arena& ar, DevPtrs& d, int gather_blocks) {
   const size_t m = an.m, n = an.n, tl = an.tl;
   d.seg_ptr = ar.take<int>(m + 1);
   d.seg_col = ar.take<int>(an.seg_col.size());
+  d.segpos = ar.take<int>(n);
+  d.xis = ar.take<double>(std::max<size_t>(an.seg_col.size(), 1));
+  d.zs = ar.take<double>(std::max<size_t>(an.seg_col.size(), 1));
   d.seg_val = ar.take<double>(an.seg_val.size());
   d.low_col = ar.take<int>(tl);
   d.lr_ptr = ar.take<int>(m + 1);
@@ -865,6 +871,7 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
   cudaStream_t s = c->stream;
   CK_CTX(c, h2d(d.seg_ptr, an.seg_ptr, s));
   CK_CTX(c, h2d(d.seg_col, an.seg_col, s));
+  CK_CTX(c, h2d(d.segpos, an.segpos, s));
   CK_CTX(c, h2d(d.seg_val, an.seg_val, s));
   CK_CTX(c, h2d(d.low_col, an.low_col, s));
   CK_CTX(c, h2d(d.lr_ptr, an.lr_ptr, s));
@@ -908,6 +915,8 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
   CK_CTX(c, cudaMemsetAsync(d.shbuf, 0, sizeof(double) * (2 * (size_t)an.m + 3), s));
   CK_CTX(c, cudaMemsetAsync(d.xi, 0, sizeof(double) * an.n, s));
   CK_CTX(c, cudaMemsetAsync(d.z, 0, sizeof(double) * an.n, s));
+  CK_CTX(c, cudaMemsetAsync(d.xis, 0, sizeof(double) * std::max<size_t>(an.seg_col.size(), 1), s));
+  CK_CTX(c, cudaMemsetAsync(d.zs, 0, sizeof(double) * std::max<size_t>(an.seg_col.size(), 1), s));
   CK_CTX(c, cudaMemsetAsync(d.y, 0, sizeof(double) * an.m, s));
   CK_CTX(c, cudaMemsetAsync(d.s, 0, sizeof(double) * an.m, s));
   CK_CTX(c, cudaMemsetAsync(d.mats, 0, sizeof(double) * std::max<long long>(an.mat_total, 1), s));
@@ -923,6 +932,7 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
   AffineArgs& a = c->aa;
   a.m = an.m; a.n = an.n; a.t_free = an.t; a.tl = an.tl; a.npsd = an.npsd;
   a.seg_ptr = d.seg_ptr; a.seg_col = d.seg_col; a.seg_val = d.seg_val;
+  a.segpos = d.segpos; a.xis = d.xis; a.zs = d.zs;
   a.low_col = d.low_col; a.lr_ptr = d.lr_ptr; a.lr_idx = d.lr_idx; a.lr_col = d.lr_col; a.lr_val = d.lr_val;
   {
     int mx = 0;
@@ -1186,6 +1196,8 @@ sosadmm_err sosadmm_set_iterate(sosadmm_ctx* c, const double* xi, const double* 
   CK_CTX(c, cudaMemcpyAsync(a.y, y, sizeof(double) * a.m, cudaMemcpyHostToDevice, c->stream));
   if (s) CK_CTX(c, cudaMemcpyAsync(a.s, s, sizeof(double) * a.m, cudaMemcpyHostToDevice, c->stream));
   else CK_CTX(c, cudaMemsetAsync(a.s, 0, sizeof(double) * a.m, c->stream));
+  const int nseg = (int)c->an.seg_col.size();
+  if (nseg > 0) k_seg_copy<<<(nseg + 255) / 256, 256, 0, c->stream>>>(a);
   DevState st{};
   st.tau = tau;
   st.kappa = kappa;
@@ -1251,6 +1263,7 @@ sosadmm_err sosadmm_project_affine(sosadmm_ctx* c, const double* w1, const doubl
   *u3 = is.u3;
   CK_CTX(c, cudaMemcpyAsync(a.xi, sxi.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
   CK_CTX(c, cudaMemcpyAsync(a.z, sz.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  if (!c->an.seg_col.empty()) k_seg_copy<<<((int)c->an.seg_col.size() + 255) / 256, 256, 0, s>>>(a);
   CK_CTX(c, cudaMemcpyAsync(a.y, sy.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s));
   CK_CTX(c, cudaMemcpyAsync(a.s, ss.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s));
   CK_CTX(c, cudaMemcpyAsync(a.st, &sst, sizeof(DevState), cudaMemcpyHostToDevice, s));
