@@ -436,7 +436,9 @@ def run_batch(args):
 
 def time_to_tol(prob, device, args):
     """Wall time from setup to the first iterate with max residual <= 1e-4 and |gamma/gamma0 - 1| <= 1e-4
-    (checked every 25 iterations; the solver's own stop rule is residual-only)."""
+    (reading C17; the solver's own stop rule is residual-only, so it is disabled here).  Every
+    iteration is checked: iterate(1), then the residuals of u^k (sosadmm_get_info's check-only pass), the
+    same rule as tests/test_gpu_convergence.py's gamma-accuracy parity against the oracle."""
     import torch
 
     from paper_1708_04174_b200 import SosAdmm
@@ -448,14 +450,15 @@ def time_to_tol(prob, device, args):
     res_stop = None
     k = 0
     while k < args.ttt_max:
-        info = gpu.iterate(25)
+        gpu.iterate(1)
+        info = gpu.info()
         k = info["iter"]
         r = max(info["res_pri"], info["res_dual"], info["res_gap"])
         if res_stop is None and r <= 1e-4:
             res_stop = k
         if r <= 1e-4 and (g0 is None or abs(-info["pobj"] / g0 - 1.0) <= 1e-4):
             return {"seconds": time.perf_counter() - t0, "iters": k, "residual_stop_iters": res_stop,
-                    "gamma": -info["pobj"], "check_stride": 25}
+                    "gamma": -info["pobj"], "check_stride": 1}
     return {"seconds": None, "iters": None, "reached": False, "max_iters": args.ttt_max,
             "residual_stop_iters": res_stop}
 

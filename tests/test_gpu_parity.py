@@ -231,3 +231,30 @@ def test_nonfinite_iterate_reported():
             gpu.iterate(1)
     finally:
         gpu.close()
+
+
+def test_first_iterates_near_max_block():
+    """Near the largest supported block (SOSADMM_MAX_BLOCK = 1280): a planted POP with n = 48 (Gram
+    N = C(50, 2) = 1225, m = C(52, 4) = 270,725; every cluster CTA at its largest row share), 5 iterates
+    against the oracle at the reading-C13 bar, plus the per-block check of xi and z."""
+    from paper_1708_04174_b200 import SosAdmm
+
+    prob = planted_pop("pop48", 48, 19, seed=2)
+    assert prob.psd_dims == [1225] and prob.m == 270725
+    gpu = SosAdmm.from_problem(prob, tol=1e-300, max_iters=1 << 40)
+    orc = HsdeOracle.from_problem(prob)
+    st = orc.initial_state()
+    try:
+        for k in range(1, 6):
+            st = orc.step(st)
+            gpu.iterate(1)
+            g = gpu.get_iterate()
+            ug = np.concatenate([g["xi"], g["y"], [g["tau"]]])
+            vg = np.concatenate([g["z"], g["s"], [g["kappa"]]])
+            scale = np.linalg.norm(np.concatenate([st.u(), st.v()]))
+            assert _rel(ug, st.u(), scale) <= 1e-9 and _rel(vg, st.v(), scale) <= 1e-9, k
+            blk = slice(prob.n_free, prob.n)
+            assert np.linalg.norm(g["xi"][blk] - st.xi[blk]) <= 1e-8 * np.linalg.norm(st.xi[blk]) + 1e-12 * scale
+            assert np.linalg.norm(g["z"][blk] - st.z[blk]) <= 1e-8 * np.linalg.norm(st.z[blk]) + 1e-12 * scale
+    finally:
+        gpu.close()
