@@ -121,7 +121,12 @@ sosadmm_err sosadmm_setup(const sosadmm_problem* prob, const sosadmm_settings* s
  * problem, settings.device = its GPU, the same id and the same block_owner (n_psd entries in
  * [0, world)).  sosadmm_iterate / sosadmm_get_info / sosadmm_get_iterate are collectives on a
  * sharded context (every rank must call them in the same order); sosadmm_get_iterate returns the
- * full iterate on every rank.  The unit entry points return E_ARG on a sharded context. */
+ * full iterate on every rank.  The unit entry points return E_ARG on a sharded context.
+ * SOSADMM_ALLREDUCE=peer (environment, read at setup) replaces the ncclAllReduce by the reduction over
+ * peer memory fused into the gather's consumer: CUDA IPC handles of the workspaces are
+ * exchanged with one ncclAllGather at setup, each iteration every rank publishes its partial sums with a
+ * release store into the peers' flag slots and k_gather_fin_peer adds all ranks' partials in rank
+ * order (requires peer access between the GPUs and a workspace allocated with cudaMalloc). */
 #define SOSADMM_NCCL_ID_BYTES 128
 sosadmm_err sosadmm_nccl_unique_id(void* id);
 sosadmm_err sosadmm_setup_sharded(const sosadmm_problem* prob, const sosadmm_settings* settings, const void* nccl_id,

@@ -177,6 +177,36 @@ def unbounded_pop(name: str, nvars: int) -> Problem:
     return assemble(name, nvars, [con], np.array([-1.0]), dict(kind="unbounded_pop", nvars=nvars))
 
 
+def edge_program(kind: str, seed: int = 0) -> Problem:
+    """Degenerate conic programs of the solver's interface (not SOS-derived), for edge-case parity:
+    * "free":   no PSD block at all, K = R^t (t = 4, m = 3): min c^T x s.t. A x = b with c = A^T y0, so every
+                feasible x is optimal with value y0^T b (closed form);
+    * "detached": a planted POP (n = 3) plus a 4 x 4 PSD block that appears in no constraint (ten empty
+                orthogonal columns, c = 0 on them): same optimum gamma0, the extra block's iterate stays 0."""
+    rng = np.random.default_rng(seed)
+    if kind == "free":
+        A = rng.standard_normal((3, 4))
+        x0, y0 = rng.standard_normal(4), rng.standard_normal(3)
+        b = A @ x0
+        c = A.T @ y0
+        import scipy.sparse as sp_
+
+        return Problem("free", sp_.csc_matrix(A), b, c, 4, [], dict(kind="free", optimum=float(y0 @ b)))
+    if kind == "detached":
+        base = planted_pop("detached", 3, 2, seed)
+        import scipy.sparse as sp_
+
+        A = sp_.hstack([base.A, sp_.csc_matrix((base.m, 10))]).tocsc()
+        c = np.concatenate([base.c, np.zeros(10)])
+        meta = dict(base.meta)
+        meta["kind"] = "detached"
+        prob = Problem("detached", A, base.b.copy(), c, base.n_free, list(base.psd_dims) + [4], meta)
+        prob.row_expo = base.row_expo
+        prob.block_info = base.block_info
+        return prob
+    raise KeyError(kind)
+
+
 def univariate_feasibility(name: str, coeffs: list[float]) -> Problem:
     """Is g0(x) = sum_k coeffs[k] x^k SOS?  (SPEC.md S:169-170 examples.)  t = 0."""
     deg = len(coeffs) - 1

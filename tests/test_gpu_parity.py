@@ -17,7 +17,7 @@ from sosgen.matrix_sos import brute_force_counts, matrix_planted_kkt, matrix_sos
 
 pytestmark = pytest.mark.gpu
 
-SMALL = ["pop6", "sq", "neg", "one", "pop3k2", "ball4", "msos2", "pop8", "unb6"]
+SMALL = ["pop6", "sq", "neg", "one", "pop3k2", "ball4", "msos2", "pop8", "unb6", "free", "detached"]
 LARGE = ["pop20", "lyap10", "box24", "pop40", "msos3", "unb10"]
 
 
@@ -38,6 +38,10 @@ def make(name):
         return matrix_sos_pop("msos2", 3, 2, 2, 2, seed=3)
     if name == "msos3":  # Y in S^{3 * 28} (cluster tridiagonalisation path)
         return matrix_sos_pop("msos3", 6, 3, 2, 3, seed=4)
+    if name in ("free", "detached"):  # degenerate: no PSD block / a block in no constraint (empty columns)
+        from sosgen.configs import edge_program
+
+        return edge_program(name)
     if name.startswith("unb"):  # dual infeasible (unbounded) program: N = 28 (Jacobi) / 66 (large-block path)
         return unbounded_pop(name, int(name[3:]))
     return make_config(name)
@@ -68,6 +72,20 @@ def test_structure_bit_exact(name, solvers):
     if name.startswith("msos"):  # Proposition 2: D = ordered-pair counts of every (alpha, i, j) row
         assert np.array_equal(D, brute_force_counts(prob).astype(np.float64))
         assert np.all(row_of[prob.n_free:] >= 0) and tl == prob.n_free
+        return
+    if name in ("free", "detached"):  # generator-made, not SOS-assembled: structure from A directly
+        A = prob.A.tocsc()
+        cnt = np.diff(A.indptr)
+        exp_row = np.full(prob.n, -2)
+        for j in range(prob.n_free, prob.n):
+            exp_row[j] = A.indices[A.indptr[j]] if cnt[j] == 1 else (-1 if cnt[j] == 0 else -2)
+        assert np.array_equal(row_of.astype(np.int64)[prob.n_free:], exp_row[prob.n_free:])
+        Dref = np.zeros(prob.m)
+        for j in range(prob.n_free, prob.n):
+            if cnt[j] == 1:
+                v = A.data[A.indptr[j]]
+                Dref[A.indices[A.indptr[j]]] += 1.0 if abs(v) == 1.0 else (2.0 if abs(v) == np.sqrt(2.0) else v * v)
+        assert np.array_equal(D, Dref)
         return
     maps, n_alpha = brute_force_structure(prob.row_expo, prob.block_info, prob.m)
     assert np.array_equal(D, n_alpha.astype(np.float64))  # exact integers
@@ -166,7 +184,7 @@ def test_first_20_iterates(name, solvers):
     assert worst_u <= 1e-9 and worst_v <= 1e-9, (worst_u, worst_v)
 
 
-@pytest.mark.parametrize("name", ["pop6", "sq", "neg", "pop3k2", "ball4", "msos2", "unb6", "unb10"])
+@pytest.mark.parametrize("name", ["pop6", "sq", "neg", "pop3k2", "ball4", "msos2", "unb6", "unb10", "free", "detached"])
 def test_convergence_parity(name, solvers):
     prob, gpu, orc = solvers(name, tol=1e-4, max_iters=5000)
     st, status, hist = orc.solve(tol=1e-4, max_iters=5000)

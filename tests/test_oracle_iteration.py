@@ -125,3 +125,27 @@ def test_table2_ball_pop(n):
         f = lambda w: pv(w[:-1] / np.linalg.norm(w[:-1]) / (1 + np.exp(-np.clip(w[-1], -50, 50))))
         best = min(best, minimize(f, w0, method="BFGS", options=dict(gtol=1e-10)).fun)
     assert abs(opt - best) <= 1e-5 * abs(best)
+
+
+def test_edge_program_free_only():
+    """No PSD block (K = R^t): min c^T x s.t. A x = b with c = A^T y0 has the closed-form optimum y0^T b."""
+    from sosgen.configs import edge_program
+
+    prob = edge_program("free")
+    o = HsdeOracle.from_problem(prob)
+    st, status, hist = o.solve(tol=1e-8, max_iters=20000)
+    assert status == Status.OPTIMAL
+    assert abs(hist[-1][3] - prob.meta["optimum"]) <= 1e-6 * max(1.0, abs(prob.meta["optimum"]))
+
+
+def test_edge_program_detached_block():
+    """A PSD block in no constraint (empty orthogonal columns): the optimum is still gamma0 and the
+    detached block's iterate stays exactly zero (its input a = xi stays 0, Pi(0) = 0)."""
+    from sosgen.configs import edge_program
+
+    prob = edge_program("detached")
+    o = HsdeOracle.from_problem(prob)
+    st, status, hist = o.solve(tol=1e-7, max_iters=20000)
+    assert status == Status.OPTIMAL
+    assert abs(-hist[-1][3] - prob.meta["gamma0"]) <= 1e-5
+    assert not st.xi[-10:].any() and not st.z[-10:].any()
