@@ -305,7 +305,9 @@ def run_ours(args):
     phase = dict(zip(PHASES, ph_ms))
     # time to 1e-4 (harness-side rule, C9): fresh solver, chunks of 25 iterations
     ttt = None
-    if rank == 0 and not args.no_ttt and not sharded:
+    # (no gamma0 -- config 2, a feasibility program that is infeasible as written, reading C6 -- has no
+    # time-to-1e-4: the harness would only run out its iteration cap)
+    if rank == 0 and not args.no_ttt and not sharded and prob.meta.get("gamma0") is not None:
         ttt = time_to_tol(prob, local, args)
     if rank != 0:
         return
