@@ -106,6 +106,143 @@ __global__ void k_dc_leaf(DcArgs a, int first_leaf, int nleaves, int buf) {
   }
 }
 
+// Bottom subtrees solved directly (replacing the lowest merge levels, whose kernels are latency-bound:
+// ~7 dependent launches per level for nodes of a few rows).  One CTA per node of size n <= DCJ_MAXN at
+// depth D - L: the node's tridiagonal with the rank-one cuts of its ancestors applied at its boundaries
+// (d_s -= |e_{s-1}|, d_{s+n-1} -= |e_{s+n-1}|, exactly the matrices the level-L merges would have
+// diagonalised), cyclic Jacobi with the round-robin ordering (two barriers per round), then the
+// eigenpairs in ascending order into lam[buf][s..s+n) and the node's diagonal block of Q[buf] — the
+// format every merge expects of its children.  Backward stable (eigen-residual ~ n eps |T|).
+constexpr int DCJ_MAXN = 16;
+constexpr int DCJ_NT = 256;
+__global__ void __launch_bounds__(DCJ_NT) k_dc_jnode(DcArgs a, int node0, int buf) {
+  if (dc_skip(a)) return;
+  const DcNode nd = a.nodes[node0 + blockIdx.x];
+  const int N = a.N, s = nd.s, n = nd.n;
+  const int Np = (n + 1) & ~1, M = Np - 1;
+  __shared__ double A[2][DCJ_MAXN * DCJ_MAXN], V[2][DCJ_MAXN * DCJ_MAXN];
+  __shared__ double cs[DCJ_MAXN], sn[DCJ_MAXN];
+  __shared__ int rot, nrm_done;
+  __shared__ double tinys;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < Np * Np; e += DCJ_NT) {
+    const int i = e % Np, j = e / Np;
+    double v = 0.0;
+    if (i < n && j < n) {
+      if (i == j) {
+        v = a.d[s + i];
+        if (i == 0 && s > 0) v -= fabs(a.e[s - 1]);
+        if (i == n - 1 && s + n < N) v -= fabs(a.e[s + n - 1]);
+      } else if (i == j + 1 || j == i + 1) {
+        v = a.e[s + min(i, j)];
+      }
+    }
+    A[0][e] = v;
+    V[0][e] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();  // A[0] complete before thread 0 reads its diagonal
+  if (tid == 0) {
+    double f = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double di = A[0][i + i * Np];
+      f = fma(di, di, f);
+      if (i + 1 < n) f = fma(2.0 * a.e[s + i], a.e[s + i], f);
+    }
+    // couplings below n eps |T|_F are left: the eigen-residual stays at the backward-error level
+    tinys = fmax((double)n * DC_EPS * sqrt(f), 1e-300);
+    nrm_done = 0;
+  }
+  __syncthreads();
+  const double tiny = tinys;
+  constexpr int PER = DCJ_MAXN * DCJ_MAXN / DCJ_NT;  // element slots per thread (fixed for the solve)
+  int ei[PER], ej[PER];
+#pragma unroll
+  for (int c = 0; c < PER; ++c) {
+    const int e = tid + c * DCJ_NT;
+    ei[c] = e % Np;
+    ej[c] = e / Np;
+  }
+  int cur = 0;
+  for (int sweep = 0; sweep < 60 && n > 1; ++sweep) {
+    if (tid == 0) rot = 0;
+    __syncthreads();
+    int r2 = 0;  // 2 r mod M
+    for (int r = 0; r < M; ++r, r2 = (r2 + 2 >= M) ? r2 + 2 - M : r2 + 2) {
+      const double* Ac = A[cur];
+      // rotation parameters of this round's pairs (one thread per pair): pairs p + q = 2 r (mod M), M vs r
+      if (tid < Np / 2) {
+        int p, q;
+        if (tid == 0) {
+          p = M;
+          q = r;
+        } else {
+          p = r + tid;
+          p -= p >= M ? M : 0;
+          q = r - tid;
+          q += q < 0 ? M : 0;
+        }
+        const double apq = Ac[p + q * Np], app = Ac[p + p * Np], aqq = Ac[q + q * Np];
+        double c = 1.0, sg = 0.0;
+        if (apq != 0.0 && fabs(apq) > tiny && apq * apq > DC_EPS * DC_EPS * fabs(app * aqq)) {
+          const double th = (aqq - app) / (2.0 * apq);
+          const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(fma(th, th, 1.0)));
+          c = rsqrt(fma(t, t, 1.0));
+          sg = t * c;
+          rot = 1;
+        }
+        cs[p] = c;
+        sn[p] = -sg;
+        cs[q] = c;
+        sn[q] = sg;
+      }
+      __syncthreads();
+      // A' = J^T A J and V' = V J elementwise (J: the round's disjoint rotations); the rotated couplings
+      // become exact zeros
+      double* An = A[cur ^ 1];
+      const double* Vc = V[cur];
+      double* Vn = V[cur ^ 1];
+      auto partner = [&](int i) {
+        if (i == M) return r;
+        int t = r2 - i;
+        t += t < 0 ? M : 0;
+        return t == i ? M : t;
+      };
+#pragma unroll
+      for (int c = 0; c < PER; ++c) {
+        const int e = tid + c * DCJ_NT;
+        if (e >= Np * Np) break;
+        const int i = ei[c], j = ej[c];
+        const int ip = partner(i), jp = partner(j);
+        const double ci = cs[i], si = sn[i], cj = cs[j], sj = sn[j];
+        double v = ci * (cj * Ac[i + j * Np] + sj * Ac[i + jp * Np]) + si * (cj * Ac[ip + j * Np] + sj * Ac[ip + jp * Np]);
+        if (j == ip && si != 0.0) v = 0.0;
+        An[e] = v;
+        Vn[e] = cj * Vc[i + j * Np] + sj * Vc[i + jp * Np];
+      }
+      cur ^= 1;
+      __syncthreads();
+    }
+    const int any = rot;
+    __syncthreads();  // every thread has read the flag before thread 0 resets it for the next sweep
+    if (!any) break;
+  }
+  // ascending order: rank of each eigenvalue (ties by index), eigenvector columns into Q[buf]
+  const double* Af = A[cur];
+  const double* Vf = V[cur];
+  double* Q = a.Q[buf];
+  for (int j = tid; j < n; j += DCJ_NT) {
+    const double lj = Af[j + j * Np];
+    int rank = 0;
+    for (int i = 0; i < n; ++i) {
+      const double li = Af[i + i * Np];
+      rank += (li < lj) || (li == lj && i < j);
+    }
+    a.lam[buf][s + rank] = lj;
+    for (int i = 0; i < n; ++i) Q[(size_t)(s + rank) * N + (s + i)] = Vf[i + j * Np];
+  }
+  (void)nrm_done;
+}
+
 // ordered stream compaction over [0, n) by one CTA of DC_NT threads: out[rank] = map(i) for the i
 // with pred(i), in increasing i; returns the count (every thread).  wcnt: DC_NT/32 ints of SMEM.
 template <class P, class M>

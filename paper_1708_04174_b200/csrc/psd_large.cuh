@@ -51,6 +51,7 @@ struct LargeBlock {
   double *V2 = nullptr, *tau2 = nullptr, *Bg = nullptr;
   unsigned* cnt = nullptr;
   std::vector<int> node_n;  // host copy: size of every D&C node (index = node id), for the work accounting
+  int jl = 0;               // levels 1..jl are replaced by the Jacobi solve of their output nodes (k_dc_jnode)
 };
 
 struct LargeEig {
@@ -331,6 +332,9 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     lb.node_n.clear();
     for (const DcNode& nd : nodes) lb.node_n.push_back(nd.n);
     lb.D = D;
+    lb.jl = 0;
+    for (int h = 1; h < D; ++h)
+      if (lmax[h] <= DCJ_MAXN) lb.jl = h;
     lb.level_node0 = l0;
     lb.level_nn = lnn;
     lb.level_nmax = lmax;
@@ -553,9 +557,12 @@ inline void large_block_dc(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool ch
     cudaMemsetAsync(lb.dc.Q[0], 0, sizeof(double) * N * N, s);
     cudaMemsetAsync(lb.dc.Q[1], 0, sizeof(double) * N * N, s);
   }
-  k_dc_leaf<<<(lb.nleaves + 127) / 128, 128, 0, s>>>(lb.dc, lb.leaf0, lb.nleaves, 0);
+  if (lb.jl > 0)  // the bottom subtrees in one launch: their root nodes' eigenpairs by Jacobi
+    k_dc_jnode<<<lb.level_nn[lb.jl], DCJ_NT, 0, s>>>(lb.dc, lb.level_node0[lb.jl], lb.jl & 1);
+  else
+    k_dc_leaf<<<(lb.nleaves + 127) / 128, 128, 0, s>>>(lb.dc, lb.leaf0, lb.nleaves, 0);
   const int wblocks = (N * 32 + DC_NT - 1) / DC_NT;
-  for (int h = 1; h <= lb.D; ++h) {
+  for (int h = lb.jl + 1; h <= lb.D; ++h) {
     const int ob = (h - 1) & 1, nb = h & 1;
     const int n0 = lb.level_node0[h], nn = lb.level_nn[h], nmax = lb.level_nmax[h];
     const bool two = side != nullptr;
@@ -666,7 +673,7 @@ inline void large_eig_launch_concurrent(LargeEig& le, cudaStream_t s, bool check
 inline int large_eig_launches(const LargeEig& le) {
   int k = 0;
   for (const auto& lb : le.blocks)
-    k += (lb.two ? 3 : (lb.ksw < lb.N - 2 ? 2 : 1)) + 2 + 1 + 7 * lb.D + 1 + 5 + (lb.two ? 1 : 0);
+    k += (lb.two ? 3 : (lb.ksw < lb.N - 2 ? 2 : 1)) + 2 + 1 + 7 * (lb.D - lb.jl) + 1 + 5 + (lb.two ? 1 : 0);
   return k;
 }
 
@@ -685,7 +692,7 @@ inline int large_block_work(const LargeBlock& lb, cudaStream_t s, double* w) {
       cudaMemcpyAsync(sel, lb.sel, 12, cudaMemcpyDeviceToHost, s) || cudaStreamSynchronize(s))
     return 1;
   double dc = 0.0, zero = 0.0;
-  for (int h = 1; h <= lb.D; ++h)
+  for (int h = lb.jl + 1; h <= lb.D; ++h)
     for (int t = 0; t < lb.level_nn[h]; ++t) {
       const int id = lb.level_node0[h] + t;
       const double n = lb.node_n[id], k = nk[id];

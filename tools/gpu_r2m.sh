@@ -1,0 +1,3 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_stages.py -q -x -k "stedc" > gpurun_out/r2m_stedc.log 2>&1; echo stedc=$?
+for c in pop20 lyap10 box24 pop40; do timeout 600 python bench.py --config $c --steps 20 --warmup 5 --no-ttt --no-cpu > gpurun_out/r2m_cfg_$c.log 2>&1; echo $c=$?; done
