@@ -46,7 +46,8 @@ def _nccl_include() -> list:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
-    cmd = [_nvcc()] + NVCC_FLAGS + _nccl_include() + ["-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES] + ["-ldl"]
+    extra = os.environ.get("SOSADMM_NVCC_EXTRA", "").split()  # experiments only (e.g. -DTRD_SUSPEND_NS=...)
+    cmd = [_nvcc()] + NVCC_FLAGS + extra + _nccl_include() + ["-o", LIB] + [os.path.join(CSRC, s) for s in SOURCES] + ["-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     r = subprocess.run(cmd, capture_output=True, text=True)
