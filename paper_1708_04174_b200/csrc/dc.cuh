@@ -107,140 +107,125 @@ __global__ void k_dc_leaf(DcArgs a, int first_leaf, int nleaves, int buf) {
 }
 
 // Bottom subtrees solved directly (replacing the lowest merge levels, whose kernels are latency-bound:
-// ~7 dependent launches per level for nodes of a few rows).  One CTA per node of size n <= DCJ_MAXN at
+// ~7 dependent launches per level for nodes of a few rows).  One warp per node of size n <= DCJ_MAXN at
 // depth D - L: the node's tridiagonal with the rank-one cuts of its ancestors applied at its boundaries
 // (d_s -= |e_{s-1}|, d_{s+n-1} -= |e_{s+n-1}|, exactly the matrices the level-L merges would have
-// diagonalised), cyclic Jacobi with the round-robin ordering (two barriers per round), then the
-// eigenpairs in ascending order into lam[buf][s..s+n) and the node's diagonal block of Q[buf] — the
-// format every merge expects of its children.  Backward stable (eigen-residual ~ n eps |T|).
+// diagonalised), then the implicit symmetric QR iteration with the Wilkinson shift (Golub-Van Loan,
+// "implicit symmetric QR step with Wilkinson shift" + deflation of negligible off-diagonals) on the
+// tridiagonal itself, and the eigenpairs in ascending order into lam[buf][s..s+n) and the node's
+// diagonal block of Q[buf] — the format every merge expects of its children.
+//   * step k of a chase: R = [[c, s], [-s, c]] with R [x; z] = [r; 0] on rows / columns (k, k+1): the
+//     2 x 2 block (a, b; b, g) -> (c^2 a + 2cs b + s^2 g, cs (g - a) + (c^2 - s^2) b; ., s^2 a - 2cs b +
+//     c^2 g), the coupling f = e_{k+1} -> c f and the bulge s f at (k+2, k); Z <- Z R^T;
+//   * the scalars (d, e in shared memory, the running a, b, x, z in registers) are computed redundantly
+//     by every lane; lane i owns row i of Z (shared memory, column-major by lane: conflict-free);
+//   * deflation: lane i tests e_i (|e_i| <= eps (|d_i| + |d_{i+1}|) or <= eps ||T||) and a ballot
+//     gives the unreduced trailing block [l, h]; the eigen-residual stays at the backward-error level
+//     n eps ||T|| of the merges above.
+// (Rounds 1-2 solved these nodes by cyclic Jacobi in a 256-thread CTA: ~60 us per launch in the graph,
+// ~110 rounds of two barriers each.)
 constexpr int DCJ_MAXN = 16;
-constexpr int DCJ_NT = 256;
-__global__ void __launch_bounds__(DCJ_NT) k_dc_jnode(DcArgs a, int node0, int buf) {
+constexpr int DCJ_NT = 32;
+__global__ void __launch_bounds__(DCJ_NT) k_dc_qrnode(DcArgs a, int node0, int buf) {
   if (dc_skip(a)) return;
+  constexpr int NM = DCJ_MAXN;
+  constexpr unsigned FULL = 0xffffffffu;
+  __shared__ double ds[NM + 1], es[NM + 1];
+  __shared__ double Zs[NM][32];
   const DcNode nd = a.nodes[node0 + blockIdx.x];
-  const int N = a.N, s = nd.s, n = nd.n;
-  const int Np = (n + 1) & ~1, M = Np - 1;
-  __shared__ double A[2][DCJ_MAXN * DCJ_MAXN], V[2][DCJ_MAXN * DCJ_MAXN];
-  __shared__ double cs[DCJ_MAXN], sn[DCJ_MAXN];
-  __shared__ int rot, nrm_done;
-  __shared__ double tinys;
-  const int tid = threadIdx.x;
-  for (int e = tid; e < Np * Np; e += DCJ_NT) {
-    const int i = e % Np, j = e / Np;
-    double v = 0.0;
-    if (i < n && j < n) {
-      if (i == j) {
-        v = a.d[s + i];
-        if (i == 0 && s > 0) v -= fabs(a.e[s - 1]);
-        if (i == n - 1 && s + n < N) v -= fabs(a.e[s + n - 1]);
-      } else if (i == j + 1 || j == i + 1) {
-        v = a.e[s + min(i, j)];
-      }
-    }
-    A[0][e] = v;
-    V[0][e] = (i == j) ? 1.0 : 0.0;
+  const int N = a.N, s = nd.s, n = nd.n, lane = threadIdx.x;
+  double dv = 0.0, ev = 0.0;
+  if (lane < n) {
+    dv = a.d[s + lane];
+    if (lane == 0 && s > 0) dv -= fabs(a.e[s - 1]);
+    if (lane == n - 1 && s + n < N) dv -= fabs(a.e[s + n - 1]);
   }
-  __syncthreads();  // A[0] complete before thread 0 reads its diagonal
-  if (tid == 0) {
-    double f = 0.0;
-    for (int i = 0; i < n; ++i) {
-      const double di = A[0][i + i * Np];
-      f = fma(di, di, f);
-      if (i + 1 < n) f = fma(2.0 * a.e[s + i], a.e[s + i], f);
-    }
-    // couplings below n eps |T|_F are left: the eigen-residual stays at the backward-error level
-    tinys = fmax((double)n * DC_EPS * sqrt(f), 1e-300);
-    nrm_done = 0;
+  if (lane + 1 < n) ev = a.e[s + lane];
+  if (lane <= NM) {
+    ds[lane] = dv;
+    es[lane] = ev;
   }
-  __syncthreads();
-  const double tiny = tinys;
-  constexpr int PER = DCJ_MAXN * DCJ_MAXN / DCJ_NT;  // element slots per thread (fixed for the solve)
-  int ei[PER], ej[PER];
 #pragma unroll
-  for (int c = 0; c < PER; ++c) {
-    const int e = tid + c * DCJ_NT;
-    ei[c] = e % Np;
-    ej[c] = e / Np;
-  }
-  int cur = 0;
-  for (int sweep = 0; sweep < 60 && n > 1; ++sweep) {
-    if (tid == 0) rot = 0;
-    __syncthreads();
-    int r2 = 0;  // 2 r mod M
-    for (int r = 0; r < M; ++r, r2 = (r2 + 2 >= M) ? r2 + 2 - M : r2 + 2) {
-      const double* Ac = A[cur];
-      // rotation parameters of this round's pairs (one thread per pair): pairs p + q = 2 r (mod M), M vs r
-      if (tid < Np / 2) {
-        int p, q;
-        if (tid == 0) {
-          p = M;
-          q = r;
-        } else {
-          p = r + tid;
-          p -= p >= M ? M : 0;
-          q = r - tid;
-          q += q < 0 ? M : 0;
-        }
-        const double apq = Ac[p + q * Np], app = Ac[p + p * Np], aqq = Ac[q + q * Np];
-        double c = 1.0, sg = 0.0;
-        if (apq != 0.0 && fabs(apq) > tiny && apq * apq > DC_EPS * DC_EPS * fabs(app * aqq)) {
-          const double th = (aqq - app) / (2.0 * apq);
-          const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(fma(th, th, 1.0)));
-          c = rsqrt(fma(t, t, 1.0));
-          sg = t * c;
-          rot = 1;
-        }
-        cs[p] = c;
-        sn[p] = -sg;
-        cs[q] = c;
-        sn[q] = sg;
-      }
-      __syncthreads();
-      // A' = J^T A J and V' = V J elementwise (J: the round's disjoint rotations); the rotated couplings
-      // become exact zeros
-      double* An = A[cur ^ 1];
-      const double* Vc = V[cur];
-      double* Vn = V[cur ^ 1];
-      auto partner = [&](int i) {
-        if (i == M) return r;
-        int t = r2 - i;
-        t += t < 0 ? M : 0;
-        return t == i ? M : t;
-      };
+  for (int k = 0; k < NM; ++k) Zs[k][lane] = (k == lane) ? 1.0 : 0.0;
+  double dm = fabs(dv), em = fabs(ev);
 #pragma unroll
-      for (int c = 0; c < PER; ++c) {
-        const int e = tid + c * DCJ_NT;
-        if (e >= Np * Np) break;
-        const int i = ei[c], j = ej[c];
-        const int ip = partner(i), jp = partner(j);
-        const double ci = cs[i], si = sn[i], cj = cs[j], sj = sn[j];
-        double v = ci * (cj * Ac[i + j * Np] + sj * Ac[i + jp * Np]) + si * (cj * Ac[ip + j * Np] + sj * Ac[ip + jp * Np]);
-        if (j == ip && si != 0.0) v = 0.0;
-        An[e] = v;
-        Vn[e] = cj * Vc[i + j * Np] + sj * Vc[i + jp * Np];
-      }
-      cur ^= 1;
-      __syncthreads();
-    }
-    const int any = rot;
-    __syncthreads();  // every thread has read the flag before thread 0 resets it for the next sweep
-    if (!any) break;
+  for (int o = 16; o > 0; o >>= 1) {
+    dm = fmax(dm, __shfl_xor_sync(FULL, dm, o));
+    em = fmax(em, __shfl_xor_sync(FULL, em, o));
   }
-  // ascending order: rank of each eigenvalue (ties by index), eigenvector columns into Q[buf]
-  const double* Af = A[cur];
-  const double* Vf = V[cur];
-  double* Q = a.Q[buf];
-  for (int j = tid; j < n; j += DCJ_NT) {
-    const double lj = Af[j + j * Np];
-    int rank = 0;
+  const double floor_abs = DC_EPS * fma(2.0, em, dm);
+  __syncwarp();
+  for (int it = 0; it < 30 * NM; ++it) {
+    bool nz = false;
+    if (lane + 1 < n) {
+      const double ae = fabs(es[lane]);
+      if (ae <= DC_EPS * (fabs(ds[lane]) + fabs(ds[lane + 1])) || ae <= floor_abs) es[lane] = 0.0;
+      else nz = true;
+    }
+    const unsigned m = __ballot_sync(FULL, nz);
+    __syncwarp();
+    if (m == 0) break;
+    const int h = 32 - __clz(m);                          // e_{h-1} != 0, e_h = 0
+    const unsigned below = ~m & ((1u << (h - 1)) - 1u);  // zero couplings below h - 1
+    const int l = below ? 32 - __clz(below) : 0;          // the unreduced block is [l, h]
+    // Wilkinson shift from the trailing 2 x 2 block (d_{h-1}, e_{h-1}; e_{h-1}, d_h)
+    const double dh1 = ds[h - 1], dh = ds[h], eh = es[h - 1];
+    const double del = 0.5 * (dh1 - dh);
+    const double h2 = fma(del, del, eh * eh);  // > 0: e_{h-1} is not negligible
+    const double hy = h2 * rsqrt(h2);
+    const double mu = dh - eh * eh / (del + (del >= 0.0 ? hy : -hy));
+    double av = ds[l], bv = es[l];  // running d_k, e_k
+    double x = av - mu, zz = bv;
+    double zk = Zs[l][lane];        // running z_k of this lane's row
+    for (int k = l; k < h; ++k) {
+      const double gv = ds[k + 1];
+      const double f = (k + 1 < h) ? es[k + 1] : 0.0;
+      const double zk1 = Zs[k + 1][lane];
+      // the chain x -> x' needs only 1 / r^2: b' = (x z (g - a) + (x^2 - z^2) b) / r^2
+      const double r2 = fma(x, x, zz * zz);
+      const double num = fma(x * zz, gv - av, (x - zz) * (x + zz) * bv);
+      double c = 1.0, sn = 0.0, r = 0.0, bn = bv;
+      if (r2 > 0.0) {
+        const double ri = rsqrt(r2);
+        c = x * ri;
+        sn = zz * ri;
+        r = r2 * ri;
+        bn = num * (ri * ri);
+      }
+      if (k > l) es[k - 1] = r;
+      const double cc = c * c, ss = sn * sn, csb = 2.0 * c * sn * bv;
+      ds[k] = fma(ss, gv, fma(cc, av, csb));
+      av = fma(ss, av, fma(cc, gv, -csb));
+      Zs[k][lane] = fma(c, zk, sn * zk1);
+      zk = fma(-sn, zk, c * zk1);
+      if (k + 1 < h) {
+        zz = sn * f;
+        bv = c * f;
+        x = bn;
+      } else {
+        ds[k + 1] = av;
+        es[k] = bn;
+        Zs[k + 1][lane] = zk;
+      }
+    }
+    __syncwarp();
+  }
+  // ascending order (ties by index): lane j ranks eigenvalue j, then the columns go out contiguously
+  int rank = 0;
+  double lj = 0.0;
+  if (lane < n) {
+    lj = ds[lane];
     for (int i = 0; i < n; ++i) {
-      const double li = Af[i + i * Np];
-      rank += (li < lj) || (li == lj && i < j);
+      const double li = ds[i];
+      rank += (li < lj) || (li == lj && i < lane);
     }
     a.lam[buf][s + rank] = lj;
-    for (int i = 0; i < n; ++i) Q[(size_t)(s + rank) * N + (s + i)] = Vf[i + j * Np];
   }
-  (void)nrm_done;
+  double* Q = a.Q[buf];
+  for (int j = 0; j < n; ++j) {
+    const int rj = __shfl_sync(FULL, rank, j);
+    if (lane < n) Q[(size_t)(s + rj) * N + (s + lane)] = Zs[j][lane];
+  }
 }
 
 // ordered stream compaction over [0, n) by one CTA of DC_NT threads: out[rank] = map(i) for the i

@@ -51,7 +51,7 @@ struct LargeBlock {
   double *V2 = nullptr, *tau2 = nullptr, *Bg = nullptr;
   unsigned* cnt = nullptr;
   std::vector<int> node_n;  // host copy: size of every D&C node (index = node id), for the work accounting
-  int jl = 0;               // levels 1..jl are replaced by the Jacobi solve of their output nodes (k_dc_jnode)
+  int jl = 0;               // levels 1..jl are replaced by the Jacobi solve of their output nodes (k_dc_qrnode)
 };
 
 struct LargeEig {
@@ -558,7 +558,7 @@ inline void large_block_dc(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool ch
     cudaMemsetAsync(lb.dc.Q[1], 0, sizeof(double) * N * N, s);
   }
   if (lb.jl > 0)  // the bottom subtrees in one launch: their root nodes' eigenpairs by Jacobi
-    k_dc_jnode<<<lb.level_nn[lb.jl], DCJ_NT, 0, s>>>(lb.dc, lb.level_node0[lb.jl], lb.jl & 1);
+    k_dc_qrnode<<<lb.level_nn[lb.jl], DCJ_NT, 0, s>>>(lb.dc, lb.level_node0[lb.jl], lb.jl & 1);
   else
     k_dc_leaf<<<(lb.nleaves + 127) / 128, 128, 0, s>>>(lb.dc, lb.leaf0, lb.nleaves, 0);
   const int wblocks = (N * 32 + DC_NT - 1) / DC_NT;
