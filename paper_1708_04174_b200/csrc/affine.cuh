@@ -103,7 +103,7 @@ constexpr int POS_PER_CTA = 1024;
 //   x_alpha  = (y_alpha + s_alpha + b_alpha w3 - g_alpha) / P_alpha
 // and, for the residuals of u^k (reading C9), (A xi)_alpha and sum_{j in seg(alpha)} (A^T y + z)_j^2.
 __global__ void __launch_bounds__(GATHER_NT) k_gather(AffineArgs a) {
-  __shared__ double sh[2 * (GATHER_NT / 32)];
+  __shared__ double sh[6 * (GATHER_NT / 32)];
   if (a.st->done) return;
   const double tau = a.st->tau;
   const int r = blockIdx.x * GATHER_NT + threadIdx.x;
@@ -145,20 +145,7 @@ __global__ void __launch_bounds__(GATHER_NT) k_gather(AffineArgs a) {
     p_dres = dres;
     p_by = br * yr;
   }
-  double v;
-  const dd bxs = dd_block_sum<GATHER_NT>(bxd, sh);
-  if (threadIdx.x == 0) {
-    a.part[PART_BX * a.gather_blocks + blockIdx.x] = bxs.hi;
-    a.part[PART_BXLO * a.gather_blocks + blockIdx.x] = bxs.lo;
-  }
-  v = block_sum<GATHER_NT>(p_pres, sh);
-  if (threadIdx.x == 0) a.part[PART_PRES * a.gather_blocks + blockIdx.x] = v;
-  v = block_sum<GATHER_NT>(p_axi, sh);
-  if (threadIdx.x == 0) a.part[PART_AXI * a.gather_blocks + blockIdx.x] = v;
-  v = block_sum<GATHER_NT>(p_dres, sh);
-  if (threadIdx.x == 0) a.part[PART_DRES * a.gather_blocks + blockIdx.x] = v;
-  v = block_sum<GATHER_NT>(p_by, sh);
-  if (threadIdx.x == 0) a.part[PART_BY * a.gather_blocks + blockIdx.x] = v;
+  gather_part_sums<GATHER_NT>(bxd, p_pres, p_axi, p_dres, p_by, sh, a.part, a.gather_blocks, blockIdx.x, false, 0.0);
 }
 
 // k_lowT: one warp per low column j:  y_t[j] = (A_low^T x)_j,  aty[j] = (A_low^T y)_j.
@@ -292,62 +279,74 @@ __global__ void __launch_bounds__(256) k_kinv_sum(AffineArgs a) {
 // 2 = affine-only (unit entry point: no termination logic, no writes to xi/z).
 constexpr int TP_NT = 512;
 __global__ void __launch_bounds__(TP_NT) k_tphase(AffineArgs a, int mode) {
-  __shared__ double sh[2 * (TP_NT / 32)];
   __shared__ double bc[10];
   DevState* st = a.st;
   if (st->done) return;
   const int tid = threadIdx.x;
-  // 1. fixed-order reductions of the gather partials (b^T x in double-double)
-  double sums[NPART];
-  for (int k = 0; k < NPART; ++k) {
-    if (k == PART_BX || k == PART_BXLO) continue;
-    double v = 0.0;
-    for (int i = tid; i < a.gather_blocks; i += TP_NT) v += a.part[k * a.gather_blocks + i];
-    v = block_sum<TP_NT>(v, sh);
-    if (tid == 0) bc[k] = v;
-  }
-  {
-    dd v{0.0, 0.0};
-    for (int i = tid; i < a.gather_blocks; i += TP_NT)
-      v = dd_add(v, dd{a.part[PART_BX * a.gather_blocks + i], a.part[PART_BXLO * a.gather_blocks + i]});
-    v = dd_block_sum<TP_NT>(v, sh);
-    if (tid == 0) {
-      bc[PART_BX] = v.hi;
-      bc[PART_BXLO] = v.lo;
-    }
+  // 1. fixed-order reductions of the gather partials (b^T x in double-double) and of the low-column
+  //    sums: the trees of block_sum / dd_block_sum (per-warp shuffle tree, then the warp partials in
+  //    warp order — the same bits), all values at once behind ONE barrier (the loads issued together)
+  constexpr int NW = TP_NT / 32;
+  __shared__ double shp[7][NW], shd[2][NW];
+  const int gb = a.gather_blocks;
+  double vals[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // PRES, AXI, DRES, BY, c^T xi, dl, dl0
+  dd bxv{0.0, 0.0};
+  for (int i = tid; i < gb; i += TP_NT) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) vals[q] += a.part[(PART_PRES + q) * gb + i];
+    bxv = dd_add(bxv, dd{a.part[PART_BX * gb + i], a.part[PART_BXLO * gb + i]});
   }
   // low / free columns: c^T xi, dual residual of low columns, (A_low xi part already in gather)
   const double tau = st->tau, kappa = st->kappa, w3 = tau + kappa;
-  double cx = 0.0, dl = 0.0, dl0 = 0.0;
   const bool sharded = a.shard_scal != nullptr;  // low-column dual sums arrive all-reduced
   for (int j = tid; j < a.tl; j += TP_NT) {
     const int col = a.low_col[j];
     const double cj = a.c_low[j];
-    cx = fma(cj, a.xi[col], cx);  // c vanishes off the (replicated) free columns
+    vals[4] = fma(cj, a.xi[col], vals[4]);  // c vanishes off the (replicated) free columns
     if (!sharded) {
       const double d0 = a.aty[j] + a.z[col];
       const double d = d0 - cj * tau;
-      dl = fma(d, d, dl);
-      dl0 = fma(d0, d0, dl0);
+      vals[5] = fma(d, d, vals[5]);
+      vals[6] = fma(d0, d0, vals[6]);
     }
   }
   if (!sharded)
     for (int j = tid; j < a.n_empty; j += TP_NT) {
       const double zj = a.z[a.empty_cols[j]];
-      dl = fma(zj, zj, dl);
-      dl0 = fma(zj, zj, dl0);
+      vals[5] = fma(zj, zj, vals[5]);
+      vals[6] = fma(zj, zj, vals[6]);
     }
-  cx = block_sum<TP_NT>(cx, sh);
-  if (tid == 0) bc[7] = cx;
-  dl = block_sum<TP_NT>(dl, sh);
-  if (tid == 0) bc[8] = sharded ? a.shard_scal[1] : dl;
-  dl0 = block_sum<TP_NT>(dl0, sh);
-  if (tid == 0) bc[9] = sharded ? a.shard_scal[2] : dl0;
+#pragma unroll
+  for (int q = 0; q < 7; ++q)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) vals[q] += __shfl_down_sync(0xffffffffu, vals[q], o);
+  bxv = dd_warp_sum(bxv);
+  {
+    const int w = tid >> 5, l = tid & 31;
+    if (l == 0) {
+#pragma unroll
+      for (int q = 0; q < 7; ++q) shp[q][w] = vals[q];
+      shd[0][w] = bxv.hi;
+      shd[1][w] = bxv.lo;
+    }
+  }
   __syncthreads();
+  if (tid < 7) {
+    double r = 0.0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) r += shp[tid][i];
+    const int slot = tid < 4 ? PART_PRES + tid : 3 + tid;  // bc[1..4] parts, bc[7..9] low sums
+    bc[slot] = (sharded && tid >= 5) ? a.shard_scal[tid - 4] : r;
+  } else if (tid == 32) {
+    dd r{0.0, 0.0};
+    for (int i = 0; i < NW; ++i) r = dd_add(r, dd{shd[0][i], shd[1][i]});
+    bc[PART_BX] = r.hi;
+    bc[PART_BXLO] = r.lo;
+  }
+  __syncthreads();
+  double sums[NPART];
   for (int k = 0; k < NPART; ++k) sums[k] = bc[k];
-  cx = bc[7];
-  dl = bc[8];
-  dl0 = bc[9];
+  const double cx = bc[7], dl = bc[8], dl0 = bc[9];
 
   // 2. residuals of u^k and the termination rule (reading C9)
   if (mode != 2 && tid == 0) {
@@ -406,13 +405,26 @@ __global__ void __launch_bounds__(TP_NT) k_tphase(AffineArgs a, int mode) {
     bz = dd_add(bz, dd_prod(a.beta_low[j], a.zt[j]));
     cq = dd_add(cq, dd_prod(a.c_low[j], q1));
   }
-  bz = dd_block_sum<TP_NT>(bz, sh);
+  bz = dd_warp_sum(bz);
+  cq = dd_warp_sum(cq);
+  {
+    const int w = tid >> 5, l = tid & 31;
+    __syncthreads();  // shp is reused
+    if (l == 0) {
+      shp[0][w] = bz.hi;
+      shp[1][w] = bz.lo;
+      shp[2][w] = cq.hi;
+      shp[3][w] = cq.lo;
+    }
+    __syncthreads();
+  }
   if (tid == 0) {
+    bz = dd{0.0, 0.0};
+    cq = dd{0.0, 0.0};
+    for (int i = 0; i < NW; ++i) bz = dd_add(bz, dd{shp[0][i], shp[1][i]});
+    for (int i = 0; i < NW; ++i) cq = dd_add(cq, dd{shp[2][i], shp[3][i]});
     bc[0] = bz.hi;
     bc[1] = bz.lo;
-  }
-  cq = dd_block_sum<TP_NT>(cq, sh);
-  if (tid == 0) {
     // zeta^T q = c^T q_1 - b^T q_2 = cq - (bx - bz), all in double-double
     dd bq2 = dd_add(dd{sums[PART_BX], sums[PART_BXLO]}, dd{-bc[0], -bc[1]});
     dd zq = dd_add(cq, dd{-bq2.hi, -bq2.lo});

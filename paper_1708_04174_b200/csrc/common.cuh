@@ -129,3 +129,44 @@ __device__ __forceinline__ dd dd_block_sum(dd v, double* sh) {  // sh: 2 * NT/32
     for (int i = 0; i < NT / 32; ++i) r = dd_add(r, dd{sh[2 * i], sh[2 * i + 1]});
   return r;  // valid in thread 0
 }
+
+// The five per-CTA partials of the gather (b^T x in double-double, then pres, axi, dres, by) with the
+// trees of dd_block_sum / block_sum — per-warp shuffle tree, then the warp partials in warp order, so the
+// same bits — but ONE barrier, and the five sums by five threads.  sh: 6 * NT/32 doubles.  dres_own:
+// thread 0 writes dres_val as the DRES partial (sharded: the all-reduced value) instead of the sum.
+template <int NT>
+__device__ __forceinline__ void gather_part_sums(dd bx, double p_pres, double p_axi, double p_dres, double p_by,
+                                                 double* sh, double* part, int gb, int blk, bool dres_own,
+                                                 double dres_val) {
+  constexpr int W = NT / 32;
+  bx = dd_warp_sum(bx);
+  double v[4] = {p_pres, p_axi, p_dres, p_by};
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_down_sync(0xffffffffu, v[q], o);
+  const int t = threadIdx.x, w = t >> 5, l = t & 31;
+  if (l == 0) {
+    sh[w] = bx.hi;
+    sh[W + w] = bx.lo;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sh[(2 + q) * W + w] = v[q];
+  }
+  __syncthreads();
+  if (t == 0) {
+    dd r{0.0, 0.0};
+    for (int i = 0; i < W; ++i) r = dd_add(r, dd{sh[i], sh[W + i]});
+    part[PART_BX * gb + blk] = r.hi;
+    part[PART_BXLO * gb + blk] = r.lo;
+    if (dres_own) part[PART_DRES * gb + blk] = dres_val;
+  } else if (t <= 4) {
+    const int q = t - 1;
+    const int k = q == 0 ? PART_PRES : (q == 1 ? PART_AXI : (q == 2 ? PART_DRES : PART_BY));
+    if (!(dres_own && k == PART_DRES)) {
+      double r = 0.0;
+#pragma unroll
+      for (int i = 0; i < W; ++i) r += sh[(2 + q) * W + i];
+      part[k * gb + blk] = r;
+    }
+  }
+}

@@ -51,7 +51,7 @@ struct LargeBlock {
   double *V2 = nullptr, *tau2 = nullptr, *Bg = nullptr;
   unsigned* cnt = nullptr;
   std::vector<int> node_n;  // host copy: size of every D&C node (index = node id), for the work accounting
-  int jl = 0;               // levels 1..jl are replaced by the Jacobi solve of their output nodes (k_dc_qrnode)
+  int jl = 0;               // levels 1..jl are replaced by the QR solve of their output nodes (k_dc_qrnode)
 };
 
 struct LargeEig {

@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(SH_NT) k_shard_scalars(AffineArgs a, ShardArgs
 
 // After the allreduce: the rest of k_gather, replicated (x = P^{-1}(w2 - g), residual partials).
 __global__ void __launch_bounds__(GATHER_NT) k_gather_fin(AffineArgs a, ShardArgs s) {
-  __shared__ double sh[2 * (GATHER_NT / 32)];
+  __shared__ double sh[6 * (GATHER_NT / 32)];
   if (a.st->done) return;
   const double tau = a.st->tau;
   const int r = blockIdx.x * GATHER_NT + threadIdx.x;
@@ -141,20 +141,8 @@ __global__ void __launch_bounds__(GATHER_NT) k_gather_fin(AffineArgs a, ShardArg
     p_axi = axi * axi;
     p_by = a.b[r] * yr;
   }
-  const dd bxs = dd_block_sum<GATHER_NT>(bxd, sh);
-  if (threadIdx.x == 0) {
-    a.part[PART_BX * a.gather_blocks + blockIdx.x] = bxs.hi;
-    a.part[PART_BXLO * a.gather_blocks + blockIdx.x] = bxs.lo;
-  }
-  double v = block_sum<GATHER_NT>(p_pres, sh);
-  if (threadIdx.x == 0) a.part[PART_PRES * a.gather_blocks + blockIdx.x] = v;
-  v = block_sum<GATHER_NT>(p_axi, sh);
-  if (threadIdx.x == 0) a.part[PART_AXI * a.gather_blocks + blockIdx.x] = v;
-  v = block_sum<GATHER_NT>(p_by, sh);
-  if (threadIdx.x == 0) {
-    a.part[PART_BY * a.gather_blocks + blockIdx.x] = v;
-    a.part[PART_DRES * a.gather_blocks + blockIdx.x] = (blockIdx.x == 0) ? s.buf[2 * a.m] : 0.0;
-  }
+  gather_part_sums<GATHER_NT>(bxd, p_pres, p_axi, 0.0, p_by, sh, a.part, a.gather_blocks, blockIdx.x, true,
+                              (blockIdx.x == 0) ? s.buf[2 * a.m] : 0.0);
 }
 
 // ---- peer mode ----
@@ -188,7 +176,7 @@ __device__ __forceinline__ double peer_ld(const double* p) {
 // (NVLink peer loads) and add them in rank order — deterministic, and the same order as the one-GPU
 // emulation's device sum.  CTA 0 also reduces the three scalars into red3 for k_tphase.
 __global__ void __launch_bounds__(GATHER_NT) k_gather_fin_peer(AffineArgs a, ShardArgs s) {
-  __shared__ double sh[2 * (GATHER_NT / 32)];
+  __shared__ double sh[6 * (GATHER_NT / 32)];
   if (a.st->done) return;
   const unsigned long long e = *s.epoch;  // = E + 1 after k_peer_signal
   if (threadIdx.x == 0) {
@@ -235,20 +223,8 @@ __global__ void __launch_bounds__(GATHER_NT) k_gather_fin_peer(AffineArgs a, Sha
     s.red3[threadIdx.x] = v;
     if (threadIdx.x == 0) dres0 = v;
   }
-  const dd bxs = dd_block_sum<GATHER_NT>(bxd, sh);
-  if (threadIdx.x == 0) {
-    a.part[PART_BX * a.gather_blocks + blockIdx.x] = bxs.hi;
-    a.part[PART_BXLO * a.gather_blocks + blockIdx.x] = bxs.lo;
-  }
-  double v = block_sum<GATHER_NT>(p_pres, sh);
-  if (threadIdx.x == 0) a.part[PART_PRES * a.gather_blocks + blockIdx.x] = v;
-  v = block_sum<GATHER_NT>(p_axi, sh);
-  if (threadIdx.x == 0) a.part[PART_AXI * a.gather_blocks + blockIdx.x] = v;
-  v = block_sum<GATHER_NT>(p_by, sh);
-  if (threadIdx.x == 0) {
-    a.part[PART_BY * a.gather_blocks + blockIdx.x] = v;
-    a.part[PART_DRES * a.gather_blocks + blockIdx.x] = (blockIdx.x == 0) ? dres0 : 0.0;
-  }
+  gather_part_sums<GATHER_NT>(bxd, p_pres, p_axi, 0.0, p_by, sh, a.part, a.gather_blocks, blockIdx.x, true,
+                              (blockIdx.x == 0) ? dres0 : 0.0);
 }
 
 // get_iterate in sharded mode: keep the owned entries of a column vector, zero the rest, so that an

@@ -85,7 +85,10 @@ def _stedc(d, e):
 
 @pytest.mark.parametrize("N,kind", [(2, "rand"), (3, "rand"), (17, "rand"), (65, "rand"), (231, "rand"),
                                     (861, "rand"), (300, "glued"), (200, "zero_e"), (129, "equal_d"),
-                                    (500, "wilkinson"), (861, "clustered"), (1280, "rand"), (1024, "clustered")])
+                                    (500, "wilkinson"), (861, "clustered"), (1280, "rand"), (1024, "clustered"),
+                                    # bottom nodes (k_dc_qrnode, n <= 16): one node, a few, graded, all zero
+                                    (16, "rand"), (5, "wilkinson"), (33, "graded"), (48, "zero_all"),
+                                    (40, "equal_d")])
 def test_stedc(N, kind):
     rng = np.random.default_rng(N + len(kind))
     if kind == "rand":
@@ -98,6 +101,11 @@ def test_stedc(N, kind):
         e[::7] = 0.0
     elif kind == "equal_d":
         d, e = np.ones(N), 1e-3 * rng.standard_normal(N - 1)
+    elif kind == "graded":  # eigenvalues over 16 orders of magnitude
+        d = 10.0 ** (-16.0 * np.arange(N) / N)
+        e = 1e-3 * np.sqrt(d[:-1] * d[1:]) * rng.standard_normal(N - 1)
+    elif kind == "zero_all":
+        d, e = np.zeros(N), np.zeros(N - 1)
     elif kind == "wilkinson":
         m = (N - 1) / 2
         d, e = np.abs(np.arange(N) - m), np.ones(N - 1)
