@@ -14,6 +14,12 @@ extern "C" {
 #endif
 /* C (M x N) = A (M x K) * op(B) with op(B) = B (K x N) or B^T (B is N x K): the DMMA GEMM. */
 int sosadmm_debug_gemm(int M, int N, int K, const double* A, const double* B, int transB, double* C);
+/* C (M x N) = op(A) B with the warm-path DMMA GEMM (dgemm.cuh): op(A) = A (M x K, transA = 0) or A^T (A is
+ * K x M, transA = 1); upper = 1 computes only the 64 x 64 tiles meeting the upper triangle (others stay 0);
+ * variant: tile configuration (dgemm.cuh DG_VARIANTS; < 0 = the production default); reps > 0 also times
+ * reps launches (*ms = mean per launch, CUDA events). */
+int sosadmm_debug_dgemm(int M, int N, int K, const double* A, int transA, int upper, const double* B, double* C,
+                        int variant, int reps, float* ms);
 /* Householder tridiagonalisation of the symmetric N x N matrix A in one thread-block cluster:
  * d (N), e (N-1), tau (N-1), V (N x N, reflector k in column k, rows k+1..N-1). */
 int sosadmm_debug_tridiag(int N, const double* A, double* d, double* e, double* tau, double* V);

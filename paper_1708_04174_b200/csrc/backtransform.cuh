@@ -138,13 +138,14 @@ inline size_t bt_apply_smem_bytes(int N) {
                            BTC_NW * BTW_NB * BTW_NC + BTW_NB * BTW_NC + 2 * BTW_NB * BTW_NB);
 }
 
-// W[:, c] = H Z[:, c0 + c] sqrt|lambda_{c0+c}|, c < r (r, c0 from k_select's sel[]).
+// W[:, c] = H Z[:, c0 + c] sqrt|lambda_{c0+c}|, c < r (r, c0 from k_select's sel[]); W has pitch ldw;
+// scale = 0 writes H Z[:, c0 + c] itself (the warm mode's cold path: every eigenvector, warm.cuh).
 // grid: BTC_P x (number of 8-column tiles), cluster (BTC_P, 1, 1).
 __global__ void __launch_bounds__(BTC_NT) k_bt_apply(const double* __restrict__ Qf, const double* __restrict__ lamf,
                                                      const double* __restrict__ V, const double* __restrict__ Tall,
                                                      const int* __restrict__ sel, double* __restrict__ W, int N,
                                                      int nref, const DevState* st, const IterScal* is,
-                                                     int check_state) {
+                                                     int check_state, int ldw, int scale) {
   if (check_state && (st->done || !is->proceed)) return;
   const int r = sel[0], c0 = sel[1];
   const int q = (int)btc_rank();
@@ -274,6 +275,7 @@ __global__ void __launch_bounds__(BTC_NT) k_bt_apply(const double* __restrict__ 
   }
   for (int e = tid; e < RS * BTW_NC; e += BTC_NT) {
     const int rr = e / BTW_NC, c = e % BTW_NC, row = rlo + rr;
-    if (row < rhi && cbase + c < r) W[(size_t)(cbase + c) * N + row] = Ws[e] * sqrt(fabs(lamf[c0 + cbase + c]));
+    if (row < rhi && cbase + c < r)
+      W[(size_t)(cbase + c) * ldw + row] = scale ? Ws[e] * sqrt(fabs(lamf[c0 + cbase + c])) : Ws[e];
   }
 }

@@ -22,6 +22,7 @@
 #include "sy2sb.cuh"
 #include "sb2st.cuh"
 #include "bt2.cuh"
+#include "warm.cuh"
 
 struct LargeBlock {
   int b = 0, N = 0, C = 1, D = 0;
@@ -52,6 +53,12 @@ struct LargeBlock {
   unsigned* cnt = nullptr;
   std::vector<int> node_n;  // host copy: size of every D&C node (index = node id), for the work accounting
   int jl = 0;               // levels 1..jl are replaced by the QR solve of their output nodes (k_dc_qrnode)
+  // warm-started projection (warm.cuh): refinement of the previous eigenvectors, cold path as fallback
+  bool warm = false;
+  WarmArgs wa{};
+  DgemmDesc* wdesc = nullptr;  // [WM_MAXS][4]: W = Af X, S = X^T W, P = X^T X, X' = X M; then Y = Xs Ss
+  int wrecon = 0;              // index of the warm reconstruction descriptor (Y Xs^T) in gdesc
+  int* sel_all = nullptr;      // [N, 0, 0]: the cold path back-transforms every column (unscaled) into X0
 };
 
 struct LargeEig {
@@ -211,7 +218,7 @@ inline size_t large_carve(const std::vector<int>& blk_N, const std::vector<int>&
     int D, leaf0, nleaves;
     dc_build_tree(N, nodes, l0, lnn, lmax, D, leaf0, nleaves, p2n);
     const size_t NN = (size_t)N * N;
-    char* p[64];  // (42 buffers per block)
+    char* p[96];  // (74 buffers per block)
     int q = 0;
     p[q++] = take(8 * N);                 // d
     p[q++] = take(8 * N);                 // e
@@ -232,7 +239,7 @@ inline size_t large_carve(const std::vector<int>& blk_N, const std::vector<int>&
     p[q++] = take(8 * N);                 // rot_pq (2 ints)
     p[q++] = take(16 * N);                // rot_cs
     p[q++] = take(4 * nodes.size());      // rot_cnt
-    p[q++] = take(sizeof(GemmDesc) * (nodes.size() + 1));
+    p[q++] = take(sizeof(GemmDesc) * (nodes.size() + 2));
     p[q++] = take(4 * 8);                 // sel [r, c0, side] + the D&C root selection (topsel)
     p[q++] = take(8 * ((size_t)3 * N + 2));  // tridiagonalisation hand-over state
     p[q++] = take(8 * (size_t)BTW_NB * BTW_NB * ((N - 2 + BTW_NB - 1) / BTW_NB));  // Twy
@@ -249,6 +256,24 @@ inline size_t large_carve(const std::vector<int>& blk_N, const std::vector<int>&
       p[q++] = take(8 * (size_t)N * KM * BW);           // V2
       p[q++] = take(8 * (size_t)N * KM);                // tau2
     }
+    {  // warm-start buffers (warm.cuh), pitch ldn = N rounded up to even
+      const size_t NL = (size_t)N * ((N + 1) & ~1);
+      const int nt = (N + 31) / 32;
+      for (int t = 0; t < 8; ++t) p[q++] = take(8 * NL);  // Af X0 X1 W S P E Mm
+      p[q++] = take(8 * N);                                // lam
+      p[q++] = take(8 * N);                                // lamt
+      for (int t = 0; t < 8; ++t) p[q++] = take(4 * (size_t)(N + 1));  // order pos diff cid cpos cl_start cl_size cl_voff
+      p[q++] = take(4 * 4);                                // sel
+      p[q++] = take(4 * (size_t)N);                        // idx
+      p[q++] = take(8 * (size_t)WM_CAP * N);               // Vcl
+      for (int t = 0; t < 3; ++t) p[q++] = take(8 * (size_t)nt * nt);  // partA cross roff
+      p[q++] = take(8 * (size_t)nt * N);                   // grow
+      p[q++] = take(8 * (size_t)nt * N);                   // gcol
+      p[q++] = take(8);                                    // rdiag
+      p[q++] = take(sizeof(WarmState));                    // ws
+      p[q++] = take(sizeof(DgemmDesc) * (WM_MAXS * 4 + 1));  // wdesc
+      p[q++] = take(4 * 4);                                // sel_all
+    }
     per_block(b, N, p, nodes, l0, lnn, lmax, D, leaf0, nleaves, p2n);
   }
   return used + 256;
@@ -258,9 +283,16 @@ inline size_t large_eig_bytes(const std::vector<int>& blk_N, const std::vector<i
   return large_carve(blk_N, large, nullptr, nullptr, [](int, int, char**, auto&, auto&, auto&, auto&, int, int, int, auto&) {});
 }
 
+// Warm-started projection (warm.cuh) on by default for the contexts of sosadmm_setup; SOSADMM_WARM=0 keeps
+// the cold path every iteration (for A/B measurements).  Not combined with the opt-in two-stage reduction.
+inline bool warm_enabled() {
+  const char* e = getenv("SOSADMM_WARM");
+  return !(e && e[0] == '0') && !ts_enabled();
+}
+
 inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std::vector<long long>& blk_mat,
                           const std::vector<int>& large, double* mats, char* base, DevState* st, IterScal* is,
-                          cudaStream_t s, std::string& msg) {
+                          cudaStream_t s, std::string& msg, bool warm = false) {
   le.st = st;
   le.is = is;
   le.blocks.clear();
@@ -324,7 +356,8 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     lb.gdesc = (GemmDesc*)p[q++];
     lb.sel = (int*)p[q++];
     dc.topsel = lb.sel + 4;
-    dc.topsel_on = 1;
+    dc.topsel_on = warm ? 0 : 1;  // the warm mode's cold path needs every eigenvector (it re-seeds X)
+    lb.warm = warm;
     double* hand = (double*)p[q++];
     lb.Twy = (double*)p[q++];
     lb.Gwy = (double*)p[q++];
@@ -341,7 +374,7 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     lb.leaf0 = leaf0;
     lb.nleaves = nleaves;
     // GEMM descriptors: one per merge node (Q_new = Q_old[:, nd] U), then the reconstruction
-    std::vector<GemmDesc> gd(nodes.size() + 1);
+    std::vector<GemmDesc> gd(nodes.size() + 2);
     for (int h = 1; h <= D; ++h) {
       const int ob = (h - 1) & 1, nb = h & 1;
       for (int t = 0; t < lnn[h]; ++t) {
@@ -361,7 +394,7 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
         g.K = nd.n;
         g.Kdev = dc.node_k + id;
         g.Ndev = dc.node_k + id;
-        if (h == D) {  // root: only the selected eigenvector columns (k_dc_topsel)
+        if (h == D && !warm) {  // root: only the selected eigenvector columns (k_dc_topsel)
           g.Ndev = dc.topsel;
           g.Noff = dc.topsel + 1;
         }
@@ -390,6 +423,7 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
       g.upper = 1;  // k_pack reads the upper triangle of the projection only
       gd[nodes.size()] = g;
     }
+    lb.wrecon = (int)nodes.size() + 1;  // filled below (warm buffers are carved after the two-stage ones)
     if (err == cudaSuccess) err = cudaMemcpyAsync(dnodes, nodes.data(), sizeof(DcNode) * nodes.size(), cudaMemcpyHostToDevice, s);
     if (err == cudaSuccess) err = cudaMemcpyAsync(dp2n, p2n.data(), 4 * p2n.size(), cudaMemcpyHostToDevice, s);
     if (err == cudaSuccess) err = cudaMemcpyAsync(lb.gdesc, gd.data(), sizeof(GemmDesc) * gd.size(), cudaMemcpyHostToDevice, s);
@@ -454,9 +488,78 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
       if (lb.two && (lb.sy_smem > (size_t)DYN_SMEM_MAX || lb.st_smem > (size_t)DYN_SMEM_MAX || sa.maxrb > 4))
         lb.two = false;  // outside the two-stage envelope (N > 1280): one-stage kernel
     }
+    {  // warm-start state and descriptors
+      const int ldn = (N + 1) & ~1, nt = (N + 31) / 32;
+      WarmArgs& wa = lb.wa;
+      wa.N = N;
+      wa.ldn = ldn;
+      wa.nt = nt;
+      wa.Mblk = lb.M;
+      double** big[8] = {&wa.Af, &wa.X0, &wa.X1, &wa.W, &wa.S, &wa.P, &wa.E, &wa.Mm};
+      for (int t = 0; t < 8; ++t) *big[t] = (double*)p[q++];
+      wa.lam = (double*)p[q++];
+      wa.lamt = (double*)p[q++];
+      int** ib[8] = {&wa.order, &wa.pos, &wa.diff, &wa.cid, &wa.cpos, &wa.cl_start, &wa.cl_size, &wa.cl_voff};
+      for (int t = 0; t < 8; ++t) *ib[t] = (int*)p[q++];
+      wa.sel = (int*)p[q++];
+      wa.idx = (int*)p[q++];
+      wa.Vcl = (double*)p[q++];
+      wa.partA = (double*)p[q++];
+      wa.cross = (double*)p[q++];
+      wa.roff = (double*)p[q++];
+      wa.grow = (double*)p[q++];
+      wa.gcol = (double*)p[q++];
+      wa.rdiag = (double*)p[q++];
+      wa.ws = (WarmState*)p[q++];
+      lb.wdesc = (DgemmDesc*)p[q++];
+      lb.sel_all = (int*)p[q++];
+      wa.lam_cold = dc.lam[D & 1];
+      wa.side = nullptr;  // le.side, set after the carve
+      wa.st = st;
+      wa.is = is;
+      std::vector<DgemmDesc> wd(WM_MAXS * 4 + 1);
+      for (int j = 0; j < WM_MAXS; ++j) {
+        double* Xc = (j & 1) ? wa.X1 : wa.X0;
+        double* Xn = (j & 1) ? wa.X0 : wa.X1;
+        DgemmDesc g{};
+        g.M = N; g.N = N; g.K = N; g.lda = ldn; g.ldb = ldn; g.ldc = ldn; g.alpha = 1.0; g.beta = 0.0;
+        g.gate = &wa.ws->gate;
+        DgemmDesc gw = g;  // W = Af X
+        gw.A = wa.Af; gw.B = Xc; gw.C = wa.W;
+        DgemmDesc gs = g;  // S = X^T W (upper)
+        gs.A = Xc; gs.transA = 1; gs.B = wa.W; gs.C = wa.S; gs.upper = 1;
+        DgemmDesc gp = gs;  // P = X^T X (upper)
+        gp.B = Xc; gp.C = wa.P;
+        DgemmDesc gx = g;  // X' = X M
+        gx.A = Xc; gx.B = wa.Mm; gx.C = Xn;
+        wd[4 * j] = gw;
+        wd[4 * j + 1] = gs;
+        wd[4 * j + 2] = gp;
+        wd[4 * j + 3] = gx;
+      }
+      {  // finish: Y = Xs Ss (Xs in W, Ss in E, Y in P; r x r from sel)
+        DgemmDesc g{};
+        g.A = wa.W; g.lda = ldn; g.B = wa.E; g.ldb = ldn; g.C = wa.P; g.ldc = ldn;
+        g.M = N; g.N = N; g.K = N; g.Ndev = wa.sel; g.Kdev = wa.sel; g.alpha = 1.0; g.beta = 0.0;
+        wd[WM_MAXS * 4] = g;
+      }
+      {  // warm reconstruction M = Y Xs^T (upper tiles) into the block matrix
+        GemmDesc g{};
+        g.A = wa.P; g.lda = ldn; g.B = wa.W; g.ldb = ldn; g.transB = 1; g.C = lb.M; g.ldc = N;
+        g.M = N; g.N = N; g.K = N; g.Kdev = wa.sel; g.alpha = 1.0; g.beta = 0.0; g.upper = 1;
+        if (err == cudaSuccess) err = cudaMemcpyAsync(lb.gdesc + lb.wrecon, &g, sizeof(g), cudaMemcpyHostToDevice, s);
+      }
+      const int sa3[4] = {N, 0, 0, 0};
+      if (err == cudaSuccess) err = cudaMemcpyAsync(lb.wdesc, wd.data(), sizeof(DgemmDesc) * wd.size(), cudaMemcpyHostToDevice, s);
+      if (err == cudaSuccess) err = cudaMemcpyAsync(lb.sel_all, sa3, sizeof(sa3), cudaMemcpyHostToDevice, s);
+      if (err == cudaSuccess) err = cudaMemsetAsync(wa.ws, 0, sizeof(WarmState), s);
+      if (err == cudaSuccess) err = cudaMemsetAsync(wa.X1, 0, 8 * (size_t)N * ldn, s);
+      if (err == cudaSuccess) err = cudaMemsetAsync(wa.X0, 0, 8 * (size_t)N * ldn, s);
+    }
     le.blocks.push_back(lb);
   });
   le.side = side_p;
+  for (auto& lb : le.blocks) lb.wa.side = side_p;
   if (err != cudaSuccess) {
     msg = cudaGetErrorString(err);
     return 1;
@@ -479,6 +582,9 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     if (err == cudaSuccess)
       err = cudaFuncSetAttribute(k_bt_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)bt_apply_smem_bytes(DC_MAXN));
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(k_warm_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WM_CL_SMEM);
+    if (err == cudaSuccess) dgemm_prepare();
     for (int bw : {8, 16}) {
       if (err == cudaSuccess)
         err = cudaFuncSetAttribute(sy2sb_kernel(bw), cudaFuncAttributeMaxDynamicSharedMemorySize, DYN_SMEM_MAX);
@@ -623,28 +729,212 @@ inline void large_block_recon(LargeEig& le, LargeBlock& lb, cudaStream_t s, bool
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, k_bt_apply, (const double*)lb.dc.Q[fb], (const double*)lb.dc.lam[fb],
                        (const double*)lb.V, (const double*)lb.Twy, (const int*)lb.sel, lb.W, N, nref, le.st,
-                       le.is, (int)check);
+                       le.is, (int)check, N, 1);
   }
   dim3 gr((N + GM_BM - 1) / GM_BM, (N + GM_BN - 1) / GM_BN, 1);
   k_gemm_f64<<<gr, GM_NT, 0, s>>>(lb.gdesc + lb.recon, le.st, le.is, check);
 }
 
+// ---- warm mode (warm.cuh) ----------------------------------------------------------------------
+__global__ void k_zero2(double* a, double* b, long long n) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    a[e] = 0.0;
+    b[e] = 0.0;
+  }
+}
+inline void large_block_warm_begin(LargeEig& le, LargeBlock& lb, cudaStream_t s, const WarmArgs& wa) {
+  (void)le;
+  k_warm_begin<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
+}
+// refinement step j: W = Af X_j, [S, P] = X_j^T [W, X_j], stop test, clusters, M = V (I + E), X_{j+1} = X_j M
+inline void large_block_warm_step(LargeEig& le, LargeBlock& lb, cudaStream_t s, int j, const WarmArgs& wa) {
+  const int N = lb.N;
+  dgemm_launch(DG_DEFAULT, lb.wdesc + 4 * j, 1, N, N, s, le.st, le.is, 1);
+  dgemm_launch(DG_DEFAULT, lb.wdesc + 4 * j + 1, 2, N, N, s, le.st, le.is, 1);
+  k_warm_diag<<<1, WM_NT, 0, s>>>(wa);
+  k_warm_scan<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
+  k_warm_decide<<<1, WM_NT, 0, s>>>(wa, j);
+  k_warm_cluster<<<WM_CLB, 256, WM_CL_SMEM, s>>>(wa);
+  k_warm_E<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
+  k_warm_M<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
+  dgemm_launch(DG_DEFAULT, lb.wdesc + 4 * j + 3, 1, N, N, s, le.st, le.is, 1);
+}
+// cold path of the warm mode: tridiagonalisation, WY factors, divide and conquer (every eigenvector),
+// back-transform of all N columns, unscaled, into X0 (pitch ldn).  side / ev as in the concurrent variant
+// (side streams sw, sd and 8 events), or sequential on s when sw == nullptr.
+inline void large_block_cold_full(LargeEig& le, LargeBlock& lb, cudaStream_t s, cudaStream_t sw = nullptr,
+                                  cudaStream_t sd = nullptr, const cudaEvent_t* evs = nullptr) {
+  const int N = lb.N, fb = lb.D & 1;
+  if (sw) {
+    cudaEventRecord(evs[6], s);
+    cudaStreamWaitEvent(sd, evs[6], 0);
+    k_zero2<<<296, 256, 0, sd>>>(lb.dc.Q[0], lb.dc.Q[1], (long long)N * N);  // (kernel: conditional body)
+    cudaEventRecord(evs[7], sd);
+    large_block_tridiag(le, lb, s, true);
+    cudaEventRecord(evs[0], s);
+    cudaStreamWaitEvent(sw, evs[0], 0);
+    large_block_wy(le, lb, sw, true);
+    cudaEventRecord(evs[1], sw);
+    large_block_dc(le, lb, s, true, sd, evs + 3);
+    cudaStreamWaitEvent(s, evs[1], 0);
+  } else {
+    large_block_tridiag(le, lb, s, true);
+    large_block_wy(le, lb, s, true);
+    large_block_dc(le, lb, s, true);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(BTC_P * ((N + BTW_NC - 1) / BTW_NC), 1, 1);
+  cfg.blockDim = dim3(BTC_NT, 1, 1);
+  cfg.dynamicSmemBytes = bt_apply_smem_bytes(N);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = BTC_P;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_bt_apply, (const double*)lb.dc.Q[fb], (const double*)lb.dc.lam[fb],
+                     (const double*)lb.V, (const double*)lb.Twy, (const int*)lb.sel_all, lb.wa.X0, N, lb.nref,
+                     le.st, le.is, 1, lb.wa.ldn, 0);
+}
+// finish (both paths): side and index list, Xs / Ss gather, Y = Xs Ss, M = Y Xs^T into the block matrix
+inline void large_block_warm_finish(LargeEig& le, LargeBlock& lb, cudaStream_t s) {
+  const int N = lb.N;
+  k_warm_select<<<1, WM_NT, 0, s>>>(lb.wa, lb.b);
+  k_warm_gather<<<296, 256, 0, s>>>(lb.wa);
+  dgemm_launch(DG_DEFAULT, lb.wdesc + 4 * WM_MAXS, 1, N, N, s, le.st, le.is, 1);
+  dim3 gr((N + GM_BM - 1) / GM_BM, (N + GM_BN - 1) / GM_BN, 1);
+  k_gemm_f64<<<gr, GM_NT, 0, s>>>(lb.gdesc + lb.wrecon, le.st, le.is, 1);
+}
+// un-graphed warm projection of one block: the refinement steps, then (host decision after a sync) the
+// cold path if they did not converge, then the finish.  ev (optional, 3 events): after the refinement /
+// cold tridiagonalisation, after the cold D&C + back-transform, after the finish.
+inline cudaError_t large_block_warm_ungraphed(LargeEig& le, LargeBlock& lb, cudaStream_t s, cudaEvent_t* ev) {
+  large_block_warm_begin(le, lb, s, lb.wa);
+  for (int j = 0; j < WM_MAXS; ++j) large_block_warm_step(le, lb, s, j, lb.wa);
+  WarmState h{};
+  cudaError_t e = cudaMemcpyAsync(&h, lb.wa.ws, sizeof(h), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return e;
+  if (h.status != 1) {
+    const int N = lb.N, fb = lb.D & 1;
+    large_block_tridiag(le, lb, s, true);
+    if (ev) cudaEventRecord(ev[0], s);
+    large_block_wy(le, lb, s, true);
+    large_block_dc(le, lb, s, true);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(BTC_P * ((N + BTW_NC - 1) / BTW_NC), 1, 1);
+    cfg.blockDim = dim3(BTC_NT, 1, 1);
+    cfg.dynamicSmemBytes = bt_apply_smem_bytes(N);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = BTC_P;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_bt_apply, (const double*)lb.dc.Q[fb], (const double*)lb.dc.lam[fb],
+                       (const double*)lb.V, (const double*)lb.Twy, (const int*)lb.sel_all, lb.wa.X0, N, lb.nref,
+                       le.st, le.is, 1, lb.wa.ldn, 0);
+  } else if (ev) {
+    cudaEventRecord(ev[0], s);
+  }
+  if (ev) cudaEventRecord(ev[1], s);
+  large_block_warm_finish(le, lb, s);
+  if (ev) cudaEventRecord(ev[2], s);
+  return cudaSuccess;
+}
+
 // Stage-major over the large blocks; ev (optional, 3 events) is recorded after the
 // tridiagonalisations, after the divide-and-conquer solves and after the reconstructions.
 inline void large_eig_launch(LargeEig& le, cudaStream_t s, bool check, cudaEvent_t* ev = nullptr) {
-  for (auto& lb : le.blocks) large_block_tridiag(le, lb, s, check);
+  bool any_cold = false;
+  for (auto& lb : le.blocks) any_cold |= !lb.warm;
+  if (!any_cold) {  // every block in warm mode (the events then bracket the last block's phases)
+    for (auto& lb : le.blocks) large_block_warm_ungraphed(le, lb, s, ev);
+    return;
+  }
+  for (auto& lb : le.blocks)
+    if (lb.warm) large_block_warm_ungraphed(le, lb, s, nullptr);
+  for (auto& lb : le.blocks)
+    if (!lb.warm) large_block_tridiag(le, lb, s, check);
   if (ev) cudaEventRecord(ev[0], s);
-  for (auto& lb : le.blocks) large_block_dc(le, lb, s, check);
+  for (auto& lb : le.blocks)
+    if (!lb.warm) large_block_dc(le, lb, s, check);
   if (ev) cudaEventRecord(ev[1], s);
-  for (auto& lb : le.blocks) large_block_recon(le, lb, s, check);
+  for (auto& lb : le.blocks)
+    if (!lb.warm) large_block_recon(le, lb, s, check);
   if (ev) cudaEventRecord(ev[2], s);
+}
+
+// Graph helpers: a conditional handle of the graph being captured on s, and an IF node appended to s's
+// capture (its body graph returned for capture-to-graph on another stream).
+inline cudaError_t graph_new_handle(cudaStream_t s, unsigned long long* h) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, nullptr, nullptr);
+  if (e != cudaSuccess) return e;
+  if (cs != cudaStreamCaptureStatusActive) return cudaErrorStreamCaptureUnsupported;
+  cudaGraphConditionalHandle hh;
+  e = cudaGraphConditionalHandleCreate(&hh, g, 0, cudaGraphCondAssignDefault);
+  *h = (unsigned long long)hh;
+  return e;
+}
+inline cudaError_t graph_if_body(cudaStream_t s, unsigned long long h, cudaGraph_t* body) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  cudaError_t e = cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &nd);
+  if (e != cudaSuccess) return e;
+  if (cs != cudaStreamCaptureStatusActive) return cudaErrorStreamCaptureUnsupported;
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = (cudaGraphConditionalHandle)h;
+  p.conditional.type = cudaGraphCondTypeIf;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  e = cudaGraphAddNode(&node, g, deps, nd, &p);
+  if (e != cudaSuccess) return e;
+  *body = p.conditional.phGraph_out[0];
+  return cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies);
+}
+
+// Warm block inside a stream capture on sb: begin, WM_MAXS refinement steps each in an IF node (set by
+// the previous step's stop test), the cold path in an IF node (set by a failed test or by begin when no
+// warm start exists), then the finish.  sbody: a stream outside any capture, for the bodies.
+inline cudaError_t large_block_warm_graph(LargeEig& le, LargeBlock& lb, cudaStream_t sb, cudaStream_t sbody,
+                                          cudaStream_t sw, cudaStream_t sd, const cudaEvent_t* evs) {
+  WarmArgs wg = lb.wa;
+  cudaError_t e = cudaSuccess;
+  for (int j = 0; j < WM_MAXS && e == cudaSuccess; ++j) e = graph_new_handle(sb, &wg.hstep[j]);
+  if (e == cudaSuccess) e = graph_new_handle(sb, &wg.hcold);
+  if (e != cudaSuccess) return e;
+  large_block_warm_begin(le, lb, sb, wg);
+  for (int j = 0; j <= WM_MAXS; ++j) {
+    cudaGraph_t body = nullptr;
+    e = graph_if_body(sb, j < WM_MAXS ? wg.hstep[j] : wg.hcold, &body);
+    if (e == cudaSuccess) e = cudaStreamBeginCaptureToGraph(sbody, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return e;
+    if (j < WM_MAXS) large_block_warm_step(le, lb, sbody, j, wg);
+    else large_block_cold_full(le, lb, sbody, sw, sd, evs);
+    cudaGraph_t out = nullptr;
+    e = cudaStreamEndCapture(sbody, &out);
+    if (e != cudaSuccess) return e;
+  }
+  large_block_warm_finish(le, lb, sb);
+  return cudaGetLastError();
 }
 
 // Concurrent variant (graph path): every large block runs its chain on its own stream (block 0 on
 // s), and inside a chain the WY factors run on a side stream beside the divide-and-conquer solve.
-// fork: event already recorded on s; aux: >= 3 * nblocks streams; evs: >= 8 * nblocks events.
-inline void large_eig_launch_concurrent(LargeEig& le, cudaStream_t s, bool check, cudaEvent_t fork,
-                                        const cudaStream_t* aux, const cudaEvent_t* evs) {
+// fork: event already recorded on s; aux: >= 3 * nblocks streams; evs: >= 8 * nblocks events;
+// body: one stream per block outside the capture (warm blocks' conditional bodies).
+inline cudaError_t large_eig_launch_concurrent(LargeEig& le, cudaStream_t s, bool check, cudaEvent_t fork,
+                                               const cudaStream_t* aux, const cudaEvent_t* evs,
+                                               const cudaStream_t* body) {
   const int nb = (int)le.blocks.size();
   for (int b = 0; b < nb; ++b) {
     LargeBlock& lb = le.blocks[b];
@@ -652,6 +942,12 @@ inline void large_eig_launch_concurrent(LargeEig& le, cudaStream_t s, bool check
     cudaStream_t sw = aux[3 * b + 1];
     cudaStream_t sd = aux[3 * b + 2];
     if (b > 0) cudaStreamWaitEvent(sb, fork, 0);
+    if (lb.warm) {
+      const cudaError_t e = large_block_warm_graph(le, lb, sb, body[b], sw, sd, evs + 8 * b);
+      if (e != cudaSuccess) return e;
+      if (b > 0) cudaEventRecord(evs[8 * b + 2], sb);
+      continue;
+    }
     // the D&C eigenvector buffers are zeroed beside the tridiagonalisation
     cudaStreamWaitEvent(sd, fork, 0);
     cudaMemsetAsync(lb.dc.Q[0], 0, sizeof(double) * lb.N * lb.N, sd);
@@ -668,12 +964,18 @@ inline void large_eig_launch_concurrent(LargeEig& le, cudaStream_t s, bool check
     if (b > 0) cudaEventRecord(evs[8 * b + 2], sb);
   }
   for (int b = 1; b < nb; ++b) cudaStreamWaitEvent(s, evs[8 * b + 2], 0);
+  return cudaSuccess;
 }
 
 inline int large_eig_launches(const LargeEig& le) {
   int k = 0;
-  for (const auto& lb : le.blocks)
+  for (const auto& lb : le.blocks) {
+    if (lb.warm) {  // begin, the refinement steps (IF nodes; an upper bound), the finish; cold path excluded
+      k += 1 + WM_MAXS * 9 + 4;
+      continue;
+    }
     k += (lb.two ? 3 : (lb.ksw < lb.N - 2 ? 2 : 1)) + 2 + 1 + 7 * (lb.D - lb.jl) + 1 + 5 + (lb.two ? 1 : 0);
+  }
   return k;
 }
 

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "affine.cuh"
+#include "dgemm.cuh"
 #include "psd_jacobi.cuh"
 #include "psd_large.cuh"
 #include "shard.cuh"
@@ -393,6 +394,7 @@ struct sosadmm_ctx {
   // parallel branches of the PSD projection inside the CUDA graph
   static constexpr int kMaxAux = 1 + 3 * 8;
   cudaStream_t aux[kMaxAux] = {};
+  cudaStream_t body[8] = {};  // capture streams of the warm blocks' conditional bodies (outside the main capture)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_blk[8 * 8] = {};
   // early-stop polling of sosadmm_iterate: pinned copies of the device state after each chunk of replays
   DevState* h_poll = nullptr;
@@ -578,7 +580,12 @@ sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev, int
                                          c->aux[0]>>>(c->ja);
       cudaEventRecord(c->ev_join, c->aux[0]);
     }
-    large_eig_launch_concurrent(c->le, s, true, c->ev_fork, c->aux + 1, c->ev_blk);
+    const cudaError_t ge = large_eig_launch_concurrent(c->le, s, true, c->ev_fork, c->aux + 1, c->ev_blk, c->body);
+    if (ge != cudaSuccess) {
+      c->err = SOSADMM_E_CUDA;
+      c->msg = std::string("large-block projection capture: ") + cudaGetErrorString(ge);
+      return c->err;
+    }
     if (has_small) cudaStreamWaitEvent(s, c->ev_join, 0);
   } else {
     if (has_small)
@@ -974,8 +981,8 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
   }
   {
     std::string lmsg;
-    if (large_eig_init(c->le, an.blk_N, an.blk_mat, an.large_blk, d.mats, large_base, d.st, d.is, s, lmsg) !=
-        0) {
+    if (large_eig_init(c->le, an.blk_N, an.blk_mat, an.large_blk, d.mats, large_base, d.st, d.is, s, lmsg,
+                       warm_enabled()) != 0) {
       c->err = SOSADMM_E_CUDA;
       c->msg = "large-block eigensolver setup: " + lmsg;
       return c->err;
@@ -989,6 +996,8 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
   if (!an.large_blk.empty() && an.large_blk.size() <= 8) {
     const int naux = 1 + 3 * (int)an.large_blk.size();
     for (int q = 0; q < naux; ++q) CK_CTX(c, cudaStreamCreateWithFlags(&c->aux[q], cudaStreamNonBlocking));
+    for (size_t q = 0; q < an.large_blk.size(); ++q)
+      CK_CTX(c, cudaStreamCreateWithFlags(&c->body[q], cudaStreamNonBlocking));
     CK_CTX(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK_CTX(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     for (int q = 0; q < 8 * (int)an.large_blk.size(); ++q)
@@ -1042,20 +1051,39 @@ sosadmm_err sosadmm_setup_sharded(const sosadmm_problem* prob, const sosadmm_set
 
 static sosadmm_err build_graph(sosadmm_ctx* c) {
   if (c->graph) return SOSADMM_OK;
-  CK_CTX(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-  const sosadmm_err le = launch_iteration(c, 1, nullptr);
-  cudaGraph_t g = nullptr;
-  const cudaError_t ee = cudaStreamEndCapture(c->stream, &g);
-  if (le != SOSADMM_OK || ee != cudaSuccess) {  // a failed capture (e.g. ncclAllReduce) is never instantiated
-    if (g) cudaGraphDestroy(g);
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    CK_CTX(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    const sosadmm_err le = launch_iteration(c, 1, nullptr);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ee = cudaStreamEndCapture(c->stream, &g);
+    cudaError_t ie = cudaErrorUnknown;
+    if (le == SOSADMM_OK && ee == cudaSuccess) {
+      ie = cudaGraphInstantiate(&c->graph, g, 0);
+      if (ie == cudaSuccess) {
+        c->graph_raw = g;
+        return SOSADMM_OK;
+      }
+      c->graph = nullptr;
+    }
+    if (g) cudaGraphDestroy(g);  // a failed capture (e.g. ncclAllReduce) is never instantiated
+    bool warm = false;
+    for (auto& lb : c->le.blocks) warm |= lb.warm;
+    if (attempt == 0 && warm && !(le != SOSADMM_OK && c->err == SOSADMM_E_NCCL)) {
+      // the warm mode's conditional nodes could not be captured / instantiated here: cold path every
+      // iteration (still correct: the D&C root then forms every eigenvector), recorded in the message
+      for (auto& lb : c->le.blocks) lb.warm = false;
+      c->msg = std::string("warm start disabled (graph capture: ") + cudaGetErrorString(ee != cudaSuccess ? ee : ie) + ")";
+      c->err = SOSADMM_OK;
+      (void)cudaGetLastError();
+      c->launches = count_launches(c);
+      continue;
+    }
     if (le != SOSADMM_OK) return c->err = le;
     c->err = SOSADMM_E_CUDA;
-    c->msg = std::string("cudaStreamEndCapture: ") + cudaGetErrorString(ee);
+    c->msg = std::string("graph capture: ") + cudaGetErrorString(ee != cudaSuccess ? ee : ie);
     return c->err;
   }
-  CK_CTX(c, cudaGraphInstantiate(&c->graph, g, 0));
-  c->graph_raw = g;
-  return SOSADMM_OK;
+  return c->err;
 }
 
 // Enqueue up to k graph replays in chunks (8, 16, ... 128).  After each chunk the device state is copied
@@ -1328,6 +1356,33 @@ sosadmm_err sosadmm_psd_work(sosadmm_ctx* c, double* work, int32_t* nblocks) {
   return SOSADMM_OK;
 }
 
+sosadmm_err sosadmm_warm_stats(sosadmm_ctx* c, int64_t* stats, int32_t* nblocks) {
+  if (!c || !nblocks) return SOSADMM_E_ARG;
+  if (c->err) return c->err;
+  CK_CTX(c, cudaSetDevice(c->device));
+  const int nb = (int)c->le.blocks.size();
+  if (stats)
+    for (int b = 0; b < std::min(nb, *nblocks); ++b) {
+      const LargeBlock& lb = c->le.blocks[b];
+      WarmState h{};
+      int sel[3] = {0, 0, 0};
+      CK_CTX(c, cudaMemcpyAsync(&h, lb.wa.ws, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+      CK_CTX(c, cudaMemcpyAsync(sel, lb.warm ? lb.wa.sel : lb.sel, sizeof(sel), cudaMemcpyDeviceToHost, c->stream));
+      CK_CTX(c, cudaStreamSynchronize(c->stream));
+      int64_t* o = stats + 8 * b;
+      o[0] = h.n_warm;
+      o[1] = h.n_cold;
+      o[2] = h.n_steps;
+      o[3] = h.n_fail;
+      o[4] = lb.warm ? 1 : 0;
+      o[5] = sel[0];
+      o[6] = lb.N;
+      o[7] = h.step;
+    }
+  *nblocks = nb;
+  return SOSADMM_OK;
+}
+
 void sosadmm_destroy(sosadmm_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
@@ -1337,6 +1392,8 @@ void sosadmm_destroy(sosadmm_ctx* c) {
   large_eig_free(c->le);
   if (c->comm) nccl().commDestroy(c->comm);
   for (auto& a : c->aux)
+    if (a) cudaStreamDestroy(a);
+  for (auto& a : c->body)
     if (a) cudaStreamDestroy(a);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
@@ -1425,6 +1482,51 @@ extern "C" int sosadmm_debug_gemm(int M, int N, int K, const double* A, const do
   k_gemm_f64<<<gr, GM_NT>>>(dg, nullptr, nullptr, 0);
   cudaError_t e = cudaDeviceSynchronize();
   if (e == cudaSuccess) cudaMemcpy(C, dC, 8ull * M * N, cudaMemcpyDeviceToHost);
+  cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(dg);
+  return e == cudaSuccess ? 0 : -4;
+}
+
+// C (M x N) = op(A) B with the warm-path DMMA GEMM (dgemm.cuh): A is M x K (transA = 0) or K x M
+// (transA = 1), B is K x N, all column-major host arrays; upper = 1 fills only the tiles meeting the upper
+// triangle (the other entries of C are left 0).  reps > 0: *ms = mean CUDA-event time of reps launches.
+extern "C" int sosadmm_debug_dgemm(int M, int N, int K, const double* A, int transA, int upper, const double* B,
+                                   double* C, int variant, int reps, float* ms) {
+  if (variant < 0) variant = DG_DEFAULT;
+  if (variant >= DG_NVAR) return -1;
+  const int ar = transA ? K : M, ac = transA ? M : K;  // stored A: ar x ac
+  const int lda = (ar + 1) & ~1, ldb = (K + 1) & ~1, ldc = (M + 1) & ~1;
+  double *dA, *dB, *dC;
+  DgemmDesc* dg;
+  if (cudaMalloc(&dA, 8ull * lda * std::max(ac, 1)) || cudaMalloc(&dB, 8ull * ldb * std::max(N, 1)) ||
+      cudaMalloc(&dC, 8ull * ldc * std::max(N, 1)) || cudaMalloc(&dg, sizeof(DgemmDesc)))
+    return -7;
+  cudaMemset(dA, 0, 8ull * lda * std::max(ac, 1));
+  cudaMemset(dB, 0, 8ull * ldb * std::max(N, 1));
+  cudaMemset(dC, 0, 8ull * ldc * std::max(N, 1));
+  cudaMemcpy2D(dA, 8ull * lda, A, 8ull * ar, 8ull * ar, ac, cudaMemcpyHostToDevice);
+  cudaMemcpy2D(dB, 8ull * ldb, B, 8ull * K, 8ull * K, N, cudaMemcpyHostToDevice);
+  DgemmDesc g{};
+  g.A = dA; g.lda = lda; g.B = dB; g.ldb = ldb; g.C = dC; g.ldc = ldc;
+  g.M = M; g.N = N; g.K = K; g.transA = transA; g.upper = upper; g.alpha = 1.0; g.beta = 0.0;
+  cudaMemcpy(dg, &g, sizeof(g), cudaMemcpyHostToDevice);
+  dgemm_prepare();
+  dgemm_launch(variant, dg, 1, M, N, nullptr, nullptr, nullptr, 0);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess && reps > 0 && ms) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) dgemm_launch(variant, dg, 1, M, N, nullptr, nullptr, nullptr, 0);
+    cudaEventRecord(e1);
+    e = cudaEventSynchronize(e1);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e0, e1);
+    *ms = t / reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  if (e == cudaSuccess) e = cudaMemcpy2D(C, 8ull * M, dC, 8ull * ldc, 8ull * M, N, cudaMemcpyDeviceToHost);
   cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(dg);
   return e == cudaSuccess ? 0 : -4;
 }

@@ -1,0 +1,693 @@
+// Warm-started large-block PSD projection ("warm-started ... from the previous
+// iteration's eigenvectors (GEMM-rich: Q^T A Q on DMMA)"; PAPER.md P:397-398 `eq:HsdeStep2` projects
+// every Gram block of u_hat - v onto S_+ once per ADMM iteration, and consecutive ADMM iterates change
+// slowly, so the previous iteration's eigenvectors X nearly diagonalise the new block a).
+//
+// Iterative refinement of the eigenvector matrix (Ogita-Aishima form, with near-degenerate clusters
+// solved exactly), every O(N^3) step a DMMA GEMM (dgemm.cuh):
+//   W = a X,  S = X^T W,  P = X^T X,  R = I - P,  lambda_i = S_ii / P_ii;
+//   clusters: runs of the sorted lambda joined by "strong" pairs |S'_ij| > theta |lambda_j - lambda_i|
+//     (S' = S + (lambda_i + lambda_j)/2 R); each cluster's block S_CC is diagonalised exactly (Jacobi,
+//     one CTA per cluster), V = blockdiag of those rotations, S~ = V^T S V, R~ = V^T R V;
+//   E_ij = (S~_ij + lambda~_j R~_ij) / (lambda~_j - lambda~_i) between clusters, R~_ij / 2 inside one;
+//   X <- X V (I + E)                                                         (one GEMM: X M, M = V (I + E)).
+// Stop test on the S of the current X (the one the projection then uses):
+//   ||S_{+-}||_F * sqrt 2 <= 1e-13 ||a||_F   (coupling across the sign split),
+//   ||I - X^T X||_F <= 1e-14 N               (orthonormality at rounding level),
+//   Gershgorin: every row's same-sign off-diagonal mass below |lambda_i| (or itself negligible),
+// so a = X [S_++ 0; 0 S_--] X^T + O(1e-13 ||a||_F) with S_++ >= 0 >= S_--, and the projection is
+//   Pi_{S+}(a) = X_+ S_++ X_+^T   or   Pi_{S+}(-a) = X_- (-S_--) X_-^T   (the side with fewer columns;
+// k_pack applies the Moreau identity for the second, as on the cold path).  The projection is
+// 1-Lipschitz, so the result is within ~1e-13 ||a||_F of the exact one: the iterates are those of an
+// exact eigensolver up to rounding (SURVEY f4 "performance variants that keep the iterates identical").
+// No convergence within WM_MAXS evaluations, a cluster above WM_CAP, or a stalled coupling -> the
+// iteration falls back to the cold path (one-cluster tridiagonalisation + divide and conquer +
+// back-transform of all N columns), which also re-seeds X; after a failure the next 2^f - 1
+// iterations go straight to the cold path (f = consecutive failures, capped).
+#pragma once
+#include "common.cuh"
+#include "dgemm.cuh"
+#include "gemm_f64.cuh"
+
+constexpr int WM_MAXS = 6;          // S evaluations per ADMM iteration (at most 5 updates)
+constexpr int WM_CAP = 64;          // largest cluster diagonalised exactly
+constexpr double WM_THETA = 0.05;   // strong coupling threshold
+constexpr double WM_TOLE = 1e-13;   // cross-sign coupling tolerance relative to ||a||_F
+constexpr double WM_TOLR = 1e-14;   // orthonormality tolerance per unit of N
+constexpr int WM_NT = 1024;         // single-CTA kernels
+constexpr int WM_SORT = 2048;       // bitonic sort capacity (N <= SOSADMM_MAX_BLOCK = 1280)
+constexpr int WM_CLB = 64;          // CTAs of the cluster kernel
+
+struct WarmState {
+  int valid;        // X0 holds the eigenvectors of a previous solve of this block
+  int gate;         // 1 while the refinement runs (every step kernel / GEMM is gated on it)
+  int status;       // 0 running, 1 converged, 2 cold path
+  int step;         // S evaluations done in this iteration
+  int cur;          // X buffer of the converged iterate
+  int ncl;          // clusters (size >= 2) of the current step
+  int fails;        // consecutive failed refinements
+  int backoff;      // iterations still sent straight to the cold path
+  int src;          // what the finish used: 0 = warm (S), 1 = cold (D&C eigenpairs)
+  int pad;
+  double normA2;    // ||a||_F^2 of this iteration
+  double eta_prev;  // coupling of the previous step
+  double eta, rn;   // last step's coupling and orthonormality defect (diagnostics)
+  long long n_warm, n_cold, n_steps, n_fail;  // counters since setup
+};
+
+struct WarmArgs {
+  int N, ldn, nt;            // nt = ceil(N / 32)
+  const double* Mblk;        // block matrix a (ld N, upper triangle valid); the projection overwrites it
+  double *Af, *X0, *X1, *W, *S, *P, *E, *Mm;
+  double *lam, *lamt;
+  int *order, *pos, *diff, *cid, *cpos, *cl_start, *cl_size, *cl_voff, *sel, *idx;
+  double* Vcl;               // cluster rotations, <= WM_CAP * N doubles
+  double *partA, *cross, *roff, *grow, *gcol;  // deterministic partial sums
+  double* rdiag;             // sum (1 - P_ii)^2
+  WarmState* ws;
+  const double* lam_cold;    // ascending eigenvalues of the cold path (D&C)
+  int* side;                 // le.side + b (k_pack: 1 = the block holds Pi(-a))
+  const DevState* st;
+  const IterScal* is;
+  unsigned long long hstep[WM_MAXS];  // graph conditional handles (0 = not in a graph)
+  unsigned long long hcold;
+};
+
+__device__ __forceinline__ bool wm_skip(const WarmArgs& a) { return a.st->done || !a.is->proceed; }
+__device__ __forceinline__ void wm_set(unsigned long long h, unsigned v) {
+  if (h) cudaGraphSetConditional((cudaGraphConditionalHandle)h, v);
+}
+// symmetric access to the upper-triangle storage of S / P (ld)
+__device__ __forceinline__ double wm_sym(const double* A, int ld, int p, int q) {
+  return p <= q ? A[(size_t)q * ld + p] : A[(size_t)p * ld + q];
+}
+
+// fixed-order block sum over WM_NT threads (result in every thread)
+__device__ __forceinline__ double wm_block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+  __syncthreads();
+  return s;
+}
+
+// ---- begin: full symmetric copy Af of a (32 x 32 tile transposes), ||a||_F^2 partials, state ----
+// grid (nt, nt), 256 threads
+__global__ void __launch_bounds__(256) k_warm_begin(WarmArgs a) {
+  if (wm_skip(a)) return;
+  __shared__ double t[32][33];
+  __shared__ double red[8];
+  const int ti = blockIdx.x, tj = blockIdx.y, tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int N = a.N;
+  double ss = 0.0;
+  for (int r = ty; r < 32; r += 8) {
+    if (ti <= tj) {  // element (i = 32 ti + tx, j = 32 tj + r): source contiguous in i
+      const int i = 32 * ti + tx, j = 32 * tj + r;
+      double v = 0.0;
+      if (i < N && j < N) v = i <= j ? a.Mblk[(size_t)j * N + i] : a.Mblk[(size_t)i * N + j];
+      t[r][tx] = v;
+    } else {         // element (i = 32 ti + r, j = 32 tj + tx), i > j: row i of the lower = column i
+      const int i = 32 * ti + r, j = 32 * tj + tx;
+      t[tx][r] = (i < N && j < N) ? a.Mblk[(size_t)i * N + j] : 0.0;
+    }
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int i = 32 * ti + tx, j = 32 * tj + r;
+    const double v = t[r][tx];
+    ss = fma(v, v, ss);
+    if (i < N && j < N) a.Af[(size_t)j * a.ldn + i] = v;
+  }
+  ss = warp_sum(ss);
+  if (tx == 0) red[ty] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < 8; ++w) s += red[w];
+    a.partA[ti * a.nt + tj] = s;
+    if (ti == 0 && tj == 0) {
+      WarmState* ws = a.ws;
+      ws->step = 0;
+      ws->ncl = 0;
+      ws->cur = 0;
+      ws->eta_prev = 1e300;
+      if (ws->valid && ws->backoff == 0) {
+        ws->gate = 1;
+        ws->status = 0;
+        wm_set(a.hstep[0], 1);
+      } else {
+        ws->gate = 0;
+        ws->status = 2;
+        if (ws->backoff > 0) ws->backoff--;
+        wm_set(a.hcold, 1);
+      }
+    }
+  }
+}
+
+// ---- per step: lambda_i = S_ii / P_ii, sorted order, zeroed link counters ----
+__global__ void __launch_bounds__(WM_NT) k_warm_diag(WarmArgs a) {
+  if (wm_skip(a) || a.ws->gate != 1) return;
+  __shared__ double key[WM_SORT];
+  __shared__ int id[WM_SORT];
+  __shared__ double red[32];
+  const int N = a.N, tid = threadIdx.x;
+  double rd = 0.0;
+  for (int t = tid; t < WM_SORT; t += WM_NT) {
+    if (t < N) {
+      const double s = a.S[(size_t)t * a.ldn + t], p = a.P[(size_t)t * a.ldn + t];
+      const double l = s / p;
+      a.lam[t] = l;
+      key[t] = l;
+      rd = fma(1.0 - p, 1.0 - p, rd);
+    } else {
+      key[t] = 1e308;
+    }
+    id[t] = t;
+  }
+  for (int t = tid; t <= N; t += WM_NT) a.diff[t] = 0;
+  rd = wm_block_sum(rd, red);
+  if (tid == 0) *a.rdiag = rd;
+  // bitonic sort of (key, id) ascending (ties by id: deterministic)
+  for (int k = 2; k <= WM_SORT; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      __syncthreads();
+      for (int t = tid; t < WM_SORT; t += WM_NT) {
+        const int u = t ^ j;
+        if (u > t) {
+          const bool up = (t & k) == 0;
+          const bool gt = key[t] > key[u] || (key[t] == key[u] && id[t] > id[u]);
+          if (gt == up) {
+            const double kk = key[t];
+            key[t] = key[u];
+            key[u] = kk;
+            const int ii = id[t];
+            id[t] = id[u];
+            id[u] = ii;
+          }
+        }
+      }
+    }
+  __syncthreads();
+  for (int t = tid; t < N; t += WM_NT) {
+    a.order[t] = id[t];
+    a.pos[id[t]] = t;
+  }
+}
+
+// ---- per step: coupling / orthonormality / Gershgorin partials and the strong pairs ----
+// grid (nt, nt) (only tiles ti <= tj work), 256 threads: lane = column, 8 row groups of 4 rows
+__global__ void __launch_bounds__(256) k_warm_scan(WarmArgs a) {
+  if (wm_skip(a) || a.ws->gate != 1) return;
+  const int ti = blockIdx.x, tj = blockIdx.y;
+  if (ti > tj) return;
+  __shared__ double colp[8][33];
+  __shared__ double red[2][8];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, N = a.N, ld = a.ldn;
+  const int j = 32 * tj + tx;
+  const bool jv = j < N;
+  const double lj = jv ? a.lam[j] : 0.0;
+  const bool gj = lj > 0.0;
+  const int pj = jv ? a.pos[j] : 0;
+  double cr = 0.0, ro = 0.0, cs = 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int i = 32 * ti + ty + 8 * q;
+    double rs = 0.0;
+    if (jv && i < j) {
+      const double s = a.S[(size_t)j * ld + i], p = a.P[(size_t)j * ld + i];
+      const double li = a.lam[i];
+      const bool gi = li > 0.0;
+      if (gi != gj) {
+        cr = fma(s, s, cr);
+      } else {
+        rs = fabs(s);
+        cs += fabs(s);
+      }
+      ro = fma(p, p, ro);
+      const double sp = fma(-0.5 * (li + lj), p, s);  // S'_ij = S_ij + lambda_bar R_ij, R_ij = -P_ij
+      if (fabs(sp) > WM_THETA * fabs(lj - li)) {
+        const int pi = a.pos[i];
+        atomicAdd(a.diff + min(pi, pj), 1);
+        atomicAdd(a.diff + max(pi, pj), -1);
+      }
+    }
+    rs = warp_sum(rs);  // row i's same-sign mass over this tile's columns (columns j > i)
+    if (tx == 0 && i < N) a.grow[(size_t)tj * N + i] = rs;
+  }
+  colp[ty][tx] = cs;
+  cr = warp_sum(cr);
+  ro = warp_sum(ro);
+  if (tx == 0) {
+    red[0][ty] = cr;
+    red[1][ty] = ro;
+  }
+  __syncthreads();
+  if (ty == 0) {
+    double c = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) c += colp[w][tx];
+    if (jv) a.gcol[(size_t)ti * N + j] = c;  // column j's mass over this tile's rows (rows i < j)
+    if (tx == 0) {
+      double c2 = 0.0, r2 = 0.0;
+      for (int w = 0; w < 8; ++w) {
+        c2 += red[0][w];
+        r2 += red[1][w];
+      }
+      a.cross[ti * a.nt + tj] = c2;
+      a.roff[ti * a.nt + tj] = r2;
+    }
+  }
+}
+
+// ---- per step: stop test, failure test, clusters ----
+__global__ void __launch_bounds__(WM_NT) k_warm_decide(WarmArgs a, int step) {
+  if (wm_skip(a) || a.ws->gate != 1) return;
+  __shared__ double red[32];
+  __shared__ int sh_ncl, sh_big, sh_unsafe;
+  __shared__ int cpre[WM_SORT];
+  WarmState* ws = a.ws;
+  const int N = a.N, nt = a.nt, tid = threadIdx.x;
+  if (tid == 0) {
+    sh_ncl = 0;
+    sh_big = 0;
+    sh_unsafe = 0;
+  }
+  // fixed-order sums of the tile partials
+  double c2 = 0.0, r2 = 0.0, a2 = 0.0;
+  for (int e = tid; e < nt * nt; e += WM_NT) {
+    const int ti = e / nt, tj = e % nt;
+    if (ti <= tj) {
+      c2 += a.cross[e];
+      r2 += a.roff[e];
+    }
+    if (step == 0) a2 += a.partA[e];
+  }
+  c2 = wm_block_sum(c2, red);
+  r2 = wm_block_sum(r2, red);
+  if (step == 0) {
+    a2 = wm_block_sum(a2, red);
+    if (tid == 0) ws->normA2 = a2;
+  }
+  __syncthreads();
+  const double nA = sqrt(ws->normA2);
+  const double eta = sqrt(2.0 * c2), rn = sqrt(2.0 * r2 + *a.rdiag);
+  // Gershgorin sign safety: row i's same-sign off-diagonal mass
+  for (int i = tid; i < N; i += WM_NT) {
+    const int ti = i >> 5;
+    double rho = 0.0;
+    for (int t = ti; t < nt; ++t) rho += a.grow[(size_t)t * N + i];
+    for (int t = 0; t <= ti; ++t) rho += a.gcol[(size_t)t * N + i];
+    if (!(fabs(a.lam[i]) > rho || rho <= WM_TOLE * nA)) atomicOr(&sh_unsafe, 1);
+  }
+  __syncthreads();
+  const bool conv = eta <= WM_TOLE * nA && rn <= WM_TOLR * N && !sh_unsafe && isfinite(eta) && isfinite(rn);
+  const bool stall = !isfinite(eta) || !isfinite(rn) || step == WM_MAXS - 1 || (step > 0 && eta > 0.5 * ws->eta_prev);
+  if (conv || stall) {
+    if (tid == 0) {
+      ws->gate = 0;
+      ws->eta = eta;
+      ws->rn = rn;
+      ws->step = step + 1;  // S evaluations of this iteration
+      if (conv) {
+        ws->status = 1;
+        ws->cur = step & 1;
+        ws->n_warm++;
+        ws->n_steps += step;
+        ws->fails = 0;
+      } else {
+        ws->status = 2;
+        ws->fails++;
+        ws->backoff = (1 << min(ws->fails, 6)) - 1;
+        ws->n_fail++;
+        ws->n_steps += step;
+        wm_set(a.hcold, 1);
+      }
+    }
+    return;
+  }
+  // clusters: prefix sums of the link counters over the sorted positions
+  for (int t = tid; t < WM_SORT; t += WM_NT) cpre[t] = t < N ? a.diff[t] : 0;
+  for (int off = 1; off < WM_SORT; off <<= 1) {  // Hillis-Steele inclusive scan
+    __syncthreads();
+    int v[WM_SORT / WM_NT];
+#pragma unroll
+    for (int q = 0; q < WM_SORT / WM_NT; ++q) {
+      const int t = tid + q * WM_NT;
+      v[q] = t >= off ? cpre[t - off] : 0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < WM_SORT / WM_NT; ++q) cpre[tid + q * WM_NT] += v[q];
+  }
+  __syncthreads();
+  // cpre[t] > 0: sorted position t is linked to t + 1
+  for (int t = tid; t < N; t += WM_NT) {
+    a.cid[a.order[t]] = -1;
+    a.cpos[a.order[t]] = 0;
+  }
+  __syncthreads();
+  for (int t = tid; t < N - 1; t += WM_NT) {
+    if (cpre[t] > 0 && (t == 0 || cpre[t - 1] <= 0)) {  // start of a run of size >= 2
+      int sz = 2;
+      while (t + sz - 1 < N - 1 && cpre[t + sz - 1] > 0 && sz <= WM_CAP) ++sz;
+      if (sz > WM_CAP) {
+        atomicOr(&sh_big, 1);
+      } else {
+        const int q = atomicAdd(&sh_ncl, 1);
+        a.cl_start[q] = t;
+        a.cl_size[q] = sz;
+        for (int u = 0; u < sz; ++u) {
+          a.cid[a.order[t + u]] = q;
+          a.cpos[a.order[t + u]] = u;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (sh_big) {
+      ws->gate = 0;
+      ws->status = 2;
+      ws->fails++;
+      ws->backoff = (1 << min(ws->fails, 6)) - 1;
+      ws->n_fail++;
+      ws->n_steps += step;
+      wm_set(a.hcold, 1);
+      return;
+    }
+    int off = 0;
+    for (int q = 0; q < sh_ncl; ++q) {
+      a.cl_voff[q] = off;
+      off += a.cl_size[q] * a.cl_size[q];
+    }
+    ws->ncl = sh_ncl;
+    ws->eta_prev = eta;
+    ws->eta = eta;
+    ws->rn = rn;
+    ws->step = step + 1;
+    if (step + 1 < WM_MAXS) wm_set(a.hstep[step + 1], 1);
+  }
+}
+
+// ---- per step: exact eigendecomposition of every cluster block S_CC (parallel-order Jacobi) ----
+// grid WM_CLB, 256 threads, WM_CL_SMEM dynamic shared memory (A and V, WM_CAP x (WM_CAP + 1) each)
+constexpr size_t WM_CL_SMEM = 2 * sizeof(double) * WM_CAP * (WM_CAP + 1);
+__global__ void __launch_bounds__(256) k_warm_cluster(WarmArgs a) {
+  if (wm_skip(a) || a.ws->gate != 1) return;
+  extern __shared__ double wm_dyn[];
+  double(*A)[WM_CAP + 1] = reinterpret_cast<double(*)[WM_CAP + 1]>(wm_dyn);
+  double(*V)[WM_CAP + 1] = reinterpret_cast<double(*)[WM_CAP + 1]>(wm_dyn + WM_CAP * (WM_CAP + 1));
+  __shared__ double cs[WM_CAP / 2], sn[WM_CAP / 2];
+  __shared__ int pp[WM_CAP / 2], qq[WM_CAP / 2];
+  __shared__ int mem[WM_CAP];
+  __shared__ double red[8];
+  const int tid = threadIdx.x, ncl = a.ws->ncl, ld = a.ldn;
+  for (int q = blockIdx.x; q < ncl; q += gridDim.x) {
+    const int c = a.cl_size[q], t0 = a.cl_start[q], voff = a.cl_voff[q];
+    const int cp = (c + 1) & ~1;  // even player count (a dummy index never rotates)
+    __syncthreads();
+    for (int u = tid; u < c; u += 256) mem[u] = a.order[t0 + u];
+    __syncthreads();
+    double f2 = 0.0;
+    for (int e = tid; e < cp * cp; e += 256) {
+      const int u = e % cp, v = e / cp;
+      const double x = (u < c && v < c) ? wm_sym(a.S, ld, mem[u], mem[v]) : 0.0;
+      A[u][v] = x;
+      V[u][v] = u == v ? 1.0 : 0.0;
+      f2 = fma(x, x, f2);
+    }
+    f2 = warp_sum(f2);
+    if ((tid & 31) == 0) red[tid >> 5] = f2;
+    __syncthreads();
+    double fro2 = 0.0;
+    for (int w = 0; w < 8; ++w) fro2 += red[w];
+    for (int sweep = 0; sweep < 40; ++sweep) {
+      double o2 = 0.0;
+      for (int e = tid; e < cp * cp; e += 256) {
+        const int u = e % cp, v = e / cp;
+        if (u != v) o2 = fma(A[u][v], A[u][v], o2);
+      }
+      o2 = warp_sum(o2);
+      __syncthreads();
+      if ((tid & 31) == 0) red[tid >> 5] = o2;
+      __syncthreads();
+      double off2 = 0.0;
+      for (int w = 0; w < 8; ++w) off2 += red[w];
+      if (off2 <= 1e-34 * fro2) break;
+      for (int r = 0; r < cp - 1; ++r) {
+        if (tid < cp / 2) {  // round-robin pairs of round r
+          const int M = cp - 1, k = tid;
+          int p, qv;
+          if (k == 0) {
+            p = M;
+            qv = r % M;
+          } else {
+            p = (r + k) % M;
+            qv = (r - k + M) % M;
+          }
+          if (p > qv) {
+            const int tmp = p;
+            p = qv;
+            qv = tmp;
+          }
+          const double apq = A[p][qv], app = A[p][p], aqq = A[qv][qv];
+          double cc = 1.0, ss = 0.0;
+          if (apq != 0.0) {
+            const double tau = (aqq - app) / (2.0 * apq);
+            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            cc = 1.0 / sqrt(1.0 + t * t);
+            ss = t * cc;
+          }
+          cs[k] = cc;
+          sn[k] = ss;
+          pp[k] = p;
+          qq[k] = qv;
+        }
+        __syncthreads();
+        // rows: A <- J^T A
+        for (int e = tid; e < (cp / 2) * cp; e += 256) {
+          const int k = e % (cp / 2), v = e / (cp / 2);
+          const int p = pp[k], qv = qq[k];
+          const double x = A[p][v], y = A[qv][v];
+          A[p][v] = cs[k] * x - sn[k] * y;
+          A[qv][v] = sn[k] * x + cs[k] * y;
+        }
+        __syncthreads();
+        // columns: A <- A J, V <- V J
+        for (int e = tid; e < (cp / 2) * cp; e += 256) {
+          const int k = e % (cp / 2), u = e / (cp / 2);
+          const int p = pp[k], qv = qq[k];
+          const double x = A[u][p], y = A[u][qv];
+          A[u][p] = cs[k] * x - sn[k] * y;
+          A[u][qv] = sn[k] * x + cs[k] * y;
+          const double vx = V[u][p], vy = V[u][qv];
+          V[u][p] = cs[k] * vx - sn[k] * vy;
+          V[u][qv] = sn[k] * vx + cs[k] * vy;
+        }
+        __syncthreads();
+      }
+    }
+    // rotated eigenvalue estimates lambda~_u = mu_u / (1 - R~_uu), R~ = V^T R V, R = I - P
+    for (int u = tid; u < c; u += 256) {
+      double ruu = 0.0;
+      for (int t = 0; t < c; ++t) {
+        double rv = 0.0;
+        for (int t2 = 0; t2 < c; ++t2) rv = fma((t == t2 ? 1.0 : 0.0) - wm_sym(a.P, ld, mem[t], mem[t2]), V[t2][u], rv);
+        ruu = fma(V[t][u], rv, ruu);
+      }
+      a.lamt[mem[u]] = A[u][u] / (1.0 - ruu);
+    }
+    for (int e = tid; e < c * c; e += 256) {
+      const int t = e % c, u = e / c;
+      a.Vcl[voff + e] = V[t][u];  // column u: eigenvector u over the members t
+    }
+  }
+}
+
+// coefficient list of rotated index i over the old basis: (members, V column) or the unit vector
+struct WmCo {
+  int n;
+  const int* mem;  // order + cl_start (members in sorted order)
+  const double* v; // V column (n entries), null = 1
+  int self;
+};
+__device__ __forceinline__ WmCo wm_coef(const WarmArgs& a, int i) {
+  WmCo r;
+  const int q = a.cid[i];
+  if (q < 0) {
+    r.n = 1;
+    r.mem = nullptr;
+    r.v = nullptr;
+    r.self = i;
+  } else {
+    const int c = a.cl_size[q];
+    r.n = c;
+    r.mem = a.order + a.cl_start[q];
+    r.v = a.Vcl + a.cl_voff[q] + (size_t)a.cpos[i] * c;
+    r.self = i;
+  }
+  return r;
+}
+
+// ---- per step: E (rotated basis), full N x N; grid (nt, nt), 256 threads ----
+__global__ void __launch_bounds__(256) k_warm_E(WarmArgs a) {
+  if (wm_skip(a) || a.ws->gate != 1) return;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, N = a.N, ld = a.ldn;
+  const int i = 32 * blockIdx.x + tx;
+  if (i >= N) return;
+  const WmCo ci = wm_coef(a, i);
+  const double li = ci.mem ? a.lamt[i] : a.lam[i];
+  const int qi = a.cid[i];
+  for (int r = ty; r < 32; r += 8) {
+    const int j = 32 * blockIdx.y + r;
+    if (j >= N) break;
+    const int qj = a.cid[j];
+    const bool same = (i == j) || (qi >= 0 && qi == qj);
+    double st = 0.0, rt = 0.0;
+    const WmCo cj = wm_coef(a, j);
+    for (int t = 0; t < ci.n; ++t) {
+      const int p = ci.mem ? ci.mem[t] : i;
+      const double vp = ci.v ? ci.v[t] : 1.0;
+      double s2 = 0.0, r2 = 0.0;
+      for (int t2 = 0; t2 < cj.n; ++t2) {
+        const int qv = cj.mem ? cj.mem[t2] : j;
+        const double vq = cj.v ? cj.v[t2] : 1.0;
+        if (!same) s2 = fma(wm_sym(a.S, ld, p, qv), vq, s2);
+        r2 = fma((p == qv ? 1.0 : 0.0) - wm_sym(a.P, ld, p, qv), vq, r2);
+      }
+      st = fma(vp, s2, st);
+      rt = fma(vp, r2, rt);
+    }
+    double e;
+    if (same) {
+      e = 0.5 * rt;
+    } else {
+      const double lj = cj.mem ? a.lamt[j] : a.lam[j];
+      const double d = lj - li;
+      e = d != 0.0 ? fma(lj, rt, st) / d : 0.5 * rt;
+    }
+    a.E[(size_t)j * ld + i] = e;
+  }
+}
+
+// ---- per step: M = V (I + E); grid (nt, nt), 256 threads ----
+__global__ void __launch_bounds__(256) k_warm_M(WarmArgs a) {
+  if (wm_skip(a) || a.ws->gate != 1) return;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, N = a.N, ld = a.ldn;
+  const int ai = 32 * blockIdx.x + tx;
+  if (ai >= N) return;
+  const int q = a.cid[ai];
+  for (int r = ty; r < 32; r += 8) {
+    const int j = 32 * blockIdx.y + r;
+    if (j >= N) break;
+    double m;
+    if (q < 0) {
+      m = (ai == j ? 1.0 : 0.0) + a.E[(size_t)j * ld + ai];
+    } else {
+      const int c = a.cl_size[q];
+      const int* mem = a.order + a.cl_start[q];
+      const double* vr = a.Vcl + a.cl_voff[q] + a.cpos[ai];  // row cpos(ai) of V_C: stride c
+      m = 0.0;
+      for (int u = 0; u < c; ++u) {
+        const int mu = mem[u];
+        m = fma(vr[(size_t)u * c], (mu == j ? 1.0 : 0.0) + a.E[(size_t)j * ld + mu], m);
+      }
+    }
+    a.Mm[(size_t)j * ld + ai] = m;
+  }
+}
+
+// ---- finish: side selection (warm S or cold eigenpairs), compact index list ----
+__global__ void __launch_bounds__(WM_NT) k_warm_select(WarmArgs a, int block_id) {
+  if (wm_skip(a)) return;
+  __shared__ int cnt[WM_NT / 32 + 1];
+  __shared__ int np_s, nn_s;
+  WarmState* ws = a.ws;
+  const int N = a.N, tid = threadIdx.x;
+  const int src = ws->status == 1 ? 0 : 1;
+  const double* lam = src == 0 ? a.lam : a.lam_cold;
+  if (tid == 0) {
+    np_s = 0;
+    nn_s = 0;
+  }
+  __syncthreads();
+  int p = 0, n = 0;
+  for (int i = tid; i < N; i += WM_NT) {
+    p += lam[i] > 0.0;
+    n += lam[i] < 0.0;
+  }
+  atomicAdd(&np_s, p);
+  atomicAdd(&nn_s, n);
+  __syncthreads();
+  const int side = np_s <= nn_s ? 0 : 1;
+  // compact list of the chosen side's indices, ascending (block scan over chunks of WM_NT)
+  int base = 0;
+  for (int c0 = 0; c0 < N; c0 += WM_NT) {
+    const int i = c0 + tid;
+    const bool f = i < N && (side == 0 ? lam[i] > 0.0 : lam[i] < 0.0);
+    const unsigned b = __ballot_sync(0xffffffffu, f);
+    const int w = tid >> 5, l = tid & 31;
+    __syncthreads();
+    if (l == 0) cnt[w] = __popc(b);
+    __syncthreads();
+    if (tid == 0) {
+      int s = 0;
+      for (int q = 0; q < WM_NT / 32; ++q) {
+        const int x = cnt[q];
+        cnt[q] = s;
+        s += x;
+      }
+      cnt[WM_NT / 32] = s;
+    }
+    __syncthreads();
+    if (f) a.idx[base + cnt[w] + __popc(b & ((1u << l) - 1u))] = i;
+    base += cnt[WM_NT / 32];
+  }
+  if (tid == 0) {
+    a.sel[0] = base;
+    a.sel[1] = 0;
+    a.sel[2] = side;
+    a.side[block_id] = side;
+    ws->src = src;
+    if (src == 1) {
+      ws->valid = 1;  // X0 = the cold path's eigenvectors
+      ws->cur = 0;
+      ws->n_cold++;
+    }
+  }
+}
+
+// ---- finish: Xs = X[:, idx] (into W), Ss = +-S[idx, idx] or +-diag(lambda) (into E), X1 -> X0 ----
+// grid >= 148, 256 threads
+__global__ void __launch_bounds__(256) k_warm_gather(WarmArgs a) {
+  if (wm_skip(a)) return;
+  const WarmState* ws = a.ws;
+  const int N = a.N, ld = a.ldn, r = a.sel[0], side = a.sel[2], src = ws->src;
+  const double sg = side ? -1.0 : 1.0;
+  const double* X = (src == 0 && ws->cur == 1) ? a.X1 : a.X0;
+  const long long n1 = (long long)N * r, n2 = (long long)r * r;
+  const long long n3 = (src == 0 && ws->cur == 1) ? (long long)N * N : 0;
+  const long long tot = n1 + n2 + n3;
+  for (long long e = blockIdx.x * 256LL + threadIdx.x; e < tot; e += (long long)gridDim.x * 256) {
+    if (e < n1) {
+      const int row = (int)(e % N), t = (int)(e / N);
+      a.W[(size_t)t * ld + row] = X[(size_t)a.idx[t] * ld + row];
+    } else if (e < n1 + n2) {
+      const long long f = e - n1;
+      const int t = (int)(f % r), u = (int)(f / r);
+      double v;
+      if (src == 0) v = sg * wm_sym(a.S, ld, a.idx[t], a.idx[u]);
+      else v = t == u ? sg * a.lam_cold[a.idx[t]] : 0.0;
+      a.E[(size_t)u * ld + t] = v;
+    } else {
+      const long long f = e - n1 - n2;
+      const int row = (int)(f % N), col = (int)(f / N);
+      a.X0[(size_t)col * ld + row] = a.X1[(size_t)col * ld + row];
+    }
+  }
+}

@@ -21,7 +21,7 @@ STATUS = {0: "RUNNING", 1: "OPTIMAL", 2: "PRIMAL_INFEASIBLE", 3: "DUAL_INFEASIBL
 EXPORTS = ["sosadmm_workspace_size", "sosadmm_setup", "sosadmm_setup_sharded", "sosadmm_nccl_unique_id",
            "sosadmm_iterate", "sosadmm_iterate_async", "sosadmm_iterate_profiled",
            "sosadmm_get_info", "sosadmm_get_iterate", "sosadmm_set_iterate", "sosadmm_get_structure",
-           "sosadmm_project_affine", "sosadmm_project_psd", "sosadmm_launches_per_iter", "sosadmm_psd_work",
+           "sosadmm_project_affine", "sosadmm_project_psd", "sosadmm_launches_per_iter", "sosadmm_psd_work", "sosadmm_warm_stats",
            "sosadmm_destroy",
            "sosadmm_strerror", "sosadmm_last_error_message"]
 
@@ -82,6 +82,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.sosadmm_project_psd.argtypes = [V, I32, P, P]
     lib.sosadmm_psd_work.argtypes = [V, P, ctypes.POINTER(I32)]
     lib.sosadmm_psd_work.restype = ctypes.c_int
+    lib.sosadmm_warm_stats.argtypes = [V, ctypes.POINTER(I64), ctypes.POINTER(I32)]
+    lib.sosadmm_warm_stats.restype = ctypes.c_int
     lib.sosadmm_launches_per_iter.argtypes = [V]
     lib.sosadmm_launches_per_iter.restype = I64
     lib.sosadmm_destroy.argtypes = [V]
@@ -218,6 +220,16 @@ class SosAdmm:
         self._check(self.lib.sosadmm_psd_work(self._ctx, _dptr(w), ctypes.byref(n)), "psd_work")
         keys = ["tridiag", "dc_gemm", "backtransform", "recon", "r", "dc_zero_merges"]
         return [dict(zip(keys, w[6 * b:6 * b + 6].tolist())) for b in range(n.value)]
+
+    def warm_stats(self) -> list:
+        """Per large block: the warm-start counters (sosadmm_warm_stats, csrc/warm.cuh)."""
+        n = ctypes.c_int32(0)
+        self._check(self.lib.sosadmm_warm_stats(self._ctx, None, ctypes.byref(n)), "warm_stats")
+        w = np.zeros(8 * max(n.value, 1), dtype=np.int64)
+        self._check(self.lib.sosadmm_warm_stats(self._ctx, w.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                                ctypes.byref(n)), "warm_stats")
+        keys = ["warm", "cold", "updates", "failed", "enabled", "r", "N", "last_evals"]
+        return [dict(zip(keys, w[8 * b:8 * b + 8].tolist())) for b in range(n.value)]
 
     def info(self) -> dict:
         info = _Info()
