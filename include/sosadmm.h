@@ -192,11 +192,12 @@ sosadmm_err sosadmm_project_psd(sosadmm_ctx* ctx, int32_t block, const double* a
  * `work` in blocks (work may be NULL to query); out: *nblocks = number of large blocks. */
 sosadmm_err sosadmm_psd_work(sosadmm_ctx* ctx, double* work, int32_t* nblocks);
 
-/* Warm-started large-block projection counters (csrc/warm.cuh), 8 int64 per large block in
+/* Warm-started large-block projection counters (csrc/warm.cuh), 10 int64 per large block in
  * setup order: [iterations projected by the warm refinement, iterations projected by the cold path
  * (tridiagonalisation + D&C + back-transform), total refinement updates of the warm iterations and of the
  * failed attempts, failed attempts, warm mode on (0/1), r (rank of the last projection's smaller spectral
- * side), N, S evaluations of the last iteration].  Same capacity protocol as sosadmm_psd_work. */
+ * side), N, S evaluations of the last iteration, cold iterations that re-seeded the eigenvectors, iterations
+ * still sent to the cold path after the last failure].  Same capacity protocol as sosadmm_psd_work. */
 sosadmm_err sosadmm_warm_stats(sosadmm_ctx* ctx, int64_t* stats, int32_t* nblocks);
 
 /* Number of kernel launches one iteration issues (for the bench's gpu_launches claim). */

@@ -54,6 +54,7 @@ struct DcArgs {
   // -1 = all)]; topsel_on = 0 keeps every eigenvector (the stage tests).
   int* topsel;
   int topsel_on;
+  const int* topsel_full;  // optional device flag: nonzero = keep every eigenvector this time (warm.cuh re-seed)
 };
 
 __device__ __forceinline__ bool dc_skip(const DcArgs& a) {
@@ -700,7 +701,7 @@ __global__ void __launch_bounds__(DC_NT) k_dc_topsel(DcArgs a, int root) {
   atomicAdd(&cnt[3], dn);
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (!a.topsel_on) {
+    if (!a.topsel_on || (a.topsel_full && *a.topsel_full)) {
       a.topsel[0] = k;
       a.topsel[1] = 0;
       a.topsel[2] = -1;

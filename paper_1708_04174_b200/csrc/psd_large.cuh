@@ -356,7 +356,8 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
     lb.gdesc = (GemmDesc*)p[q++];
     lb.sel = (int*)p[q++];
     dc.topsel = lb.sel + 4;
-    dc.topsel_on = warm ? 0 : 1;  // the warm mode's cold path needs every eigenvector (it re-seeds X)
+    dc.topsel_on = 1;  // the warm mode's cold path keeps every eigenvector only when it re-seeds X (topsel_full)
+    dc.topsel_full = nullptr;
     lb.warm = warm;
     double* hand = (double*)p[q++];
     lb.Twy = (double*)p[q++];
@@ -394,7 +395,7 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
         g.K = nd.n;
         g.Kdev = dc.node_k + id;
         g.Ndev = dc.node_k + id;
-        if (h == D && !warm) {  // root: only the selected eigenvector columns (k_dc_topsel)
+        if (h == D) {  // root: only the selected eigenvector columns (k_dc_topsel)
           g.Ndev = dc.topsel;
           g.Noff = dc.topsel + 1;
         }
@@ -514,6 +515,7 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
       lb.wdesc = (DgemmDesc*)p[q++];
       lb.sel_all = (int*)p[q++];
       wa.lam_cold = dc.lam[D & 1];
+      if (warm) lb.dc.topsel_full = &wa.ws->need_full;
       wa.side = nullptr;  // le.side, set after the carve
       wa.st = st;
       wa.is = is;
@@ -759,12 +761,12 @@ inline void large_block_warm_step(LargeEig& le, LargeBlock& lb, cudaStream_t s, 
   k_warm_M<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
   dgemm_launch(DG_DEFAULT, lb.wdesc + 4 * j + 3, 1, N, N, s, le.st, le.is, 1);
 }
-// cold path of the warm mode: tridiagonalisation, WY factors, divide and conquer (every eigenvector),
-// back-transform of all N columns, unscaled, into X0 (pitch ldn).  side / ev as in the concurrent variant
-// (side streams sw, sd and 8 events), or sequential on s when sw == nullptr.
-inline void large_block_cold_full(LargeEig& le, LargeBlock& lb, cudaStream_t s, cudaStream_t sw = nullptr,
-                                  cudaStream_t sd = nullptr, const cudaEvent_t* evs = nullptr) {
-  const int N = lb.N, fb = lb.D & 1;
+// cold path of the warm mode: tridiagonalisation, WY factors, divide and conquer (every eigenvector when
+// it re-seeds X, else the projected side only: k_dc_topsel reads ws->need_full); with side streams
+// (sw, sd and 8 events) as in the concurrent variant, or sequential on s when sw == nullptr.
+inline void large_block_cold(LargeEig& le, LargeBlock& lb, cudaStream_t s, cudaStream_t sw = nullptr,
+                             cudaStream_t sd = nullptr, const cudaEvent_t* evs = nullptr) {
+  const int N = lb.N;
   if (sw) {
     cudaEventRecord(evs[6], s);
     cudaStreamWaitEvent(sd, evs[6], 0);
@@ -782,6 +784,10 @@ inline void large_block_cold_full(LargeEig& le, LargeBlock& lb, cudaStream_t s, 
     large_block_wy(le, lb, s, true);
     large_block_dc(le, lb, s, true);
   }
+}
+// full tail of the cold path: every eigenvector back-transformed, unscaled, into X0 (pitch ldn)
+inline void large_block_bt_all(LargeEig& le, LargeBlock& lb, cudaStream_t s) {
+  const int N = lb.N, fb = lb.D & 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(BTC_P * ((N + BTW_NC - 1) / BTW_NC), 1, 1);
   cfg.blockDim = dim3(BTC_NT, 1, 1);
@@ -798,7 +804,7 @@ inline void large_block_cold_full(LargeEig& le, LargeBlock& lb, cudaStream_t s, 
                      (const double*)lb.V, (const double*)lb.Twy, (const int*)lb.sel_all, lb.wa.X0, N, lb.nref,
                      le.st, le.is, 1, lb.wa.ldn, 0);
 }
-// finish (both paths): side and index list, Xs / Ss gather, Y = Xs Ss, M = Y Xs^T into the block matrix
+// finish (warm success or full cold tail): side and index list, Xs / Ss gather, Y = Xs Ss, M = Y Xs^T
 inline void large_block_warm_finish(LargeEig& le, LargeBlock& lb, cudaStream_t s) {
   const int N = lb.N;
   k_warm_select<<<1, WM_NT, 0, s>>>(lb.wa, lb.b);
@@ -807,42 +813,37 @@ inline void large_block_warm_finish(LargeEig& le, LargeBlock& lb, cudaStream_t s
   dim3 gr((N + GM_BM - 1) / GM_BM, (N + GM_BN - 1) / GM_BN, 1);
   k_gemm_f64<<<gr, GM_NT, 0, s>>>(lb.gdesc + lb.wrecon, le.st, le.is, 1);
 }
-// un-graphed warm projection of one block: the refinement steps, then (host decision after a sync) the
-// cold path if they did not converge, then the finish.  ev (optional, 3 events): after the refinement /
-// cold tridiagonalisation, after the cold D&C + back-transform, after the finish.
+// un-graphed warm projection of one block: the refinement steps, then (host decisions after a sync) the
+// cold path and its tail, or the finish.  ev (optional, 3 events): after the refinement / cold
+// tridiagonalisation, after the cold D&C + back-transform, after the reconstruction.
 inline cudaError_t large_block_warm_ungraphed(LargeEig& le, LargeBlock& lb, cudaStream_t s, cudaEvent_t* ev) {
   large_block_warm_begin(le, lb, s, lb.wa);
   for (int j = 0; j < WM_MAXS; ++j) large_block_warm_step(le, lb, s, j, lb.wa);
   WarmState h{};
+  DevState hs{};
   cudaError_t e = cudaMemcpyAsync(&h, lb.wa.ws, sizeof(h), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&hs, le.st, sizeof(hs), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return e;
-  if (h.status != 1) {
-    const int N = lb.N, fb = lb.D & 1;
+  if (h.status != 1 && !hs.done) {
     large_block_tridiag(le, lb, s, true);
     if (ev) cudaEventRecord(ev[0], s);
     large_block_wy(le, lb, s, true);
     large_block_dc(le, lb, s, true);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(BTC_P * ((N + BTW_NC - 1) / BTW_NC), 1, 1);
-    cfg.blockDim = dim3(BTC_NT, 1, 1);
-    cfg.dynamicSmemBytes = bt_apply_smem_bytes(N);
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = BTC_P;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_bt_apply, (const double*)lb.dc.Q[fb], (const double*)lb.dc.lam[fb],
-                       (const double*)lb.V, (const double*)lb.Twy, (const int*)lb.sel_all, lb.wa.X0, N, lb.nref,
-                       le.st, le.is, 1, lb.wa.ldn, 0);
-  } else if (ev) {
-    cudaEventRecord(ev[0], s);
+    k_warm_cold_switch<<<1, 1, 0, s>>>(lb.wa);  // (counter only: no graph handles here)
+    if (h.need_full) {
+      large_block_bt_all(le, lb, s);
+      if (ev) cudaEventRecord(ev[1], s);
+      large_block_warm_finish(le, lb, s);
+    } else {
+      if (ev) cudaEventRecord(ev[1], s);
+      large_block_recon(le, lb, s, true, false);
+    }
+  } else {
+    if (ev) cudaEventRecord(ev[0], s);
+    if (ev) cudaEventRecord(ev[1], s);
+    large_block_warm_finish(le, lb, s);
   }
-  if (ev) cudaEventRecord(ev[1], s);
-  large_block_warm_finish(le, lb, s);
   if (ev) cudaEventRecord(ev[2], s);
   return cudaSuccess;
 }
@@ -902,29 +903,43 @@ inline cudaError_t graph_if_body(cudaStream_t s, unsigned long long h, cudaGraph
   return cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies);
 }
 
-// Warm block inside a stream capture on sb: begin, WM_MAXS refinement steps each in an IF node (set by
-// the previous step's stop test), the cold path in an IF node (set by a failed test or by begin when no
-// warm start exists), then the finish.  sbody: a stream outside any capture, for the bodies.
+// Warm block inside a stream capture on sb (every branch an IF node, its body captured to graph on sbody):
+//   begin -> step 0 .. WM_MAXS-1 (each set by begin / the previous stop test) -> cold eigensolver (set by
+//   begin or a failed test; ends with k_warm_cold_switch) -> full tail (bt of every column + finish) or
+//   partial tail (k_select + bt of the projected side + reconstruction) -> warm finish (set on success).
 inline cudaError_t large_block_warm_graph(LargeEig& le, LargeBlock& lb, cudaStream_t sb, cudaStream_t sbody,
                                           cudaStream_t sw, cudaStream_t sd, const cudaEvent_t* evs) {
   WarmArgs wg = lb.wa;
   cudaError_t e = cudaSuccess;
   for (int j = 0; j < WM_MAXS && e == cudaSuccess; ++j) e = graph_new_handle(sb, &wg.hstep[j]);
-  if (e == cudaSuccess) e = graph_new_handle(sb, &wg.hcold);
+  for (unsigned long long* h : {&wg.hcold, &wg.hfull, &wg.hpart, &wg.hfin})
+    if (e == cudaSuccess) e = graph_new_handle(sb, h);
   if (e != cudaSuccess) return e;
   large_block_warm_begin(le, lb, sb, wg);
-  for (int j = 0; j <= WM_MAXS; ++j) {
+  const int nbody = WM_MAXS + 4;
+  for (int j = 0; j < nbody; ++j) {
+    const unsigned long long h = j < WM_MAXS ? wg.hstep[j] : (j == WM_MAXS ? wg.hcold : (j == WM_MAXS + 1 ? wg.hfull : (j == WM_MAXS + 2 ? wg.hpart : wg.hfin)));
     cudaGraph_t body = nullptr;
-    e = graph_if_body(sb, j < WM_MAXS ? wg.hstep[j] : wg.hcold, &body);
+    e = graph_if_body(sb, h, &body);
     if (e == cudaSuccess) e = cudaStreamBeginCaptureToGraph(sbody, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) return e;
-    if (j < WM_MAXS) large_block_warm_step(le, lb, sbody, j, wg);
-    else large_block_cold_full(le, lb, sbody, sw, sd, evs);
+    if (j < WM_MAXS) {
+      large_block_warm_step(le, lb, sbody, j, wg);
+    } else if (j == WM_MAXS) {
+      large_block_cold(le, lb, sbody, sw, sd, evs);
+      k_warm_cold_switch<<<1, 1, 0, sbody>>>(wg);
+    } else if (j == WM_MAXS + 1) {
+      large_block_bt_all(le, lb, sbody);
+      large_block_warm_finish(le, lb, sbody);
+    } else if (j == WM_MAXS + 2) {
+      large_block_recon(le, lb, sbody, true, false);
+    } else {
+      large_block_warm_finish(le, lb, sbody);
+    }
     cudaGraph_t out = nullptr;
     e = cudaStreamEndCapture(sbody, &out);
     if (e != cudaSuccess) return e;
   }
-  large_block_warm_finish(le, lb, sb);
   return cudaGetLastError();
 }
 

@@ -571,7 +571,9 @@ sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev, int
   if (a.pos_ctas > 0) k_scatter<<<a.pos_ctas, POS_NT, 0, s>>>(a, 0);
   if (ev) cudaEventRecord(ev[2], s);
   const bool has_small = !c->an.small_blk.empty(), has_large = !c->an.large_blk.empty();
-  if (!ev && has_large && c->aux_ok) {
+  cudaStreamCaptureStatus capst = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &capst);
+  if (!ev && has_large && c->aux_ok && capst == cudaStreamCaptureStatusActive) {
     // graph path: Jacobi blocks, every large block's chain and its WY factors on parallel branches
     cudaEventRecord(c->ev_fork, s);
     if (has_small) {
@@ -1369,7 +1371,7 @@ sosadmm_err sosadmm_warm_stats(sosadmm_ctx* c, int64_t* stats, int32_t* nblocks)
       CK_CTX(c, cudaMemcpyAsync(&h, lb.wa.ws, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
       CK_CTX(c, cudaMemcpyAsync(sel, lb.warm ? lb.wa.sel : lb.sel, sizeof(sel), cudaMemcpyDeviceToHost, c->stream));
       CK_CTX(c, cudaStreamSynchronize(c->stream));
-      int64_t* o = stats + 8 * b;
+      int64_t* o = stats + 10 * b;
       o[0] = h.n_warm;
       o[1] = h.n_cold;
       o[2] = h.n_steps;
@@ -1378,6 +1380,8 @@ sosadmm_err sosadmm_warm_stats(sosadmm_ctx* c, int64_t* stats, int32_t* nblocks)
       o[5] = sel[0];
       o[6] = lb.N;
       o[7] = h.step;
+      o[8] = h.n_seed;
+      o[9] = h.backoff;
     }
   *nblocks = nb;
   return SOSADMM_OK;

@@ -48,11 +48,12 @@ struct WarmState {
   int fails;        // consecutive failed refinements
   int backoff;      // iterations still sent straight to the cold path
   int src;          // what the finish used: 0 = warm (S), 1 = cold (D&C eigenpairs)
-  int pad;
+  int need_full;    // the cold path of this iteration re-seeds X (every eigenvector): the next one tries warm
   double normA2;    // ||a||_F^2 of this iteration
   double eta_prev;  // coupling of the previous step
   double eta, rn;   // last step's coupling and orthonormality defect (diagnostics)
-  long long n_warm, n_cold, n_steps, n_fail;  // counters since setup
+  long long n_warm, n_cold, n_steps, n_fail;  // counters since setup: warm / cold iterations, refinement
+  long long n_seed;                            // updates, failed attempts, cold iterations that re-seeded X
 };
 
 struct WarmArgs {
@@ -69,8 +70,8 @@ struct WarmArgs {
   int* side;                 // le.side + b (k_pack: 1 = the block holds Pi(-a))
   const DevState* st;
   const IterScal* is;
-  unsigned long long hstep[WM_MAXS];  // graph conditional handles (0 = not in a graph)
-  unsigned long long hcold;
+  unsigned long long hstep[WM_MAXS];  // graph conditional handles (0 = not in a graph): refinement steps,
+  unsigned long long hcold, hfull, hpart, hfin;  // cold eigensolver, its full / partial tail, warm finish
 };
 
 __device__ __forceinline__ bool wm_skip(const WarmArgs& a) { return a.st->done || !a.is->proceed; }
@@ -138,11 +139,13 @@ __global__ void __launch_bounds__(256) k_warm_begin(WarmArgs a) {
       if (ws->valid && ws->backoff == 0) {
         ws->gate = 1;
         ws->status = 0;
+        ws->need_full = 0;
         wm_set(a.hstep[0], 1);
       } else {
         ws->gate = 0;
         ws->status = 2;
         if (ws->backoff > 0) ws->backoff--;
+        ws->need_full = ws->backoff == 0;  // only the iteration before the next attempt re-seeds X
         wm_set(a.hcold, 1);
       }
     }
@@ -319,10 +322,12 @@ __global__ void __launch_bounds__(WM_NT) k_warm_decide(WarmArgs a, int step) {
         ws->n_warm++;
         ws->n_steps += step;
         ws->fails = 0;
+        wm_set(a.hfin, 1);
       } else {
         ws->status = 2;
         ws->fails++;
         ws->backoff = (1 << min(ws->fails, 6)) - 1;
+        ws->need_full = 0;
         ws->n_fail++;
         ws->n_steps += step;
         wm_set(a.hcold, 1);
@@ -375,6 +380,7 @@ __global__ void __launch_bounds__(WM_NT) k_warm_decide(WarmArgs a, int step) {
       ws->status = 2;
       ws->fails++;
       ws->backoff = (1 << min(ws->fails, 6)) - 1;
+      ws->need_full = 0;
       ws->n_fail++;
       ws->n_steps += step;
       wm_set(a.hcold, 1);
@@ -602,6 +608,14 @@ __global__ void __launch_bounds__(256) k_warm_M(WarmArgs a) {
   }
 }
 
+// ---- end of the cold path: which tail runs (full re-seed + finish, or the partial-spectrum recon) ----
+__global__ void k_warm_cold_switch(WarmArgs a) {
+  if (wm_skip(a)) return;
+  a.ws->n_cold++;
+  if (a.ws->need_full) wm_set(a.hfull, 1);
+  else wm_set(a.hpart, 1);
+}
+
 // ---- finish: side selection (warm S or cold eigenpairs), compact index list ----
 __global__ void __launch_bounds__(WM_NT) k_warm_select(WarmArgs a, int block_id) {
   if (wm_skip(a)) return;
@@ -657,7 +671,7 @@ __global__ void __launch_bounds__(WM_NT) k_warm_select(WarmArgs a, int block_id)
     if (src == 1) {
       ws->valid = 1;  // X0 = the cold path's eigenvectors
       ws->cur = 0;
-      ws->n_cold++;
+      ws->n_seed++;
     }
   }
 }

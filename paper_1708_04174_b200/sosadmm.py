@@ -225,11 +225,11 @@ class SosAdmm:
         """Per large block: the warm-start counters (sosadmm_warm_stats, csrc/warm.cuh)."""
         n = ctypes.c_int32(0)
         self._check(self.lib.sosadmm_warm_stats(self._ctx, None, ctypes.byref(n)), "warm_stats")
-        w = np.zeros(8 * max(n.value, 1), dtype=np.int64)
+        w = np.zeros(10 * max(n.value, 1), dtype=np.int64)
         self._check(self.lib.sosadmm_warm_stats(self._ctx, w.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                                                 ctypes.byref(n)), "warm_stats")
-        keys = ["warm", "cold", "updates", "failed", "enabled", "r", "N", "last_evals"]
-        return [dict(zip(keys, w[8 * b:8 * b + 8].tolist())) for b in range(n.value)]
+        keys = ["warm", "cold", "updates", "failed", "enabled", "r", "N", "last_evals", "seeds", "backoff"]
+        return [dict(zip(keys, w[10 * b:10 * b + 10].tolist())) for b in range(n.value)]
 
     def info(self) -> dict:
         info = _Info()
