@@ -753,7 +753,7 @@ inline void large_block_warm_step(LargeEig& le, LargeBlock& lb, cudaStream_t s, 
   const int N = lb.N;
   dgemm_launch(DG_DEFAULT, lb.wdesc + 4 * j, 1, N, N, s, le.st, le.is, 1);
   dgemm_launch(DG_DEFAULT, lb.wdesc + 4 * j + 1, 2, N, N, s, le.st, le.is, 1);
-  k_warm_diag<<<1, WM_NT, 0, s>>>(wa);
+  k_warm_diag<<<wa.nt, 256, 0, s>>>(wa);
   k_warm_scan<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
   k_warm_decide<<<1, WM_NT, 0, s>>>(wa, j);
   k_warm_cluster<<<WM_CLB, 256, WM_CL_SMEM, s>>>(wa);

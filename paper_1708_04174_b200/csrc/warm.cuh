@@ -152,53 +152,52 @@ __global__ void __launch_bounds__(256) k_warm_begin(WarmArgs a) {
   }
 }
 
-// ---- per step: lambda_i = S_ii / P_ii, sorted order, zeroed link counters ----
-__global__ void __launch_bounds__(WM_NT) k_warm_diag(WarmArgs a) {
+// ---- per step: lambda_i = S_ii / P_ii, sorted order (rank by counting), zeroed link counters ----
+// grid nt CTAs of 256 threads: CTA b ranks i in [32 b, 32 b + 32) against every lambda (8 warps x a
+// slice of j each); ties by index, so the order is exact and deterministic.
+__global__ void __launch_bounds__(256) k_warm_diag(WarmArgs a) {
   if (wm_skip(a) || a.ws->gate != 1) return;
   __shared__ double key[WM_SORT];
-  __shared__ int id[WM_SORT];
-  __shared__ double red[32];
-  const int N = a.N, tid = threadIdx.x;
+  __shared__ int cnt[8][33];
+  __shared__ double red[8];
+  const int N = a.N, ld = a.ldn, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   double rd = 0.0;
-  for (int t = tid; t < WM_SORT; t += WM_NT) {
-    if (t < N) {
-      const double s = a.S[(size_t)t * a.ldn + t], p = a.P[(size_t)t * a.ldn + t];
-      const double l = s / p;
-      a.lam[t] = l;
-      key[t] = l;
-      rd = fma(1.0 - p, 1.0 - p, rd);
-    } else {
-      key[t] = 1e308;
-    }
-    id[t] = t;
+  for (int t = tid; t < N; t += 256) {
+    const double p = a.P[(size_t)t * ld + t];
+    key[t] = a.S[(size_t)t * ld + t] / p;
+    if (blockIdx.x == 0) rd = fma(1.0 - p, 1.0 - p, rd);
   }
-  for (int t = tid; t <= N; t += WM_NT) a.diff[t] = 0;
-  rd = wm_block_sum(rd, red);
-  if (tid == 0) *a.rdiag = rd;
-  // bitonic sort of (key, id) ascending (ties by id: deterministic)
-  for (int k = 2; k <= WM_SORT; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      __syncthreads();
-      for (int t = tid; t < WM_SORT; t += WM_NT) {
-        const int u = t ^ j;
-        if (u > t) {
-          const bool up = (t & k) == 0;
-          const bool gt = key[t] > key[u] || (key[t] == key[u] && id[t] > id[u]);
-          if (gt == up) {
-            const double kk = key[t];
-            key[t] = key[u];
-            key[u] = kk;
-            const int ii = id[t];
-            id[t] = id[u];
-            id[u] = ii;
-          }
-        }
-      }
-    }
   __syncthreads();
-  for (int t = tid; t < N; t += WM_NT) {
-    a.order[t] = id[t];
-    a.pos[id[t]] = t;
+  const int i = 32 * blockIdx.x + lane;
+  const double ki = i < N ? key[i] : 0.0;
+  const int per = (N + 7) / 8, j0 = w * per, j1 = min(N, j0 + per);
+  int c = 0;
+  if (i < N)
+    for (int j = j0; j < j1; ++j) {
+      const double kj = key[j];
+      c += (kj < ki || (kj == ki && j < i)) ? 1 : 0;
+    }
+  cnt[w][lane] = c;
+  if (blockIdx.x == 0) {
+    rd = warp_sum(rd);
+    if (lane == 0) red[w] = rd;
+  }
+  __syncthreads();
+  if (w == 0 && i < N) {
+    int r = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) r += cnt[q][lane];
+    a.lam[i] = ki;
+    a.order[r] = i;
+    a.pos[i] = r;
+  }
+  if (blockIdx.x == 0) {
+    for (int t = tid; t <= N; t += 256) a.diff[t] = 0;
+    if (tid == 0) {
+      double s2 = 0.0;
+      for (int q = 0; q < 8; ++q) s2 += red[q];
+      *a.rdiag = s2;
+    }
   }
 }
 
@@ -541,41 +540,78 @@ __device__ __forceinline__ WmCo wm_coef(const WarmArgs& a, int i) {
 }
 
 // ---- per step: E (rotated basis), full N x N; grid (nt, nt), 256 threads ----
+// The 32 x 32 tile of S and P a CTA needs is staged through shared memory from the upper-triangle storage
+// (coalesced in both halves); pairs involving a cluster member take the general path (global reads).
 __global__ void __launch_bounds__(256) k_warm_E(WarmArgs a) {
   if (wm_skip(a) || a.ws->gate != 1) return;
+  __shared__ double St[32][33], Pt[32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, N = a.N, ld = a.ldn;
-  const int i = 32 * blockIdx.x + tx;
-  if (i >= N) return;
-  const WmCo ci = wm_coef(a, i);
-  const double li = ci.mem ? a.lamt[i] : a.lam[i];
-  const int qi = a.cid[i];
+  const int ti = blockIdx.x, tj = blockIdx.y;
+  // stage: St[r][c] = S(32 ti + c, 32 tj + r)
   for (int r = ty; r < 32; r += 8) {
-    const int j = 32 * blockIdx.y + r;
+    if (ti <= tj) {  // (i = 32 ti + tx, j = 32 tj + r): upper part read down the columns
+      const int i = 32 * ti + tx, j = 32 * tj + r;
+      double sv = 0.0, pv = 0.0;
+      if (i < N && j < N) {
+        sv = wm_sym(a.S, ld, i, j);
+        pv = wm_sym(a.P, ld, i, j);
+      }
+      St[r][tx] = sv;
+      Pt[r][tx] = pv;
+    } else {         // (i = 32 ti + r, j = 32 tj + tx), i > j: S(j, i) = column i of the upper triangle
+      const int i = 32 * ti + r, j = 32 * tj + tx;
+      double sv = 0.0, pv = 0.0;
+      if (i < N && j < N) {
+        sv = a.S[(size_t)i * ld + j];
+        pv = a.P[(size_t)i * ld + j];
+      }
+      St[tx][r] = sv;
+      Pt[tx][r] = pv;
+    }
+  }
+  __syncthreads();
+  const int i = 32 * ti + tx;
+  if (i >= N) return;
+  const int qi = a.cid[i];
+  const double li = qi >= 0 ? a.lamt[i] : a.lam[i];
+  for (int r = ty; r < 32; r += 8) {
+    const int j = 32 * tj + r;
     if (j >= N) break;
     const int qj = a.cid[j];
-    const bool same = (i == j) || (qi >= 0 && qi == qj);
-    double st = 0.0, rt = 0.0;
-    const WmCo cj = wm_coef(a, j);
-    for (int t = 0; t < ci.n; ++t) {
-      const int p = ci.mem ? ci.mem[t] : i;
-      const double vp = ci.v ? ci.v[t] : 1.0;
-      double s2 = 0.0, r2 = 0.0;
-      for (int t2 = 0; t2 < cj.n; ++t2) {
-        const int qv = cj.mem ? cj.mem[t2] : j;
-        const double vq = cj.v ? cj.v[t2] : 1.0;
-        if (!same) s2 = fma(wm_sym(a.S, ld, p, qv), vq, s2);
-        r2 = fma((p == qv ? 1.0 : 0.0) - wm_sym(a.P, ld, p, qv), vq, r2);
-      }
-      st = fma(vp, s2, st);
-      rt = fma(vp, r2, rt);
-    }
     double e;
-    if (same) {
-      e = 0.5 * rt;
+    if (qi < 0 && qj < 0) {  // both singletons: S~ = S, R~ = R
+      const double rt = (i == j ? 1.0 : 0.0) - Pt[r][tx];
+      if (i == j) {
+        e = 0.5 * rt;
+      } else {
+        const double lj = a.lam[j];
+        const double d = lj - li;
+        e = d != 0.0 ? fma(lj, rt, St[r][tx]) / d : 0.5 * rt;
+      }
     } else {
-      const double lj = cj.mem ? a.lamt[j] : a.lam[j];
-      const double d = lj - li;
-      e = d != 0.0 ? fma(lj, rt, st) / d : 0.5 * rt;
+      const bool same = (i == j) || (qi >= 0 && qi == qj);
+      double st = 0.0, rt = 0.0;
+      const WmCo ci = wm_coef(a, i), cj = wm_coef(a, j);
+      for (int t = 0; t < ci.n; ++t) {
+        const int p = ci.mem ? ci.mem[t] : i;
+        const double vp = ci.v ? ci.v[t] : 1.0;
+        double s2 = 0.0, r2 = 0.0;
+        for (int t2 = 0; t2 < cj.n; ++t2) {
+          const int qv = cj.mem ? cj.mem[t2] : j;
+          const double vq = cj.v ? cj.v[t2] : 1.0;
+          if (!same) s2 = fma(wm_sym(a.S, ld, p, qv), vq, s2);
+          r2 = fma((p == qv ? 1.0 : 0.0) - wm_sym(a.P, ld, p, qv), vq, r2);
+        }
+        st = fma(vp, s2, st);
+        rt = fma(vp, r2, rt);
+      }
+      if (same) {
+        e = 0.5 * rt;
+      } else {
+        const double lj = qj >= 0 ? a.lamt[j] : a.lam[j];
+        const double d = lj - li;
+        e = d != 0.0 ? fma(lj, rt, st) / d : 0.5 * rt;
+      }
     }
     a.E[(size_t)j * ld + i] = e;
   }

@@ -35,12 +35,17 @@ def run(M, N, K, tA, up, var=-1, reps=50):
     else:
         err = np.max(np.abs(C - ref))
         fl = 2.0 * M * N * K
-    tf = fl / (ms.value * 1e-3) / 1e12
+    tf = fl / (ms.value * 1e-3) / 1e12 if ms.value > 0 else 0.0
     print(f"v{var} M={M} N={N} K={K} tA={tA} upper={up}: max err {err:.2e}  {ms.value*1e3:.1f} us  {tf:.2f} TF/s "
           f"({100*tf/37.1:.0f}% of DMMA peak)", flush=True)
     return err
 
 
+if len(sys.argv) > 1 and sys.argv[1] == "--ncu":  # one launch per variant (ncu capture)
+    for var in range(10):
+        run(861, 861, 861, 0, 0, var=var, reps=0)
+        run(861, 861, 861, 1, 1, var=var, reps=0)
+    sys.exit(0)
 for var in range(10):
     for args in [(861, 861, 861, 0, 0), (861, 861, 861, 1, 1), (861, 1722, 861, 1, 1), (231, 231, 231, 0, 0)]:
         e = run(*args, var=var)
