@@ -48,7 +48,7 @@ CONFIG_DESC = {"pop6": "n=6 quartic POP, config 0", "pop20": "n=20 quartic POP, 
 DMMA_PEAK_TFLOPS = 37.1   # profiles/r02_probe_fp64.log: mma.sync m8n8k4 f64 (SASS DMMA); round 1 printed 74.3 with
 #                           the probe counting 2x512 flop per m8n8k4; one is 8*8*4 = 256 FMA = 512 flop
 DFMA_PEAK_TFLOPS = 34.2   # same probe, scalar DFMA
-DG_VARIANT_DESC = "CTA tile 32 x 64, two k-groups of 4 warps, 4-stage 16-byte cp.async ring"
+DG_VARIANT_DESC = "CTA tile 32 x 32, 8 warps as two k-groups of 2 x 2 warps (16 x 16 warp tiles), 32-deep k slices, 2-stage 16-byte cp.async ring"
 
 
 def hbm_peak():

@@ -196,9 +196,19 @@ __global__ void __launch_bounds__(32 * WM * WN * KG) k_dgemm(const DgemmDesc* __
   X(6, 64, 64, 32, 2, 2, 3, 2)    \
   X(7, 32, 32, 16, 1, 2, 4, 2)    \
   X(8, 64, 32, 16, 2, 2, 4, 2)    \
-  X(9, 32, 64, 32, 1, 4, 3, 4)
-constexpr int DG_NVAR = 10;
-constexpr int DG_DEFAULT = 3;
+  X(9, 32, 64, 32, 1, 4, 3, 4)    \
+  X(10, 32, 32, 16, 1, 2, 4, 4)   \
+  X(11, 32, 32, 32, 1, 2, 3, 2)   \
+  X(12, 32, 32, 32, 1, 2, 3, 4)   \
+  X(13, 32, 32, 16, 2, 2, 4, 2)   \
+  X(14, 32, 32, 16, 2, 2, 4, 1)   \
+  X(15, 32, 32, 32, 2, 2, 3, 2)   \
+  X(16, 32, 32, 32, 2, 2, 2, 2)   \
+  X(17, 32, 32, 64, 2, 2, 2, 2)   \
+  X(18, 32, 32, 32, 2, 2, 3, 4)   \
+  X(19, 32, 64, 32, 2, 2, 3, 2)
+constexpr int DG_NVAR = 20;
+constexpr int DG_DEFAULT = 16;
 
 // set the dynamic shared-memory attribute of every variant (outside any stream capture)
 inline void dgemm_prepare() {

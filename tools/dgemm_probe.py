@@ -42,12 +42,12 @@ def run(M, N, K, tA, up, var=-1, reps=50):
 
 
 if len(sys.argv) > 1 and sys.argv[1] == "--ncu":  # one launch per variant (ncu capture)
-    for var in range(10):
+    for var in range(20):
         run(861, 861, 861, 0, 0, var=var, reps=0)
         run(861, 861, 861, 1, 1, var=var, reps=0)
     sys.exit(0)
-for var in range(10):
-    for args in [(861, 861, 861, 0, 0), (861, 861, 861, 1, 1), (861, 1722, 861, 1, 1), (231, 231, 231, 0, 0)]:
+for var in [7, 15, 16, 17, 18, 19]:
+    for args in [(861, 861, 861, 0, 0), (861, 861, 861, 1, 1), (231, 231, 231, 0, 0)]:
         e = run(*args, var=var)
         assert e < 1e-11, (var, args)
 for args in [(64, 64, 16, 0, 0), (100, 37, 53, 1, 0), (861, 861, 861, 0, 0), (861, 861, 861, 1, 0),
