@@ -11,8 +11,10 @@ CUDA events on the library's stream; barrier + synchronize around the region; ma
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--start S] [--impl reference] [--config pop40] [--batch B]
 
-Timed window: the solve first advances S iterations (default 2000, about 40 % of config 4's 4,871-iteration
-residual stop), then W warm-up steps, then the K timed steps: the window samples the body of a solve,
+Timed window: the solve first advances S iterations (default: 40 % of the config's solve to the 1e-4
+gamma-accuracy point measured on the oracle -- 8,454 iterations for config 4, so S = 3,382; config 2 has no
+such point and uses 40 % of its 2,000-iteration budget), then W warm-up steps, then the K timed steps: the
+window samples the body of a solve,
 where the warm-started PSD projection (csrc/warm.cuh) runs, not its first iterations (which go through the
 cold eigensolver until the iterates settle).  The whole-solve figure (cold start included) is the
 time-to-1e-4 line and its iters/s.
@@ -43,6 +45,11 @@ CONFIG_INDEX = {"pop6": 0, "pop20": 1, "lyap10": 2, "box24": 3, "pop40": 4}
 CONFIG_DESC = {"pop6": "n=6 quartic POP, config 0", "pop20": "n=20 quartic POP, config 1",
                "lyap10": "n=10 Lyapunov program, config 2", "box24": "n=24 box-constrained POP, config 3",
                "pop40": "n=40 quartic POP, config 4"}
+
+# start of the timed window: 40 % of the iterations the oracle needs to reach max residual <= 1e-4 and
+# |gamma/gamma0 - 1| <= 1e-4 (reading C17: 122 / 1,473 / 1,323 / 8,454 on configs 0 / 1 / 3 / 4;
+# config 2, infeasible as written, runs its 2,000-iteration budget)
+DEFAULT_START = {"pop6": 49, "pop20": 589, "lyap10": 800, "box24": 529, "pop40": 3382}
 
 # roofline denominators: measured on this pool's B200s
 DMMA_PEAK_TFLOPS = 37.1   # profiles/r02_probe_fp64.log: mma.sync m8n8k4 f64 (SASS DMMA); round 1 printed 74.3 with
@@ -636,7 +643,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--start", type=int, default=2000, help="iterations advanced before the warm-up")
+    ap.add_argument("--start", type=int, default=-1,
+                    help="iterations advanced before the warm-up (default: DEFAULT_START of the config)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="pop40")
     ap.add_argument("--seed", type=int, default=0)
@@ -648,6 +656,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.start < 0:
+        args.start = DEFAULT_START.get(args.config, 0)
     if args.impl == "reference":
         run_reference(args)
     elif args.batch > 1:

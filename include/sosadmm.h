@@ -196,8 +196,9 @@ sosadmm_err sosadmm_psd_work(sosadmm_ctx* ctx, double* work, int32_t* nblocks);
  * setup order: [iterations projected by the warm refinement, iterations projected by the cold path
  * (tridiagonalisation + D&C + back-transform), total refinement updates of the warm iterations and of the
  * failed attempts, failed attempts, warm mode on (0/1), r (rank of the last projection's smaller spectral
- * side), N, S evaluations of the last iteration, cold iterations that re-seeded the eigenvectors, iterations
- * still sent to the cold path after the last failure].  Same capacity protocol as sosadmm_psd_work. */
+ * side), N, S evaluations of the last iteration, cold iterations that re-seeded the eigenvectors, reason of
+ * the last failed attempt (1 no convergence within the step budget, 2 stalled coupling, 3 cluster above the
+ * exact-solve cap, 4 non-finite)].  Same capacity protocol as sosadmm_psd_work. */
 sosadmm_err sosadmm_warm_stats(sosadmm_ctx* ctx, int64_t* stats, int32_t* nblocks);
 
 /* Number of kernel launches one iteration issues (for the bench's gpu_launches claim). */

@@ -20,6 +20,11 @@ int sosadmm_debug_gemm(int M, int N, int K, const double* A, const double* B, in
  * reps launches (*ms = mean per launch, CUDA events). */
 int sosadmm_debug_dgemm(int M, int N, int K, const double* A, int transA, int upper, const double* B, double* C,
                         int variant, int reps, float* ms);
+/* Warm-started projection (csrc/warm.cuh) of one symmetric block, 64 < N <= 1280: a0 through the cold path
+ * (seeding the eigenvectors), then a1 through the warm refinement (cold fallback if it does not converge);
+ * out0 / out1 = Pi_{S+}(a0), Pi_{S+}(a1) (full, column-major); stats = [status of the a1 projection (1 warm,
+ * 2 cold), S evaluations, clusters of its last step, r, side, refinement updates]. */
+int sosadmm_debug_warm_project(int N, const double* a0, const double* a1, double* out0, double* out1, int* stats);
 /* Householder tridiagonalisation of the symmetric N x N matrix A in one thread-block cluster:
  * d (N), e (N-1), tau (N-1), V (N x N, reflector k in column k, rows k+1..N-1). */
 int sosadmm_debug_tridiag(int N, const double* A, double* d, double* e, double* tau, double* V);

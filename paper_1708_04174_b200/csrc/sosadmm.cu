@@ -1381,7 +1381,7 @@ sosadmm_err sosadmm_warm_stats(sosadmm_ctx* c, int64_t* stats, int32_t* nblocks)
       o[6] = lb.N;
       o[7] = h.step;
       o[8] = h.n_seed;
-      o[9] = h.backoff;
+      o[9] = h.why;
     }
   *nblocks = nb;
   return SOSADMM_OK;
@@ -1442,7 +1442,7 @@ struct DebugLarge {
   double* mats = nullptr;
   char* base = nullptr;
   cudaStream_t s = nullptr;
-  int init(int N) {
+  int init(int N, bool warm = false) {
     if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) return -4;
     std::vector<int> blk_N{N}, large{0};
     std::vector<long long> blk_mat{0};
@@ -1456,7 +1456,7 @@ struct DebugLarge {
     h.proceed = 1;
     cudaMemcpy(is, &h, sizeof(h), cudaMemcpyHostToDevice);
     std::string msg;
-    if (large_eig_init(le, blk_N, blk_mat, large, mats, base, st, is, s, msg)) return -4;
+    if (large_eig_init(le, blk_N, blk_mat, large, mats, base, st, is, s, msg, warm)) return -4;
     return cudaStreamSynchronize(s) ? -4 : 0;
   }
   ~DebugLarge() {
@@ -1533,6 +1533,49 @@ extern "C" int sosadmm_debug_dgemm(int M, int N, int K, const double* A, int tra
   if (e == cudaSuccess) e = cudaMemcpy2D(C, 8ull * M, dC, 8ull * ldc, 8ull * M, N, cudaMemcpyDeviceToHost);
   cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(dg);
   return e == cudaSuccess ? 0 : -4;
+}
+
+// Warm-started projection of one block (tests/test_gpu_warm.py): a0 through the cold path (which seeds the
+// eigenvectors), then a1 through the warm refinement (cold fallback if it does not converge).  out0 / out1:
+// Pi_{S+}(a0), Pi_{S+}(a1), full N x N column-major; stats = [status of the a1 projection (1 warm, 2 cold),
+// S evaluations, clusters of the last step, r, side, refinement updates].
+extern "C" int sosadmm_debug_warm_project(int N, const double* a0, const double* a1, double* out0, double* out1,
+                                          int* stats) {
+  if (N <= 64 || N > 1280) return -1;
+  DebugLarge dl;
+  int rc = dl.init(N, true);
+  if (rc) return rc;
+  LargeBlock& lb = dl.le.blocks[0];
+  for (int pass = 0; pass < 2; ++pass) {
+    const double* a = pass ? a1 : a0;
+    double* out = pass ? out1 : out0;
+    cudaMemcpyAsync(dl.mats, a, 8ull * N * N, cudaMemcpyHostToDevice, dl.s);
+    if (large_block_warm_ungraphed(dl.le, lb, dl.s, nullptr) != cudaSuccess) return -4;
+    std::vector<double> M((size_t)N * N);
+    int side = 0;
+    cudaMemcpyAsync(M.data(), dl.mats, 8ull * N * N, cudaMemcpyDeviceToHost, dl.s);
+    cudaMemcpyAsync(&side, dl.le.side, 4, cudaMemcpyDeviceToHost, dl.s);
+    WarmState h{};
+    int sel[3] = {0, 0, 0};
+    cudaMemcpyAsync(&h, lb.wa.ws, sizeof(h), cudaMemcpyDeviceToHost, dl.s);
+    cudaMemcpyAsync(sel, h.status == 1 ? lb.wa.sel : lb.sel, sizeof(sel), cudaMemcpyDeviceToHost, dl.s);
+    if (cudaStreamSynchronize(dl.s) != cudaSuccess) return -4;
+    // the block holds the upper triangle of Pi(a) (side 0) or Pi(-a) (side 1: Pi(a) = a + Pi(-a))
+    for (int j = 0; j < N; ++j)
+      for (int i = 0; i < N; ++i) {
+        const double m = i <= j ? M[(size_t)j * N + i] : M[(size_t)i * N + j];
+        out[(size_t)j * N + i] = side ? a[(size_t)j * N + i] + m : m;
+      }
+    if (pass == 1 && stats) {
+      stats[0] = h.status;
+      stats[1] = h.step;
+      stats[2] = h.ncl;
+      stats[3] = sel[0];
+      stats[4] = side;
+      stats[5] = (int)h.n_steps;
+    }
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }
 
 extern "C" int sosadmm_debug_tridiag(int N, const double* A, double* d, double* e, double* tau, double* V) {

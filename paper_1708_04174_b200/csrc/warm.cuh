@@ -29,7 +29,7 @@
 #include "dgemm.cuh"
 #include "gemm_f64.cuh"
 
-constexpr int WM_MAXS = 6;          // S evaluations per ADMM iteration (at most 5 updates)
+constexpr int WM_MAXS = 10;         // S evaluations per ADMM iteration (at most 9 updates)
 constexpr int WM_CAP = 64;          // largest cluster diagonalised exactly
 constexpr double WM_THETA = 0.05;   // strong coupling threshold
 constexpr double WM_TOLE = 1e-13;   // cross-sign coupling tolerance relative to ||a||_F
@@ -54,6 +54,9 @@ struct WarmState {
   double eta, rn;   // last step's coupling and orthonormality defect (diagnostics)
   long long n_warm, n_cold, n_steps, n_fail;  // counters since setup: warm / cold iterations, refinement
   long long n_seed;                            // updates, failed attempts, cold iterations that re-seeded X
+  int why;          // last failure: 1 = no convergence within WM_MAXS, 2 = stalled coupling, 3 = cluster > WM_CAP,
+                    // 4 = non-finite
+  int maxcl;        // largest cluster of the last step
 };
 
 struct WarmArgs {
@@ -270,7 +273,7 @@ __global__ void __launch_bounds__(256) k_warm_scan(WarmArgs a) {
 __global__ void __launch_bounds__(WM_NT) k_warm_decide(WarmArgs a, int step) {
   if (wm_skip(a) || a.ws->gate != 1) return;
   __shared__ double red[32];
-  __shared__ int sh_ncl, sh_big, sh_unsafe;
+  __shared__ int sh_ncl, sh_big, sh_unsafe, sh_maxcl;
   __shared__ int cpre[WM_SORT];
   WarmState* ws = a.ws;
   const int N = a.N, nt = a.nt, tid = threadIdx.x;
@@ -278,6 +281,7 @@ __global__ void __launch_bounds__(WM_NT) k_warm_decide(WarmArgs a, int step) {
     sh_ncl = 0;
     sh_big = 0;
     sh_unsafe = 0;
+    sh_maxcl = 0;
   }
   // fixed-order sums of the tile partials
   double c2 = 0.0, r2 = 0.0, a2 = 0.0;
@@ -329,6 +333,7 @@ __global__ void __launch_bounds__(WM_NT) k_warm_decide(WarmArgs a, int step) {
         ws->need_full = 0;
         ws->n_fail++;
         ws->n_steps += step;
+        ws->why = (!isfinite(eta) || !isfinite(rn)) ? 4 : (step == WM_MAXS - 1 ? 1 : 2);
         wm_set(a.hcold, 1);
       }
     }
@@ -361,8 +366,10 @@ __global__ void __launch_bounds__(WM_NT) k_warm_decide(WarmArgs a, int step) {
       while (t + sz - 1 < N - 1 && cpre[t + sz - 1] > 0 && sz <= WM_CAP) ++sz;
       if (sz > WM_CAP) {
         atomicOr(&sh_big, 1);
+        atomicMax(&sh_maxcl, sz);
       } else {
         const int q = atomicAdd(&sh_ncl, 1);
+        atomicMax(&sh_maxcl, sz);
         a.cl_start[q] = t;
         a.cl_size[q] = sz;
         for (int u = 0; u < sz; ++u) {
@@ -375,6 +382,7 @@ __global__ void __launch_bounds__(WM_NT) k_warm_decide(WarmArgs a, int step) {
   __syncthreads();
   if (tid == 0) {
     if (sh_big) {
+      ws->why = 3;
       ws->gate = 0;
       ws->status = 2;
       ws->fails++;
@@ -391,6 +399,7 @@ __global__ void __launch_bounds__(WM_NT) k_warm_decide(WarmArgs a, int step) {
       off += a.cl_size[q] * a.cl_size[q];
     }
     ws->ncl = sh_ncl;
+    ws->maxcl = sh_maxcl;
     ws->eta_prev = eta;
     ws->eta = eta;
     ws->rn = rn;
@@ -574,6 +583,9 @@ __global__ void __launch_bounds__(256) k_warm_E(WarmArgs a) {
   if (i >= N) return;
   const int qi = a.cid[i];
   const double li = qi >= 0 ? a.lamt[i] : a.lam[i];
+  // no clusters this step: V = I, so M = I + E is written here and k_warm_M has nothing to do
+  const bool direct = a.ws->ncl == 0;
+  double* out = direct ? a.Mm : a.E;
   for (int r = ty; r < 32; r += 8) {
     const int j = 32 * tj + r;
     if (j >= N) break;
@@ -613,13 +625,13 @@ __global__ void __launch_bounds__(256) k_warm_E(WarmArgs a) {
         e = d != 0.0 ? fma(lj, rt, st) / d : 0.5 * rt;
       }
     }
-    a.E[(size_t)j * ld + i] = e;
+    out[(size_t)j * ld + i] = direct ? (i == j ? 1.0 : 0.0) + e : e;
   }
 }
 
 // ---- per step: M = V (I + E); grid (nt, nt), 256 threads ----
 __global__ void __launch_bounds__(256) k_warm_M(WarmArgs a) {
-  if (wm_skip(a) || a.ws->gate != 1) return;
+  if (wm_skip(a) || a.ws->gate != 1 || a.ws->ncl == 0) return;  // (ncl == 0: k_warm_E wrote M)
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, N = a.N, ld = a.ldn;
   const int ai = 32 * blockIdx.x + tx;
   if (ai >= N) return;

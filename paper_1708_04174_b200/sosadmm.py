@@ -228,7 +228,7 @@ class SosAdmm:
         w = np.zeros(10 * max(n.value, 1), dtype=np.int64)
         self._check(self.lib.sosadmm_warm_stats(self._ctx, w.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                                                 ctypes.byref(n)), "warm_stats")
-        keys = ["warm", "cold", "updates", "failed", "enabled", "r", "N", "last_evals", "seeds", "backoff"]
+        keys = ["warm", "cold", "updates", "failed", "enabled", "r", "N", "last_evals", "seeds", "last_fail_reason"]
         return [dict(zip(keys, w[10 * b:10 * b + 10].tolist())) for b in range(n.value)]
 
     def info(self) -> dict:

@@ -238,3 +238,28 @@ def test_tridiag_two_stage(N):
     lam_T = sla.eigh_tridiagonal(d, e, eigvals_only=True)
     lam_A = np.linalg.eigvalsh(A)
     assert np.max(np.abs(lam_T - lam_A)) <= 1e-12 * np.abs(lam_A).max() * np.sqrt(N)
+
+
+@pytest.mark.parametrize("M,N,K,tA,up", [(861, 861, 861, 0, 0), (861, 861, 861, 1, 1), (231, 231, 231, 1, 0),
+                                         (65, 33, 7, 0, 0), (100, 37, 53, 1, 0), (1280, 1280, 1280, 1, 1),
+                                         (300, 5, 1, 0, 0), (7, 9, 1, 1, 0), (129, 129, 2, 1, 1)])
+@pytest.mark.parametrize("variant", [-1, 0, 7])
+def test_warm_dgemm(M, N, K, tA, up, variant):
+    """The warm path's DMMA GEMM (dgemm.cuh) against numpy: op(A) = A or A^T, odd sizes (the 16-byte
+    copies' zero-filled tails), upper-tile mode (only the tiles meeting the upper triangle are formed)."""
+    L = lib()
+    L.sosadmm_debug_dgemm.argtypes = [ctypes.c_int] * 3 + [P, ctypes.c_int, ctypes.c_int, P, P, ctypes.c_int,
+                                                           ctypes.c_int, ctypes.POINTER(ctypes.c_float)]
+    rng = np.random.default_rng(M * 7 + N * 3 + K + tA)
+    A = np.asfortranarray(rng.standard_normal((K, M) if tA else (M, K)))
+    B = np.asfortranarray(rng.standard_normal((K, N)))
+    C = np.zeros((M, N), order="F")
+    ms = ctypes.c_float(0)
+    assert L.sosadmm_debug_dgemm(M, N, K, dp(A), tA, up, dp(B), dp(C), variant, 0, ctypes.byref(ms)) == 0
+    ref = (A.T if tA else A) @ B
+    tol = 1e-14 * max(1, K) * np.abs(A).max() * np.abs(B).max()
+    if up:
+        iu = np.triu_indices(min(M, N))
+        assert np.max(np.abs(C[iu] - ref[iu])) <= tol
+    else:
+        assert np.max(np.abs(C - ref)) <= tol
