@@ -20,6 +20,8 @@ struct DgemmDesc {
   int lda, ldb, ldc;
   int transA;          // 0: op(A)(i, k) = A[k lda + i];  1: op(A)(i, k) = A[i lda + k]
   int upper;           // 1: only tiles with row0 <= last column of the tile
+  int mirror;          // 1 (with upper, beta = 0): C(j, i) = C(i, j) written for i < j, the lower triangle
+                       //   mirrors the upper bit for bit (diagonal tiles keep only their i <= j entries)
   double alpha, beta;
   const int* gate;     // optional: the product runs only while *gate == 1 (warm.cuh state)
   const int* Ndev;     // optional: N = *Ndev (a device-chosen rank, captured once in the CUDA graph)
@@ -179,7 +181,14 @@ __global__ void __launch_bounds__(32 * WM * WN * KG) k_dgemm(const DgemmDesc* __
         if (gj < N) {
           double* cp = g.C + (size_t)gj * g.ldc + gi;
           const double v = g.alpha * acc[a][b][h];
-          *cp = (g.beta == 0.0) ? v : fma(g.beta, *cp, v);
+          if (g.mirror) {
+            if (gi <= gj) {
+              *cp = v;
+              if (gi < gj) g.C[(size_t)gi * g.ldc + gj] = v;
+            }
+          } else {
+            *cp = (g.beta == 0.0) ? v : fma(g.beta, *cp, v);
+          }
         }
       }
   }

@@ -56,7 +56,7 @@ struct LargeBlock {
   // warm-started projection (warm.cuh): refinement of the previous eigenvectors, cold path as fallback
   bool warm = false;
   WarmArgs wa{};
-  DgemmDesc* wdesc = nullptr;  // [WM_MAXS][4]: W = Af X, S = X^T W, P = X^T X, X' = X M; then Y = Xs Ss
+  DgemmDesc* wdesc = nullptr;  // [WM_MAXS][5]: W = Af X, S = X^T W, P = X^T X, X' = X M, W' = W M; then Y = Xs Ss
   int wrecon = 0;              // index of the warm reconstruction descriptor (Y Xs^T) in gdesc
   int* sel_all = nullptr;      // [N, 0, 0]: the cold path back-transforms every column (unscaled) into X0
 };
@@ -259,10 +259,10 @@ inline size_t large_carve(const std::vector<int>& blk_N, const std::vector<int>&
     {  // warm-start buffers (warm.cuh), pitch ldn = N rounded up to even
       const size_t NL = (size_t)N * ((N + 1) & ~1);
       const int nt = (N + 31) / 32;
-      for (int t = 0; t < 8; ++t) p[q++] = take(8 * NL);  // Af X0 X1 W S P E Mm
+      for (int t = 0; t < 12; ++t) p[q++] = take(8 * NL);  // Af X0 X1 W W1 S P E Mm Y Srot Rrot
       p[q++] = take(8 * N);                                // lam
       p[q++] = take(8 * N);                                // lamt
-      for (int t = 0; t < 8; ++t) p[q++] = take(4 * (size_t)(N + 1));  // order pos diff cid cpos cl_start cl_size cl_voff
+      for (int t = 0; t < 9; ++t) p[q++] = take(4 * (size_t)(N + 1));  // order pos diff cid cpos cl_start cl_size cl_voff cl_rbase
       p[q++] = take(4 * 4);                                // sel
       p[q++] = take(4 * (size_t)N);                        // idx
       p[q++] = take(8 * (size_t)WM_CAP * N);               // Vcl
@@ -271,7 +271,7 @@ inline size_t large_carve(const std::vector<int>& blk_N, const std::vector<int>&
       p[q++] = take(8 * (size_t)nt * N);                   // gcol
       p[q++] = take(8);                                    // rdiag
       p[q++] = take(sizeof(WarmState));                    // ws
-      p[q++] = take(sizeof(DgemmDesc) * (WM_MAXS * 4 + 1));  // wdesc
+      p[q++] = take(sizeof(DgemmDesc) * (WM_MAXS * 5 + 1));  // wdesc
       p[q++] = take(4 * 4);                                // sel_all
     }
     per_block(b, N, p, nodes, l0, lnn, lmax, D, leaf0, nleaves, p2n);
@@ -496,12 +496,13 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
       wa.ldn = ldn;
       wa.nt = nt;
       wa.Mblk = lb.M;
-      double** big[8] = {&wa.Af, &wa.X0, &wa.X1, &wa.W, &wa.S, &wa.P, &wa.E, &wa.Mm};
-      for (int t = 0; t < 8; ++t) *big[t] = (double*)p[q++];
+      double** big[12] = {&wa.Af, &wa.X0, &wa.X1, &wa.W, &wa.W1, &wa.S, &wa.P, &wa.E, &wa.Mm, &wa.Y, &wa.Srot, &wa.Rrot};
+      for (int t = 0; t < 12; ++t) *big[t] = (double*)p[q++];
       wa.lam = (double*)p[q++];
       wa.lamt = (double*)p[q++];
-      int** ib[8] = {&wa.order, &wa.pos, &wa.diff, &wa.cid, &wa.cpos, &wa.cl_start, &wa.cl_size, &wa.cl_voff};
-      for (int t = 0; t < 8; ++t) *ib[t] = (int*)p[q++];
+      int** ib[9] = {&wa.order, &wa.pos, &wa.diff, &wa.cid, &wa.cpos, &wa.cl_start, &wa.cl_size, &wa.cl_voff,
+                     &wa.cl_rbase};
+      for (int t = 0; t < 9; ++t) *ib[t] = (int*)p[q++];
       wa.sel = (int*)p[q++];
       wa.idx = (int*)p[q++];
       wa.Vcl = (double*)p[q++];
@@ -519,35 +520,44 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
       wa.side = nullptr;  // le.side, set after the carve
       wa.st = st;
       wa.is = is;
-      std::vector<DgemmDesc> wd(WM_MAXS * 4 + 1);
+      // step j works on X_j = X[j & 1] and W_j = a X_j = W[j & 1]: step 0 forms W_0 = a X_0 and P_0 (unless
+      // the previous iteration's certified P of the same X survives, ws->pgate = 0); every update forms
+      // X_{j+1} = X_j M and W_{j+1} = W_j M in ONE batched launch (same M), so later steps skip a X.
+      std::vector<DgemmDesc> wd(WM_MAXS * 5 + 1);
       for (int j = 0; j < WM_MAXS; ++j) {
         double* Xc = (j & 1) ? wa.X1 : wa.X0;
         double* Xn = (j & 1) ? wa.X0 : wa.X1;
+        double* Wc = (j & 1) ? wa.W1 : wa.W;
+        double* Wn = (j & 1) ? wa.W : wa.W1;
         DgemmDesc g{};
         g.M = N; g.N = N; g.K = N; g.lda = ldn; g.ldb = ldn; g.ldc = ldn; g.alpha = 1.0; g.beta = 0.0;
         g.gate = &wa.ws->gate;
-        DgemmDesc gw = g;  // W = Af X
-        gw.A = wa.Af; gw.B = Xc; gw.C = wa.W;
+        DgemmDesc gw = g;  // W_0 = Af X_0 (step 0 only)
+        gw.A = wa.Af; gw.B = Xc; gw.C = Wc;
         DgemmDesc gs = g;  // S = X^T W (upper)
-        gs.A = Xc; gs.transA = 1; gs.B = wa.W; gs.C = wa.S; gs.upper = 1;
+        gs.A = Xc; gs.transA = 1; gs.B = Wc; gs.C = wa.S; gs.upper = 1; gs.mirror = 1;
         DgemmDesc gp = gs;  // P = X^T X (upper)
         gp.B = Xc; gp.C = wa.P;
+        if (j == 0) gp.gate = &wa.ws->pgate;
         DgemmDesc gx = g;  // X' = X M
         gx.A = Xc; gx.B = wa.Mm; gx.C = Xn;
-        wd[4 * j] = gw;
-        wd[4 * j + 1] = gs;
-        wd[4 * j + 2] = gp;
-        wd[4 * j + 3] = gx;
+        DgemmDesc gv = g;  // W' = W M
+        gv.A = Wc; gv.B = wa.Mm; gv.C = Wn;
+        wd[5 * j] = gw;
+        wd[5 * j + 1] = gs;
+        wd[5 * j + 2] = gp;
+        wd[5 * j + 3] = gx;
+        wd[5 * j + 4] = gv;
       }
-      {  // finish: Y = Xs Ss (Xs in W, Ss in E, Y in P; r x r from sel)
+      {  // finish: Y = Xs Ss (Xs in Mm, Ss in E, Y in Y; r x r from sel)
         DgemmDesc g{};
-        g.A = wa.W; g.lda = ldn; g.B = wa.E; g.ldb = ldn; g.C = wa.P; g.ldc = ldn;
+        g.A = wa.Mm; g.lda = ldn; g.B = wa.E; g.ldb = ldn; g.C = wa.Y; g.ldc = ldn;
         g.M = N; g.N = N; g.K = N; g.Ndev = wa.sel; g.Kdev = wa.sel; g.alpha = 1.0; g.beta = 0.0;
-        wd[WM_MAXS * 4] = g;
+        wd[WM_MAXS * 5] = g;
       }
       {  // warm reconstruction M = Y Xs^T (upper tiles) into the block matrix
         GemmDesc g{};
-        g.A = wa.P; g.lda = ldn; g.B = wa.W; g.ldb = ldn; g.transB = 1; g.C = lb.M; g.ldc = N;
+        g.A = wa.Y; g.lda = ldn; g.B = wa.Mm; g.ldb = ldn; g.transB = 1; g.C = lb.M; g.ldc = N;
         g.M = N; g.N = N; g.K = N; g.Kdev = wa.sel; g.alpha = 1.0; g.beta = 0.0; g.upper = 1;
         if (err == cudaSuccess) err = cudaMemcpyAsync(lb.gdesc + lb.wrecon, &g, sizeof(g), cudaMemcpyHostToDevice, s);
       }
@@ -751,15 +761,16 @@ inline void large_block_warm_begin(LargeEig& le, LargeBlock& lb, cudaStream_t s,
 // refinement step j: W = Af X_j, [S, P] = X_j^T [W, X_j], stop test, clusters, M = V (I + E), X_{j+1} = X_j M
 inline void large_block_warm_step(LargeEig& le, LargeBlock& lb, cudaStream_t s, int j, const WarmArgs& wa) {
   const int N = lb.N;
-  dgemm_launch(DG_DEFAULT, lb.wdesc + 4 * j, 1, N, N, s, le.st, le.is, 1);
-  dgemm_launch(DG_DEFAULT, lb.wdesc + 4 * j + 1, 2, N, N, s, le.st, le.is, 1);
+  if (j == 0) dgemm_launch(DG_DEFAULT, lb.wdesc, 1, N, N, s, le.st, le.is, 1);  // W_0 = a X_0
+  dgemm_launch(DG_DEFAULT, lb.wdesc + 5 * j + 1, 2, N, N, s, le.st, le.is, 1);   // S, P (upper tiles)
   k_warm_diag<<<wa.nt, 256, 0, s>>>(wa);
   k_warm_scan<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
   k_warm_decide<<<1, WM_NT, 0, s>>>(wa, j);
-  k_warm_cluster<<<WM_CLB, 256, WM_CL_SMEM, s>>>(wa);
+  k_warm_cluster<<<WM_CLB, WM_CLT, WM_CL_SMEM, s>>>(wa);
+  k_warm_rot<<<dim3(wa.nt, 32), 256, 0, s>>>(wa);
   k_warm_E<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
   k_warm_M<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
-  dgemm_launch(DG_DEFAULT, lb.wdesc + 4 * j + 3, 1, N, N, s, le.st, le.is, 1);
+  dgemm_launch(DG_DEFAULT, lb.wdesc + 5 * j + 3, 2, N, N, s, le.st, le.is, 1);   // X M, W M
 }
 // cold path of the warm mode: tridiagonalisation, WY factors, divide and conquer (every eigenvector when
 // it re-seeds X, else the projected side only: k_dc_topsel reads ws->need_full); with side streams
@@ -809,7 +820,7 @@ inline void large_block_warm_finish(LargeEig& le, LargeBlock& lb, cudaStream_t s
   const int N = lb.N;
   k_warm_select<<<1, WM_NT, 0, s>>>(lb.wa, lb.b);
   k_warm_gather<<<296, 256, 0, s>>>(lb.wa);
-  dgemm_launch(DG_DEFAULT, lb.wdesc + 4 * WM_MAXS, 1, N, N, s, le.st, le.is, 1);
+  dgemm_launch(DG_DEFAULT, lb.wdesc + 5 * WM_MAXS, 1, N, N, s, le.st, le.is, 1);
   dim3 gr((N + GM_BM - 1) / GM_BM, (N + GM_BN - 1) / GM_BN, 1);
   k_gemm_f64<<<gr, GM_NT, 0, s>>>(lb.gdesc + lb.wrecon, le.st, le.is, 1);
 }
@@ -986,7 +997,7 @@ inline int large_eig_launches(const LargeEig& le) {
   int k = 0;
   for (const auto& lb : le.blocks) {
     if (lb.warm) {  // begin, the refinement steps (IF nodes; an upper bound), the finish; cold path excluded
-      k += 1 + WM_MAXS * 9 + 4;
+      k += 1 + 1 + WM_MAXS * 9 + 4;
       continue;
     }
     k += (lb.two ? 3 : (lb.ksw < lb.N - 2 ? 2 : 1)) + 2 + 1 + 7 * (lb.D - lb.jl) + 1 + 5 + (lb.two ? 1 : 0);

@@ -14,11 +14,12 @@
 // Stop test on the S of the current X (the one the projection then uses):
 //   ||S_{+-}||_F * sqrt 2 <= 1e-13 ||a||_F   (coupling across the sign split),
 //   ||I - X^T X||_F <= 1e-14 N               (orthonormality at rounding level),
-//   Gershgorin: every row's same-sign off-diagonal mass below |lambda_i| (or itself negligible),
-// so a = X [S_++ 0; 0 S_--] X^T + O(1e-13 ||a||_F) with S_++ >= 0 >= S_--, and the projection is
+//   Gershgorin: the rows whose same-sign off-diagonal mass rho_i reaches |lambda_i| have
+//   (sum rho_i^2)^(1/2) <= 1e-12 ||a||_F (the wrong-sign part of a diagonal block is bounded by it),
+// so a = X [S_++ 0; 0 S_--] X^T + O(1e-13 ||a||_F) with S_++, -S_-- PSD up to O(1e-12 ||a||_F), and the projection is
 //   Pi_{S+}(a) = X_+ S_++ X_+^T   or   Pi_{S+}(-a) = X_- (-S_--) X_-^T   (the side with fewer columns;
 // k_pack applies the Moreau identity for the second, as on the cold path).  The projection is
-// 1-Lipschitz, so the result is within ~1e-13 ||a||_F of the exact one: the iterates are those of an
+// 1-Lipschitz, so the result is within ~1e-12 ||a||_F of the exact one: the iterates are those of an
 // exact eigensolver up to rounding (SURVEY f4 "performance variants that keep the iterates identical").
 // No convergence within WM_MAXS evaluations, a cluster above WM_CAP, or a stalled coupling -> the
 // iteration falls back to the cold path (one-cluster tridiagonalisation + divide and conquer +
@@ -34,6 +35,7 @@ constexpr int WM_CAP = 64;          // largest cluster diagonalised exactly
 constexpr double WM_THETA = 0.05;   // strong coupling threshold
 constexpr double WM_TOLE = 1e-13;   // cross-sign coupling tolerance relative to ||a||_F
 constexpr double WM_TOLR = 1e-14;   // orthonormality tolerance per unit of N
+constexpr double WM_TOLG = 1e-12;   // Gershgorin sign-uncertainty bound relative to ||a||_F
 constexpr int WM_NT = 1024;         // single-CTA kernels
 constexpr int WM_SORT = 2048;       // bitonic sort capacity (N <= SOSADMM_MAX_BLOCK = 1280)
 constexpr int WM_CLB = 64;          // CTAs of the cluster kernel
@@ -49,6 +51,8 @@ struct WarmState {
   int backoff;      // iterations still sent straight to the cold path
   int src;          // what the finish used: 0 = warm (S), 1 = cold (D&C eigenpairs)
   int need_full;    // the cold path of this iteration re-seeds X (every eigenvector): the next one tries warm
+  int pgate;        // 1: step 0 forms P = X^T X (0: the previous iteration certified this X and its P is kept)
+  int p_valid;      // the P buffer holds X0^T X0 of the current X0
   double normA2;    // ||a||_F^2 of this iteration
   double eta_prev;  // coupling of the previous step
   double eta, rn;   // last step's coupling and orthonormality defect (diagnostics)
@@ -62,9 +66,10 @@ struct WarmState {
 struct WarmArgs {
   int N, ldn, nt;            // nt = ceil(N / 32)
   const double* Mblk;        // block matrix a (ld N, upper triangle valid); the projection overwrites it
-  double *Af, *X0, *X1, *W, *S, *P, *E, *Mm;
+  double *Af, *X0, *X1, *W, *W1, *S, *P, *E, *Mm, *Y;
+  double *Srot, *Rrot;       // rotated rows (V_C^T S)[u, :], (V_C^T R)[u, :] of every cluster member (slot rows)
   double *lam, *lamt;
-  int *order, *pos, *diff, *cid, *cpos, *cl_start, *cl_size, *cl_voff, *sel, *idx;
+  int *order, *pos, *diff, *cid, *cpos, *cl_start, *cl_size, *cl_voff, *cl_rbase, *sel, *idx;
   double* Vcl;               // cluster rotations, <= WM_CAP * N doubles
   double *partA, *cross, *roff, *grow, *gcol;  // deterministic partial sums
   double* rdiag;             // sum (1 - P_ii)^2
@@ -81,10 +86,9 @@ __device__ __forceinline__ bool wm_skip(const WarmArgs& a) { return a.st->done |
 __device__ __forceinline__ void wm_set(unsigned long long h, unsigned v) {
   if (h) cudaGraphSetConditional((cudaGraphConditionalHandle)h, v);
 }
-// symmetric access to the upper-triangle storage of S / P (ld)
-__device__ __forceinline__ double wm_sym(const double* A, int ld, int p, int q) {
-  return p <= q ? A[(size_t)q * ld + p] : A[(size_t)p * ld + q];
-}
+// entry (p, q) of S / P: the GEMM writes the upper triangle and mirrors it (bitwise symmetric storage),
+// so the column-major read is coalesced along p whichever triangle (p, q) lies in
+__device__ __forceinline__ double wm_sym(const double* A, int ld, int p, int q) { return A[(size_t)q * ld + p]; }
 
 // fixed-order block sum over WM_NT threads (result in every thread)
 __device__ __forceinline__ double wm_block_sum(double v, double* red) {
@@ -141,11 +145,13 @@ __global__ void __launch_bounds__(256) k_warm_begin(WarmArgs a) {
       ws->eta_prev = 1e300;
       if (ws->valid && ws->backoff == 0) {
         ws->gate = 1;
+        ws->pgate = ws->p_valid ? 0 : 1;
         ws->status = 0;
         ws->need_full = 0;
         wm_set(a.hstep[0], 1);
       } else {
         ws->gate = 0;
+        ws->pgate = 0;
         ws->status = 2;
         if (ws->backoff > 0) ws->backoff--;
         ws->need_full = ws->backoff == 0;  // only the iteration before the next attempt re-seeds X
@@ -273,14 +279,13 @@ __global__ void __launch_bounds__(256) k_warm_scan(WarmArgs a) {
 __global__ void __launch_bounds__(WM_NT) k_warm_decide(WarmArgs a, int step) {
   if (wm_skip(a) || a.ws->gate != 1) return;
   __shared__ double red[32];
-  __shared__ int sh_ncl, sh_big, sh_unsafe, sh_maxcl;
+  __shared__ int sh_ncl, sh_big, sh_maxcl;
   __shared__ int cpre[WM_SORT];
   WarmState* ws = a.ws;
   const int N = a.N, nt = a.nt, tid = threadIdx.x;
   if (tid == 0) {
     sh_ncl = 0;
     sh_big = 0;
-    sh_unsafe = 0;
     sh_maxcl = 0;
   }
   // fixed-order sums of the tile partials
@@ -302,17 +307,29 @@ __global__ void __launch_bounds__(WM_NT) k_warm_decide(WarmArgs a, int step) {
   __syncthreads();
   const double nA = sqrt(ws->normA2);
   const double eta = sqrt(2.0 * c2), rn = sqrt(2.0 * r2 + *a.rdiag);
-  // Gershgorin sign safety: row i's same-sign off-diagonal mass
+  // Gershgorin sign safety: row i's same-sign off-diagonal mass rho_i.  A row whose disc reaches across
+  // zero (|lambda_i| <= rho_i) can hide an eigenvalue of the wrong sign of size <= rho_i in its diagonal
+  // block, so the projection error it can cause is bounded by (sum of those rho_i^2)^(1/2): required at
+  // rounding level, <= WM_TOLG ||a||_F (near-zero eigenvalues keep rho_i at the floor of the S product).
+  double g2 = 0.0;
   for (int i = tid; i < N; i += WM_NT) {
     const int ti = i >> 5;
+    // fixed trip count, independent loads (the L2 latencies overlap); tile order t ascending
     double rho = 0.0;
-    for (int t = ti; t < nt; ++t) rho += a.grow[(size_t)t * N + i];
-    for (int t = 0; t <= ti; ++t) rho += a.gcol[(size_t)t * N + i];
-    if (!(fabs(a.lam[i]) > rho || rho <= WM_TOLE * nA)) atomicOr(&sh_unsafe, 1);
+#pragma unroll 8
+    for (int t = 0; t < nt; ++t) {
+      const double gr = t >= ti ? a.grow[(size_t)t * N + i] : 0.0;
+      const double gc = t <= ti ? a.gcol[(size_t)t * N + i] : 0.0;
+      rho += gr + gc;
+    }
+    if (!(fabs(a.lam[i]) > rho)) g2 = fma(rho, rho, g2);
   }
-  __syncthreads();
-  const bool conv = eta <= WM_TOLE * nA && rn <= WM_TOLR * N && !sh_unsafe && isfinite(eta) && isfinite(rn);
-  const bool stall = !isfinite(eta) || !isfinite(rn) || step == WM_MAXS - 1 || (step > 0 && eta > 0.5 * ws->eta_prev);
+  g2 = wm_block_sum(g2, red);
+  const bool cross_ok = eta <= WM_TOLE * nA;
+  const bool conv = cross_ok && rn <= WM_TOLR * N && sqrt(g2) <= WM_TOLG * nA && isfinite(eta) && isfinite(rn);
+  // a coupling that stops halving while still above the tolerance means the update is not converging
+  const bool stall = !isfinite(eta) || !isfinite(rn) || step == WM_MAXS - 1 ||
+                     (step > 0 && !cross_ok && eta > 0.5 * ws->eta_prev);
   if (conv || stall) {
     if (tid == 0) {
       ws->gate = 0;
@@ -393,10 +410,12 @@ __global__ void __launch_bounds__(WM_NT) k_warm_decide(WarmArgs a, int step) {
       wm_set(a.hcold, 1);
       return;
     }
-    int off = 0;
+    int off = 0, rb = 0;
     for (int q = 0; q < sh_ncl; ++q) {
       a.cl_voff[q] = off;
+      a.cl_rbase[q] = rb;
       off += a.cl_size[q] * a.cl_size[q];
+      rb += a.cl_size[q];
     }
     ws->ncl = sh_ncl;
     ws->maxcl = sh_maxcl;
@@ -409,40 +428,51 @@ __global__ void __launch_bounds__(WM_NT) k_warm_decide(WarmArgs a, int step) {
 }
 
 // ---- per step: exact eigendecomposition of every cluster block S_CC (parallel-order Jacobi) ----
-// grid WM_CLB, 256 threads, WM_CL_SMEM dynamic shared memory (A and V, WM_CAP x (WM_CAP + 1) each)
-constexpr size_t WM_CL_SMEM = 2 * sizeof(double) * WM_CAP * (WM_CAP + 1);
-__global__ void __launch_bounds__(256) k_warm_cluster(WarmArgs a) {
+// grid WM_CLB, 256 threads, WM_CL_SMEM dynamic shared memory: A and V ping-pong (2 x 2 x WM_CAP x
+// (WM_CAP + 1)).  A round: the cp/2 rotation parameters of the round-robin pairs (one thread each), then
+// A' = J^T A J and V' = V J elementwise from the other buffer (each element reads the four entries of its
+// two pairs): two barriers per round.  A sweep ends the solve once off(A)^2 <= (4 eps)^2 ||A||_F^2.
+constexpr int WM_CLT = 1024;  // threads of the cluster kernel
+constexpr size_t WM_CL_SMEM = 5 * sizeof(double) * WM_CAP * (WM_CAP + 1);
+__global__ void __launch_bounds__(WM_CLT) k_warm_cluster(WarmArgs a) {
   if (wm_skip(a) || a.ws->gate != 1) return;
   extern __shared__ double wm_dyn[];
-  double(*A)[WM_CAP + 1] = reinterpret_cast<double(*)[WM_CAP + 1]>(wm_dyn);
-  double(*V)[WM_CAP + 1] = reinterpret_cast<double(*)[WM_CAP + 1]>(wm_dyn + WM_CAP * (WM_CAP + 1));
-  __shared__ double cs[WM_CAP / 2], sn[WM_CAP / 2];
-  __shared__ int pp[WM_CAP / 2], qq[WM_CAP / 2];
+  typedef double Row[WM_CAP + 1];
+  Row* Ab[2] = {reinterpret_cast<Row*>(wm_dyn), reinterpret_cast<Row*>(wm_dyn + WM_CAP * (WM_CAP + 1))};
+  Row* Vb[2] = {reinterpret_cast<Row*>(wm_dyn + 2 * WM_CAP * (WM_CAP + 1)),
+                reinterpret_cast<Row*>(wm_dyn + 3 * WM_CAP * (WM_CAP + 1))};
+  __shared__ double cs[WM_CAP], sn[WM_CAP];  // per index: the rotation of its pair, signed for its role
+  __shared__ int mate[WM_CAP];
   __shared__ int mem[WM_CAP];
-  __shared__ double red[8];
+  __shared__ double red[WM_CLT / 32];
+  Row* Rc = reinterpret_cast<Row*>(wm_dyn + 4 * WM_CAP * (WM_CAP + 1));  // R_CC, then R_CC V
   const int tid = threadIdx.x, ncl = a.ws->ncl, ld = a.ldn;
   for (int q = blockIdx.x; q < ncl; q += gridDim.x) {
     const int c = a.cl_size[q], t0 = a.cl_start[q], voff = a.cl_voff[q];
     const int cp = (c + 1) & ~1;  // even player count (a dummy index never rotates)
     __syncthreads();
-    for (int u = tid; u < c; u += 256) mem[u] = a.order[t0 + u];
+    for (int u = tid; u < c; u += WM_CLT) mem[u] = a.order[t0 + u];
     __syncthreads();
     double f2 = 0.0;
-    for (int e = tid; e < cp * cp; e += 256) {
+    for (int e = tid; e < cp * cp; e += WM_CLT) {
       const int u = e % cp, v = e / cp;
-      const double x = (u < c && v < c) ? wm_sym(a.S, ld, mem[u], mem[v]) : 0.0;
-      A[u][v] = x;
-      V[u][v] = u == v ? 1.0 : 0.0;
+      const bool in = u < c && v < c;
+      const double x = in ? wm_sym(a.S, ld, mem[u], mem[v]) : 0.0;
+      Ab[0][u][v] = x;
+      Vb[0][u][v] = u == v ? 1.0 : 0.0;
+      Rc[u][v] = in ? (u == v ? 1.0 : 0.0) - wm_sym(a.P, ld, mem[u], mem[v]) : 0.0;
       f2 = fma(x, x, f2);
     }
     f2 = warp_sum(f2);
     if ((tid & 31) == 0) red[tid >> 5] = f2;
     __syncthreads();
     double fro2 = 0.0;
-    for (int w = 0; w < 8; ++w) fro2 += red[w];
-    for (int sweep = 0; sweep < 40; ++sweep) {
+    for (int w = 0; w < WM_CLT / 32; ++w) fro2 += red[w];
+    int cur = 0;
+    for (int sweep = 0; sweep < 30; ++sweep) {
+      Row* A = Ab[cur];
       double o2 = 0.0;
-      for (int e = tid; e < cp * cp; e += 256) {
+      for (int e = tid; e < cp * cp; e += WM_CLT) {
         const int u = e % cp, v = e / cp;
         if (u != v) o2 = fma(A[u][v], A[u][v], o2);
       }
@@ -451,10 +481,14 @@ __global__ void __launch_bounds__(256) k_warm_cluster(WarmArgs a) {
       if ((tid & 31) == 0) red[tid >> 5] = o2;
       __syncthreads();
       double off2 = 0.0;
-      for (int w = 0; w < 8; ++w) off2 += red[w];
-      if (off2 <= 1e-34 * fro2) break;
+      for (int w = 0; w < WM_CLT / 32; ++w) off2 += red[w];
+      if (off2 <= 2e-30 * fro2) break;
       for (int r = 0; r < cp - 1; ++r) {
-        if (tid < cp / 2) {  // round-robin pairs of round r
+        Row* Ao = Ab[cur];
+        Row* Vo = Vb[cur];
+        Row* An = Ab[cur ^ 1];
+        Row* Vn = Vb[cur ^ 1];
+        if (tid < cp / 2) {  // round-robin pair of round r
           const int M = cp - 1, k = tid;
           int p, qv;
           if (k == 0) {
@@ -469,56 +503,104 @@ __global__ void __launch_bounds__(256) k_warm_cluster(WarmArgs a) {
             p = qv;
             qv = tmp;
           }
-          const double apq = A[p][qv], app = A[p][p], aqq = A[qv][qv];
+          const double apq = Ao[p][qv], app = Ao[p][p], aqq = Ao[qv][qv];
           double cc = 1.0, ss = 0.0;
-          if (apq != 0.0) {
+          if (fabs(apq) > 1e-300) {
             const double tau = (aqq - app) / (2.0 * apq);
             const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
             cc = 1.0 / sqrt(1.0 + t * t);
             ss = t * cc;
           }
-          cs[k] = cc;
-          sn[k] = ss;
-          pp[k] = p;
-          qq[k] = qv;
+          // column p' = c col_p - s col_q, column q' = s col_p + c col_q
+          cs[p] = cc;
+          sn[p] = -ss;
+          mate[p] = qv;
+          cs[qv] = cc;
+          sn[qv] = ss;
+          mate[qv] = p;
         }
         __syncthreads();
-        // rows: A <- J^T A
-        for (int e = tid; e < (cp / 2) * cp; e += 256) {
-          const int k = e % (cp / 2), v = e / (cp / 2);
-          const int p = pp[k], qv = qq[k];
-          const double x = A[p][v], y = A[qv][v];
-          A[p][v] = cs[k] * x - sn[k] * y;
-          A[qv][v] = sn[k] * x + cs[k] * y;
+        // A' = J^T A J, V' = V J: entry (u, v) from the 2 x 2 blocks of u's and v's pairs
+        for (int e = tid; e < cp * cp; e += WM_CLT) {
+          const int u = e % cp, v = e / cp;
+          const int uu = mate[u], vv = mate[v];
+          const double cu = cs[u], su = sn[u], cv = cs[v], sv = sn[v];
+          // (J^T A)_{u, .} = c_u A_{u, .} + s_u A_{uu, .} ; then (.. J)_{., v} = c_v (.)_{., v} + s_v (.)_{., vv}
+          const double r0 = fma(cu, Ao[u][v], su * Ao[uu][v]);
+          const double r1 = fma(cu, Ao[u][vv], su * Ao[uu][vv]);
+          An[u][v] = fma(cv, r0, sv * r1);
+          Vn[u][v] = fma(cv, Vo[u][v], sv * Vo[u][vv]);
         }
-        __syncthreads();
-        // columns: A <- A J, V <- V J
-        for (int e = tid; e < (cp / 2) * cp; e += 256) {
-          const int k = e % (cp / 2), u = e / (cp / 2);
-          const int p = pp[k], qv = qq[k];
-          const double x = A[u][p], y = A[u][qv];
-          A[u][p] = cs[k] * x - sn[k] * y;
-          A[u][qv] = sn[k] * x + cs[k] * y;
-          const double vx = V[u][p], vy = V[u][qv];
-          V[u][p] = cs[k] * vx - sn[k] * vy;
-          V[u][qv] = sn[k] * vx + cs[k] * vy;
-        }
+        cur ^= 1;
         __syncthreads();
       }
     }
-    // rotated eigenvalue estimates lambda~_u = mu_u / (1 - R~_uu), R~ = V^T R V, R = I - P
-    for (int u = tid; u < c; u += 256) {
+    Row* A = Ab[cur];
+    Row* V = Vb[cur];
+    // rotated eigenvalue estimates lambda~_u = mu_u / (1 - R~_uu), R~ = V^T R V, R = I - P:
+    // RV = R_CC V into the free ping-pong buffer, then R~_uu = sum_t V[t][u] RV[t][u]
+    Row* RV = Ab[cur ^ 1];
+    __syncthreads();
+    for (int e = tid; e < c * c; e += WM_CLT) {
+      const int t = e % c, u = e / c;
+      double x = 0.0;
+      for (int t2 = 0; t2 < c; ++t2) x = fma(Rc[t][t2], V[t2][u], x);
+      RV[t][u] = x;
+    }
+    __syncthreads();
+    for (int u = tid; u < c; u += WM_CLT) {
       double ruu = 0.0;
-      for (int t = 0; t < c; ++t) {
-        double rv = 0.0;
-        for (int t2 = 0; t2 < c; ++t2) rv = fma((t == t2 ? 1.0 : 0.0) - wm_sym(a.P, ld, mem[t], mem[t2]), V[t2][u], rv);
-        ruu = fma(V[t][u], rv, ruu);
-      }
+      for (int t = 0; t < c; ++t) ruu = fma(V[t][u], RV[t][u], ruu);
       a.lamt[mem[u]] = A[u][u] / (1.0 - ruu);
     }
-    for (int e = tid; e < c * c; e += 256) {
+    for (int e = tid; e < c * c; e += WM_CLT) {
       const int t = e % c, u = e / c;
       a.Vcl[voff + e] = V[t][u];  // column u: eigenvector u over the members t
+    }
+  }
+}
+
+// ---- per step: rotated rows of the cluster members, (V_C^T S)[u, j] and (V_C^T R)[u, j] for every j ----
+// grid (nt, ncl capped), 256 threads = 32 columns x 8 row groups; S and P are stored full (mirrored), so
+// row m of S is column m: coalesced along j.
+__global__ void __launch_bounds__(256) k_warm_rot(WarmArgs a) {
+  if (wm_skip(a) || a.ws->gate != 1) return;
+  __shared__ double Vs[WM_CAP * WM_CAP];
+  __shared__ int mem[WM_CAP];
+  const int ncl = a.ws->ncl, N = a.N, ld = a.ldn;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int j = 32 * blockIdx.x + tx;
+  for (int q = blockIdx.y; q < ncl; q += gridDim.y) {
+    const int c = a.cl_size[q], rb = a.cl_rbase[q];
+    __syncthreads();
+    for (int e = threadIdx.x; e < c * c; e += 256) Vs[e] = a.Vcl[a.cl_voff[q] + e];
+    for (int u = threadIdx.x; u < c; u += 256) mem[u] = a.order[a.cl_start[q] + u];
+    __syncthreads();
+    if (j >= N) continue;
+    double sr[WM_CAP / 8], rr[WM_CAP / 8];
+#pragma unroll
+    for (int k = 0; k < WM_CAP / 8; ++k) sr[k] = rr[k] = 0.0;
+    for (int t = 0; t < c; ++t) {
+      const int m = mem[t];
+      const double sv = a.S[(size_t)m * ld + j];
+      const double rv = (m == j ? 1.0 : 0.0) - a.P[(size_t)m * ld + j];
+#pragma unroll
+      for (int k = 0; k < WM_CAP / 8; ++k) {
+        const int u = ty + 8 * k;
+        if (u < c) {
+          const double v = Vs[t + u * c];
+          sr[k] = fma(v, sv, sr[k]);
+          rr[k] = fma(v, rv, rr[k]);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < WM_CAP / 8; ++k) {
+      const int u = ty + 8 * k;
+      if (u < c) {
+        a.Srot[(size_t)(rb + u) * ld + j] = sr[k];
+        a.Rrot[(size_t)(rb + u) * ld + j] = rr[k];
+      }
     }
   }
 }
@@ -549,34 +631,23 @@ __device__ __forceinline__ WmCo wm_coef(const WarmArgs& a, int i) {
 }
 
 // ---- per step: E (rotated basis), full N x N; grid (nt, nt), 256 threads ----
-// The 32 x 32 tile of S and P a CTA needs is staged through shared memory from the upper-triangle storage
-// (coalesced in both halves); pairs involving a cluster member take the general path (global reads).
+// The 32 x 32 tile of S and P a CTA needs is staged through shared memory; pairs involving a cluster
+// member take the general path (global reads along the cluster's member columns).
 __global__ void __launch_bounds__(256) k_warm_E(WarmArgs a) {
   if (wm_skip(a) || a.ws->gate != 1) return;
   __shared__ double St[32][33], Pt[32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, N = a.N, ld = a.ldn;
   const int ti = blockIdx.x, tj = blockIdx.y;
-  // stage: St[r][c] = S(32 ti + c, 32 tj + r)
+  // stage: St[r][c] = S(32 ti + c, 32 tj + r) (full symmetric storage: straight column reads)
   for (int r = ty; r < 32; r += 8) {
-    if (ti <= tj) {  // (i = 32 ti + tx, j = 32 tj + r): upper part read down the columns
-      const int i = 32 * ti + tx, j = 32 * tj + r;
-      double sv = 0.0, pv = 0.0;
-      if (i < N && j < N) {
-        sv = wm_sym(a.S, ld, i, j);
-        pv = wm_sym(a.P, ld, i, j);
-      }
-      St[r][tx] = sv;
-      Pt[r][tx] = pv;
-    } else {         // (i = 32 ti + r, j = 32 tj + tx), i > j: S(j, i) = column i of the upper triangle
-      const int i = 32 * ti + r, j = 32 * tj + tx;
-      double sv = 0.0, pv = 0.0;
-      if (i < N && j < N) {
-        sv = a.S[(size_t)i * ld + j];
-        pv = a.P[(size_t)i * ld + j];
-      }
-      St[tx][r] = sv;
-      Pt[tx][r] = pv;
+    const int i = 32 * ti + tx, j = 32 * tj + r;
+    double sv = 0.0, pv = 0.0;
+    if (i < N && j < N) {
+      sv = a.S[(size_t)j * ld + i];
+      pv = a.P[(size_t)j * ld + i];
     }
+    St[r][tx] = sv;
+    Pt[r][tx] = pv;
   }
   __syncthreads();
   const int i = 32 * ti + tx;
@@ -601,21 +672,27 @@ __global__ void __launch_bounds__(256) k_warm_E(WarmArgs a) {
         e = d != 0.0 ? fma(lj, rt, St[r][tx]) / d : 0.5 * rt;
       }
     } else {
+      // rotated rows: slot of a cluster member = its cluster's row base + its position in the cluster
       const bool same = (i == j) || (qi >= 0 && qi == qj);
       double st = 0.0, rt = 0.0;
-      const WmCo ci = wm_coef(a, i), cj = wm_coef(a, j);
-      for (int t = 0; t < ci.n; ++t) {
-        const int p = ci.mem ? ci.mem[t] : i;
-        const double vp = ci.v ? ci.v[t] : 1.0;
-        double s2 = 0.0, r2 = 0.0;
-        for (int t2 = 0; t2 < cj.n; ++t2) {
-          const int qv = cj.mem ? cj.mem[t2] : j;
-          const double vq = cj.v ? cj.v[t2] : 1.0;
-          if (!same) s2 = fma(wm_sym(a.S, ld, p, qv), vq, s2);
-          r2 = fma((p == qv ? 1.0 : 0.0) - wm_sym(a.P, ld, p, qv), vq, r2);
+      if (qi >= 0 && qj < 0) {         // S~_ij = (V^T S)[i, j]
+        const size_t si = (size_t)(a.cl_rbase[qi] + a.cpos[i]) * ld;
+        st = a.Srot[si + j];
+        rt = a.Rrot[si + j];
+      } else if (qi < 0 && qj >= 0) {  // S~_ij = S~_ji = (V^T S)[j, i]
+        const size_t sj = (size_t)(a.cl_rbase[qj] + a.cpos[j]) * ld;
+        st = a.Srot[sj + i];
+        rt = a.Rrot[sj + i];
+      } else {                         // both in clusters: S~_ij = sum_t (V^T S)[i, m_t] V_C(j)[t, u_j]
+        const size_t si = (size_t)(a.cl_rbase[qi] + a.cpos[i]) * ld;
+        const int c = a.cl_size[qj];
+        const int* mem = a.order + a.cl_start[qj];
+        const double* vj = a.Vcl + a.cl_voff[qj] + (size_t)a.cpos[j] * c;
+        for (int t = 0; t < c; ++t) {
+          const int m = mem[t];
+          if (!same) st = fma(a.Srot[si + m], vj[t], st);
+          rt = fma(a.Rrot[si + m], vj[t], rt);
         }
-        st = fma(vp, s2, st);
-        rt = fma(vp, r2, rt);
       }
       if (same) {
         e = 0.5 * rt;
@@ -716,6 +793,7 @@ __global__ void __launch_bounds__(WM_NT) k_warm_select(WarmArgs a, int block_id)
     a.sel[2] = side;
     a.side[block_id] = side;
     ws->src = src;
+    ws->p_valid = src == 0;  // a certified warm X keeps its P (X1 is copied to X0 bit for bit)
     if (src == 1) {
       ws->valid = 1;  // X0 = the cold path's eigenvectors
       ws->cur = 0;
@@ -724,7 +802,7 @@ __global__ void __launch_bounds__(WM_NT) k_warm_select(WarmArgs a, int block_id)
   }
 }
 
-// ---- finish: Xs = X[:, idx] (into W), Ss = +-S[idx, idx] or +-diag(lambda) (into E), X1 -> X0 ----
+// ---- finish: Xs = X[:, idx] (into Mm), Ss = +-S[idx, idx] or +-diag(lambda) (into E), X1 -> X0 ----
 // grid >= 148, 256 threads
 __global__ void __launch_bounds__(256) k_warm_gather(WarmArgs a) {
   if (wm_skip(a)) return;
@@ -738,7 +816,7 @@ __global__ void __launch_bounds__(256) k_warm_gather(WarmArgs a) {
   for (long long e = blockIdx.x * 256LL + threadIdx.x; e < tot; e += (long long)gridDim.x * 256) {
     if (e < n1) {
       const int row = (int)(e % N), t = (int)(e / N);
-      a.W[(size_t)t * ld + row] = X[(size_t)a.idx[t] * ld + row];
+      a.Mm[(size_t)t * ld + row] = X[(size_t)a.idx[t] * ld + row];
     } else if (e < n1 + n2) {
       const long long f = e - n1;
       const int t = (int)(f % r), u = (int)(f / r);
