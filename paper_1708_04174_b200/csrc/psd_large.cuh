@@ -259,7 +259,7 @@ inline size_t large_carve(const std::vector<int>& blk_N, const std::vector<int>&
     {  // warm-start buffers (warm.cuh), pitch ldn = N rounded up to even
       const size_t NL = (size_t)N * ((N + 1) & ~1);
       const int nt = (N + 31) / 32;
-      for (int t = 0; t < 12; ++t) p[q++] = take(8 * NL);  // Af X0 X1 W W1 S P E Mm Y Srot Rrot
+      for (int t = 0; t < 13; ++t) p[q++] = take(8 * NL);  // Af X0 X1 W W1 S P E Mm Y Srot Rrot Esum
       p[q++] = take(8 * N);                                // lam
       p[q++] = take(8 * N);                                // lamt
       for (int t = 0; t < 9; ++t) p[q++] = take(4 * (size_t)(N + 1));  // order pos diff cid cpos cl_start cl_size cl_voff cl_rbase
@@ -271,7 +271,7 @@ inline size_t large_carve(const std::vector<int>& blk_N, const std::vector<int>&
       p[q++] = take(8 * (size_t)nt * N);                   // gcol
       p[q++] = take(8);                                    // rdiag
       p[q++] = take(sizeof(WarmState));                    // ws
-      p[q++] = take(sizeof(DgemmDesc) * (WM_MAXS * 5 + 1));  // wdesc
+      p[q++] = take(sizeof(DgemmDesc) * (WM_MAXS * 5 + 2));  // wdesc
       p[q++] = take(4 * 4);                                // sel_all
     }
     per_block(b, N, p, nodes, l0, lnn, lmax, D, leaf0, nleaves, p2n);
@@ -496,8 +496,13 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
       wa.ldn = ldn;
       wa.nt = nt;
       wa.Mblk = lb.M;
-      double** big[12] = {&wa.Af, &wa.X0, &wa.X1, &wa.W, &wa.W1, &wa.S, &wa.P, &wa.E, &wa.Mm, &wa.Y, &wa.Srot, &wa.Rrot};
-      for (int t = 0; t < 12; ++t) *big[t] = (double*)p[q++];
+      double** big[13] = {&wa.Af, &wa.X0, &wa.X1, &wa.W, &wa.W1, &wa.S, &wa.P, &wa.E, &wa.Mm, &wa.Y, &wa.Srot, &wa.Rrot,
+                          &wa.Esum};
+      for (int t = 0; t < 13; ++t) *big[t] = (double*)p[q++];
+      {
+        const char* e = getenv("SOSADMM_WARM_PRED");
+        wa.predict = (e && e[0] == '0') ? 0 : 1;
+      }
       wa.lam = (double*)p[q++];
       wa.lamt = (double*)p[q++];
       int** ib[9] = {&wa.order, &wa.pos, &wa.diff, &wa.cid, &wa.cpos, &wa.cl_start, &wa.cl_size, &wa.cl_voff,
@@ -523,7 +528,7 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
       // step j works on X_j = X[j & 1] and W_j = a X_j = W[j & 1]: step 0 forms W_0 = a X_0 and P_0 (unless
       // the previous iteration's certified P of the same X survives, ws->pgate = 0); every update forms
       // X_{j+1} = X_j M and W_{j+1} = W_j M in ONE batched launch (same M), so later steps skip a X.
-      std::vector<DgemmDesc> wd(WM_MAXS * 5 + 1);
+      std::vector<DgemmDesc> wd(WM_MAXS * 5 + 2);
       for (int j = 0; j < WM_MAXS; ++j) {
         double* Xc = (j & 1) ? wa.X1 : wa.X0;
         double* Xn = (j & 1) ? wa.X0 : wa.X1;
@@ -554,6 +559,12 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
         g.A = wa.Mm; g.lda = ldn; g.B = wa.E; g.ldb = ldn; g.C = wa.Y; g.ldc = ldn;
         g.M = N; g.N = N; g.K = N; g.Ndev = wa.sel; g.Kdev = wa.sel; g.alpha = 1.0; g.beta = 0.0;
         wd[WM_MAXS * 5] = g;
+      }
+      {  // predictor: X1 = X0 (I + Esum), gated on ws->pred
+        DgemmDesc g{};
+        g.A = wa.X0; g.lda = ldn; g.B = wa.Mm; g.ldb = ldn; g.C = wa.X1; g.ldc = ldn;
+        g.M = N; g.N = N; g.K = N; g.alpha = 1.0; g.beta = 0.0; g.gate = &wa.ws->pred;
+        wd[WM_MAXS * 5 + 1] = g;
       }
       {  // warm reconstruction M = Y Xs^T (upper tiles) into the block matrix
         GemmDesc g{};
@@ -755,7 +766,10 @@ __global__ void k_zero2(double* a, double* b, long long n) {
   }
 }
 inline void large_block_warm_begin(LargeEig& le, LargeBlock& lb, cudaStream_t s, const WarmArgs& wa) {
-  (void)le;
+  if (wa.predict) {
+    k_warm_pred<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
+    dgemm_launch(DG_DEFAULT, lb.wdesc + 5 * WM_MAXS + 1, 1, lb.N, lb.N, s, le.st, le.is, 1);
+  }
   k_warm_begin<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
 }
 // refinement step j: W = Af X_j, [S, P] = X_j^T [W, X_j], stop test, clusters, M = V (I + E), X_{j+1} = X_j M

@@ -52,6 +52,10 @@ struct WarmState {
   int src;          // what the finish used: 0 = warm (S), 1 = cold (D&C eigenpairs)
   int need_full;    // the cold path of this iteration re-seeds X (every eigenvector): the next one tries warm
   int pgate;        // 1: step 0 forms P = X^T X (0: the previous iteration certified this X and its P is kept)
+  int pred;         // 1: this iteration starts from the predicted X0 (I + Esum) (k_warm_pred)
+  int pred_ok;      // Esum holds the previous iteration's whole rotation generator (sum of M - I) and the
+                    // trajectory looked smooth there (no cluster at step 0, <= 3 evaluations predicted / 4 not)
+  int cl0;          // clusters formed at step 0 of this iteration
   int p_valid;      // the P buffer holds X0^T X0 of the current X0
   double normA2;    // ||a||_F^2 of this iteration
   double eta_prev;  // coupling of the previous step
@@ -68,6 +72,8 @@ struct WarmArgs {
   const double* Mblk;        // block matrix a (ld N, upper triangle valid); the projection overwrites it
   double *Af, *X0, *X1, *W, *W1, *S, *P, *E, *Mm, *Y;
   double *Srot, *Rrot;       // rotated rows (V_C^T S)[u, :], (V_C^T R)[u, :] of every cluster member (slot rows)
+  double* Esum;              // sum of (M - I) over the refinement steps: the first-order rotation generator
+  int predict;               // 1: start each warm iteration from X0 (I + Esum) of the previous one
   double *lam, *lamt;
   int *order, *pos, *diff, *cid, *cpos, *cl_start, *cl_size, *cl_voff, *cl_rbase, *sel, *idx;
   double* Vcl;               // cluster rotations, <= WM_CAP * N doubles
@@ -103,6 +109,27 @@ __device__ __forceinline__ double wm_block_sum(double v, double* red) {
   return s;
 }
 
+// ---- predictor (before begin): the eigenvectors move smoothly along the ADMM trajectory, so the
+// previous iteration's rotation, X_{k-1} = X_{k-2} (I + Esum) to first order, is applied once more:
+// M = I + Esum, then X1 = X0 M (gated GEMM) and begin copies X1 to X0.  Esum keeps that generator (the
+// refinement steps add their corrections to it); without a valid generator it restarts from zero.
+// grid (nt, nt), 256 threads
+__global__ void __launch_bounds__(256) k_warm_pred(WarmArgs a) {
+  if (wm_skip(a)) return;
+  const WarmState* ws = a.ws;
+  const bool cond = a.predict && ws->valid && ws->backoff == 0 && ws->pred_ok;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, N = a.N, ld = a.ldn;
+  const int i = 32 * blockIdx.x + tx;
+  for (int r = ty; r < 32 && i < N; r += 8) {
+    const int j = 32 * blockIdx.y + r;
+    if (j >= N) break;
+    const size_t e = (size_t)j * ld + i;
+    if (cond) a.Mm[e] = (i == j ? 1.0 : 0.0) + a.Esum[e];
+    else a.Esum[e] = 0.0;
+  }
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) a.ws->pred = cond ? 1 : 0;
+}
+
 // ---- begin: full symmetric copy Af of a (32 x 32 tile transposes), ||a||_F^2 partials, state ----
 // grid (nt, nt), 256 threads
 __global__ void __launch_bounds__(256) k_warm_begin(WarmArgs a) {
@@ -124,11 +151,15 @@ __global__ void __launch_bounds__(256) k_warm_begin(WarmArgs a) {
     }
   }
   __syncthreads();
+  const bool pred = a.ws->pred;
   for (int r = ty; r < 32; r += 8) {
     const int i = 32 * ti + tx, j = 32 * tj + r;
     const double v = t[r][tx];
     ss = fma(v, v, ss);
-    if (i < N && j < N) a.Af[(size_t)j * a.ldn + i] = v;
+    if (i < N && j < N) {
+      a.Af[(size_t)j * a.ldn + i] = v;
+      if (pred) a.X0[(size_t)j * a.ldn + i] = a.X1[(size_t)j * a.ldn + i];  // the predicted start
+    }
   }
   ss = warp_sum(ss);
   if (tx == 0) red[ty] = ss;
@@ -141,17 +172,19 @@ __global__ void __launch_bounds__(256) k_warm_begin(WarmArgs a) {
       WarmState* ws = a.ws;
       ws->step = 0;
       ws->ncl = 0;
+      ws->cl0 = 0;
       ws->cur = 0;
       ws->eta_prev = 1e300;
       if (ws->valid && ws->backoff == 0) {
         ws->gate = 1;
-        ws->pgate = ws->p_valid ? 0 : 1;
+        ws->pgate = (ws->p_valid && !ws->pred) ? 0 : 1;
         ws->status = 0;
         ws->need_full = 0;
         wm_set(a.hstep[0], 1);
       } else {
         ws->gate = 0;
         ws->pgate = 0;
+        ws->pred_ok = 0;
         ws->status = 2;
         if (ws->backoff > 0) ws->backoff--;
         ws->need_full = ws->backoff == 0;  // only the iteration before the next attempt re-seeds X
@@ -351,6 +384,7 @@ __global__ void __launch_bounds__(WM_NT) k_warm_decide(WarmArgs a, int step) {
         ws->n_fail++;
         ws->n_steps += step;
         ws->why = (!isfinite(eta) || !isfinite(rn)) ? 4 : (step == WM_MAXS - 1 ? 1 : 2);
+        ws->pred_ok = 0;
         wm_set(a.hcold, 1);
       }
     }
@@ -400,6 +434,7 @@ __global__ void __launch_bounds__(WM_NT) k_warm_decide(WarmArgs a, int step) {
   if (tid == 0) {
     if (sh_big) {
       ws->why = 3;
+      ws->pred_ok = 0;
       ws->gate = 0;
       ws->status = 2;
       ws->fails++;
@@ -419,6 +454,7 @@ __global__ void __launch_bounds__(WM_NT) k_warm_decide(WarmArgs a, int step) {
     }
     ws->ncl = sh_ncl;
     ws->maxcl = sh_maxcl;
+    if (step == 0) ws->cl0 = sh_ncl > 0;
     ws->eta_prev = eta;
     ws->eta = eta;
     ws->rn = rn;
@@ -703,6 +739,7 @@ __global__ void __launch_bounds__(256) k_warm_E(WarmArgs a) {
       }
     }
     out[(size_t)j * ld + i] = direct ? (i == j ? 1.0 : 0.0) + e : e;
+    if (direct && a.predict) a.Esum[(size_t)j * ld + i] += e;
   }
 }
 
@@ -730,6 +767,7 @@ __global__ void __launch_bounds__(256) k_warm_M(WarmArgs a) {
       }
     }
     a.Mm[(size_t)j * ld + ai] = m;
+    if (a.predict) a.Esum[(size_t)j * ld + ai] += m - (ai == j ? 1.0 : 0.0);
   }
 }
 
@@ -794,6 +832,10 @@ __global__ void __launch_bounds__(WM_NT) k_warm_select(WarmArgs a, int block_id)
     a.side[block_id] = side;
     ws->src = src;
     ws->p_valid = src == 0;  // a certified warm X keeps its P (X1 is copied to X0 bit for bit)
+    // its rotation generator (Esum) predicts the next iteration's start -- only while the trajectory is
+    // smooth: a cluster at step 0 (near-degenerate eigenvalues moving) or more evaluations than the
+    // unpredicted steady state switch the predictor off until an iteration converges quickly again
+    ws->pred_ok = src == 0 && !ws->cl0 && ws->step <= (ws->pred ? 3 : 4);
     if (src == 1) {
       ws->valid = 1;  // X0 = the cold path's eigenvectors
       ws->cur = 0;
