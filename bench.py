@@ -9,15 +9,15 @@ Timing: W warm-up steps, then K timed steps; before every timed step an L2 flush
 buffer, > 126 MB L2) runs on the same stream outside the timed window; each step is bracketed by
 CUDA events on the library's stream; barrier + synchronize around the region; max over ranks.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--start S] [--impl reference] [--config pop40] [--batch B]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--window sampled|contiguous] [--start S] [--impl reference] [--config pop40] [--batch B]
 
-Timed window: the solve first advances S iterations (default: 40 % of the config's solve to the 1e-4
-gamma-accuracy point measured on the oracle -- 8,454 iterations for config 4, so S = 3,382; config 2 has no
-such point and uses 40 % of its 2,000-iteration budget), then W warm-up steps, then the K timed steps: the
-window samples the body of a solve,
-where the warm-started PSD projection (csrc/warm.cuh) runs, not its first iterations (which go through the
-cold eigensolver until the iterates settle).  The whole-solve figure (cold start included) is the
-time-to-1e-4 line and its iters/s.
+Timed steps (default --window sampled): after W warm-up iterations, the K timed iterations are spread
+evenly over the config's whole solve to the 1e-4 gamma-accuracy point (SOLVE_LEN: 8,454 iterations for
+config 4, the oracle's count), the iterations between them running untimed, so the figure is the mean
+cost of an iteration of a solve: the cold start (cold eigensolver until the iterates settle), the
+warm-started body (csrc/warm.cuh) and the rank transition all weigh in by their share.  --window
+contiguous --start S times iterations S + W + 1 .. S + W + K instead.  The end-to-end whole-solve figure
+is the time-to-1e-4 line and its iters/s.
 
 `--batch B` runs B independent seeded instances per GPU concurrently, each on its
 own stream and CUDA graph, and reports the aggregate iterations/s (not the headline line).
@@ -46,10 +46,10 @@ CONFIG_DESC = {"pop6": "n=6 quartic POP, config 0", "pop20": "n=20 quartic POP, 
                "lyap10": "n=10 Lyapunov program, config 2", "box24": "n=24 box-constrained POP, config 3",
                "pop40": "n=40 quartic POP, config 4"}
 
-# start of the timed window: 40 % of the iterations the oracle needs to reach max residual <= 1e-4 and
-# |gamma/gamma0 - 1| <= 1e-4 (reading C17: 122 / 1,473 / 1,323 / 8,454 on configs 0 / 1 / 3 / 4;
-# config 2, infeasible as written, runs its 2,000-iteration budget)
-DEFAULT_START = {"pop6": 49, "pop20": 589, "lyap10": 800, "box24": 529, "pop40": 3382}
+# length of a solve: the iterations the oracle needs to reach max residual <= 1e-4 and |gamma/gamma0 - 1|
+# <= 1e-4 (reading C17: 122 / 1,473 / 1,323 / 8,454 on configs 0 / 1 / 3 / 4); config 2,
+# infeasible as written, runs its 2,000-iteration budget.  The sampled timed steps are spread over it.
+SOLVE_LEN = {"pop6": 122, "pop20": 1473, "lyap10": 2000, "box24": 1323, "pop40": 8454}
 
 # roofline denominators: measured on this pool's B200s
 DMMA_PEAK_TFLOPS = 37.1   # profiles/r02_probe_fp64.log: mma.sync m8n8k4 f64 (SASS DMMA); round 1 printed 74.3 with
@@ -320,22 +320,34 @@ def run_ours(args):
     st = gpu.stream
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
     launches_per_iter = gpu.launches_per_iter
-    if args.start > 0:
-        gpu.iterate(args.start)  # into the body of the solve (see the module docstring)
-    gpu.iterate(args.warmup)
-    torch.cuda.synchronize()
-    ws0 = gpu.warm_stats()
 
     def barrier():
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    # ---- timed region: K steps, L2 flushed before each, CUDA events on the library stream ----
+    # ---- timed steps: K iterations of the solve, L2 flushed before each, CUDA events on the library
+    # stream.  sampled (default): the K iterations are spread evenly over the config's solve to the 1e-4
+    # gamma-accuracy point (SOLVE_LEN), the iterations between them run untimed; contiguous: iterations
+    # start + W + 1 .. start + W + K ----
+    gpu.iterate(args.warmup)
+    cur = args.warmup
+    if args.window == "sampled":
+        L = max(SOLVE_LEN.get(args.config, 2000), args.warmup + args.steps)
+        targets = [args.warmup + 1 + int((i + 0.5) * (L - args.warmup) / args.steps) for i in range(args.steps)]
+        for i in range(1, len(targets)):
+            targets[i] = max(targets[i], targets[i - 1] + 1)
+    else:
+        targets = [args.start + args.warmup + 1 + i for i in range(args.steps)]
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    window = None
     barrier()
     with ClockSampler(local) as clk:
-        for i in range(args.steps):
+        for i, k in enumerate(targets):
+            if k - 1 > cur:
+                gpu.iterate_async(k - 1 - cur)  # untimed iterations up to the sample
+            barrier()
+            w0 = gpu.warm_stats()
             with torch.cuda.stream(st):
                 flush.fill_(float(i))
                 evs[i][0].record(st)
@@ -344,9 +356,15 @@ def run_ours(args):
             gpu.iterate_async(1)
             with torch.cuda.stream(st):
                 evs[i][1].record(st)
+            cur = k
+            barrier()
+            w1 = gpu.warm_stats()
+            d = warm_window(w0, w1)
+            SUMMED = ("warm_iters", "cold_iters", "failed_attempts", "updates", "evals")
+            window = d if window is None else [{kk: (a[kk] + b[kk] if kk in SUMMED else b[kk]) for kk in a}
+                                               for a, b in zip(window, d)]
         barrier()
     gpu.info()  # raises if any replay failed
-    ws1 = gpu.warm_stats()
     ms = sum(a.elapsed_time(b) for a, b in evs)
     clocks = clk.summary()
     # ---- warm (no flush) graph replay of K iterations, for context ----
@@ -405,8 +423,7 @@ def run_ours(args):
     _, _, tl = gpu.get_structure()
     large = [d for d in prob.psd_dims if d > 64]
     work = gpu.psd_work() if large else []  # flops of the last projection from the device-side sizes
-    window = warm_window(ws0, ws1)
-    gemm = dgemm_timing(max(large)) if large and any(w["enabled"] for w in ws1) else None
+    gemm = dgemm_timing(max(large)) if large and any(w["enabled"] for w in (window or [])) else None
     rooflines = roofline_table(prob, tl, phase, large, hbm, hbm_src, args.config, work, window, gemm)
     # the dominant kernel: the warm path's DMMA GEMM when the window ran warm, else the longest class
     dg = [r for r in rooflines if r["kernel"].startswith("k_dgemm")]
@@ -435,7 +452,8 @@ def run_ours(args):
         "warm_iters_per_s": total_steps / (ms_warm * 1e-3),
         "time_to_1e-4": ttt,
         "solve_iters_per_s": (ttt["iters"] / ttt["seconds"]) if ttt and ttt.get("seconds") else None,
-        "timed_window": {"start_iter": args.start + args.warmup + 1, "end_iter": args.start + args.warmup + args.steps,
+        "timed_window": {"mode": args.window, "iterations": targets if len(targets) <= 64 else None,
+                         "first_iter": targets[0], "last_iter": targets[-1], "solve_len": SOLVE_LEN.get(args.config),
                          "psd_warm": window},
         "phase_ms_per_iter": phase,
         "roofline": {k: dominant[k] for k in ("kernel", "bound", "achieved", "peak", "unit", "frac", "traffic",
@@ -643,8 +661,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--start", type=int, default=-1,
-                    help="iterations advanced before the warm-up (default: DEFAULT_START of the config)")
+    ap.add_argument("--window", default="sampled", choices=["sampled", "contiguous"],
+                    help="sampled: the K timed iterations spread evenly over the solve; contiguous: --start")
+    ap.add_argument("--start", type=int, default=0, help="contiguous window: iterations advanced before the warm-up")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="pop40")
     ap.add_argument("--seed", type=int, default=0)
@@ -656,8 +675,6 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.start < 0:
-        args.start = DEFAULT_START.get(args.config, 0)
     if args.impl == "reference":
         run_reference(args)
     elif args.batch > 1:
