@@ -269,7 +269,10 @@ inline size_t large_carve(const std::vector<int>& blk_N, const std::vector<int>&
       for (int t = 0; t < 3; ++t) p[q++] = take(8 * (size_t)nt * nt);  // partA cross roff
       p[q++] = take(8 * (size_t)nt * N);                   // grow
       p[q++] = take(8 * (size_t)nt * N);                   // gcol
-      p[q++] = take(8);                                    // rdiag
+      p[q++] = take(8 * (size_t)nt);                       // rdpart
+      p[q++] = take(8 * (size_t)nt);                       // g2part
+      p[q++] = take(4 * (size_t)(nt + 2));                 // cnt
+      p[q++] = take(8 * (size_t)WM_PAIRS);                 // pairs
       p[q++] = take(sizeof(WarmState));                    // ws
       p[q++] = take(sizeof(DgemmDesc) * (WM_MAXS * 5 + 2));  // wdesc
       p[q++] = take(4 * 4);                                // sel_all
@@ -516,7 +519,10 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
       wa.roff = (double*)p[q++];
       wa.grow = (double*)p[q++];
       wa.gcol = (double*)p[q++];
-      wa.rdiag = (double*)p[q++];
+      wa.rdpart = (double*)p[q++];
+      wa.g2part = (double*)p[q++];
+      wa.cnt = (int*)p[q++];
+      wa.pairs = (int*)p[q++];
       wa.ws = (WarmState*)p[q++];
       lb.wdesc = (DgemmDesc*)p[q++];
       lb.sel_all = (int*)p[q++];
@@ -777,9 +783,7 @@ inline void large_block_warm_step(LargeEig& le, LargeBlock& lb, cudaStream_t s, 
   const int N = lb.N;
   if (j == 0) dgemm_launch(DG_DEFAULT, lb.wdesc, 1, N, N, s, le.st, le.is, 1);  // W_0 = a X_0
   dgemm_launch(DG_DEFAULT, lb.wdesc + 5 * j + 1, 2, N, N, s, le.st, le.is, 1);   // S, P (upper tiles)
-  k_warm_diag<<<wa.nt, 256, 0, s>>>(wa);
-  k_warm_scan<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
-  k_warm_decide<<<1, WM_NT, 0, s>>>(wa, j);
+  k_warm_scan<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa, j);
   k_warm_cluster<<<WM_CLB, WM_CLT, WM_CL_SMEM, s>>>(wa);
   k_warm_rot<<<dim3(wa.nt, 32), 256, 0, s>>>(wa);
   k_warm_E<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
@@ -1011,7 +1015,7 @@ inline int large_eig_launches(const LargeEig& le) {
   int k = 0;
   for (const auto& lb : le.blocks) {
     if (lb.warm) {  // begin, the refinement steps (IF nodes; an upper bound), the finish; cold path excluded
-      k += 1 + 1 + WM_MAXS * 9 + 4;
+      k += 3 + 1 + WM_MAXS * 7 + 4;
       continue;
     }
     k += (lb.two ? 3 : (lb.ksw < lb.N - 2 ? 2 : 1)) + 2 + 1 + 7 * (lb.D - lb.jl) + 1 + 5 + (lb.two ? 1 : 0);

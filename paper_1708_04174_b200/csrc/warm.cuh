@@ -39,6 +39,7 @@ constexpr double WM_TOLG = 1e-12;   // Gershgorin sign-uncertainty bound relativ
 constexpr int WM_NT = 1024;         // single-CTA kernels
 constexpr int WM_SORT = 2048;       // bitonic sort capacity (N <= SOSADMM_MAX_BLOCK = 1280)
 constexpr int WM_CLB = 64;          // CTAs of the cluster kernel
+constexpr int WM_PAIRS = 1 << 16;   // strong-pair list capacity (more: the step gives up, as for a big cluster)
 
 struct WarmState {
   int valid;        // X0 holds the eigenvectors of a previous solve of this block
@@ -78,7 +79,9 @@ struct WarmArgs {
   int *order, *pos, *diff, *cid, *cpos, *cl_start, *cl_size, *cl_voff, *cl_rbase, *sel, *idx;
   double* Vcl;               // cluster rotations, <= WM_CAP * N doubles
   double *partA, *cross, *roff, *grow, *gcol;  // deterministic partial sums
-  double* rdiag;             // sum (1 - P_ii)^2
+  double *rdpart, *g2part;   // per row block: sum (1 - P_ii)^2, Gershgorin partial
+  int* cnt;                  // nt row-block counters, the grid counter and the strong-pair count of k_warm_scan
+  int* pairs;                // strong pairs (i, j) of the step, at most WM_PAIRS
   WarmState* ws;
   const double* lam_cold;    // ascending eigenvalues of the cold path (D&C)
   int* side;                 // le.side + b (k_pack: 1 = the block holds Pi(-a))
@@ -152,6 +155,11 @@ __global__ void __launch_bounds__(256) k_warm_begin(WarmArgs a) {
   }
   __syncthreads();
   const bool pred = a.ws->pred;
+  if (ti == 0) {  // the fused scan's link and completion counters start from zero
+    for (int q = tj * 256 + threadIdx.x; q <= N; q += a.nt * 256) a.diff[q] = 0;
+    if (tj == 0)
+      for (int q = threadIdx.x; q <= a.nt + 1; q += 256) a.cnt[q] = 0;
+  }
   for (int r = ty; r < 32; r += 8) {
     const int i = 32 * ti + tx, j = 32 * tj + r;
     const double v = t[r][tx];
@@ -194,176 +202,211 @@ __global__ void __launch_bounds__(256) k_warm_begin(WarmArgs a) {
   }
 }
 
-// ---- per step: lambda_i = S_ii / P_ii, sorted order (rank by counting), zeroed link counters ----
-// grid nt CTAs of 256 threads: CTA b ranks i in [32 b, 32 b + 32) against every lambda (8 warps x a
-// slice of j each); ties by index, so the order is exact and deterministic.
-__global__ void __launch_bounds__(256) k_warm_diag(WarmArgs a) {
-  if (wm_skip(a) || a.ws->gate != 1) return;
-  __shared__ double key[WM_SORT];
-  __shared__ int cnt[8][33];
-  __shared__ double red[8];
-  const int N = a.N, ld = a.ldn, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  double rd = 0.0;
-  for (int t = tid; t < N; t += 256) {
-    const double p = a.P[(size_t)t * ld + t];
-    key[t] = a.S[(size_t)t * ld + t] / p;
-    if (blockIdx.x == 0) rd = fma(1.0 - p, 1.0 - p, rd);
-  }
-  __syncthreads();
-  const int i = 32 * blockIdx.x + lane;
-  const double ki = i < N ? key[i] : 0.0;
-  const int per = (N + 7) / 8, j0 = w * per, j1 = min(N, j0 + per);
-  int c = 0;
-  if (i < N)
-    for (int j = j0; j < j1; ++j) {
-      const double kj = key[j];
-      c += (kj < ki || (kj == ki && j < i)) ? 1 : 0;
-    }
-  cnt[w][lane] = c;
-  if (blockIdx.x == 0) {
-    rd = warp_sum(rd);
-    if (lane == 0) red[w] = rd;
-  }
-  __syncthreads();
-  if (w == 0 && i < N) {
-    int r = 0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) r += cnt[q][lane];
-    a.lam[i] = ki;
-    a.order[r] = i;
-    a.pos[i] = r;
-  }
-  if (blockIdx.x == 0) {
-    for (int t = tid; t <= N; t += 256) a.diff[t] = 0;
-    if (tid == 0) {
-      double s2 = 0.0;
-      for (int q = 0; q < 8; ++q) s2 += red[q];
-      *a.rdiag = s2;
-    }
-  }
-}
+// ---- per step: ONE fused pass over the upper 32 x 32 tiles of S and P (grid (nt, nt), 256 threads; the
+// tiles below the diagonal exit at once) ----
+//  (1) lambda of every index (diag S / diag P, all N into shared memory) and the ranks of the tile's 32 rows
+//      and 32 columns by counting (ties by index: an exact, deterministic order); the diagonal tiles publish
+//      lam, pos, order and their rows' (1 - P_ii)^2;
+//  (2) the tile's coupling / orthonormality partials, same-sign row / column masses and strong pairs;
+//  (3) row-block completion: the CTA that brings a row block's nt + 1 contributions together sums its rows'
+//      rho_i in tile order and writes the block's Gershgorin partial;
+//  (4) the last CTA of the grid runs the stop test and builds the clusters (fixed-order sums throughout).
+__device__ void wm_decide(const WarmArgs& a, int step, double* red, int* cpre, double* lam_s, int* flags);
 
-// ---- per step: coupling / orthonormality / Gershgorin partials and the strong pairs ----
-// grid (nt, nt) (only tiles ti <= tj work), 256 threads: lane = column, 8 row groups of 4 rows
-__global__ void __launch_bounds__(256) k_warm_scan(WarmArgs a) {
+__global__ void __launch_bounds__(256) k_warm_scan(WarmArgs a, int step) {
   if (wm_skip(a) || a.ws->gate != 1) return;
-  const int ti = blockIdx.x, tj = blockIdx.y;
+  const int ti = blockIdx.x, tj = blockIdx.y, nt = a.nt;
   if (ti > tj) return;
+  __shared__ double lrow[32], lcol[32];
   __shared__ double colp[8][33];
-  __shared__ double red[2][8];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, N = a.N, ld = a.ldn;
+  __shared__ double red[32];
+  __shared__ int cpre[WM_SORT];
+  __shared__ double lam_s[WM_SORT];
+  __shared__ int flags[4];  // [0] ncl, [1] big, [2] maxcl, [3] last-CTA flag
+  __shared__ int done_blk[2];
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5, N = a.N, ld = a.ldn;
+  if (tid < 64) {  // lambda of the tile's rows (tid < 32) and columns
+    const int idx = tid < 32 ? 32 * ti + tid : 32 * tj + tid - 32;
+    double l = 0.0;
+    if (idx < N) l = a.S[(size_t)idx * ld + idx] / a.P[(size_t)idx * ld + idx];
+    if (tid < 32) lrow[tid] = l;
+    else lcol[tid - 32] = l;
+    if (ti == tj && tid < 32 && idx < N) a.lam[idx] = l;
+  }
+  __syncthreads();
+  // (2) the tile's pairs i < j
   const int j = 32 * tj + tx;
   const bool jv = j < N;
-  const double lj = jv ? a.lam[j] : 0.0;
+  const double lj = lcol[tx];
   const bool gj = lj > 0.0;
-  const int pj = jv ? a.pos[j] : 0;
   double cr = 0.0, ro = 0.0, cs = 0.0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const int i = 32 * ti + ty + 8 * q;
+    const int rr = ty + 8 * q, i = 32 * ti + rr;
     double rs = 0.0;
     if (jv && i < j) {
-      const double s = a.S[(size_t)j * ld + i], p = a.P[(size_t)j * ld + i];
-      const double li = a.lam[i];
+      const double sv = a.S[(size_t)j * ld + i], pv = a.P[(size_t)j * ld + i];
+      const double li = lrow[rr];
       const bool gi = li > 0.0;
       if (gi != gj) {
-        cr = fma(s, s, cr);
+        cr = fma(sv, sv, cr);
       } else {
-        rs = fabs(s);
-        cs += fabs(s);
+        rs = fabs(sv);
+        cs += fabs(sv);
       }
-      ro = fma(p, p, ro);
-      const double sp = fma(-0.5 * (li + lj), p, s);  // S'_ij = S_ij + lambda_bar R_ij, R_ij = -P_ij
-      if (fabs(sp) > WM_THETA * fabs(lj - li)) {
-        const int pi = a.pos[i];
-        atomicAdd(a.diff + min(pi, pj), 1);
-        atomicAdd(a.diff + max(pi, pj), -1);
+      ro = fma(pv, pv, ro);
+      const double sp = fma(-0.5 * (li + lj), pv, sv);  // S'_ij = S_ij + lambda_bar R_ij, R_ij = -P_ij
+      if (fabs(sp) > WM_THETA * fabs(lj - li)) {       // strong pair: listed for the cluster build
+        const int k = atomicAdd(a.cnt + nt + 1, 1);
+        if (k < WM_PAIRS) {
+          a.pairs[2 * k] = i;
+          a.pairs[2 * k + 1] = j;
+        }
       }
     }
-    rs = warp_sum(rs);  // row i's same-sign mass over this tile's columns (columns j > i)
+    rs = warp_sum(rs);  // row i's same-sign mass over this tile's columns (j > i)
     if (tx == 0 && i < N) a.grow[(size_t)tj * N + i] = rs;
   }
   colp[ty][tx] = cs;
   cr = warp_sum(cr);
   ro = warp_sum(ro);
   if (tx == 0) {
-    red[0][ty] = cr;
-    red[1][ty] = ro;
+    red[ty] = cr;
+    red[8 + ty] = ro;
   }
   __syncthreads();
   if (ty == 0) {
     double c = 0.0;
 #pragma unroll
     for (int w = 0; w < 8; ++w) c += colp[w][tx];
-    if (jv) a.gcol[(size_t)ti * N + j] = c;  // column j's mass over this tile's rows (rows i < j)
+    if (jv) a.gcol[(size_t)ti * N + j] = c;  // column j's mass over this tile's rows (i < j)
     if (tx == 0) {
       double c2 = 0.0, r2 = 0.0;
       for (int w = 0; w < 8; ++w) {
-        c2 += red[0][w];
-        r2 += red[1][w];
+        c2 += red[w];
+        r2 += red[8 + w];
       }
-      a.cross[ti * a.nt + tj] = c2;
-      a.roff[ti * a.nt + tj] = r2;
+      a.cross[ti * nt + tj] = c2;
+      a.roff[ti * nt + tj] = r2;
     }
   }
-}
-
-// ---- per step: stop test, failure test, clusters ----
-__global__ void __launch_bounds__(WM_NT) k_warm_decide(WarmArgs a, int step) {
-  if (wm_skip(a) || a.ws->gate != 1) return;
-  __shared__ double red[32];
-  __shared__ int sh_ncl, sh_big, sh_maxcl;
-  __shared__ int cpre[WM_SORT];
-  WarmState* ws = a.ws;
-  const int N = a.N, nt = a.nt, tid = threadIdx.x;
+  if (ti == tj && ty == 1) {  // the block's (1 - P_ii)^2
+    const int i = 32 * ti + tx;
+    double d = 0.0;
+    if (i < N) {
+      const double p = a.P[(size_t)i * ld + i];
+      d = (1.0 - p) * (1.0 - p);
+    }
+    d = warp_sum(d);
+    if (tx == 0) a.rdpart[ti] = d;
+  }
+  // (3) row-block completion
+  __threadfence();
+  __syncthreads();
   if (tid == 0) {
-    sh_ncl = 0;
-    sh_big = 0;
-    sh_maxcl = 0;
-  }
-  // fixed-order sums of the tile partials
-  double c2 = 0.0, r2 = 0.0, a2 = 0.0;
-  for (int e = tid; e < nt * nt; e += WM_NT) {
-    const int ti = e / nt, tj = e % nt;
-    if (ti <= tj) {
-      c2 += a.cross[e];
-      r2 += a.roff[e];
+    done_blk[0] = done_blk[1] = -1;
+    if (ti == tj) {
+      if (atomicAdd(a.cnt + ti, 2) + 2 == nt + 1) done_blk[0] = ti;
+    } else {
+      if (atomicAdd(a.cnt + ti, 1) + 1 == nt + 1) done_blk[0] = ti;
+      if (atomicAdd(a.cnt + tj, 1) + 1 == nt + 1) done_blk[1] = tj;
     }
-    if (step == 0) a2 += a.partA[e];
-  }
-  c2 = wm_block_sum(c2, red);
-  r2 = wm_block_sum(r2, red);
-  if (step == 0) {
-    a2 = wm_block_sum(a2, red);
-    if (tid == 0) ws->normA2 = a2;
   }
   __syncthreads();
-  const double nA = sqrt(ws->normA2);
-  const double eta = sqrt(2.0 * c2), rn = sqrt(2.0 * r2 + *a.rdiag);
-  // Gershgorin sign safety: row i's same-sign off-diagonal mass rho_i.  A row whose disc reaches across
-  // zero (|lambda_i| <= rho_i) can hide an eigenvalue of the wrong sign of size <= rho_i in its diagonal
-  // block, so the projection error it can cause is bounded by (sum of those rho_i^2)^(1/2): required at
-  // rounding level, <= WM_TOLG ||a||_F (near-zero eigenvalues keep rho_i at the floor of the S product).
-  double g2 = 0.0;
-  for (int i = tid; i < N; i += WM_NT) {
-    const int ti = i >> 5;
-    // fixed trip count, independent loads (the L2 latencies overlap); tile order t ascending
+  for (int h = 0; h < 2; ++h) {
+    const int t = done_blk[h];
+    if (t < 0) continue;
+    __threadfence();
+    // rows i = 32 t + r; 8 threads per row take the terms tt = g, g + 8, ... (grow: tt >= t, gcol: tt <= t)
+    const int r = tid & 31, g = tid >> 5, i = 32 * t + r;
     double rho = 0.0;
-#pragma unroll 8
-    for (int t = 0; t < nt; ++t) {
-      const double gr = t >= ti ? a.grow[(size_t)t * N + i] : 0.0;
-      const double gc = t <= ti ? a.gcol[(size_t)t * N + i] : 0.0;
-      rho += gr + gc;
+    if (i < N)
+      for (int tt = g; tt < nt; tt += 8) {
+        if (tt >= t) rho += __ldcg(a.grow + (size_t)tt * N + i);
+        if (tt <= t) rho += __ldcg(a.gcol + (size_t)tt * N + i);
+      }
+    colp[g][r] = rho;
+    __syncthreads();
+    if (g == 0) {
+      double rr = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) rr += colp[w][r];
+      double g2 = 0.0;
+      if (i < N) {
+        const double li = __ldcg(a.S + (size_t)i * ld + i) / __ldcg(a.P + (size_t)i * ld + i);
+        if (!(fabs(li) > rr)) g2 = rr * rr;
+      }
+      g2 = warp_sum(g2);
+      if (r == 0) a.g2part[t] = g2;
     }
-    if (!(fabs(a.lam[i]) > rho)) g2 = fma(rho, rho, g2);
+    __syncthreads();
   }
-  g2 = wm_block_sum(g2, red);
+  // (4) the last CTA runs the stop test
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) flags[3] = atomicAdd(a.cnt + nt, 1) + 1 == nt * (nt + 1) / 2;
+  __syncthreads();
+  if (!flags[3]) return;
+  __threadfence();
+  wm_decide(a, step, red, cpre, lam_s, flags);
+}
+
+// the stop test and the clusters (256 threads of the grid's last CTA)
+__device__ void wm_decide(const WarmArgs& a, int step, double* red, int* cpre, double* lam_s, int* flags) {
+  WarmState* ws = a.ws;
+  const int N = a.N, nt = a.nt, tid = threadIdx.x;
+  constexpr int T = 256;
+  auto bsum = [&](double v) {
+    v = warp_sum(v);
+    __syncthreads();
+    if ((tid & 31) == 0) red[tid >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int w = 0; w < T / 32; ++w) s += red[w];
+    __syncthreads();
+    return s;
+  };
+  if (tid == 0) {
+    flags[0] = 0;
+    flags[1] = 0;
+    flags[2] = 0;
+  }
+  double c2 = 0.0, r2 = 0.0, a2 = 0.0, rd = 0.0, g2 = 0.0;
+  for (int e = tid; e < nt * nt; e += T) {
+    const int ti = e / nt, tj = e % nt;
+    if (ti <= tj) {
+      c2 += __ldcg(a.cross + e);
+      r2 += __ldcg(a.roff + e);
+    }
+    if (step == 0) a2 += __ldcg(a.partA + e);
+  }
+  for (int t = tid; t < nt; t += T) {
+    rd += __ldcg(a.rdpart + t);
+    g2 += __ldcg(a.g2part + t);
+  }
+  const int npairs = __ldcg(a.cnt + nt + 1);
+  c2 = bsum(c2);
+  r2 = bsum(r2);
+  rd = bsum(rd);
+  g2 = bsum(g2);
+  if (step == 0) {
+    a2 = bsum(a2);
+    if (tid == 0) ws->normA2 = a2;
+  }
+  // counters back to zero for the next step (every other CTA is done with them)
+  for (int t = tid; t <= nt + 1; t += T) a.cnt[t] = 0;
+  __syncthreads();
+  const double nA = sqrt(ws->normA2);
+  const double eta = sqrt(2.0 * c2), rn = sqrt(2.0 * r2 + rd);
+  // Gershgorin sign safety: the rows whose same-sign off-diagonal mass rho_i reaches |lambda_i| can hide a
+  // wrong-sign eigenvalue of size <= rho_i in their diagonal block: (sum of those rho_i^2)^(1/2) must be at
+  // rounding level, <= WM_TOLG ||a||_F (near-zero eigenvalues keep rho_i at the floor of the S product).
   const bool cross_ok = eta <= WM_TOLE * nA;
   const bool conv = cross_ok && rn <= WM_TOLR * N && sqrt(g2) <= WM_TOLG * nA && isfinite(eta) && isfinite(rn);
   // a coupling that stops halving while still above the tolerance means the update is not converging
   const bool stall = !isfinite(eta) || !isfinite(rn) || step == WM_MAXS - 1 ||
                      (step > 0 && !cross_ok && eta > 0.5 * ws->eta_prev);
-  if (conv || stall) {
+  if (conv || stall || npairs > WM_PAIRS) {
     if (tid == 0) {
       ws->gate = 0;
       ws->eta = eta;
@@ -383,44 +426,80 @@ __global__ void __launch_bounds__(WM_NT) k_warm_decide(WarmArgs a, int step) {
         ws->need_full = 0;
         ws->n_fail++;
         ws->n_steps += step;
-        ws->why = (!isfinite(eta) || !isfinite(rn)) ? 4 : (step == WM_MAXS - 1 ? 1 : 2);
+        ws->why = (!isfinite(eta) || !isfinite(rn)) ? 4 : (stall ? (step == WM_MAXS - 1 ? 1 : 2) : 3);
         ws->pred_ok = 0;
         wm_set(a.hcold, 1);
       }
     }
     return;
   }
-  // clusters: prefix sums of the link counters over the sorted positions
-  for (int t = tid; t < WM_SORT; t += WM_NT) cpre[t] = t < N ? a.diff[t] : 0;
+  if (npairs == 0) {  // no strong pair: every index is its own cluster
+    for (int t = tid; t < N; t += T) a.cid[t] = -1;
+    if (tid == 0) {
+      ws->ncl = 0;
+      ws->maxcl = 0;
+      if (step == 0) ws->cl0 = 0;
+      ws->eta_prev = eta;
+      ws->eta = eta;
+      ws->rn = rn;
+      ws->step = step + 1;
+      if (step + 1 < WM_MAXS) wm_set(a.hstep[step + 1], 1);
+    }
+    return;
+  }
+  // sorted order of lambda (rank by counting; ties by index: exact and deterministic)
+  for (int t = tid; t < N; t += T) lam_s[t] = __ldcg(a.lam + t);
+  __syncthreads();
+  for (int i = tid; i < N; i += T) {
+    const double ki = lam_s[i];
+    int c0 = 0, c1 = 0;
+    int jj = 0;
+    for (; jj + 1 < N; jj += 2) {
+      const double k0 = lam_s[jj], k1 = lam_s[jj + 1];
+      c0 += (k0 < ki || (k0 == ki && jj < i)) ? 1 : 0;
+      c1 += (k1 < ki || (k1 == ki && jj + 1 < i)) ? 1 : 0;
+    }
+    if (jj < N) c0 += (lam_s[jj] < ki || (lam_s[jj] == ki && jj < i)) ? 1 : 0;
+    a.pos[i] = c0 + c1;
+    a.order[c0 + c1] = i;
+  }
+  // link counters of the strong pairs over the sorted positions, then their prefix sums
+  for (int t = tid; t < WM_SORT; t += T) cpre[t] = 0;
+  __syncthreads();
+  for (int k = tid; k < npairs; k += T) {
+    const int pi = __ldcg(a.pos + a.pairs[2 * k]), pj = __ldcg(a.pos + a.pairs[2 * k + 1]);
+    atomicAdd(&cpre[min(pi, pj)], 1);
+    atomicAdd(&cpre[max(pi, pj)], -1);
+  }
   for (int off = 1; off < WM_SORT; off <<= 1) {  // Hillis-Steele inclusive scan
     __syncthreads();
-    int v[WM_SORT / WM_NT];
+    int v[WM_SORT / T];
 #pragma unroll
-    for (int q = 0; q < WM_SORT / WM_NT; ++q) {
-      const int t = tid + q * WM_NT;
+    for (int q = 0; q < WM_SORT / T; ++q) {
+      const int t = tid + q * T;
       v[q] = t >= off ? cpre[t - off] : 0;
     }
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < WM_SORT / WM_NT; ++q) cpre[tid + q * WM_NT] += v[q];
+    for (int q = 0; q < WM_SORT / T; ++q) cpre[tid + q * T] += v[q];
   }
   __syncthreads();
   // cpre[t] > 0: sorted position t is linked to t + 1
-  for (int t = tid; t < N; t += WM_NT) {
+  for (int t = tid; t < N; t += T) {
     a.cid[a.order[t]] = -1;
     a.cpos[a.order[t]] = 0;
   }
   __syncthreads();
-  for (int t = tid; t < N - 1; t += WM_NT) {
+  for (int t = tid; t < N - 1; t += T) {
     if (cpre[t] > 0 && (t == 0 || cpre[t - 1] <= 0)) {  // start of a run of size >= 2
       int sz = 2;
       while (t + sz - 1 < N - 1 && cpre[t + sz - 1] > 0 && sz <= WM_CAP) ++sz;
       if (sz > WM_CAP) {
-        atomicOr(&sh_big, 1);
-        atomicMax(&sh_maxcl, sz);
+        atomicOr(&flags[1], 1);
+        atomicMax(&flags[2], sz);
       } else {
-        const int q = atomicAdd(&sh_ncl, 1);
-        atomicMax(&sh_maxcl, sz);
+        const int q = atomicAdd(&flags[0], 1);
+        atomicMax(&flags[2], sz);
         a.cl_start[q] = t;
         a.cl_size[q] = sz;
         for (int u = 0; u < sz; ++u) {
@@ -432,7 +511,7 @@ __global__ void __launch_bounds__(WM_NT) k_warm_decide(WarmArgs a, int step) {
   }
   __syncthreads();
   if (tid == 0) {
-    if (sh_big) {
+    if (flags[1]) {
       ws->why = 3;
       ws->pred_ok = 0;
       ws->gate = 0;
@@ -446,15 +525,15 @@ __global__ void __launch_bounds__(WM_NT) k_warm_decide(WarmArgs a, int step) {
       return;
     }
     int off = 0, rb = 0;
-    for (int q = 0; q < sh_ncl; ++q) {
+    for (int q = 0; q < flags[0]; ++q) {
       a.cl_voff[q] = off;
       a.cl_rbase[q] = rb;
       off += a.cl_size[q] * a.cl_size[q];
       rb += a.cl_size[q];
     }
-    ws->ncl = sh_ncl;
-    ws->maxcl = sh_maxcl;
-    if (step == 0) ws->cl0 = sh_ncl > 0;
+    ws->ncl = flags[0];
+    ws->maxcl = flags[2];
+    if (step == 0) ws->cl0 = flags[0] > 0;
     ws->eta_prev = eta;
     ws->eta = eta;
     ws->rn = rn;

@@ -42,7 +42,7 @@ def run(M, N, K, tA, up, var=-1, reps=50):
 
 
 if len(sys.argv) > 1 and sys.argv[1] == "--ncu":  # one launch per variant (ncu capture)
-    for var in range(20):
+    for var in ([int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else range(20)):
         run(861, 861, 861, 0, 0, var=var, reps=0)
         run(861, 861, 861, 1, 1, var=var, reps=0)
     sys.exit(0)
