@@ -192,6 +192,11 @@ sosadmm_err sosadmm_project_psd(sosadmm_ctx* ctx, int32_t block, const double* a
  * `work` in blocks (work may be NULL to query); out: *nblocks = number of large blocks. */
 sosadmm_err sosadmm_psd_work(sosadmm_ctx* ctx, double* work, int32_t* nblocks);
 
+/* Residual history (measurement; reading C9 residuals of u^k as the in-graph check computed them during
+ * iteration k + 1): up to *count entries of 5 doubles [k, pres, dres, gap, pobj], newest first, consecutive
+ * k; the ring holds the last 1,024 iterations.  In: *count = capacity in entries; out: entries written. */
+sosadmm_err sosadmm_residual_history(sosadmm_ctx* ctx, double* out, int32_t* count);
+
 /* Warm-started large-block projection counters (csrc/warm.cuh), 10 int64 per large block in
  * setup order: [iterations projected by the warm refinement, iterations projected by the cold path
  * (tridiagonalisation + D&C + back-transform), total refinement updates of the warm iterations and of the

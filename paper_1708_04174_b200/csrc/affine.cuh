@@ -78,6 +78,7 @@ struct AffineArgs {
   double* part;
   int gather_blocks;
   double* kpart;  // symmetric K^{-1} apply (tl >= KINV_SYM_MIN): nt x nt x KT per-tile partials
+  double* hist;   // residual history: slot k mod SOS_HIST = (k, pres, dres, gap, pobj) of u^k (k_tphase)
   double* asvec;  // PSD part of u_hat_xi - z (size npsd)
   // PSD blocks
   int nblk;
@@ -93,6 +94,7 @@ struct AffineArgs {
 };
 
 constexpr int GATHER_NT = 256;
+constexpr int SOS_HIST = 1024;  // residual history ring (sosadmm_residual_history)
 constexpr int POS_NT = 256;
 constexpr int POS_PER_CTA = 1024;
 
@@ -368,6 +370,14 @@ __global__ void __launch_bounds__(TP_NT) k_tphase(AffineArgs a, int mode) {
     st->res_dual = dres;
     st->res_gap = gap;
     st->pobj = pobj;
+    if (a.hist && mode == 0) {  // the residuals of u^k, k = st->iter, in the history ring
+      double* hq = a.hist + 5 * (size_t)(st->iter % SOS_HIST);
+      hq[0] = (double)st->iter;
+      hq[1] = pres;
+      hq[2] = dres;
+      hq[3] = gap;
+      hq[4] = pobj;
+    }
     st->dobj = dobj;
     st->pinf = pinf;
     st->dinf = dinf;

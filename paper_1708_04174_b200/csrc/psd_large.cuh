@@ -778,17 +778,48 @@ inline void large_block_warm_begin(LargeEig& le, LargeBlock& lb, cudaStream_t s,
   }
   k_warm_begin<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
 }
-// refinement step j: W = Af X_j, [S, P] = X_j^T [W, X_j], stop test, clusters, M = V (I + E), X_{j+1} = X_j M
-inline void large_block_warm_step(LargeEig& le, LargeBlock& lb, cudaStream_t s, int j, const WarmArgs& wa) {
+// refinement step j: W = Af X_j, [S, P] = X_j^T [W, X_j], stop test, clusters, M = V (I + E), X_{j+1} = X_j M.
+// nest (graph capture only: s captures the step's IF body, nest is a stream outside any capture): the
+// cluster kernels and k_warm_M go into nested IF nodes the stop test sets only when clusters exist, so a
+// step without clusters launches GEMM, scan, E, GEMM only.
+inline cudaError_t graph_new_handle(cudaStream_t s, unsigned long long* h);
+inline cudaError_t graph_if_body(cudaStream_t s, unsigned long long h, cudaGraph_t* body);
+inline cudaError_t large_block_warm_step(LargeEig& le, LargeBlock& lb, cudaStream_t s, int j, const WarmArgs& wa0,
+                                         cudaStream_t nest = nullptr) {
   const int N = lb.N;
+  WarmArgs wa = wa0;
+  cudaError_t e = cudaSuccess;
+  if (nest) {
+    e = graph_new_handle(s, &wa.hclA);
+    if (e == cudaSuccess) e = graph_new_handle(s, &wa.hclB);
+    if (e != cudaSuccess) return e;
+  }
   if (j == 0) dgemm_launch(DG_DEFAULT, lb.wdesc, 1, N, N, s, le.st, le.is, 1);  // W_0 = a X_0
   dgemm_launch(DG_DEFAULT, lb.wdesc + 5 * j + 1, 2, N, N, s, le.st, le.is, 1);   // S, P (upper tiles)
   k_warm_scan<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa, j);
-  k_warm_cluster<<<WM_CLB, WM_CLT, WM_CL_SMEM, s>>>(wa);
-  k_warm_rot<<<dim3(wa.nt, 32), 256, 0, s>>>(wa);
+  auto nested = [&](unsigned long long h, auto&& body_fn) -> cudaError_t {
+    if (!nest) {
+      body_fn(s);
+      return cudaSuccess;
+    }
+    cudaGraph_t body = nullptr;
+    cudaError_t ee = graph_if_body(s, h, &body);
+    if (ee == cudaSuccess) ee = cudaStreamBeginCaptureToGraph(nest, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (ee != cudaSuccess) return ee;
+    body_fn(nest);
+    cudaGraph_t out = nullptr;
+    return cudaStreamEndCapture(nest, &out);
+  };
+  e = nested(wa.hclA, [&](cudaStream_t q) {
+    k_warm_cluster<<<WM_CLB, WM_CLT, WM_CL_SMEM, q>>>(wa);
+    k_warm_rot<<<dim3(wa.nt, 32), 256, 0, q>>>(wa);
+  });
+  if (e != cudaSuccess) return e;
   k_warm_E<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
-  k_warm_M<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
+  e = nested(wa.hclB, [&](cudaStream_t q) { k_warm_M<<<dim3(wa.nt, wa.nt), 256, 0, q>>>(wa); });
+  if (e != cudaSuccess) return e;
   dgemm_launch(DG_DEFAULT, lb.wdesc + 5 * j + 3, 2, N, N, s, le.st, le.is, 1);   // X M, W M
+  return cudaSuccess;
 }
 // cold path of the warm mode: tridiagonalisation, WY factors, divide and conquer (every eigenvector when
 // it re-seeds X, else the projected side only: k_dc_topsel reads ws->need_full); with side streams
@@ -937,7 +968,8 @@ inline cudaError_t graph_if_body(cudaStream_t s, unsigned long long h, cudaGraph
 //   begin or a failed test; ends with k_warm_cold_switch) -> full tail (bt of every column + finish) or
 //   partial tail (k_select + bt of the projected side + reconstruction) -> warm finish (set on success).
 inline cudaError_t large_block_warm_graph(LargeEig& le, LargeBlock& lb, cudaStream_t sb, cudaStream_t sbody,
-                                          cudaStream_t sw, cudaStream_t sd, const cudaEvent_t* evs) {
+                                          cudaStream_t sw, cudaStream_t sd, const cudaEvent_t* evs,
+                                          cudaStream_t snest = nullptr) {
   WarmArgs wg = lb.wa;
   cudaError_t e = cudaSuccess;
   for (int j = 0; j < WM_MAXS && e == cudaSuccess; ++j) e = graph_new_handle(sb, &wg.hstep[j]);
@@ -953,7 +985,12 @@ inline cudaError_t large_block_warm_graph(LargeEig& le, LargeBlock& lb, cudaStre
     if (e == cudaSuccess) e = cudaStreamBeginCaptureToGraph(sbody, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) return e;
     if (j < WM_MAXS) {
-      large_block_warm_step(le, lb, sbody, j, wg);
+      e = large_block_warm_step(le, lb, sbody, j, wg, snest);
+      if (e != cudaSuccess) {
+        cudaGraph_t out = nullptr;
+        cudaStreamEndCapture(sbody, &out);
+        return e;
+      }
     } else if (j == WM_MAXS) {
       large_block_cold(le, lb, sbody, sw, sd, evs);
       k_warm_cold_switch<<<1, 1, 0, sbody>>>(wg);
@@ -978,7 +1015,7 @@ inline cudaError_t large_block_warm_graph(LargeEig& le, LargeBlock& lb, cudaStre
 // body: one stream per block outside the capture (warm blocks' conditional bodies).
 inline cudaError_t large_eig_launch_concurrent(LargeEig& le, cudaStream_t s, bool check, cudaEvent_t fork,
                                                const cudaStream_t* aux, const cudaEvent_t* evs,
-                                               const cudaStream_t* body) {
+                                               const cudaStream_t* body, const cudaStream_t* nest = nullptr) {
   const int nb = (int)le.blocks.size();
   for (int b = 0; b < nb; ++b) {
     LargeBlock& lb = le.blocks[b];
@@ -987,7 +1024,7 @@ inline cudaError_t large_eig_launch_concurrent(LargeEig& le, cudaStream_t s, boo
     cudaStream_t sd = aux[3 * b + 2];
     if (b > 0) cudaStreamWaitEvent(sb, fork, 0);
     if (lb.warm) {
-      const cudaError_t e = large_block_warm_graph(le, lb, sb, body[b], sw, sd, evs + 8 * b);
+      const cudaError_t e = large_block_warm_graph(le, lb, sb, body[b], sw, sd, evs + 8 * b, nest ? nest[b] : nullptr);
       if (e != cudaSuccess) return e;
       if (b > 0) cudaEventRecord(evs[8 * b + 2], sb);
       continue;

@@ -354,6 +354,7 @@ struct DevPtrs {
   double* jvp;         // warm-start eigenvectors of the small blocks
   long long* blk_vp;
   double *shbuf, *shpart;
+  double* hist;        // residual history ring (affine.cuh SOS_HIST entries of 5 doubles)
   unsigned long long *pflags, *pepoch;  // peer mode: [PEER_MAXW] arrival epochs, the round counter
   double** ppeer_buf;                    // [PEER_MAXW] device pointers (peer mode)
   unsigned long long** ppeer_flags;      // [PEER_MAXW]
@@ -395,11 +396,13 @@ struct sosadmm_ctx {
   static constexpr int kMaxAux = 1 + 3 * 8;
   cudaStream_t aux[kMaxAux] = {};
   cudaStream_t body[8] = {};  // capture streams of the warm blocks' conditional bodies (outside the main capture)
+  cudaStream_t nest[8] = {};  // and of the bodies nested inside them
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_blk[8 * 8] = {};
   // early-stop polling of sosadmm_iterate: pinned copies of the device state after each chunk of replays
   DevState* h_poll = nullptr;
   cudaEvent_t ev_poll[2] = {};
   bool aux_ok = false;
+  bool nest_ok = true;  // nested conditional nodes in the warm step bodies (cleared if the capture rejects them)
 };
 
 namespace {
@@ -466,6 +469,7 @@ void carve(const Analysis& an, Arena& ar, DevPtrs& d, int gather_blocks) {
     d.kpart = ar.take<double>(nt * nt * KT);
   }
   d.part = ar.take<double>((size_t)NPART * gather_blocks);
+  d.hist = ar.take<double>((size_t)5 * SOS_HIST);
   d.asvec = ar.take<double>(an.npsd);
   d.mats = ar.take<double>((size_t)an.mat_total);
   d.tmp = ar.take<double>(std::max<size_t>(n, 1));
@@ -582,7 +586,8 @@ sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev, int
                                          c->aux[0]>>>(c->ja);
       cudaEventRecord(c->ev_join, c->aux[0]);
     }
-    const cudaError_t ge = large_eig_launch_concurrent(c->le, s, true, c->ev_fork, c->aux + 1, c->ev_blk, c->body);
+    const cudaError_t ge = large_eig_launch_concurrent(c->le, s, true, c->ev_fork, c->aux + 1, c->ev_blk, c->body,
+                                                       c->nest_ok ? c->nest : nullptr);
     if (ge != cudaSuccess) {
       c->err = SOSADMM_E_CUDA;
       c->msg = std::string("large-block projection capture: ") + cudaGetErrorString(ge);
@@ -878,6 +883,10 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
 
   // ---- upload -----------------------------------------------------------------------------
   cudaStream_t s = c->stream;
+  {
+    const std::vector<double> h0((size_t)5 * SOS_HIST, -1.0);  // empty history slots
+    CK_CTX(c, h2d(d.hist, h0, s));
+  }
   CK_CTX(c, h2d(d.seg_ptr, an.seg_ptr, s));
   CK_CTX(c, h2d(d.seg_col, an.seg_col, s));
   CK_CTX(c, h2d(d.segpos, an.segpos, s));
@@ -958,6 +967,7 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
   a.xi = d.xi; a.z = d.z; a.y = d.y; a.s = d.s; a.st = d.st; a.is = d.is;
   a.x = d.x; a.uhat2 = d.uhat2; a.yt = d.yt; a.zt = d.zt; a.ulow = d.ulow; a.aty = d.aty; a.kpart = d.kpart;
   a.part = d.part; a.gather_blocks = c->gather_blocks; a.asvec = d.asvec;
+  a.hist = d.hist;
   a.nblk = an.nblk; a.blk_col = d.blk_col; a.blk_N = d.blk_N; a.blk_mat = d.blk_mat; a.mats = d.mats;
   a.cta_blk = d.cta_blk; a.cta_q0 = d.cta_q0; a.pos_ctas = (int)an.cta_blk.size();
   c->d_tmp = d.tmp;
@@ -998,8 +1008,10 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
   if (!an.large_blk.empty() && an.large_blk.size() <= 8) {
     const int naux = 1 + 3 * (int)an.large_blk.size();
     for (int q = 0; q < naux; ++q) CK_CTX(c, cudaStreamCreateWithFlags(&c->aux[q], cudaStreamNonBlocking));
-    for (size_t q = 0; q < an.large_blk.size(); ++q)
+    for (size_t q = 0; q < an.large_blk.size(); ++q) {
       CK_CTX(c, cudaStreamCreateWithFlags(&c->body[q], cudaStreamNonBlocking));
+      CK_CTX(c, cudaStreamCreateWithFlags(&c->nest[q], cudaStreamNonBlocking));
+    }
     CK_CTX(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK_CTX(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     for (int q = 0; q < 8 * (int)an.large_blk.size(); ++q)
@@ -1053,7 +1065,7 @@ sosadmm_err sosadmm_setup_sharded(const sosadmm_problem* prob, const sosadmm_set
 
 static sosadmm_err build_graph(sosadmm_ctx* c) {
   if (c->graph) return SOSADMM_OK;
-  for (int attempt = 0; attempt < 2; ++attempt) {
+  for (int attempt = 0; attempt < 3; ++attempt) {
     CK_CTX(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     const sosadmm_err le = launch_iteration(c, 1, nullptr);
     cudaGraph_t g = nullptr;
@@ -1070,7 +1082,16 @@ static sosadmm_err build_graph(sosadmm_ctx* c) {
     if (g) cudaGraphDestroy(g);  // a failed capture (e.g. ncclAllReduce) is never instantiated
     bool warm = false;
     for (auto& lb : c->le.blocks) warm |= lb.warm;
-    if (attempt == 0 && warm && !(le != SOSADMM_OK && c->err == SOSADMM_E_NCCL)) {
+    if (attempt == 0 && warm && c->nest_ok && !(le != SOSADMM_OK && c->err == SOSADMM_E_NCCL)) {
+      // nested conditional nodes rejected here: capture again with the cluster kernels unconditional
+      c->nest_ok = false;
+      c->msg = std::string("nested conditional nodes disabled (graph capture: ") +
+               cudaGetErrorString(ee != cudaSuccess ? ee : ie) + ")";
+      c->err = SOSADMM_OK;
+      (void)cudaGetLastError();
+      continue;
+    }
+    if (attempt <= 1 && warm && !(le != SOSADMM_OK && c->err == SOSADMM_E_NCCL)) {
       // the warm mode's conditional nodes could not be captured / instantiated here: cold path every
       // iteration (still correct: the D&C root then forms every eigenvector), recorded in the message
       for (auto& lb : c->le.blocks) lb.warm = false;
@@ -1358,6 +1379,29 @@ sosadmm_err sosadmm_psd_work(sosadmm_ctx* c, double* work, int32_t* nblocks) {
   return SOSADMM_OK;
 }
 
+sosadmm_err sosadmm_residual_history(sosadmm_ctx* c, double* out, int32_t* count) {
+  if (!c || !out || !count) return SOSADMM_E_ARG;
+  if (c->err) return c->err;
+  CK_CTX(c, cudaSetDevice(c->device));
+  const int n = std::min<int>(*count, SOS_HIST);
+  std::vector<double> h((size_t)5 * SOS_HIST);
+  CK_CTX(c, cudaMemcpyAsync(h.data(), c->dp.hist, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+  CK_CTX(c, cudaStreamSynchronize(c->stream));
+  // newest first: u^{k-1} was checked during iteration k (k = the device's iteration count), walking back
+  DevState hs{};
+  CK_CTX(c, cudaMemcpy(&hs, c->aa.st, sizeof(hs), cudaMemcpyDeviceToHost));
+  const long long best = hs.iter - 1;
+  const int slot = best >= 0 ? (int)(best % SOS_HIST) : 0;
+  int k = 0;
+  for (; k < n && best >= 0; ++k) {
+    const int q = ((slot - k) % SOS_HIST + SOS_HIST) % SOS_HIST;
+    if (h[5 * q] < 0 || (long long)h[5 * q] != best - k) break;
+    for (int f = 0; f < 5; ++f) out[5 * k + f] = h[5 * q + f];
+  }
+  *count = k;
+  return SOSADMM_OK;
+}
+
 sosadmm_err sosadmm_warm_stats(sosadmm_ctx* c, int64_t* stats, int32_t* nblocks) {
   if (!c || !nblocks) return SOSADMM_E_ARG;
   if (c->err) return c->err;
@@ -1398,6 +1442,8 @@ void sosadmm_destroy(sosadmm_ctx* c) {
   for (auto& a : c->aux)
     if (a) cudaStreamDestroy(a);
   for (auto& a : c->body)
+    if (a) cudaStreamDestroy(a);
+  for (auto& a : c->nest)
     if (a) cudaStreamDestroy(a);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);

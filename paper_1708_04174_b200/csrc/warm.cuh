@@ -89,6 +89,7 @@ struct WarmArgs {
   const IterScal* is;
   unsigned long long hstep[WM_MAXS];  // graph conditional handles (0 = not in a graph): refinement steps,
   unsigned long long hcold, hfull, hpart, hfin;  // cold eigensolver, its full / partial tail, warm finish
+  unsigned long long hclA, hclB;      // (per step body) the cluster kernels / k_warm_M run only with clusters
 };
 
 __device__ __forceinline__ bool wm_skip(const WarmArgs& a) { return a.st->done || !a.is->proceed; }
@@ -533,6 +534,10 @@ __device__ void wm_decide(const WarmArgs& a, int step, double* red, int* cpre, d
     }
     ws->ncl = flags[0];
     ws->maxcl = flags[2];
+    if (flags[0] > 0) {
+      wm_set(a.hclA, 1);
+      wm_set(a.hclB, 1);
+    }
     if (step == 0) ws->cl0 = flags[0] > 0;
     ws->eta_prev = eta;
     ws->eta = eta;

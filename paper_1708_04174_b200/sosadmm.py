@@ -21,7 +21,7 @@ STATUS = {0: "RUNNING", 1: "OPTIMAL", 2: "PRIMAL_INFEASIBLE", 3: "DUAL_INFEASIBL
 EXPORTS = ["sosadmm_workspace_size", "sosadmm_setup", "sosadmm_setup_sharded", "sosadmm_nccl_unique_id",
            "sosadmm_iterate", "sosadmm_iterate_async", "sosadmm_iterate_profiled",
            "sosadmm_get_info", "sosadmm_get_iterate", "sosadmm_set_iterate", "sosadmm_get_structure",
-           "sosadmm_project_affine", "sosadmm_project_psd", "sosadmm_launches_per_iter", "sosadmm_psd_work", "sosadmm_warm_stats",
+           "sosadmm_project_affine", "sosadmm_project_psd", "sosadmm_launches_per_iter", "sosadmm_psd_work", "sosadmm_warm_stats", "sosadmm_residual_history",
            "sosadmm_destroy",
            "sosadmm_strerror", "sosadmm_last_error_message"]
 
@@ -84,6 +84,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.sosadmm_psd_work.restype = ctypes.c_int
     lib.sosadmm_warm_stats.argtypes = [V, ctypes.POINTER(I64), ctypes.POINTER(I32)]
     lib.sosadmm_warm_stats.restype = ctypes.c_int
+    lib.sosadmm_residual_history.argtypes = [V, P, ctypes.POINTER(I32)]
+    lib.sosadmm_residual_history.restype = ctypes.c_int
     lib.sosadmm_launches_per_iter.argtypes = [V]
     lib.sosadmm_launches_per_iter.restype = I64
     lib.sosadmm_destroy.argtypes = [V]
@@ -220,6 +222,13 @@ class SosAdmm:
         self._check(self.lib.sosadmm_psd_work(self._ctx, _dptr(w), ctypes.byref(n)), "psd_work")
         keys = ["tridiag", "dc_gemm", "backtransform", "recon", "r", "dc_zero_merges"]
         return [dict(zip(keys, w[6 * b:6 * b + 6].tolist())) for b in range(n.value)]
+
+    def residual_history(self, cap: int = 1024) -> np.ndarray:
+        """Rows (k, pres, dres, gap, pobj) of the last iterates u^k, oldest first (sosadmm_residual_history)."""
+        out = np.zeros(5 * cap)
+        n = ctypes.c_int32(cap)
+        self._check(self.lib.sosadmm_residual_history(self._ctx, _dptr(out), ctypes.byref(n)), "residual_history")
+        return out[:5 * n.value].reshape(n.value, 5)[::-1].copy()
 
     def warm_stats(self) -> list:
         """Per large block: the warm-start counters (sosadmm_warm_stats, csrc/warm.cuh)."""
