@@ -2,8 +2,6 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
-#include <cstdlib>
-#include <utility>
 
 #define SOS_WARP 32
 
@@ -74,36 +72,6 @@ __device__ __forceinline__ void cp_async8z(void* smem, const void* gmem, bool va
 }
 
 __device__ __forceinline__ bool sos_finite(double x) { return isfinite(x); }
-
-// Programmatic dependent launch: a kernel launched with cudaLaunchAttributeProgrammaticStreamSerialization
-// may be scheduled before its predecessor finishes; it waits here (griddepcontrol.wait) before touching
-// the predecessor's results.  A no-op for an ordinary launch.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-
-// launch with the programmatic-serialization attribute (sos_pdl_on(): SOSADMM_PDL != 0)
-inline bool sos_pdl_on() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("SOSADMM_PDL");
-    on = (e && e[0] == '0') ? 0 : 1;
-  }
-  return on == 1;
-}
-template <typename... KArgs, typename... Args>
-inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                              Args&&... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = sos_pdl_on() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
-}
 
 constexpr double SOS_RT2 = 1.4142135623730951;       // fl(sqrt 2)
 constexpr double SOS_IRT2 = 0.70710678118654757;     // fl(1/sqrt 2)

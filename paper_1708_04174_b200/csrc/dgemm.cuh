@@ -58,7 +58,6 @@ struct DgCfg {
 template <int BM, int BN, int BK, int WM, int WN, int ST, int KG>
 __global__ void __launch_bounds__(32 * WM * WN * KG) k_dgemm(const DgemmDesc* __restrict__ descs, const DevState* st,
                                                              const IterScal* is, int check_state) {
-  pdl_wait();
   using Cf = DgCfg<BM, BN, BK, WM, WN, ST, KG>;
   constexpr int NT = Cf::NT, TM = Cf::TM, TN = Cf::TN, LDA0 = Cf::LDA0, LDK = Cf::LDK;
   if (check_state && (st->done || !is->proceed)) return;
@@ -235,7 +234,7 @@ inline void dgemm_launch(int variant, const DgemmDesc* d_descs, int batch, int m
   if (variant == V) {                                                                                        \
     using Cf = DgCfg<BM, BN, BK, WM, WN, ST, KG>;                                                            \
     dim3 gr((maxM + BM - 1) / BM, (maxN + BN - 1) / BN, batch);                                              \
-    launch_pdl(k_dgemm<BM, BN, BK, WM, WN, ST, KG>, gr, dim3(Cf::NT), Cf::SMEM, s, d_descs, st, is, check);   \
+    k_dgemm<BM, BN, BK, WM, WN, ST, KG><<<gr, Cf::NT, Cf::SMEM, s>>>(d_descs, st, is, check);                    \
     return;                                                                                                  \
   }
   DG_VARIANTS(DG_CASE)

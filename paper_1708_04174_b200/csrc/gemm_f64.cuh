@@ -42,7 +42,6 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
 // out-of-range elements are zero-filled by the copy itself.
 __global__ void __launch_bounds__(GM_NT) k_gemm_f64(const GemmDesc* __restrict__ descs, const DevState* st,
                                                     const IterScal* is, int check_state) {
-  pdl_wait();
   if (check_state && (st->done || !is->proceed)) return;
   const GemmDesc g = descs[blockIdx.z];
   if (g.skip) return;

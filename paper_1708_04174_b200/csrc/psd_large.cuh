@@ -773,10 +773,10 @@ __global__ void k_zero2(double* a, double* b, long long n) {
 }
 inline void large_block_warm_begin(LargeEig& le, LargeBlock& lb, cudaStream_t s, const WarmArgs& wa) {
   if (wa.predict) {
-    launch_pdl(k_warm_pred, dim3(wa.nt, wa.nt), dim3(256), 0, s, wa);
+    k_warm_pred<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
     dgemm_launch(DG_DEFAULT, lb.wdesc + 5 * WM_MAXS + 1, 1, lb.N, lb.N, s, le.st, le.is, 1);
   }
-  launch_pdl(k_warm_begin, dim3(wa.nt, wa.nt), dim3(256), 0, s, wa);
+  k_warm_begin<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
 }
 // refinement step j: W = Af X_j, [S, P] = X_j^T [W, X_j], stop test, clusters, M = V (I + E), X_{j+1} = X_j M.
 // nest (graph capture only: s captures the step's IF body, nest is a stream outside any capture): the
@@ -796,7 +796,7 @@ inline cudaError_t large_block_warm_step(LargeEig& le, LargeBlock& lb, cudaStrea
   }
   if (j == 0) dgemm_launch(DG_DEFAULT, lb.wdesc, 1, N, N, s, le.st, le.is, 1);  // W_0 = a X_0
   dgemm_launch(DG_DEFAULT, lb.wdesc + 5 * j + 1, 2, N, N, s, le.st, le.is, 1);   // S, P (upper tiles)
-  launch_pdl(k_warm_scan, dim3(wa.nt, wa.nt), dim3(256), 0, s, wa, j);
+  k_warm_scan<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa, j);
   auto nested = [&](unsigned long long h, auto&& body_fn) -> cudaError_t {
     if (!nest) {
       body_fn(s);
@@ -811,12 +811,12 @@ inline cudaError_t large_block_warm_step(LargeEig& le, LargeBlock& lb, cudaStrea
     return cudaStreamEndCapture(nest, &out);
   };
   e = nested(wa.hclA, [&](cudaStream_t q) {
-    launch_pdl(k_warm_cluster, dim3(WM_CLB), dim3(WM_CLT), WM_CL_SMEM, q, wa);
-    launch_pdl(k_warm_rot, dim3(wa.nt, 32), dim3(256), 0, q, wa);
+    k_warm_cluster<<<WM_CLB, WM_CLT, WM_CL_SMEM, q>>>(wa);
+    k_warm_rot<<<dim3(wa.nt, 32), 256, 0, q>>>(wa);
   });
   if (e != cudaSuccess) return e;
-  launch_pdl(k_warm_E, dim3(wa.nt, wa.nt), dim3(256), 0, s, wa);
-  e = nested(wa.hclB, [&](cudaStream_t q) { launch_pdl(k_warm_M, dim3(wa.nt, wa.nt), dim3(256), 0, q, wa); });
+  k_warm_E<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
+  e = nested(wa.hclB, [&](cudaStream_t q) { k_warm_M<<<dim3(wa.nt, wa.nt), 256, 0, q>>>(wa); });
   if (e != cudaSuccess) return e;
   dgemm_launch(DG_DEFAULT, lb.wdesc + 5 * j + 3, 2, N, N, s, le.st, le.is, 1);   // X M, W M
   return cudaSuccess;
@@ -867,12 +867,11 @@ inline void large_block_bt_all(LargeEig& le, LargeBlock& lb, cudaStream_t s) {
 // finish (warm success or full cold tail): side and index list, Xs / Ss gather, Y = Xs Ss, M = Y Xs^T
 inline void large_block_warm_finish(LargeEig& le, LargeBlock& lb, cudaStream_t s) {
   const int N = lb.N;
-  launch_pdl(k_warm_select, dim3(1), dim3(WM_NT), 0, s, lb.wa, lb.b);
-  launch_pdl(k_warm_gather, dim3(296), dim3(256), 0, s, lb.wa);
+  k_warm_select<<<1, WM_NT, 0, s>>>(lb.wa, lb.b);
+  k_warm_gather<<<296, 256, 0, s>>>(lb.wa);
   dgemm_launch(DG_DEFAULT, lb.wdesc + 5 * WM_MAXS, 1, N, N, s, le.st, le.is, 1);
   dim3 gr((N + GM_BM - 1) / GM_BM, (N + GM_BN - 1) / GM_BN, 1);
-  launch_pdl(k_gemm_f64, gr, dim3(GM_NT), 0, s, (const GemmDesc*)(lb.gdesc + lb.wrecon), (const DevState*)le.st,
-             (const IterScal*)le.is, 1);
+  k_gemm_f64<<<gr, GM_NT, 0, s>>>(lb.gdesc + lb.wrecon, le.st, le.is, 1);
 }
 // un-graphed warm projection of one block: the refinement steps, then (host decisions after a sync) the
 // cold path and its tail, or the finish.  ev (optional, 3 events): after the refinement / cold

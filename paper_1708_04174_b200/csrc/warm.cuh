@@ -119,7 +119,6 @@ __device__ __forceinline__ double wm_block_sum(double v, double* red) {
 // refinement steps add their corrections to it); without a valid generator it restarts from zero.
 // grid (nt, nt), 256 threads
 __global__ void __launch_bounds__(256) k_warm_pred(WarmArgs a) {
-  pdl_wait();
   if (wm_skip(a)) return;
   const WarmState* ws = a.ws;
   const bool cond = a.predict && ws->valid && ws->backoff == 0 && ws->pred_ok;
@@ -138,7 +137,6 @@ __global__ void __launch_bounds__(256) k_warm_pred(WarmArgs a) {
 // ---- begin: full symmetric copy Af of a (32 x 32 tile transposes), ||a||_F^2 partials, state ----
 // grid (nt, nt), 256 threads
 __global__ void __launch_bounds__(256) k_warm_begin(WarmArgs a) {
-  pdl_wait();
   if (wm_skip(a)) return;
   __shared__ double t[32][33];
   __shared__ double red[8];
@@ -217,7 +215,6 @@ __global__ void __launch_bounds__(256) k_warm_begin(WarmArgs a) {
 __device__ void wm_decide(const WarmArgs& a, int step, double* red, int* cpre, double* lam_s, int* flags);
 
 __global__ void __launch_bounds__(256) k_warm_scan(WarmArgs a, int step) {
-  pdl_wait();
   if (wm_skip(a) || a.ws->gate != 1) return;
   const int ti = blockIdx.x, tj = blockIdx.y, nt = a.nt;
   if (ti > tj) return;
@@ -558,7 +555,6 @@ __device__ void wm_decide(const WarmArgs& a, int step, double* red, int* cpre, d
 constexpr int WM_CLT = 1024;  // threads of the cluster kernel
 constexpr size_t WM_CL_SMEM = 5 * sizeof(double) * WM_CAP * (WM_CAP + 1);
 __global__ void __launch_bounds__(WM_CLT) k_warm_cluster(WarmArgs a) {
-  pdl_wait();
   if (wm_skip(a) || a.ws->gate != 1) return;
   extern __shared__ double wm_dyn[];
   typedef double Row[WM_CAP + 1];
@@ -688,7 +684,6 @@ __global__ void __launch_bounds__(WM_CLT) k_warm_cluster(WarmArgs a) {
 // grid (nt, ncl capped), 256 threads = 32 columns x 8 row groups; S and P are stored full (mirrored), so
 // row m of S is column m: coalesced along j.
 __global__ void __launch_bounds__(256) k_warm_rot(WarmArgs a) {
-  pdl_wait();
   if (wm_skip(a) || a.ws->gate != 1) return;
   __shared__ double Vs[WM_CAP * WM_CAP];
   __shared__ int mem[WM_CAP];
@@ -759,7 +754,6 @@ __device__ __forceinline__ WmCo wm_coef(const WarmArgs& a, int i) {
 // The 32 x 32 tile of S and P a CTA needs is staged through shared memory; pairs involving a cluster
 // member take the general path (global reads along the cluster's member columns).
 __global__ void __launch_bounds__(256) k_warm_E(WarmArgs a) {
-  pdl_wait();
   if (wm_skip(a) || a.ws->gate != 1) return;
   __shared__ double St[32][33], Pt[32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, N = a.N, ld = a.ldn;
@@ -835,7 +829,6 @@ __global__ void __launch_bounds__(256) k_warm_E(WarmArgs a) {
 
 // ---- per step: M = V (I + E); grid (nt, nt), 256 threads ----
 __global__ void __launch_bounds__(256) k_warm_M(WarmArgs a) {
-  pdl_wait();
   if (wm_skip(a) || a.ws->gate != 1 || a.ws->ncl == 0) return;  // (ncl == 0: k_warm_E wrote M)
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, N = a.N, ld = a.ldn;
   const int ai = 32 * blockIdx.x + tx;
@@ -872,7 +865,6 @@ __global__ void k_warm_cold_switch(WarmArgs a) {
 
 // ---- finish: side selection (warm S or cold eigenpairs), compact index list ----
 __global__ void __launch_bounds__(WM_NT) k_warm_select(WarmArgs a, int block_id) {
-  pdl_wait();
   if (wm_skip(a)) return;
   __shared__ int cnt[WM_NT / 32 + 1];
   __shared__ int np_s, nn_s;
@@ -939,7 +931,6 @@ __global__ void __launch_bounds__(WM_NT) k_warm_select(WarmArgs a, int block_id)
 // ---- finish: Xs = X[:, idx] (into Mm), Ss = +-S[idx, idx] or +-diag(lambda) (into E), X1 -> X0 ----
 // grid >= 148, 256 threads
 __global__ void __launch_bounds__(256) k_warm_gather(WarmArgs a) {
-  pdl_wait();
   if (wm_skip(a)) return;
   const WarmState* ws = a.ws;
   const int N = a.N, ld = a.ldn, r = a.sel[0], side = a.sel[2], src = ws->src;
