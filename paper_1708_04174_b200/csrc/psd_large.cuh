@@ -259,17 +259,19 @@ inline size_t large_carve(const std::vector<int>& blk_N, const std::vector<int>&
     {  // warm-start buffers (warm.cuh), pitch ldn = N rounded up to even
       const size_t NL = (size_t)N * ((N + 1) & ~1);
       const int nt = (N + 31) / 32;
-      for (int t = 0; t < 13; ++t) p[q++] = take(8 * NL);  // Af X0 X1 W W1 S P E Mm Y Srot Rrot Esum
+      for (int t = 0; t < 14; ++t) p[q++] = take(8 * NL);  // Af X0 X1 W W1 S P E Mm Y Srot Rrot Esum Eprev
       p[q++] = take(8 * N);                                // lam
       p[q++] = take(8 * N);                                // lamt
       for (int t = 0; t < 9; ++t) p[q++] = take(4 * (size_t)(N + 1));  // order pos diff cid cpos cl_start cl_size cl_voff cl_rbase
       p[q++] = take(4 * 4);                                // sel
       p[q++] = take(4 * (size_t)N);                        // idx
       p[q++] = take(8 * (size_t)WM_CAP * N);               // Vcl
-      for (int t = 0; t < 3; ++t) p[q++] = take(8 * (size_t)nt * nt);  // partA cross roff
+      p[q++] = take(8 * (size_t)nt * nt);                  // partA
+      p[q++] = take(8 * (size_t)nt * nt);                  // cross
+      p[q++] = take(8 * 3 * (size_t)nt * nt);              // roff (three sign classes)
       p[q++] = take(8 * (size_t)nt * N);                   // grow
       p[q++] = take(8 * (size_t)nt * N);                   // gcol
-      p[q++] = take(8 * (size_t)nt);                       // rdpart
+      p[q++] = take(8 * 5 * (size_t)nt);                   // rdpart (defect, two weighted defects, two sign counts)
       p[q++] = take(8 * (size_t)nt);                       // g2part
       p[q++] = take(4 * (size_t)(nt + 2));                 // cnt
       p[q++] = take(8 * (size_t)WM_PAIRS);                 // pairs
@@ -499,12 +501,20 @@ inline int large_eig_init(LargeEig& le, const std::vector<int>& blk_N, const std
       wa.ldn = ldn;
       wa.nt = nt;
       wa.Mblk = lb.M;
-      double** big[13] = {&wa.Af, &wa.X0, &wa.X1, &wa.W, &wa.W1, &wa.S, &wa.P, &wa.E, &wa.Mm, &wa.Y, &wa.Srot, &wa.Rrot,
-                          &wa.Esum};
-      for (int t = 0; t < 13; ++t) *big[t] = (double*)p[q++];
+      double** big[14] = {&wa.Af, &wa.X0, &wa.X1, &wa.W, &wa.W1, &wa.S, &wa.P, &wa.E, &wa.Mm, &wa.Y, &wa.Srot, &wa.Rrot,
+                          &wa.Esum, &wa.Eprev};
+      for (int t = 0; t < 14; ++t) *big[t] = (double*)p[q++];
       {
         const char* e = getenv("SOSADMM_WARM_PRED");
-        wa.predict = (e && e[0] == '0') ? 0 : 1;
+        wa.predict = (e && e[0] == '0') ? 0 : ((e && e[0] == '2') ? 2 : 1);
+      }
+      {
+        const char* e = getenv("SOSADMM_WARM_BACKOFF");
+        wa.bo_cap = e ? std::max(1, std::min(6, atoi(e))) : 3;
+      }
+      {
+        const char* e = getenv("SOSADMM_WARM_WTEST");
+        wa.wtest = (e && e[0] == '0') ? 0 : 1;
       }
       wa.lam = (double*)p[q++];
       wa.lamt = (double*)p[q++];
@@ -972,13 +982,24 @@ inline cudaError_t large_block_warm_graph(LargeEig& le, LargeBlock& lb, cudaStre
                                           cudaStream_t snest = nullptr) {
   WarmArgs wg = lb.wa;
   cudaError_t e = cudaSuccess;
-  for (int j = 0; j < WM_MAXS && e == cudaSuccess; ++j) e = graph_new_handle(sb, &wg.hstep[j]);
+  // the first `unc` refinement steps as plain nodes (their kernels gated on ws->gate) instead of IF nodes
+  int unc = 3;
+  if (const char* ev = getenv("SOSADMM_WARM_UNCOND")) unc = std::max(0, std::min(WM_MAXS, atoi(ev)));
+  for (int j = 0; j < WM_MAXS && e == cudaSuccess; ++j) {
+    if (j < unc) wg.hstep[j] = 0;
+    else e = graph_new_handle(sb, &wg.hstep[j]);
+  }
   for (unsigned long long* h : {&wg.hcold, &wg.hfull, &wg.hpart, &wg.hfin})
     if (e == cudaSuccess) e = graph_new_handle(sb, h);
   if (e != cudaSuccess) return e;
   large_block_warm_begin(le, lb, sb, wg);
   const int nbody = WM_MAXS + 4;
   for (int j = 0; j < nbody; ++j) {
+    if (j < unc) {
+      e = large_block_warm_step(le, lb, sb, j, wg, snest);
+      if (e != cudaSuccess) return e;
+      continue;
+    }
     const unsigned long long h = j < WM_MAXS ? wg.hstep[j] : (j == WM_MAXS ? wg.hcold : (j == WM_MAXS + 1 ? wg.hfull : (j == WM_MAXS + 2 ? wg.hpart : wg.hfin)));
     cudaGraph_t body = nullptr;
     e = graph_if_body(sb, h, &body);

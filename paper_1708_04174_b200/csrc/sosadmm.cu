@@ -1624,6 +1624,30 @@ extern "C" int sosadmm_debug_warm_project(int N, const double* a0, const double*
   return cudaGetLastError() == cudaSuccess ? 0 : -4;
 }
 
+// Diagnostics: the warm refinement's per-evaluation trace of the last iteration of large block b
+// (out: 4 x WM_MAXS + 8 doubles = coupling / ||a||_F, projected side's orthonormality defect / N, Gershgorin
+// bound / ||a||_F, [evaluations, clusters at step 0, predicted start, status, why, backoff, fails, largest
+// cluster], the other side's orthonormality defect / N);
+// -1 for a bad block index.
+extern "C" int sosadmm_debug_warm_trace(sosadmm_ctx* c, int b, double* out) {
+  if (!c || !out || b < 0 || b >= (int)c->le.blocks.size()) return -1;
+  const LargeBlock& lb = c->le.blocks[b];
+  WarmState h{};
+  if (cudaMemcpyAsync(&h, lb.wa.ws, sizeof(h), cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess)
+    return -4;
+  for (int j = 0; j < WM_MAXS; ++j) {
+    out[j] = h.tr_eta[j];
+    out[WM_MAXS + j] = h.tr_rn[j];
+    out[2 * WM_MAXS + j] = h.tr_g[j];
+  }
+  const double tail[8] = {(double)h.step, (double)h.cl0, (double)h.pred, (double)h.status, (double)h.why,
+                          (double)h.backoff, (double)h.fails, (double)h.maxcl};
+  for (int j = 0; j < 8; ++j) out[3 * WM_MAXS + j] = tail[j];
+  for (int j = 0; j < WM_MAXS; ++j) out[3 * WM_MAXS + 8 + j] = h.tr_ro[j];
+  return 0;
+}
+
 extern "C" int sosadmm_debug_tridiag(int N, const double* A, double* d, double* e, double* tau, double* V) {
   if (N < 3) return -1;
   DebugLarge dl;

@@ -13,7 +13,9 @@
 //   X <- X V (I + E)                                                         (one GEMM: X M, M = V (I + E)).
 // Stop test on the S of the current X (the one the projection then uses):
 //   ||S_{+-}||_F * sqrt 2 <= 1e-13 ||a||_F   (coupling across the sign split),
-//   ||I - X^T X||_F <= 1e-14 N               (orthonormality at rounding level),
+//   ||D o (sigma_i lambda_i + sigma_j lambda_j)||_F <= 1e-13 ||a||_F   (D = X^T X - I weighted by the eigenvalues
+//                                            of the projected side s, sigma = membership of s: reading C19),
+//   ||D||_F <= 1e-8 N                        (a well-conditioned basis),
 //   Gershgorin: the rows whose same-sign off-diagonal mass rho_i reaches |lambda_i| have
 //   (sum rho_i^2)^(1/2) <= 1e-12 ||a||_F (the wrong-sign part of a diagonal block is bounded by it),
 // so a = X [S_++ 0; 0 S_--] X^T + O(1e-13 ||a||_F) with S_++, -S_-- PSD up to O(1e-12 ||a||_F), and the projection is
@@ -34,7 +36,7 @@ constexpr int WM_MAXS = 10;         // S evaluations per ADMM iteration (at most
 constexpr int WM_CAP = 64;          // largest cluster diagonalised exactly
 constexpr double WM_THETA = 0.05;   // strong coupling threshold
 constexpr double WM_TOLE = 1e-13;   // cross-sign coupling tolerance relative to ||a||_F
-constexpr double WM_TOLR = 1e-14;   // orthonormality tolerance per unit of N
+constexpr double WM_TOLO = 1e-8;    // unweighted orthonormality defect per unit of N (basis conditioning)
 constexpr double WM_TOLG = 1e-12;   // Gershgorin sign-uncertainty bound relative to ||a||_F
 constexpr int WM_NT = 1024;         // single-CTA kernels
 constexpr int WM_SORT = 2048;       // bitonic sort capacity (N <= SOSADMM_MAX_BLOCK = 1280)
@@ -54,6 +56,7 @@ struct WarmState {
   int need_full;    // the cold path of this iteration re-seeds X (every eigenvector): the next one tries warm
   int pgate;        // 1: step 0 forms P = X^T X (0: the previous iteration certified this X and its P is kept)
   int pred;         // 1: this iteration starts from the predicted X0 (I + Esum) (k_warm_pred)
+  int pred_last;    // the previous iteration's pred (k_warm_begin copies it after the predictor ran)
   int pred_ok;      // Esum holds the previous iteration's whole rotation generator (sum of M - I) and the
                     // trajectory looked smooth there (no cluster at step 0, <= 3 evaluations predicted / 4 not)
   int cl0;          // clusters formed at step 0 of this iteration
@@ -66,6 +69,8 @@ struct WarmState {
   int why;          // last failure: 1 = no convergence within WM_MAXS, 2 = stalled coupling, 3 = cluster > WM_CAP,
                     // 4 = non-finite
   int maxcl;        // largest cluster of the last step
+  double tr_eta[WM_MAXS], tr_rn[WM_MAXS], tr_g[WM_MAXS], tr_ro[WM_MAXS];  // diagnostics: per S evaluation of the last
+                    // iteration, coupling / ||a||_F, orthonormality defect / N, Gershgorin bound / ||a||_F
 };
 
 struct WarmArgs {
@@ -74,7 +79,10 @@ struct WarmArgs {
   double *Af, *X0, *X1, *W, *W1, *S, *P, *E, *Mm, *Y;
   double *Srot, *Rrot;       // rotated rows (V_C^T S)[u, :], (V_C^T R)[u, :] of every cluster member (slot rows)
   double* Esum;              // sum of (M - I) over the refinement steps: the first-order rotation generator
-  int predict;               // 1: start each warm iteration from X0 (I + Esum) of the previous one
+  double* Eprev;             // the previous iteration's generator (second-order predictor)
+  int predict;               // 1: start each warm iteration from X0 (I + Esum) of the previous one; 2: extrapolated
+  int wtest;                 // 1: eigenvalue-weighted orthonormality test (C19); 0: ||I - X^T X||_F <= 1e-14 N
+  int bo_cap;                // backoff after f consecutive failures: 2^min(f, bo_cap) - 1 cold iterations
   double *lam, *lamt;
   int *order, *pos, *diff, *cid, *cpos, *cl_start, *cl_size, *cl_voff, *cl_rbase, *sel, *idx;
   double* Vcl;               // cluster rotations, <= WM_CAP * N doubles
@@ -116,20 +124,36 @@ __device__ __forceinline__ double wm_block_sum(double v, double* red) {
 // ---- predictor (before begin): the eigenvectors move smoothly along the ADMM trajectory, so the
 // previous iteration's rotation, X_{k-1} = X_{k-2} (I + Esum) to first order, is applied once more:
 // M = I + Esum, then X1 = X0 M (gated GEMM) and begin copies X1 to X0.  Esum keeps that generator (the
-// refinement steps add their corrections to it); without a valid generator it restarts from zero.
+// refinement steps add their corrections to it); without a valid generator it restarts from zero.  With
+// predict == 2 and two consecutive valid generators, the generator is extrapolated linearly (2 G_k - G_{k-1}):
+// the ADMM trajectory changes geometrically slowly, so the first-order start's error eps G_k drops to ~eps^2 G_k.
 // grid (nt, nt), 256 threads
 __global__ void __launch_bounds__(256) k_warm_pred(WarmArgs a) {
   if (wm_skip(a)) return;
   const WarmState* ws = a.ws;
   const bool cond = a.predict && ws->valid && ws->backoff == 0 && ws->pred_ok;
+  // second order (predict == 2): Eprev holds the generator before Esum's when the previous iteration was predicted too
+  const bool o2 = cond && a.predict == 2 && ws->pred_last;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, N = a.N, ld = a.ldn;
   const int i = 32 * blockIdx.x + tx;
   for (int r = ty; r < 32 && i < N; r += 8) {
     const int j = 32 * blockIdx.y + r;
     if (j >= N) break;
     const size_t e = (size_t)j * ld + i;
-    if (cond) a.Mm[e] = (i == j ? 1.0 : 0.0) + a.Esum[e];
-    else a.Esum[e] = 0.0;
+    if (cond) {
+      double g = a.Esum[e];
+      if (o2) {  // linear extrapolation of the generator: G_k + (G_k - G_{k-1})
+        const double gp = a.Eprev[e];
+        a.Eprev[e] = g;
+        g = 2.0 * g - gp;
+        a.Esum[e] = g;
+      } else if (a.predict == 2) {
+        a.Eprev[e] = g;
+      }
+      a.Mm[e] = (i == j ? 1.0 : 0.0) + g;
+    } else {
+      a.Esum[e] = 0.0;
+    }
   }
   if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) a.ws->pred = cond ? 1 : 0;
 }
@@ -179,6 +203,7 @@ __global__ void __launch_bounds__(256) k_warm_begin(WarmArgs a) {
     a.partA[ti * a.nt + tj] = s;
     if (ti == 0 && tj == 0) {
       WarmState* ws = a.ws;
+      ws->pred_last = ws->pred;
       ws->step = 0;
       ws->ncl = 0;
       ws->cl0 = 0;
@@ -240,7 +265,7 @@ __global__ void __launch_bounds__(256) k_warm_scan(WarmArgs a, int step) {
   const bool jv = j < N;
   const double lj = lcol[tx];
   const bool gj = lj > 0.0;
-  double cr = 0.0, ro = 0.0, cs = 0.0;
+  double cr = 0.0, ro = 0.0, wp = 0.0, wm = 0.0, cs = 0.0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int rr = ty + 8 * q, i = 32 * ti + rr;
@@ -256,6 +281,10 @@ __global__ void __launch_bounds__(256) k_warm_scan(WarmArgs a, int step) {
         cs += fabs(sv);
       }
       ro = fma(pv, pv, ro);
+      // X^T X defect weighted by the eigenvalues of the projected side (either side: decided at the end)
+      const double up = fmax(li, 0.0) + fmax(lj, 0.0), um = fmin(li, 0.0) + fmin(lj, 0.0);
+      wp = fma(pv * up, pv * up, wp);
+      wm = fma(pv * um, pv * um, wm);
       const double sp = fma(-0.5 * (li + lj), pv, sv);  // S'_ij = S_ij + lambda_bar R_ij, R_ij = -P_ij
       if (fabs(sp) > WM_THETA * fabs(lj - li)) {       // strong pair: listed for the cluster build
         const int k = atomicAdd(a.cnt + nt + 1, 1);
@@ -271,9 +300,13 @@ __global__ void __launch_bounds__(256) k_warm_scan(WarmArgs a, int step) {
   colp[ty][tx] = cs;
   cr = warp_sum(cr);
   ro = warp_sum(ro);
+  wp = warp_sum(wp);
+  wm = warp_sum(wm);
   if (tx == 0) {
     red[ty] = cr;
     red[8 + ty] = ro;
+    red[16 + ty] = wp;
+    red[24 + ty] = wm;
   }
   __syncthreads();
   if (ty == 0) {
@@ -282,24 +315,43 @@ __global__ void __launch_bounds__(256) k_warm_scan(WarmArgs a, int step) {
     for (int w = 0; w < 8; ++w) c += colp[w][tx];
     if (jv) a.gcol[(size_t)ti * N + j] = c;  // column j's mass over this tile's rows (i < j)
     if (tx == 0) {
-      double c2 = 0.0, r2 = 0.0;
+      double c2 = 0.0, r2[3] = {0.0, 0.0, 0.0};
       for (int w = 0; w < 8; ++w) {
         c2 += red[w];
-        r2 += red[8 + w];
+        r2[0] += red[8 + w];
+        r2[1] += red[16 + w];
+        r2[2] += red[24 + w];
       }
       a.cross[ti * nt + tj] = c2;
-      a.roff[ti * nt + tj] = r2;
+      for (int c = 0; c < 3; ++c) a.roff[(size_t)c * nt * nt + ti * nt + tj] = r2[c];
     }
   }
-  if (ti == tj && ty == 1) {  // the block's (1 - P_ii)^2
+  if (ti == tj && ty == 1) {  // the block's (1 - P_ii)^2, weighted by (2 lambda_i)^2 per side, and its sign counts
     const int i = 32 * ti + tx;
-    double d = 0.0;
+    double d = 0.0, dp = 0.0, dm = 0.0, np = 0.0, nn = 0.0;
     if (i < N) {
-      const double p = a.P[(size_t)i * ld + i];
+      const double p = a.P[(size_t)i * ld + i], li = lrow[tx];
       d = (1.0 - p) * (1.0 - p);
+      if (li > 0.0) {
+        dp = 4.0 * li * li * d;
+        np = 1.0;
+      } else if (li < 0.0) {
+        dm = 4.0 * li * li * d;
+        nn = 1.0;
+      }
     }
     d = warp_sum(d);
-    if (tx == 0) a.rdpart[ti] = d;
+    dp = warp_sum(dp);
+    dm = warp_sum(dm);
+    np = warp_sum(np);
+    nn = warp_sum(nn);
+    if (tx == 0) {
+      a.rdpart[ti] = d;
+      a.rdpart[nt + ti] = dp;
+      a.rdpart[2 * nt + ti] = dm;
+      a.rdpart[3 * nt + ti] = np;
+      a.rdpart[4 * nt + ti] = nn;
+    }
   }
   // (3) row-block completion
   __threadfence();
@@ -372,23 +424,36 @@ __device__ void wm_decide(const WarmArgs& a, int step, double* red, int* cpre, d
     flags[1] = 0;
     flags[2] = 0;
   }
-  double c2 = 0.0, r2 = 0.0, a2 = 0.0, rd = 0.0, g2 = 0.0;
+  double c2 = 0.0, r2 = 0.0, wp = 0.0, wm = 0.0, a2 = 0.0, rd = 0.0, rdp = 0.0, rdm = 0.0, np = 0.0, nn = 0.0, g2 = 0.0;
+  const size_t nt2 = (size_t)nt * nt;
   for (int e = tid; e < nt * nt; e += T) {
     const int ti = e / nt, tj = e % nt;
     if (ti <= tj) {
       c2 += __ldcg(a.cross + e);
       r2 += __ldcg(a.roff + e);
+      wp += __ldcg(a.roff + nt2 + e);
+      wm += __ldcg(a.roff + 2 * nt2 + e);
     }
     if (step == 0) a2 += __ldcg(a.partA + e);
   }
   for (int t = tid; t < nt; t += T) {
     rd += __ldcg(a.rdpart + t);
+    rdp += __ldcg(a.rdpart + nt + t);
+    rdm += __ldcg(a.rdpart + 2 * nt + t);
+    np += __ldcg(a.rdpart + 3 * nt + t);
+    nn += __ldcg(a.rdpart + 4 * nt + t);
     g2 += __ldcg(a.g2part + t);
   }
   const int npairs = __ldcg(a.cnt + nt + 1);
   c2 = bsum(c2);
   r2 = bsum(r2);
+  wp = bsum(wp);
+  wm = bsum(wm);
   rd = bsum(rd);
+  rdp = bsum(rdp);
+  rdm = bsum(rdm);
+  np = bsum(np);
+  nn = bsum(nn);
   g2 = bsum(g2);
   if (step == 0) {
     a2 = bsum(a2);
@@ -398,14 +463,31 @@ __device__ void wm_decide(const WarmArgs& a, int step, double* red, int* cpre, d
   for (int t = tid; t <= nt + 1; t += T) a.cnt[t] = 0;
   __syncthreads();
   const double nA = sqrt(ws->normA2);
-  const double eta = sqrt(2.0 * c2), rn = sqrt(2.0 * r2 + rd);
+  // orthonormality (reading C19): with X = Q (I + F), D = X^T X - I = F + F^T and the projected side s (k_warm_select's
+  // rule: lambda > 0 when #(lambda > 0) <= #(lambda < 0)), the first-order error of X_s S_ss X_s^T is
+  //   F_os Lambda_s (+ transpose) and D_ss o (lambda_i + lambda_j),  |F_ij lambda_j| <= |lambda_j D_ij| + |S_ij| (i in o),
+  // so the certificate needs the coupling and the lambda-WEIGHTED defect ||D_ij (sigma_i lambda_i + sigma_j lambda_j)||_F
+  // (sigma = membership of s) at the coupling tolerance; the unweighted defect only has to keep the basis well
+  // conditioned (second-order terms), ||D||_F <= WM_TOLO N
+  const bool pos_side = np <= nn;
+  const double eta = sqrt(2.0 * c2);
+  const double rn = sqrt(2.0 * (pos_side ? wp : wm) + (pos_side ? rdp : rdm));
+  const double ro = sqrt(2.0 * r2 + rd);
   // Gershgorin sign safety: the rows whose same-sign off-diagonal mass rho_i reaches |lambda_i| can hide a
   // wrong-sign eigenvalue of size <= rho_i in their diagonal block: (sum of those rho_i^2)^(1/2) must be at
   // rounding level, <= WM_TOLG ||a||_F (near-zero eigenvalues keep rho_i at the floor of the S product).
+  if (tid == 0) {
+    ws->tr_eta[step] = eta / nA;
+    ws->tr_rn[step] = rn / nA;
+    ws->tr_ro[step] = ro / N;
+    ws->tr_g[step] = sqrt(g2) / nA;
+  }
   const bool cross_ok = eta <= WM_TOLE * nA;
-  const bool conv = cross_ok && rn <= WM_TOLR * N && sqrt(g2) <= WM_TOLG * nA && isfinite(eta) && isfinite(rn);
+  const bool orth_ok = a.wtest ? (rn <= WM_TOLE * nA && ro <= WM_TOLO * N) : ro <= 1e-14 * N;
+  const bool conv = cross_ok && orth_ok && sqrt(g2) <= WM_TOLG * nA && isfinite(eta) &&
+                    isfinite(rn) && isfinite(ro);
   // a coupling that stops halving while still above the tolerance means the update is not converging
-  const bool stall = !isfinite(eta) || !isfinite(rn) || step == WM_MAXS - 1 ||
+  const bool stall = !isfinite(eta) || !isfinite(rn) || !isfinite(ro) || step == WM_MAXS - 1 ||
                      (step > 0 && !cross_ok && eta > 0.5 * ws->eta_prev);
   if (conv || stall || npairs > WM_PAIRS) {
     if (tid == 0) {
@@ -423,7 +505,7 @@ __device__ void wm_decide(const WarmArgs& a, int step, double* red, int* cpre, d
       } else {
         ws->status = 2;
         ws->fails++;
-        ws->backoff = (1 << min(ws->fails, 6)) - 1;
+        ws->backoff = (1 << min(ws->fails, a.bo_cap)) - 1;
         ws->need_full = 0;
         ws->n_fail++;
         ws->n_steps += step;
@@ -518,7 +600,7 @@ __device__ void wm_decide(const WarmArgs& a, int step, double* red, int* cpre, d
       ws->gate = 0;
       ws->status = 2;
       ws->fails++;
-      ws->backoff = (1 << min(ws->fails, 6)) - 1;
+      ws->backoff = (1 << min(ws->fails, a.bo_cap)) - 1;
       ws->need_full = 0;
       ws->n_fail++;
       ws->n_steps += step;
