@@ -42,6 +42,7 @@ struct AffineArgs {
   const int* lr_idx;
   const int* lr_col;   // low_col[lr_idx[e]] (the gather's direct column index)
   int row_lanes;       // k_rowupdate lanes per row: 8 when some row has >= 16 low-rank entries, else 1
+  int fuse_low;        // 1: k_tphase forms A_low^T x and K^{-1} y_t itself (t' <= FUSE_LOW_TL, few entries): two launches less
   const double* lr_val;
   const int* lc_ptr;
   const int* lc_row;
@@ -150,13 +151,10 @@ __global__ void __launch_bounds__(GATHER_NT) k_gather(AffineArgs a) {
   gather_part_sums<GATHER_NT>(bxd, p_pres, p_axi, p_dres, p_by, sh, a.part, a.gather_blocks, blockIdx.x, false, 0.0);
 }
 
-// k_lowT: one warp per low column j:  y_t[j] = (A_low^T x)_j,  aty[j] = (A_low^T y)_j.
-__global__ void __launch_bounds__(256) k_lowT(AffineArgs a) {
-  if (a.st->done) return;
-  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (wid >= a.tl) return;
+// One warp, low column j:  y_t[j] = (A_low^T x)_j,  aty[j] = (A_low^T y)_j.
+__device__ __forceinline__ void lowT_column(const AffineArgs& a, int j, int lane) {
   double sx = 0.0, sy = 0.0;
-  for (int e = a.lc_ptr[wid] + lane; e < a.lc_ptr[wid + 1]; e += 32) {
+  for (int e = a.lc_ptr[j] + lane; e < a.lc_ptr[j + 1]; e += 32) {
     const int r = a.lc_row[e];
     const double v = a.lc_val[e];
     sx = fma(v, a.x[r], sx);
@@ -165,22 +163,35 @@ __global__ void __launch_bounds__(256) k_lowT(AffineArgs a) {
   sx = warp_sum(sx);
   sy = warp_sum(sy);
   if (lane == 0) {
-    a.yt[wid] = sx;
-    a.aty[wid] = sy;
+    a.yt[j] = sx;
+    a.aty[j] = sy;
   }
 }
 
-// k_kinv: one warp per row i:  z_t[i] = sum_j Kinv[i, j] y_t[j]  (P:874 with the cached factor
-// applied as an explicit SPD inverse; K symmetric so row i = column i).
+// One warp, row i:  z_t[i] = sum_j Kinv[i, j] y_t[j]  (P:874 with the cached factor applied as an
+// explicit SPD inverse; K symmetric so row i = column i).
+__device__ __forceinline__ void kinv_row(const AffineArgs& a, int i, int lane) {
+  const double* row = a.Kinv + (size_t)i * a.ldk;
+  double acc = 0.0;
+  for (int j = lane; j < a.tl; j += 32) acc = fma(row[j], a.yt[j], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) a.zt[i] = acc;
+}
+
+// k_lowT: one warp per low column.
+__global__ void __launch_bounds__(256) k_lowT(AffineArgs a) {
+  if (a.st->done) return;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= a.tl) return;
+  lowT_column(a, wid, lane);
+}
+
+// k_kinv: one warp per row.
 __global__ void __launch_bounds__(256) k_kinv(AffineArgs a) {
   if (a.st->done) return;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wid >= a.tl) return;
-  const double* row = a.Kinv + (size_t)wid * a.ldk;
-  double acc = 0.0;
-  for (int j = lane; j < a.tl; j += 32) acc = fma(row[j], a.yt[j], acc);
-  acc = warp_sum(acc);
-  if (lane == 0) a.zt[wid] = acc;
+  kinv_row(a, wid, lane);
 }
 
 // Symmetric K^{-1} apply for large t' (config 3: t' = 7,801, K^{-1} = 487 MB, HBM-bound): read only
@@ -280,11 +291,20 @@ __global__ void __launch_bounds__(256) k_kinv_sum(AffineArgs a) {
 // k_tphase: single CTA.  mode 0 = full iteration, 1 = check-only (residuals of u^k, no update),
 // 2 = affine-only (unit entry point: no termination logic, no writes to xi/z).
 constexpr int TP_NT = 512;
+constexpr int FUSE_LOW_TL = 16;     // a.fuse_low: t' <= 16 and nnz(A_low) <= 4096 (configs 0, 1, 4: t' = 1), so
+constexpr int FUSE_LOW_NNZ = 4096;  //   this CTA's 16 warps do k_lowT's and k_kinv's work (the same warp sums: same bits)
 __global__ void __launch_bounds__(TP_NT) k_tphase(AffineArgs a, int mode) {
   __shared__ double bc[10];
   DevState* st = a.st;
   if (st->done) return;
   const int tid = threadIdx.x;
+  if (a.fuse_low) {
+    const int w = tid >> 5, lane = tid & 31;
+    if (w < a.tl) lowT_column(a, w, lane);
+    __syncthreads();  // y_t (global) written by this CTA's warps, read by them below
+    if (w < a.tl) kinv_row(a, w, lane);
+    __syncthreads();
+  }
   // 1. fixed-order reductions of the gather partials (b^T x in double-double) and of the low-column
   //    sums: the trees of block_sum / dd_block_sum (per-warp shuffle tree, then the warp partials in
   //    warp order — the same bits), all values at once behind ONE barrier (the loads issued together)

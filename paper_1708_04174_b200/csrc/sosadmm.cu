@@ -521,6 +521,15 @@ void launch_kinv(const AffineArgs& a, cudaStream_t s) {
   }
 }
 
+// y_t = A_low^T x, z_t = K^{-1} y_t, then the single-CTA tau phase; for small t' the tau phase does all three
+void launch_low_tphase(const AffineArgs& a, cudaStream_t s, int mode) {
+  if (!a.fuse_low) {
+    k_lowT<<<std::max(1, (a.tl * 32 + 255) / 256), 256, 0, s>>>(a);
+    launch_kinv(a, s);
+  }
+  k_tphase<<<1, TP_NT, 0, s>>>(a, mode);
+}
+
 void launch_rowupdate(const AffineArgs& a, cudaStream_t s, int write_state) {
   if (a.row_lanes == 8)
     k_rowupdate8<<<(int)(((long long)a.m * 8 + 255) / 256), 256, 0, s>>>(a, write_state);
@@ -534,7 +543,6 @@ void launch_rowupdate(const AffineArgs& a, cudaStream_t s, int write_state) {
 sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev, int phase = 0) {
   AffineArgs& a = c->aa;
   cudaStream_t s = c->stream;
-  const int tlw = std::max(1, (a.tl * 32 + 255) / 256);
   if (ev) cudaEventRecord(ev[0], s);
   if (c->sp.sharded) {
     if (c->sp.emulated && phase == 0) {
@@ -566,9 +574,7 @@ sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev, int
   } else {
     k_gather<<<c->gather_blocks, GATHER_NT, 0, s>>>(a);
   }
-  k_lowT<<<tlw, 256, 0, s>>>(a);
-  launch_kinv(a, s);
-  k_tphase<<<1, TP_NT, 0, s>>>(a, mode_full ? 0 : 1);
+  launch_low_tphase(a, s, mode_full ? 0 : 1);
   if (!mode_full) return SOSADMM_OK;
   launch_rowupdate(a, s, 1);
   if (ev) cudaEventRecord(ev[1], s);
@@ -614,6 +620,7 @@ sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev, int
 int64_t count_launches(const sosadmm_ctx* c) {
   int64_t k = c->sp.sharded ? 9 : 6;  // gather (sharded: 4 kernels + allreduce), lowT, kinv, tphase, rowupdate, pack
   if (c->an.tl >= KINV_SYM_MIN) k += 1;  // symmetric K^{-1} apply: tiles + fixed-order sum
+  if (c->aa.fuse_low) k -= 2;            // k_tphase does k_lowT's and k_kinv's work
   if (c->aa.pos_ctas > 0) k += 1;
   if (!c->an.small_blk.empty()) k += 1;
   if (!c->an.large_blk.empty()) k += large_eig_launches(c->le);
@@ -956,6 +963,7 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
     int mx = 0;
     for (int r = 0; r < an.m; ++r) mx = std::max(mx, an.lr_ptr[r + 1] - an.lr_ptr[r]);
     a.row_lanes = mx >= 16 ? 8 : 1;
+    a.fuse_low = (an.tl <= FUSE_LOW_TL && an.lr_ptr[an.m] <= FUSE_LOW_NNZ && !getenv("SOSADMM_NO_FUSE_LOW")) ? 1 : 0;
   }
   a.lc_ptr = d.lc_ptr; a.lc_row = d.lc_row; a.lc_val = d.lc_val;
   a.c_low = d.c_low; a.h1_low = d.h1_low; a.beta_low = d.beta_low; a.Kinv = d.Kinv;
@@ -1293,11 +1301,8 @@ sosadmm_err sosadmm_project_affine(sosadmm_ctx* c, const double* w1, const doubl
   std::vector<double> zero_n(n, 0.0), zero_m(m, 0.0);
   if (sosadmm_set_iterate(c, w1, w2, zero_n.data(), zero_m.data(), w3, 0.0, 0)) return c->err;
   cudaStream_t s = c->stream;
-  const int tlw = std::max(1, (a.tl * 32 + 255) / 256);
   k_gather<<<c->gather_blocks, GATHER_NT, 0, s>>>(a);
-  k_lowT<<<tlw, 256, 0, s>>>(a);
-  launch_kinv(a, s);
-  k_tphase<<<1, TP_NT, 0, s>>>(a, 2);
+  launch_low_tphase(a, s, 2);
   launch_rowupdate(a, s, 0);
   if (a.pos_ctas > 0) k_scatter<<<a.pos_ctas, POS_NT, 0, s>>>(a, 1);
   if (check_async(c)) return c->err;

@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(256) k_warm_begin(WarmArgs a) {
 //  (3) row-block completion: the CTA that brings a row block's nt + 1 contributions together sums its rows'
 //      rho_i in tile order and writes the block's Gershgorin partial;
 //  (4) the last CTA of the grid runs the stop test and builds the clusters (fixed-order sums throughout).
-__device__ void wm_decide(const WarmArgs& a, int step, double* red, int* cpre, double* lam_s, int* flags);
+__device__ void wm_decide(const WarmArgs& a, int step, double* red, double* red11, int* cpre, double* lam_s, int* flags);
 
 __global__ void __launch_bounds__(256) k_warm_scan(WarmArgs a, int step) {
   if (wm_skip(a) || a.ws->gate != 1) return;
@@ -357,13 +357,15 @@ __global__ void __launch_bounds__(256) k_warm_scan(WarmArgs a, int step) {
   __threadfence();
   __syncthreads();
   if (tid == 0) {
-    done_blk[0] = done_blk[1] = -1;
+    done_blk[0] = -1;
     if (ti == tj) {
       if (atomicAdd(a.cnt + ti, 2) + 2 == nt + 1) done_blk[0] = ti;
     } else {
       if (atomicAdd(a.cnt + ti, 1) + 1 == nt + 1) done_blk[0] = ti;
-      if (atomicAdd(a.cnt + tj, 1) + 1 == nt + 1) done_blk[1] = tj;
     }
+  } else if (tid == 32) {  // the column block's counter from another warp: both atomics in flight together
+    done_blk[1] = -1;
+    if (ti != tj && atomicAdd(a.cnt + tj, 1) + 1 == nt + 1) done_blk[1] = tj;
   }
   __syncthreads();
   for (int h = 0; h < 2; ++h) {
@@ -372,7 +374,11 @@ __global__ void __launch_bounds__(256) k_warm_scan(WarmArgs a, int step) {
     __threadfence();
     // rows i = 32 t + r; 8 threads per row take the terms tt = g, g + 8, ... (grow: tt >= t, gcol: tt <= t)
     const int r = tid & 31, g = tid >> 5, i = 32 * t + r;
-    double rho = 0.0;
+    double rho = 0.0, sd = 0.0, pd = 1.0;
+    if (g == 0 && i < N) {  // the row's diagonal entries, in flight together with the masses below
+      sd = __ldcg(a.S + (size_t)i * ld + i);
+      pd = __ldcg(a.P + (size_t)i * ld + i);
+    }
     if (i < N)
       for (int tt = g; tt < nt; tt += 8) {
         if (tt >= t) rho += __ldcg(a.grow + (size_t)tt * N + i);
@@ -386,7 +392,7 @@ __global__ void __launch_bounds__(256) k_warm_scan(WarmArgs a, int step) {
       for (int w = 0; w < 8; ++w) rr += colp[w][r];
       double g2 = 0.0;
       if (i < N) {
-        const double li = __ldcg(a.S + (size_t)i * ld + i) / __ldcg(a.P + (size_t)i * ld + i);
+        const double li = sd / pd;
         if (!(fabs(li) > rr)) g2 = rr * rr;
       }
       g2 = warp_sum(g2);
@@ -401,11 +407,11 @@ __global__ void __launch_bounds__(256) k_warm_scan(WarmArgs a, int step) {
   __syncthreads();
   if (!flags[3]) return;
   __threadfence();
-  wm_decide(a, step, red, cpre, lam_s, flags);
+  wm_decide(a, step, red, &colp[0][0], cpre, lam_s, flags);  // colp (264 doubles) is free by now
 }
 
 // the stop test and the clusters (256 threads of the grid's last CTA)
-__device__ void wm_decide(const WarmArgs& a, int step, double* red, int* cpre, double* lam_s, int* flags) {
+__device__ void wm_decide(const WarmArgs& a, int step, double* red, double* red11, int* cpre, double* lam_s, int* flags) {
   WarmState* ws = a.ws;
   const int N = a.N, nt = a.nt, tid = threadIdx.x;
   constexpr int T = 256;
@@ -445,19 +451,23 @@ __device__ void wm_decide(const WarmArgs& a, int step, double* red, int* cpre, d
     g2 += __ldcg(a.g2part + t);
   }
   const int npairs = __ldcg(a.cnt + nt + 1);
-  c2 = bsum(c2);
-  r2 = bsum(r2);
-  wp = bsum(wp);
-  wm = bsum(wm);
-  rd = bsum(rd);
-  rdp = bsum(rdp);
-  rdm = bsum(rdm);
-  np = bsum(np);
-  nn = bsum(nn);
-  g2 = bsum(g2);
-  if (step == 0) {
-    a2 = bsum(a2);
-    if (tid == 0) ws->normA2 = a2;
+  {  // all eleven sums behind ONE barrier pair: bsum's tree (per-warp shuffle tree, warp partials in warp order)
+    double v[11] = {c2, r2, wp, wm, rd, rdp, rdm, np, nn, g2, a2};
+#pragma unroll
+    for (int q = 0; q < 11; ++q) v[q] = warp_sum(v[q]);
+    __syncthreads();
+    if ((tid & 31) == 0)
+#pragma unroll
+      for (int q = 0; q < 11; ++q) red11[q * (T / 32) + (tid >> 5)] = v[q];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 11; ++q) {
+      double t = 0.0;
+      for (int w = 0; w < T / 32; ++w) t += red11[q * (T / 32) + w];
+      v[q] = t;
+    }
+    c2 = v[0], r2 = v[1], wp = v[2], wm = v[3], rd = v[4], rdp = v[5], rdm = v[6], np = v[7], nn = v[8], g2 = v[9];
+    if (step == 0 && tid == 0) ws->normA2 = v[10];
   }
   // counters back to zero for the next step (every other CTA is done with them)
   for (int t = tid; t <= nt + 1; t += T) a.cnt[t] = 0;

@@ -98,3 +98,27 @@ def test_iterate_stops_enqueueing_after_termination():
     assert np.array_equal(_iterates(s), _iterates(r))
     s.close()
     r.close()
+
+
+@pytest.mark.parametrize("name", ["pop6", "pop20"])
+def test_fused_low_phase_bit_identical(name, monkeypatch):
+    """For t' <= 16 k_tphase does k_lowT's and k_kinv's work itself (two launches less; the same warp
+    sums).  The iterates must be BIT-identical to the three-launch chain (SOSADMM_NO_FUSE_LOW=1, read
+    at setup), which test_gpu_parity.py checks against the oracle."""
+    from paper_1708_04174_b200 import SosAdmm
+
+    prob = make_config(name)
+    out = []
+    for env in (None, "1"):
+        if env is None:
+            monkeypatch.delenv("SOSADMM_NO_FUSE_LOW", raising=False)
+        else:
+            monkeypatch.setenv("SOSADMM_NO_FUSE_LOW", env)
+        s = SosAdmm.from_problem(prob, max_iters=10_000)
+        info = s.iterate(40)
+        out.append((info, _iterates(s)))
+        s.close()
+    (ia, va), (ib, vb) = out
+    assert ia["iter"] == ib["iter"] == 40
+    assert np.array_equal(va, vb)
+    assert ia["res_pri"] == ib["res_pri"] and ia["res_dual"] == ib["res_dual"]
