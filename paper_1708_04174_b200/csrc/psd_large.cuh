@@ -781,10 +781,18 @@ __global__ void k_zero2(double* a, double* b, long long n) {
     b[e] = 0.0;
   }
 }
-inline void large_block_warm_begin(LargeEig& le, LargeBlock& lb, cudaStream_t s, const WarmArgs& wa) {
+// the predictor X1 = X0 (I + G): reads only what the previous iteration left (X0, Esum, the warm state), so
+// in the CUDA graph it runs on a branch beside the affine projection (launch_iteration) instead of after it
+inline void large_block_warm_pred(LargeEig& le, LargeBlock& lb, cudaStream_t s) {
+  k_warm_pred<<<dim3(lb.wa.nt, lb.wa.nt), 256, 0, s>>>(lb.wa);
+  dgemm_launch(DG_DEFAULT, lb.wdesc + 5 * WM_MAXS + 1, 1, lb.N, lb.N, s, le.st, le.is, 1);
+}
+// pred_done: the predictor already ran on another branch; s joins it here
+inline void large_block_warm_begin(LargeEig& le, LargeBlock& lb, cudaStream_t s, const WarmArgs& wa,
+                                   cudaEvent_t pred_done = nullptr) {
   if (wa.predict) {
-    k_warm_pred<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
-    dgemm_launch(DG_DEFAULT, lb.wdesc + 5 * WM_MAXS + 1, 1, lb.N, lb.N, s, le.st, le.is, 1);
+    if (pred_done) cudaStreamWaitEvent(s, pred_done, 0);
+    else large_block_warm_pred(le, lb, s);
   }
   k_warm_begin<<<dim3(wa.nt, wa.nt), 256, 0, s>>>(wa);
 }
@@ -979,7 +987,7 @@ inline cudaError_t graph_if_body(cudaStream_t s, unsigned long long h, cudaGraph
 //   partial tail (k_select + bt of the projected side + reconstruction) -> warm finish (set on success).
 inline cudaError_t large_block_warm_graph(LargeEig& le, LargeBlock& lb, cudaStream_t sb, cudaStream_t sbody,
                                           cudaStream_t sw, cudaStream_t sd, const cudaEvent_t* evs,
-                                          cudaStream_t snest = nullptr) {
+                                          cudaStream_t snest = nullptr, cudaEvent_t pred_done = nullptr) {
   WarmArgs wg = lb.wa;
   cudaError_t e = cudaSuccess;
   // the first `unc` refinement steps as plain nodes (their kernels gated on ws->gate) instead of IF nodes
@@ -992,7 +1000,7 @@ inline cudaError_t large_block_warm_graph(LargeEig& le, LargeBlock& lb, cudaStre
   for (unsigned long long* h : {&wg.hcold, &wg.hfull, &wg.hpart, &wg.hfin})
     if (e == cudaSuccess) e = graph_new_handle(sb, h);
   if (e != cudaSuccess) return e;
-  large_block_warm_begin(le, lb, sb, wg);
+  large_block_warm_begin(le, lb, sb, wg, pred_done);
   const int nbody = WM_MAXS + 4;
   for (int j = 0; j < nbody; ++j) {
     if (j < unc) {
@@ -1036,7 +1044,8 @@ inline cudaError_t large_block_warm_graph(LargeEig& le, LargeBlock& lb, cudaStre
 // body: one stream per block outside the capture (warm blocks' conditional bodies).
 inline cudaError_t large_eig_launch_concurrent(LargeEig& le, cudaStream_t s, bool check, cudaEvent_t fork,
                                                const cudaStream_t* aux, const cudaEvent_t* evs,
-                                               const cudaStream_t* body, const cudaStream_t* nest = nullptr) {
+                                               const cudaStream_t* body, const cudaStream_t* nest = nullptr,
+                                               const cudaEvent_t* pred_done = nullptr) {
   const int nb = (int)le.blocks.size();
   for (int b = 0; b < nb; ++b) {
     LargeBlock& lb = le.blocks[b];
@@ -1045,7 +1054,8 @@ inline cudaError_t large_eig_launch_concurrent(LargeEig& le, cudaStream_t s, boo
     cudaStream_t sd = aux[3 * b + 2];
     if (b > 0) cudaStreamWaitEvent(sb, fork, 0);
     if (lb.warm) {
-      const cudaError_t e = large_block_warm_graph(le, lb, sb, body[b], sw, sd, evs + 8 * b, nest ? nest[b] : nullptr);
+      const cudaError_t e = large_block_warm_graph(le, lb, sb, body[b], sw, sd, evs + 8 * b, nest ? nest[b] : nullptr,
+                                                   pred_done ? pred_done[b] : nullptr);
       if (e != cudaSuccess) return e;
       if (b > 0) cudaEventRecord(evs[8 * b + 2], sb);
       continue;

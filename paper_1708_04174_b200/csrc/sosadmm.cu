@@ -398,6 +398,10 @@ struct sosadmm_ctx {
   cudaStream_t body[8] = {};  // capture streams of the warm blocks' conditional bodies (outside the main capture)
   cudaStream_t nest[8] = {};  // and of the bodies nested inside them
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_blk[8 * 8] = {};
+  // warm predictor branches (one per large block), forked at the start of the iteration beside the affine chain
+  cudaStream_t pre[8] = {};
+  cudaEvent_t ev_pre0 = nullptr, ev_pre[8] = {};
+  bool early_pred = true;  // SOSADMM_EARLY_PRED=0: the predictor after the scatter, as on the un-graphed path
   // early-stop polling of sosadmm_iterate: pinned copies of the device state after each chunk of replays
   DevState* h_poll = nullptr;
   cudaEvent_t ev_poll[2] = {};
@@ -544,6 +548,30 @@ sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev, int
   AffineArgs& a = c->aa;
   cudaStream_t s = c->stream;
   if (ev) cudaEventRecord(ev[0], s);
+  // graph path: the warm blocks' predictor (k_warm_pred + one GEMM; inputs = what the previous iteration left)
+  // forks here and runs beside the affine chain; large_block_warm_begin joins it.  Its kernels read the
+  // done / proceed flags k_tphase is about to write: at worst the predictor of the stopping iteration runs
+  // (it touches only the warm start buffers, and nothing runs after the stop).
+  cudaEvent_t pred_done[8] = {};
+  bool any_pred = false;
+  {
+    cudaStreamCaptureStatus cap0 = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap0);
+    if (mode_full && !ev && phase == 0 && !c->sp.emulated && c->early_pred && c->aux_ok && cap0 == cudaStreamCaptureStatusActive) {
+      for (size_t b = 0; b < c->le.blocks.size() && b < 8; ++b) any_pred |= c->le.blocks[b].warm && c->le.blocks[b].wa.predict;
+      if (any_pred) {
+        cudaEventRecord(c->ev_pre0, s);
+        for (size_t b = 0; b < c->le.blocks.size() && b < 8; ++b) {
+          LargeBlock& lb = c->le.blocks[b];
+          if (!(lb.warm && lb.wa.predict)) continue;
+          cudaStreamWaitEvent(c->pre[b], c->ev_pre0, 0);
+          large_block_warm_pred(c->le, lb, c->pre[b]);
+          cudaEventRecord(c->ev_pre[b], c->pre[b]);
+          pred_done[b] = c->ev_pre[b];
+        }
+      }
+    }
+  }
   if (c->sp.sharded) {
     if (c->sp.emulated && phase == 0) {
       c->err = SOSADMM_E_ARG;
@@ -593,7 +621,7 @@ sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev, int
       cudaEventRecord(c->ev_join, c->aux[0]);
     }
     const cudaError_t ge = large_eig_launch_concurrent(c->le, s, true, c->ev_fork, c->aux + 1, c->ev_blk, c->body,
-                                                       c->nest_ok ? c->nest : nullptr);
+                                                       c->nest_ok ? c->nest : nullptr, any_pred ? pred_done : nullptr);
     if (ge != cudaSuccess) {
       c->err = SOSADMM_E_CUDA;
       c->msg = std::string("large-block projection capture: ") + cudaGetErrorString(ge);
@@ -1019,7 +1047,11 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
     for (size_t q = 0; q < an.large_blk.size(); ++q) {
       CK_CTX(c, cudaStreamCreateWithFlags(&c->body[q], cudaStreamNonBlocking));
       CK_CTX(c, cudaStreamCreateWithFlags(&c->nest[q], cudaStreamNonBlocking));
+      CK_CTX(c, cudaStreamCreateWithFlags(&c->pre[q], cudaStreamNonBlocking));
+      CK_CTX(c, cudaEventCreateWithFlags(&c->ev_pre[q], cudaEventDisableTiming));
     }
+    CK_CTX(c, cudaEventCreateWithFlags(&c->ev_pre0, cudaEventDisableTiming));
+    if (const char* ep = getenv("SOSADMM_EARLY_PRED")) c->early_pred = atoi(ep) != 0;
     CK_CTX(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK_CTX(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     for (int q = 0; q < 8 * (int)an.large_blk.size(); ++q)
@@ -1450,6 +1482,11 @@ void sosadmm_destroy(sosadmm_ctx* c) {
     if (a) cudaStreamDestroy(a);
   for (auto& a : c->nest)
     if (a) cudaStreamDestroy(a);
+  for (auto& a : c->pre)
+    if (a) cudaStreamDestroy(a);
+  for (auto& e : c->ev_pre)
+    if (e) cudaEventDestroy(e);
+  if (c->ev_pre0) cudaEventDestroy(c->ev_pre0);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   for (auto& e : c->ev_poll)
