@@ -148,6 +148,14 @@ sosadmm_err sosadmm_iterate(sosadmm_ctx* ctx, int64_t k, sosadmm_info* out);
  * On a sharded context it is a collective like sosadmm_iterate. */
 sosadmm_err sosadmm_iterate_async(sosadmm_ctx* ctx, int64_t k);
 
+/* Scheduling hint for SURVEY §8(f) f1 (no arithmetic: the iterates of `eq:ADMMSteps` are the same bit for
+ * bit either way).  shared != 0: the context shares its GPU with other concurrently iterating instances, so
+ * its iteration graph keeps the warm-start predictor of the large-block PSD projection in line instead of
+ * forking it beside the affine projection (measured: the fork gains 2 % for a lone instance and costs
+ * 8-18 % of a batch's aggregate rate).  Default 0.  Waits for the context's enqueued work and drops an
+ * already built graph (rebuilt by the next iterate call).  E_ARG on a NULL context. */
+sosadmm_err sosadmm_set_shared_gpu(sosadmm_ctx* ctx, int shared);
+
 /* Same iterations launched without the CUDA graph, with CUDA events (on the library's stream)
  * around each phase; adds the phase durations (ms) to ms_phase[0..SOSADMM_NPHASE-1] = {affine
  * gather..row update, scatter, small-block Jacobi projections, large-block tridiagonalisation,

@@ -401,7 +401,8 @@ struct sosadmm_ctx {
   // warm predictor branches (one per large block), forked at the start of the iteration beside the affine chain
   cudaStream_t pre[8] = {};
   cudaEvent_t ev_pre0 = nullptr, ev_pre[8] = {};
-  bool early_pred = true;  // SOSADMM_EARLY_PRED=0: the predictor after the scatter, as on the un-graphed path
+  bool early_pred = true;  // SOSADMM_EARLY_PRED=0 / sosadmm_set_shared_gpu: the predictor after the scatter, as un-graphed
+  bool no_early_pred_env = false;
   // early-stop polling of sosadmm_iterate: pinned copies of the device state after each chunk of replays
   DevState* h_poll = nullptr;
   cudaEvent_t ev_poll[2] = {};
@@ -1051,7 +1052,8 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
       CK_CTX(c, cudaEventCreateWithFlags(&c->ev_pre[q], cudaEventDisableTiming));
     }
     CK_CTX(c, cudaEventCreateWithFlags(&c->ev_pre0, cudaEventDisableTiming));
-    if (const char* ep = getenv("SOSADMM_EARLY_PRED")) c->early_pred = atoi(ep) != 0;
+    if (const char* ep = getenv("SOSADMM_EARLY_PRED")) c->no_early_pred_env = atoi(ep) == 0;
+    c->early_pred = !c->no_early_pred_env;
     CK_CTX(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CK_CTX(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     for (int q = 0; q < 8 * (int)an.large_blk.size(); ++q)
@@ -1202,6 +1204,23 @@ sosadmm_err sosadmm_iterate_async(sosadmm_ctx* c, int64_t k) {
   if (build_graph(c)) return c->err;
   for (int64_t i = 0; i < k; ++i) CK_CTX(c, cudaGraphLaunch(c->graph, c->stream));
   return check_async(c);
+}
+
+sosadmm_err sosadmm_set_shared_gpu(sosadmm_ctx* c, int shared) {
+  if (!c) return SOSADMM_E_ARG;
+  if (c->err) return c->err;
+  const bool want = shared == 0 && !c->no_early_pred_env;
+  if (want == c->early_pred) return SOSADMM_OK;
+  CK_CTX(c, cudaSetDevice(c->device));
+  CK_CTX(c, cudaStreamSynchronize(c->stream));
+  c->early_pred = want;
+  if (c->graph) {  // rebuilt by the next iterate call
+    cudaGraphExecDestroy(c->graph);
+    c->graph = nullptr;
+    if (c->graph_raw) cudaGraphDestroy(c->graph_raw);
+    c->graph_raw = nullptr;
+  }
+  return SOSADMM_OK;
 }
 
 sosadmm_err sosadmm_iterate_profiled(sosadmm_ctx* c, int64_t k, sosadmm_info* out, double* ms_phase) {

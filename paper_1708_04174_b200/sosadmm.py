@@ -19,7 +19,7 @@ STATUS = {0: "RUNNING", 1: "OPTIMAL", 2: "PRIMAL_INFEASIBLE", 3: "DUAL_INFEASIBL
           5: "INCONCLUSIVE"}
 
 EXPORTS = ["sosadmm_workspace_size", "sosadmm_setup", "sosadmm_setup_sharded", "sosadmm_nccl_unique_id",
-           "sosadmm_iterate", "sosadmm_iterate_async", "sosadmm_iterate_profiled",
+           "sosadmm_iterate", "sosadmm_iterate_async", "sosadmm_set_shared_gpu", "sosadmm_iterate_profiled",
            "sosadmm_get_info", "sosadmm_get_iterate", "sosadmm_set_iterate", "sosadmm_get_structure",
            "sosadmm_project_affine", "sosadmm_project_psd", "sosadmm_launches_per_iter", "sosadmm_psd_work", "sosadmm_warm_stats", "sosadmm_residual_history",
            "sosadmm_destroy",
@@ -74,6 +74,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.sosadmm_iterate.argtypes = [V, I64, ctypes.POINTER(_Info)]
     lib.sosadmm_iterate_profiled.argtypes = [V, I64, ctypes.POINTER(_Info), P]
     lib.sosadmm_iterate_async.argtypes = [V, I64]
+    lib.sosadmm_set_shared_gpu.argtypes = [V, I32]
     lib.sosadmm_get_info.argtypes = [V, ctypes.POINTER(_Info)]
     lib.sosadmm_get_iterate.argtypes = [V, P, P, P, P, P, P, ctypes.POINTER(I64)]
     lib.sosadmm_set_iterate.argtypes = [V, P, P, P, P, D, D, I64]
@@ -207,6 +208,10 @@ class SosAdmm:
         """Enqueue k iterations on this instance's stream and return at once (see iterate_batch)."""
         self._check(self.lib.sosadmm_iterate_async(self._ctx, int(k)), "iterate_async")
 
+    def set_shared_gpu(self, shared: bool) -> None:
+        """Scheduling hint (sosadmm_set_shared_gpu): other instances iterate on this GPU at the same time."""
+        self._check(self.lib.sosadmm_set_shared_gpu(self._ctx, 1 if shared else 0), "set_shared_gpu")
+
     def iterate_profiled(self, k: int):
         info = _Info()
         ms = np.zeros(NPHASE)
@@ -322,6 +327,9 @@ def iterate_batch(solvers, k: int, chunk: int = 256) -> list:
         raise ValueError("k must be >= 0 and chunk >= 1")
     left = [int(k)] * len(solvers)
     active = list(range(len(solvers)))
+    if len(solvers) > 1:
+        for s in solvers:
+            s.set_shared_gpu(True)  # scheduling hint only: the iterates do not change
     while active:
         for i in active:
             n = min(chunk, left[i])

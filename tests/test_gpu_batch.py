@@ -122,3 +122,29 @@ def test_fused_low_phase_bit_identical(name, monkeypatch):
     assert ia["iter"] == ib["iter"] == 40
     assert np.array_equal(va, vb)
     assert ia["res_pri"] == ib["res_pri"] and ia["res_dual"] == ib["res_dual"]
+
+
+def test_shared_gpu_hint_changes_no_iterate():
+    """sosadmm_set_shared_gpu is a scheduling hint: with it the warm-start predictor of the large-block
+    projection stays in line, without it the CUDA graph forks it beside the affine chain.  The predictor
+    reads only what the previous iteration left, so the iterates are BIT-identical either way, also when the
+    hint is flipped in the middle of a solve (the graph is rebuilt).  pop20: N = 231, predictor active."""
+    from paper_1708_04174_b200 import SosAdmm
+
+    prob = make_config("pop20")
+    out = []
+    for mode in ("lone", "shared", "flip"):
+        s = SosAdmm.from_problem(prob, tol=1e-300, max_iters=1 << 30)
+        if mode == "shared":
+            s.set_shared_gpu(True)
+        s.iterate(300)
+        if mode == "flip":
+            s.set_shared_gpu(True)
+        info = s.iterate(300)
+        ws = s.warm_stats()
+        out.append((info, _iterates(s), ws))
+        s.close()
+    assert out[0][2][0]["warm"] > 400  # the refinement (and its predictor) carried the solve
+    for info, v, _ in out[1:]:
+        assert info["iter"] == out[0][0]["iter"] == 600
+        assert np.array_equal(v, out[0][1])
