@@ -127,6 +127,16 @@ def eig_flops(N: int) -> float:
     return (4.0 / 3.0 + 2.0 + 1.0) * N ** 3
 
 
+def host_tl(prob) -> int:
+    """t' = columns of A_low: the free columns plus the PSD columns that break partial
+    orthogonality (more than one entry, or a cost entry), counted on the host so that both arms print the
+    same workload string (the CUDA arm reads the same number back from the device's structure)."""
+    A = prob.A.tocsc()
+    nn = np.diff(A.indptr)[prob.n_free:]
+    c = np.asarray(prob.c).ravel()[prob.n_free:]
+    return int(prob.n_free + ((nn > 1) | (c != 0)).sum())
+
+
 def affine_bytes(prob, tl: int) -> float:
     """Algorithmic HBM bytes of the affine projection per iteration:
     36 L + 68 m + 24 nnz(A_low) + 4 t'(t'+1) (the K^{-1} apply reads one triangle of the symmetric
@@ -664,7 +674,8 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic (seeded, BASELINE.json config {CONFIG_INDEX.get(args.config, '?')})",
         "config": {"workload": f"{args.config} (N={'+'.join(str(d) for d in sorted(set(prob.psd_dims), reverse=True))}, "
-                               f"{len(prob.psd_dims)} PSD blocks, m={prob.m}) seed {args.seed}", "l2": "n/a (CPU)"},
+                               f"{len(prob.psd_dims)} PSD blocks, m={prob.m}, t'={host_tl(prob)}) seed {args.seed}",
+                   "l2": "n/a (CPU)"},
         "cpu_baseline": {"value": v, "unit": "iters/s", "cores": 1, "kind": "oracle",
                          "sample": f"{args.steps} oracle iterations after {args.warmup} warm-up, 1 BLAS thread"},
         "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
