@@ -20,6 +20,8 @@ struct JacobiArgs {
   double* vp;            // warm start: per small block the N x N eigenvectors of the
   const long long* blk_vp;  //   previous solve at vp + blk_vp[b] (identity before the first)
   int warm;              // 1 = start from B = P^T A P with P the previous eigenvectors
+  int blocked;           // 1 = a round updates 2 x 2 blocks per thread (one shared-memory read per output): selects the
+                         //     kernel instantiation on the host (jacobi_kernel)
 };
 
 // Round r of the tournament for Np players (Np even): slot k -> pair (p, q).
@@ -44,7 +46,7 @@ __device__ __forceinline__ void rr_pair(int r, int k, int Np, int& p, int& q) {
 // new input; Jacobi runs on B = P^T A P (measured on pop6: 8.6 -> 4.9 sweeps, tools/
 // warm_jacobi_probe.py) and the eigenvectors are P V_B.  Every 64th iteration starts cold (P = I)
 // so that the rounding of the accumulated product never builds up.
-template <int MAXN, int NT>
+template <int MAXN, int NT, bool BLK>
 __global__ void __launch_bounds__(NT) k_psd_jacobi(JacobiArgs a) {
   if (a.check_state && (a.st->done || !a.is->proceed)) return;
   const int b = a.small_blk[blockIdx.x];
@@ -154,6 +156,41 @@ __global__ void __launch_bounds__(NT) k_psd_jacobi(JacobiArgs a) {
   // parameter threads: the LAST Np/2 threads of the CTA, whose second element slot is empty when
   // Np^2 <= NT (MAXN) + NT - Np/2 (e.g. pop6's Np = 28 at NT = 512), so the round's longest thread
   // carries one element update fewer
+  // Blocked round update (a.blocked): work items of a round are the (Np/2)^2 blocks {p_a, q_a} x {p_b, q_b} of
+  // A' = J^T A J (pairs a, b = tournament slots: four reads, four outputs) and the Np x Np/2 row-pair items
+  // (i, {p_b, q_b}) of V' = V J (two reads, two outputs): one shared-memory read per output instead of four /
+  // two (the elementwise pass is shared-memory-bandwidth bound: 63 KB per round at N = 28).  The slot
+  // decomposition of a thread's items is fixed for the whole solve.
+  const int H = Np >> 1;
+  constexpr int PERI = BLK ? (MAXN / 2 * (MAXN / 2) + MAXN * (MAXN / 2) + NT - 1) / NT : 1;
+  short ia[PERI], ib[PERI];  // item (ia, ib): A block of slots (ia, ib) if ia < H, else V item (row ia - H, slot ib)
+#pragma unroll
+  for (int cnt = 0; cnt < (BLK ? PERI : 0); ++cnt) {
+    const int it = tid + cnt * NT;
+    int x = -1, y = 0;
+    if (it < H * H) {  // slot a fastest: consecutive lanes read consecutive rows p_a (descending q_a)
+      x = it % H;
+      y = it / H;
+    } else if (it < H * H + Np * H) {
+      const int v = it - H * H;
+      x = H + v % Np;
+      y = v / Np;
+    }
+    ia[cnt] = (short)x;
+    ib[cnt] = (short)y;
+  }
+  // pair of slot k in round r without a division (0 <= r, k < M)
+  auto slot_pair = [&](int r, int k, int& p, int& q) {
+    if (k == 0) {
+      p = M;
+      q = r;
+    } else {
+      p = r + k;
+      p -= p >= M ? M : 0;
+      q = r - k;
+      q += q < 0 ? M : 0;
+    }
+  };
   const int pt = tid - (NT - Np / 2);
   if (tid < 4) nrot[tid] = 0;
   __syncthreads();
@@ -182,6 +219,46 @@ __global__ void __launch_bounds__(NT) k_psd_jacobi(JacobiArgs a) {
         return (j == ip && bi != 0.0) ? 0.0 : na;  // the coupling of a rotated pair: exact zero
       };
       double off2 = 0.0;  // this thread's share of off(A')^2, summed in a sweep's last round
+      if constexpr (BLK) {
+        // out(i, j) of the 2 x 2 coupling: rows (i, ip) with (ai, bi), columns (j, jp) with (aj, bj); x = A[i, j],
+        // y = A[i, jp], z = A[ip, j], w = A[ip, jp] -- elem()'s expression
+        auto rot = [](double ai, double bi, double aj, double bj, double x, double y, double z, double w) {
+          return ai * (aj * x + bj * y) + bi * (aj * z + bj * w);
+        };
+#pragma unroll
+        for (int cnt = 0; cnt < PERI; ++cnt) {
+          const int x = ia[cnt], kb = ib[cnt];
+          if (x < 0) continue;
+          int pb, qb;
+          slot_pair(r, kb, pb, qb);
+          const double cb = al[pb], sb = be[pb];  // (al, be)[qb] = (cb, -sb)
+          if (x < H) {
+            int pa, qa;
+            slot_pair(r, x, pa, qa);
+            const double ca = al[pa], sa = be[pa];
+            const double a00 = A[pa + pb * Np], a01 = A[pa + qb * Np], a10 = A[qa + pb * Np], a11 = A[qa + qb * Np];
+            double n00 = rot(ca, sa, cb, sb, a00, a01, a10, a11);    // (pa, pb)
+            double n01 = rot(ca, sa, cb, -sb, a01, a00, a11, a10);   // (pa, qb)
+            double n10 = rot(ca, -sa, cb, sb, a10, a11, a00, a01);   // (qa, pb)
+            double n11 = rot(ca, -sa, cb, -sb, a11, a10, a01, a00);  // (qa, qb)
+            if (x == kb) {  // the rotated pair itself: its coupling is an exact zero
+              if (sa != 0.0) n01 = n10 = 0.0;
+              off2 = fma(n01, n01, fma(n10, n10, off2));
+            } else {
+              off2 = fma(n00, n00, fma(n01, n01, fma(n10, n10, fma(n11, n11, off2))));
+            }
+            An[pa + pb * Np] = n00;
+            An[pa + qb * Np] = n01;
+            An[qa + pb * Np] = n10;
+            An[qa + qb * Np] = n11;
+          } else {
+            const int i = x - H;
+            const double v0 = V[i + pb * Np], v1 = V[i + qb * Np];
+            Vn[i + pb * Np] = cb * v0 + sb * v1;
+            Vn[i + qb * Np] = cb * v1 - sb * v0;
+          }
+        }
+      } else {
 #pragma unroll
       for (int cnt = 0; cnt < PER; ++cnt) {
         const int e = tid + cnt * NT;
@@ -193,6 +270,7 @@ __global__ void __launch_bounds__(NT) k_psd_jacobi(JacobiArgs a) {
           Vn[e] = al[j] * V[i + j * Np] + be[j] * V[i + jp * Np];
           off2 = i != j ? fma(v, v, off2) : off2;
         }
+      }
       }
       if (r == M - 1) {
         off2 = warp_sum(off2);
@@ -253,7 +331,8 @@ inline size_t jacobi_smem_bytes(int N) {
 
 typedef void (*JacobiKernel)(JacobiArgs);
 constexpr int JAC_NT32 = 512;  // threads for blocks N <= 32 (measured: 64 / 128 / 256 / 512 / 1024 -> 0.27 / 0.17 / 0.14 / 0.12 / 0.13 ms on pop6)
-inline JacobiKernel jacobi_kernel(int max_small_N) {
-  return max_small_N <= 32 ? k_psd_jacobi<32, JAC_NT32> : k_psd_jacobi<64, JAC_NT>;
+inline JacobiKernel jacobi_kernel(int max_small_N, int blocked) {
+  if (blocked) return max_small_N <= 32 ? k_psd_jacobi<32, JAC_NT32, true> : k_psd_jacobi<64, JAC_NT, true>;
+  return max_small_N <= 32 ? k_psd_jacobi<32, JAC_NT32, false> : k_psd_jacobi<64, JAC_NT, false>;
 }
 inline int jacobi_threads(int max_small_N) { return max_small_N <= 32 ? JAC_NT32 : JAC_NT; }

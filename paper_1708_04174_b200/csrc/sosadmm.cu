@@ -617,7 +617,7 @@ sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev, int
     cudaEventRecord(c->ev_fork, s);
     if (has_small) {
       cudaStreamWaitEvent(c->aux[0], c->ev_fork, 0);
-      jacobi_kernel(c->an.max_small_N)<<<(int)c->an.small_blk.size(), jacobi_threads(c->an.max_small_N), jacobi_smem_bytes(c->an.max_small_N),
+      jacobi_kernel(c->an.max_small_N, c->ja.blocked)<<<(int)c->an.small_blk.size(), jacobi_threads(c->an.max_small_N), jacobi_smem_bytes(c->an.max_small_N),
                                          c->aux[0]>>>(c->ja);
       cudaEventRecord(c->ev_join, c->aux[0]);
     }
@@ -631,7 +631,7 @@ sosadmm_err launch_iteration(sosadmm_ctx* c, int mode_full, cudaEvent_t* ev, int
     if (has_small) cudaStreamWaitEvent(s, c->ev_join, 0);
   } else {
     if (has_small)
-      jacobi_kernel(c->an.max_small_N)<<<(int)c->an.small_blk.size(), jacobi_threads(c->an.max_small_N), jacobi_smem_bytes(c->an.max_small_N),
+      jacobi_kernel(c->an.max_small_N, c->ja.blocked)<<<(int)c->an.small_blk.size(), jacobi_threads(c->an.max_small_N), jacobi_smem_bytes(c->an.max_small_N),
                                          s>>>(c->ja);
     if (ev) cudaEventRecord(ev[3], s);
     if (has_large) {
@@ -1022,10 +1022,12 @@ static sosadmm_err setup_impl(const sosadmm_problem* prob, const sosadmm_setting
   ja.mats = d.mats; ja.blk_mat = d.blk_mat; ja.blk_N = d.blk_N; ja.small_blk = d.small_blk;
   ja.st = d.st; ja.is = d.is; ja.check_state = 1;
   ja.vp = d.jvp; ja.blk_vp = d.blk_vp; ja.warm = 1;
+  ja.blocked = 1;  // SOSADMM_JACOBI_BLOCKED=0: the elementwise round update (A/B runs)
+  if (const char* jb = getenv("SOSADMM_JACOBI_BLOCKED")) ja.blocked = atoi(jb) != 0;
   if (!an.small_blk.empty()) {
     // the attribute is per kernel and process-wide: set the template's bound, never a per-context
     // size (a later context with smaller blocks would otherwise shrink it under an earlier one)
-    CK_CTX(c, cudaFuncSetAttribute(jacobi_kernel(an.max_small_N), cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK_CTX(c, cudaFuncSetAttribute(jacobi_kernel(an.max_small_N, c->ja.blocked), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)jacobi_smem_bytes(an.max_small_N <= 32 ? 32 : JAC_MAXN)));
   }
   {
@@ -1405,7 +1407,7 @@ sosadmm_err sosadmm_project_psd(sosadmm_ctx* c, int32_t block, const double* a_s
   CK_CTX(c, cudaMemcpyAsync(c->d_tmp + off, a_svec, sizeof(double) * L, cudaMemcpyHostToDevice, s));
   k_unpack_block<<<(int)((L + 255) / 256), 256, 0, s>>>(a, block, c->d_tmp + off);
   if (!c->an.small_blk.empty())
-    jacobi_kernel(c->an.max_small_N)<<<(int)c->an.small_blk.size(), jacobi_threads(c->an.max_small_N), jacobi_smem_bytes(c->an.max_small_N),
+    jacobi_kernel(c->an.max_small_N, c->ja.blocked)<<<(int)c->an.small_blk.size(), jacobi_threads(c->an.max_small_N), jacobi_smem_bytes(c->an.max_small_N),
                                          s>>>(c->ja);
   if (!c->an.large_blk.empty()) large_eig_launch(c->le, s, true);
   if (a.pos_ctas > 0) k_pack<<<a.pos_ctas, POS_NT, 0, s>>>(a, c->d_tmp, 0);
